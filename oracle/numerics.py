@@ -1,0 +1,81 @@
+"""Elementwise numerics of the target decoder, float64.
+
+Precision reading (SURVEY amb. A12; the paper states no precision anywhere, P:16/P:744 only quote
+marketing TFLOPS): tensors that live in HBM are bf16-valued (weights, embeddings, cached K
+(post-RoPE) and V, the residual stream after each add, every GEMM input operand and the
+final-norm output).  `bf16` below rounds an exact (float64) value to the nearest bf16 value,
+ties to even.  All other arithmetic is float64.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def bf16(x):
+    """Round to nearest bfloat16 (8 significant bits, 8-bit exponent), ties to even.
+
+    x = m * 2**e with m in [0.5, 1); bf16 spacing at x is 2**(e-8), or the subnormal spacing
+    2**-133 below 2**-126.  Division/multiplication by powers of two is exact in float64 and
+    np.rint rounds half to even.  Pinned against torch's fp32->bf16 converter.
+    """
+    x = np.asarray(x, dtype=np.float64)
+    m, e = np.frexp(x)
+    e = np.maximum(e - 8, -133)
+    spacing = np.ldexp(1.0, e)
+    y = np.rint(x / spacing) * spacing
+    y = np.where(np.abs(y) >= 2.0 ** 128, np.copysign(np.inf, x), y)   # overflow past bf16 max
+    return np.where(np.isfinite(x), y, x)
+
+
+def f32(x):
+    """Round to float32 (IEEE RNE), returned as float64."""
+    return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def rmsnorm(x, g, eps):
+    """RMSNorm (Llama/Qwen, SURVEY amb. A13): x / sqrt(mean(x^2) + eps) * g, over the last axis."""
+    x = np.asarray(x, np.float64)
+    ms = np.mean(x * x, axis=-1, keepdims=True)
+    return x / np.sqrt(ms + eps) * g
+
+
+def rope_angles(pos, head_dim, theta):
+    """Rotary angles pos * theta^(-2i/hd), i < hd/2 (SURVEY amb. A14, rotate-half convention)."""
+    i = np.arange(head_dim // 2, dtype=np.float64)
+    inv_freq = np.power(float(theta), -2.0 * i / head_dim)
+    return np.asarray(pos, np.float64)[..., None] * inv_freq
+
+
+def rope(x, pos, theta):
+    """Rotate-half RoPE.  x [..., heads, hd], pos broadcastable to x.shape[:-2].
+
+    out[:h] = x[:h] cos - x[h:] sin ;  out[h:] = x[h:] cos + x[:h] sin   (h = hd/2)
+    """
+    x = np.asarray(x, np.float64)
+    hd = x.shape[-1]
+    ang = rope_angles(pos, hd, theta)[..., None, :]        # [..., 1, hd/2]
+    c, s = np.cos(ang), np.sin(ang)
+    x1, x2 = x[..., : hd // 2], x[..., hd // 2:]
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+def silu(x):
+    x = np.asarray(x, np.float64)
+    return x / (1.0 + np.exp(-x))
+
+
+def softmax(s, axis=-1):
+    s = np.asarray(s, np.float64)
+    m = np.max(s, axis=axis, keepdims=True)
+    e = np.exp(s - m)
+    return e / np.sum(e, axis=axis, keepdims=True)
+
+
+def attention(q, k, v):
+    """Scaled-dot-product attention of one query set over one key set (SURVEY amb. A15).
+
+    q [nq, hd], k [nk, hd], v [nk, hd] -> [nq, hd]; scores q.k/sqrt(hd), softmax over keys.
+    """
+    hd = q.shape[-1]
+    s = (q @ k.T) / np.sqrt(hd)
+    return softmax(s, axis=-1) @ v
