@@ -1,0 +1,439 @@
+"""Benchmark: verified tokens/sec of batched tree verification on B200 (BASELINE.json metric).
+
+Workload (N=1 and per GPU): cfg2 = BASELINE.json configs[1] — Llama-3-8B-shaped random-init
+decoder, 16 requests x 32-node draft trees (pooled top-budget trees, D=7, b=4),
+committed contexts ~ U[768, 1280] (mean 1k, synthetic KV), greedy verification, acceptance
+planted to the paper's tokens/verify profile (3.98 +- 1.55, Table 1).
+A step = one specedge_verify_batch(auto_commit=1) (all of SURVEY §8(a) a1-a11) + a rewind of the
+cached lengths so every step sees identical inputs.  Multi-GPU: one process per GPU, each an
+independent replica with its own 16 requests (weak scaling, no collective on the data path;
+SURVEY §8(e) replicas).
+
+--impl reference: the CPU oracle (oracle/, numpy float64) on the box's host cores, on a bounded
+sample of the same workload, extrapolated to the metric's unit (this tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "verified tokens/sec (accepted+bonus) per box at 1/2/4/8 B200; p50 verify-step latency"
+UNIT = "tokens/s"
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop_ev.set()
+            self.t.join()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------ workload
+def build_trees(wl, rank, vocab):
+    from synth.trees import pooled_tree
+    trees = []
+    for r in range(wl.n_requests):
+        rng = np.random.default_rng([1000 + int(wl.name[-1]), rank, r])
+        trees.append(pooled_tree(rng, wl.n_nodes, wl.depth, wl.branching, vocab))
+    return trees
+
+
+def contexts(wl, rank):
+    rng = np.random.default_rng([wl.ctx_seed, rank])
+    return [int(x) for x in rng.integers(wl.ctx_lo, wl.ctx_hi + 1, wl.n_requests)]
+
+
+def setup_gpu(wl, rank, device):
+    import torch
+    from paper_2505_17052_b200 import api
+    from synth.plant import plant, draw_accept_lengths
+    shape = wl.shape
+    ctx = contexts(wl, rank)
+    max_ctx = max(ctx) + wl.n_nodes + 64
+    model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64)
+    pages = sum((c + wl.n_nodes + 2 + 63) // 64 for c in ctx) + 8
+    pool = api.KVPool(model, pages, wl.n_requests + 2)
+    handles = []
+    for r, c in enumerate(ctx):
+        h = pool.alloc(c + wl.n_nodes + 2)
+        pool.fill_random(h, c - 1, wl.ctx_seed, rank * 1000 + r)
+        handles.append(h)
+    rng = np.random.default_rng([wl.ctx_seed + 7, rank])
+    roots = [int(t) for t in rng.integers(0, shape.vocab, wl.n_requests)]
+    sessions = [(rank << 32) | (1000 + r) for r in range(wl.n_requests)]
+    trees = build_trees(wl, rank, shape.vocab)
+    R = sum(t.n + 1 for t in trees)
+    ws = model.workspace(wl.n_requests, R, max_ctx)
+    mode = 1 if wl.mode == "sample" else 0
+
+    def make_batch(ts):
+        return api.Batch.from_host(handles, ctx, roots, sessions, [0] * wl.n_requests, ts,
+                                   device=f"cuda:{device}", max_context_len=max_ctx)
+
+    def targets(ts):
+        b = make_batch(ts)
+        out = api.verify(model, pool, b, ws, mode=mode, temperature=wl.temperature, seed=wl.weight_seed,
+                         auto_commit=False)
+        rt = out.row_target.cpu().numpy()
+        off = b.node_offset.cpu().numpy()
+        return [rt[off[i] + i: off[i + 1] + i + 1] for i in range(wl.n_requests)]
+
+    accept = draw_accept_lengths(np.random.default_rng([wl.ctx_seed + 11, rank]), trees, wl.accept_mu,
+                                 wl.accept_sigma)
+    trees = plant(trees, targets, accept, shape.vocab, np.random.default_rng([wl.ctx_seed + 13, rank]))
+    batch = make_batch(trees)
+    out = api.verify(model, pool, batch, ws, mode=mode, temperature=wl.temperature, seed=wl.weight_seed,
+                     auto_commit=False)
+    torch.cuda.synchronize()
+    got = out.accepted_len.cpu().numpy().tolist()
+    status = out.status.cpu().numpy().tolist()
+    assert all(s == 0 for s in status), status
+    return dict(api=api, model=model, pool=pool, ws=ws, batch=batch, handles=handles, ctx=ctx, mode=mode,
+                trees=trees, planted=accept, accepted=got, R=R)
+
+
+def algorithmic_work(wl, st):
+    """Algorithmic flops and bytes per launch of each kernel kind."""
+    s = wl.shape
+    R = st["R"]
+    hd, H, KV, d, F, V = s.head_dim, s.n_heads, s.n_kv, s.d, s.ffn, s.vocab
+    qkv = (H + 2 * KV) * hd
+    gemms = {
+        "gemm_qkv": (qkv, d), "gemm_o": (d, H * hd), "gemm_gateup": (2 * F, d), "gemm_down": (d, F),
+        "gemm_lmhead": (V, d),
+    }
+    work = {}
+    for k, (n_out, kk) in gemms.items():
+        work[k] = dict(flops=2.0 * R * n_out * kk, bytes=2.0 * n_out * kk + 2.0 * R * kk + 2.0 * R * n_out)
+    # attention per layer: prefix K/V read + tree K/V read, Q read, O write
+    kv_tok = 2 * KV * hd * 2
+    prefix = sum(c - 1 for c in st["ctx"])
+    work["attention"] = dict(bytes=float(prefix * kv_tok + R * kv_tok + 2 * R * H * hd * 2),
+                             flops=float(4 * hd * H * sum((c - 1) * (t.n + 1) for c, t in zip(st["ctx"], st["trees"]))))
+    return work
+
+
+def run_gpu(args, world, rank, local):
+    import torch
+    from synth.configs import WORKLOADS
+    wl = WORKLOADS[args.workload]
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    st = setup_gpu(wl, rank, local)
+    api, model, pool, ws, batch = st["api"], st["model"], st["pool"], st["ws"], st["batch"]
+    lib = model.lib
+    handles, L0 = st["handles"], [c - 1 for c in st["ctx"]]
+    stream = torch.cuda.current_stream()
+
+    def step():
+        out = api.verify(model, pool, batch, ws, mode=st["mode"], temperature=wl.temperature,
+                         seed=wl.weight_seed, auto_commit=True, out=outs)
+        pool.set_len(handles, L0)
+        return out
+
+    outs = api.Outputs.alloc(batch, f"cuda:{local}")
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    tokens_per_step = int(sum(a + 1 for a in st["accepted"]))
+    # ---- timed region: K steps, per-step CUDA events, per-kernel events inside the library
+    import ctypes as C
+    nk = len(api.L.KERNEL_KINDS)
+    lib.specedge_kernel_times(None, None, 1)
+    lib.specedge_set_kernel_timing(1)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            step()
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    lib.specedge_set_kernel_timing(0)
+    launches = api.last_launch_count() * args.steps
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    kms = (C.c_float * nk)()
+    kcnt = (C.c_int32 * nk)()
+    lib.specedge_kernel_times(kms, kcnt, 1)
+    acc = outs.accepted_len.cpu().numpy()
+    assert int((acc + 1).sum()) == tokens_per_step, "accepted counts changed between steps"
+    if dist:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * tokens_per_step * args.steps / (total_ms / 1e3)
+
+    # ---- end-to-end through the host-buffer C-ABI entry point (copies inside the timed region)
+    hb = api.HostBatch.of(batch)
+    ho = api.host_outputs(hb)
+    for _ in range(2):
+        api.verify_host(model, pool, hb, ws, ho, mode=st["mode"], temperature=wl.temperature, seed=wl.weight_seed)
+        pool.set_len(handles, L0)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        api.verify_host(model, pool, hb, ws, ho, mode=st["mode"], temperature=wl.temperature, seed=wl.weight_seed)
+        pool.set_len(handles, L0)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_tokens = int((ho["accepted_len"].numpy() + 1).sum())
+    B, T, R = hb.num_requests, hb.total_nodes, hb.total_nodes + hb.num_requests
+    h2d = hb.nbytes()
+    d2h = 4 * (3 * B + 2 * T + 2 * R)
+
+    # ---- roofline of the dominant kernel (largest share of the timed step)
+    kinds = api.L.KERNEL_KINDS
+    share = {kinds[i]: float(kms[i]) for i in range(nk)}
+    dom = max(share, key=share.get)
+    work = algorithmic_work(wl, st)
+    peaks = _peaks()
+    roof = None
+    if dom in work:
+        per_launch_ms = share[dom] / max(1, kcnt[kinds.index(dom)])
+        w = work[dom]
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(wl.name, {}).get(dom)
+        if dom.startswith("gemm"):
+            peak = peaks.get("bf16_tflops_sustained", 1415.3)
+            ach = w["flops"] / (per_launch_ms / 1e3) / 1e12
+            roof = dict(kernel=dom, bound="tensor", achieved=round(ach, 1), peak=peak, unit="TFLOP/s",
+                        frac=round(ach / peak, 4), traffic=traffic,
+                        algorithmic_flops_per_launch=w["flops"], launch_ms=round(per_launch_ms, 4),
+                        peak_source="MEASURED_PEAKS.json bf16_tflops_sustained")
+        else:
+            peak = peaks.get("hbm_gbs", 6456.2)
+            ach = w["bytes"] / (per_launch_ms / 1e3) / 1e9
+            roof = dict(kernel=dom, bound="hbm", achieved=round(ach, 1), peak=peak, unit="GB/s",
+                        frac=round(ach / peak, 4), traffic=traffic,
+                        algorithmic_bytes_per_launch=w["bytes"], launch_ms=round(per_launch_ms, 4),
+                        peak_source="MEASURED_PEAKS.json hbm_gbs")
+    kernel_table = {kinds[i]: dict(ms_per_step=round(float(kms[i]) / args.steps, 4), launches=int(kcnt[i]) // args.steps)
+                    for i in range(nk) if kcnt[i]}
+    for k, w in work.items():
+        if k in kernel_table and kernel_table[k]["launches"]:
+            per = kernel_table[k]["ms_per_step"] / kernel_table[k]["launches"] / 1e3
+            kernel_table[k]["tflops"] = round(w["flops"] / per / 1e12, 1)
+            kernel_table[k]["gbs"] = round(w["bytes"] / per / 1e9, 1)
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    result = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{wl.name}: {wl.shape.name}-shaped random-init, {wl.n_requests} requests x "
+                               f"{wl.n_nodes}-node trees (D={wl.depth}, b={wl.branching}), ctx U[{wl.ctx_lo},"
+                               f"{wl.ctx_hi}], {wl.mode}",
+                   "requests_per_gpu": wl.n_requests, "rows_per_step": st["R"], "tokens_per_step_per_gpu": tokens_per_step,
+                   "planted_tokens_per_verify": round(tokens_per_step / wl.n_requests, 3),
+                   "l2": "inputs larger than L2 (16 GB of weights streamed every step)",
+                   "parallelism": f"replicas x{world}"},
+        "p50_ms": round(statistics.median(step_ms), 4), "p90_ms": round(float(np.quantile(step_ms, 0.9)), 4),
+        "rows_per_s": round(world * st["R"] * args.steps / (total_ms / 1e3), 1),
+        "roofline": roof, "kernels": kernel_table,
+        "e2e": {"value": round(world * e2e_tokens * args.steps / (e2e_ms / 1e3), 1), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches), "clocks": clk.result(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        result["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
+    print(json.dumps(result), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------- CPU oracle arm
+class OracleSample:
+    """The oracle, as it stands, on a bounded sample of the same workload: request 0's draft tree
+    (33 rows) through layer 0 of the model against its synthetic context, plus the LM head over a
+    4096-row vocab slice.  One sample ~ 1 s; extrapolated linearly to all layers, the full vocab
+    and all rows of the step.  Weight generation is setup (not timed)."""
+
+    VSLICE = 4096
+
+    def __init__(self, wl, rank=0):
+        from oracle.model import Weights, Cache, gen_kv_fill
+        from synth.plant import draw_accept_lengths
+        self.wl = wl
+        s = wl.shape
+        self.ctx = contexts(wl, rank)
+        self.trees = build_trees(wl, rank, s.vocab)
+        one = type(s)(**{**s.as_dict(), "n_layers": 1})
+        self.W = Weights(one, wl.weight_seed)
+        self.W.layer(0)
+        self.lm = self.W.lm_head_block(0, self.VSLICE)
+        L = self.ctx[0] - 1
+        self.cache = Cache(one)
+        self.cache.k[0] = gen_kv_fill(wl.ctx_seed, rank * 1000, 0, 0, L, s.n_kv, s.head_dim)
+        self.cache.v[0] = gen_kv_fill(wl.ctx_seed, rank * 1000, 0, 1, L, s.n_kv, s.head_dim)
+        acc = draw_accept_lengths(np.random.default_rng([wl.ctx_seed + 11, rank]), self.trees, wl.accept_mu,
+                                  wl.accept_sigma)
+        self.tokens_per_step = sum(a + 1 for a in acc)
+        self.rows = sum(t.n + 1 for t in self.trees)
+        try:
+            from threadpoolctl import threadpool_info
+            self.cores = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+        except Exception:
+            self.cores = os.cpu_count()
+
+    def step_seconds(self):
+        from oracle.model import tree_forward
+        s = self.wl.shape
+        t0 = time.perf_counter()
+        hf, _, _ = tree_forward(self.W, self.cache, 1, self.trees[0].parent, self.trees[0].token)
+        t_layer = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        _ = hf @ self.lm.T
+        t_lm = (time.perf_counter() - t0) * s.vocab / self.VSLICE
+        return (t_layer * s.n_layers + t_lm) * self.rows / (self.trees[0].n + 1)
+
+    def describe(self):
+        s = self.wl.shape
+        return (f"oracle (numpy fp64) on request 0 ({self.trees[0].n + 1} rows) of {self.wl.name}: layer 0 of "
+                f"{s.n_layers} + LM head over {self.VSLICE}/{s.vocab} vocab rows, extrapolated to {s.n_layers} "
+                f"layers, full vocab, {self.rows} rows; {self.tokens_per_step} verified tokens/step (planted)")
+
+
+def cpu_baseline(wl, budget_s=20.0, rank=0):
+    smp = OracleSample(wl, rank)
+    secs = []
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s or len(secs) < 3:
+        secs.append(smp.step_seconds())
+        if len(secs) >= 50:
+            break
+    t_step = float(np.median(secs))
+    return {"value": round(smp.tokens_per_step / t_step, 4), "unit": UNIT, "cores": smp.cores, "kind": "oracle",
+            "sample": smp.describe() + f"; median of {len(secs)} samples",
+            "seconds_per_step_extrapolated": round(t_step, 2)}
+
+
+def run_reference(args, world, rank):
+    from synth.configs import WORKLOADS
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.workload]
+    t_all = time.perf_counter()
+    smp = OracleSample(wl, rank)
+    for _ in range(args.warmup):
+        smp.step_seconds()
+    secs = [smp.step_seconds() for _ in range(max(1, args.steps))]
+    t_step = float(np.median(secs))
+    v = smp.tokens_per_step / t_step
+    cb = {"value": round(v, 4), "unit": UNIT, "cores": smp.cores, "kind": "oracle", "sample": smp.describe()}
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_step, 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{wl.name}: {wl.shape.name}-shaped, {wl.n_requests} requests x {wl.n_nodes}-node "
+                                  f"trees (oracle sample, extrapolated)", "parallelism": "cpu"},
+           "cpu_baseline": cb, "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                                       "d2h_bytes_per_step": 0},
+           "wall_s": round(time.perf_counter() - t_all, 1)}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    world, rank, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_gpu(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

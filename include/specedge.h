@@ -1,0 +1,240 @@
+/*
+ * specedge.h — C ABI of libspecedge: B200 (sm_100a) server-side batched verification of
+ * edge-drafted token trees, the hot path of SpecEdge (arXiv 2505.17052).
+ *
+ * What the path computes (citations: P:n = PAPER.md line n, S:n = SPEC.md line n, SURVEY =
+ * SURVEY.md section, "amb. Ax" = a reading of an unstated detail, listed in DESIGN.md):
+ *   - P:171 (§4.1): "edge GPUs generate candidate tokens and send them to the server, which
+ *     verifies them in a single forward pass.  The server returns both the verified tokens
+ *     and one additional token", preserving "the exact output distribution of the server
+ *     model".
+ *   - P:315-316 (§4.3): heterogeneous batches, "custom attention masking for each token
+ *     sequence in the batch ... without cross-sequence interference".  (The paper pads KV to
+ *     the longest sequence; this library uses a paged, ragged KV cache instead.)
+ *   - P:599 (App. A): draft trees of budget 32 pruned by cumulative log-probability.
+ *
+ * One verify step = tree prep (validate, depth, RoPE position, ancestor bitmask) -> embedding
+ * gather -> per layer {RMSNorm, QKV GEMM + RoPE + tree K/V write, tree-masked paged split-KV
+ * attention, O-proj + residual, RMSNorm, gate/up GEMM + SwiGLU, down + residual} -> final norm
+ * + LM head fused with a vocab-wide argmax (greedy) or Gumbel-max (sampled) reduction, logits
+ * never written to HBM -> accept walk + bonus -> KV commit (compaction of the root and the
+ * accepted nodes' K/V into the cache).
+ *
+ * Conventions
+ *   - Every function returns a specedge_status: SPECEDGE_OK (0) or a negative API error code.
+ *     API errors are detected on the host BEFORE any launch; outputs are then untouched.
+ *   - Per-request data errors are written to out->status[r] on the device (positive codes);
+ *     an errored request gets accepted_len 0, bonus -1, no commit, and does not affect the
+ *     other requests.
+ *   - `stream` is a cudaStream_t passed as void*.  Calls are stream-ordered and never
+ *     synchronise the host, except the *_host entry points and the setup calls documented as
+ *     synchronous.
+ *   - "device" pointers are CUDA device memory owned by the caller unless stated otherwise.
+ *     The library owns weights, the KV page pool, block tables and the RoPE table.  The
+ *     verify workspace is caller-owned (size from specedge_workspace_size).
+ *   - Thread safety: one host thread per model / pool at a time.
+ */
+#ifndef SPECEDGE_H_
+#define SPECEDGE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t specedge_status;
+typedef struct specedge_model specedge_model;
+typedef struct specedge_kvpool specedge_kvpool;
+
+/* ---- API error codes (negative, host-detected) ---- */
+#define SPECEDGE_OK 0
+#define SPECEDGE_E_INVALID (-1)      /* null pointer, non-positive size, bad mode, bad handle */
+#define SPECEDGE_E_CUDA (-2)         /* a CUDA runtime/driver call failed */
+#define SPECEDGE_E_OOM (-3)          /* device allocation or KV pages exhausted */
+#define SPECEDGE_E_WORKSPACE (-4)    /* workspace too small for this call */
+#define SPECEDGE_E_UNSUPPORTED (-5)  /* shape outside what the kernels support */
+#define SPECEDGE_E_DEVICE (-6)       /* device is not sm_100 */
+
+/* ---- per-request status codes (device-written, out->status[r]) ---- */
+#define SPECEDGE_REQ_OK 0
+#define SPECEDGE_REQ_E_TREE 1         /* parent[i] not in {-1} U [0, i) */
+#define SPECEDGE_REQ_E_TREE_SIZE 2    /* N > 64 nodes                            (amb. A5) */
+#define SPECEDGE_REQ_E_TOKEN 3        /* root or draft token outside [0, V)              */
+#define SPECEDGE_REQ_E_DUP_SIBLING 4  /* two children of one parent share a token */
+#define SPECEDGE_REQ_E_CONTEXT 5      /* context_len != cached + 1, or > max_context_len
+                                         ("context-length mismatch -> protocol error") */
+#define SPECEDGE_REQ_E_KV_CAPACITY 6  /* cached + deepest path + 1 exceeds the handle's capacity */
+#define SPECEDGE_REQ_E_HANDLE 7       /* KV handle not allocated */
+/* validation order (first failing check wins): HANDLE, TREE_SIZE, TREE, TOKEN, DUP_SIBLING,
+   CONTEXT, KV_CAPACITY — identical to oracle/verify.py:validate for the shared codes. */
+
+/* ---- verification modes (SURVEY amb. A7-A9) ---- */
+#define SPECEDGE_GREEDY 0       /* y = argmax_v logit, ties -> lowest id */
+#define SPECEDGE_SAMPLE_TREE 1  /* y = argmax_v (logit/T + Gumbel(seed, round, session, slot, v)) */
+
+#define SPECEDGE_MAX_NODES 64
+#define SPECEDGE_PAGE_TOKENS 64
+
+/* Decoder shape (Llama/Qwen3 family, SURVEY amb. A13-A16; no biases, untied LM head).
+ * Supported: head_dim in {16, 32, 64, 128}; d, n_heads*head_dim, ffn multiples of 64;
+ * n_heads % n_kv == 0. */
+typedef struct {
+  int32_t n_layers, d, n_heads, n_kv, head_dim, ffn, vocab;
+  float eps;            /* RMSNorm epsilon */
+  double rope_theta;    /* RoPE base (rotate-half convention, amb. A14) */
+  int32_t max_position; /* RoPE table length; positions must be < max_position */
+} specedge_model_config;
+
+/* Create a model on `device` with synthetic bf16 weights that are a pure function of
+ * `weight_seed` (Philox4x32-10, generated on the device; bit-identical to the
+ * oracle's generator).  Synchronous.  *out receives an owned handle. */
+specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t weight_seed,
+                                      int32_t device, specedge_model** out);
+specedge_status specedge_model_destroy(specedge_model* model);
+
+/* KV page pool of `num_pages` pages x 64 tokens x all layers (bf16 K and V), zero-initialised,
+ * with room for `max_handles` sessions.  Synchronous. */
+specedge_status specedge_kvpool_create(specedge_model* model, int32_t num_pages,
+                                       int32_t max_handles, specedge_kvpool** out);
+specedge_status specedge_kvpool_destroy(specedge_kvpool* pool);
+/* Reserve pages for a session able to hold `capacity_tokens` cached tokens; returns the handle
+ * (>= 0) in *out_handle with cached length 0.  E_OOM if pages or handles are exhausted.
+ * Synchronous (host allocator + one small H2D copy). */
+specedge_status specedge_kv_alloc(specedge_kvpool* pool, int32_t capacity_tokens,
+                                  int32_t* out_handle);
+specedge_status specedge_kv_free(specedge_kvpool* pool, int32_t handle);
+/* Set the cached length of n sessions (host arrays), stream-ordered (used to rewind a session
+ * between benchmark steps).  Lengths must be <= capacity. */
+specedge_status specedge_kv_set_len(specedge_kvpool* pool, const int32_t* handles,
+                                    const int32_t* lens, int32_t n, void* stream);
+/* Read the cached lengths of n sessions into host array `lens` (synchronous). */
+specedge_status specedge_kv_get_len(specedge_kvpool* pool, const int32_t* handles, int32_t* lens,
+                                    int32_t n);
+/* Fill positions [0, n_tokens) of a session with synthetic K/V (element =
+ * bf16(int24 * 2^-23) from Philox keyed (seed, position, layer*2+kv, stream_id ^ 'KVFI')) and
+ * set its cached length to n_tokens.  Performance runs only; parity runs prefill for real. */
+specedge_status specedge_kv_fill_random(specedge_kvpool* pool, int32_t handle, int32_t n_tokens,
+                                        uint64_t seed, uint32_t stream_id, void* stream);
+
+/* Bytes of workspace a verify / prefill call needs for up to max_requests requests,
+ * max_rows = sum of (nodes + 1) rows, and contexts up to max_context_len tokens. */
+specedge_status specedge_workspace_size(const specedge_model* model, int32_t max_requests,
+                                        int32_t max_rows, int32_t max_context_len,
+                                        size_t* bytes);
+
+/* Prefill (outside the measured path): run the decoder over host tokens[0..n-2] of a
+ * session whose cached length is 0 and cache their K/V (chunked causal chain verification on
+ * the same kernels).  tokens[n-1] becomes the first root.  Stream-ordered; the host array is
+ * copied before return. */
+specedge_status specedge_prefill(specedge_model* model, specedge_kvpool* pool, int32_t handle,
+                                 const int32_t* tokens_host, int32_t n, void* workspace,
+                                 size_t ws_bytes, void* stream);
+
+/* ---- the hot path ---- */
+typedef struct {
+  /* host scalars */
+  int32_t num_requests;     /* B >= 1 */
+  int32_t total_nodes;      /* sum_r N_r (root excluded, amb. A1); rows R = total_nodes + B */
+  int32_t max_nodes;        /* >= max_r N_r, <= 64 */
+  int32_t max_context_len;  /* >= max_r context_len[r] (grid sizing; checked per request) */
+  int32_t mode;             /* SPECEDGE_GREEDY | SPECEDGE_SAMPLE_TREE */
+  float temperature;        /* used iff mode == SAMPLE_TREE; T < 1e-6 => GREEDY */
+  uint64_t seed;            /* sampling seed (amb. A9) */
+  int32_t auto_commit;      /* 1: also commit accepted K/V (== calling specedge_kv_commit) */
+  /* device arrays (caller-owned, valid until the stream passes this call) */
+  const int32_t* kv;             /* [B] KV handle per request */
+  const int32_t* context_len;    /* [B] committed tokens C_r = cached + 1 (amb. A2) */
+  const int32_t* root_token;     /* [B] last committed token (previous bonus) */
+  const uint64_t* session_id;    /* [B] RNG key part */
+  const uint32_t* round;         /* [B] RNG key part: per-session verify counter */
+  const int32_t* node_offset;    /* [B+1] CSR offsets into the node arrays */
+  const int32_t* parent;         /* [total_nodes] -1 = child of root, else local index < i */
+  const int32_t* token;          /* [total_nodes] draft tokens */
+  const float* draft_logprob;    /* [total_nodes] log q, nullable; unused by GREEDY and
+                                    SAMPLE_TREE (SURVEY Lemma, amb. A23) */
+} specedge_verify_in;
+
+typedef struct {                 /* device arrays, caller-allocated */
+  int32_t* status;               /* [B] per-request status (SPECEDGE_REQ_*) */
+  int32_t* accepted_len;         /* [B] a_r: accepted draft nodes (tokens/verify = a_r + 1) */
+  int32_t* accepted_token;       /* [total_nodes] CSR by node_offset, first a_r valid */
+  int32_t* accepted_node;        /* [total_nodes] node indices of the accepted root path */
+  int32_t* bonus;                /* [B] the one additional token; -1 on error */
+  int32_t* row_target;           /* [R] nullable: target token y per slot (slot 0 = root) */
+  float* row_score;              /* [R] nullable: top-1 score (max logit, or max Gumbel score) */
+} specedge_verify_out;
+
+/* Verify a batch.  Row r's slots occupy rows node_offset[r] + r ... node_offset[r+1] + r
+ * (slot 0 = root, slot i+1 = node i).  Errors: E_INVALID (null/mismatched arguments,
+ * max_nodes > 64, bad mode), E_WORKSPACE, E_UNSUPPORTED, E_CUDA. */
+specedge_status specedge_verify_batch(specedge_model* model, specedge_kvpool* pool,
+                                      const specedge_verify_in* in, specedge_verify_out* out,
+                                      void* workspace, size_t ws_bytes, void* stream);
+
+/* Commit the K/V of the root and the accepted nodes of a previous verify_batch (same `in`,
+ * `out`, same workspace, no other verify on that workspace in between).  Applies at most once:
+ * a request whose cached length already moved is skipped and gets status E_CONTEXT. */
+specedge_status specedge_kv_commit(specedge_model* model, specedge_kvpool* pool,
+                                   const specedge_verify_in* in, specedge_verify_out* out,
+                                   void* workspace, size_t ws_bytes, void* stream);
+
+/* End-to-end entry point with HOST buffers (same fields; every pointer in `in`/`out` is host
+ * memory, pinned for best results).  Copies the inputs into the workspace, verifies, copies
+ * the outputs back and synchronises `stream` before returning. */
+specedge_status specedge_verify_batch_host(specedge_model* model, specedge_kvpool* pool,
+                                           const specedge_verify_in* in_host,
+                                           specedge_verify_out* out_host, void* workspace,
+                                           size_t ws_bytes, void* stream);
+
+/* ---- test introspection (used by tests/ only; never on the verify path) ---- */
+/* Logical weight rows back to the host as bf16 bits: tensor ids as in oracle/model.py
+ * (1 embed, 2 wq, 3 wk, 4 wv, 5 wo, 6 wg, 7 wu, 8 wd, 9 lm_head, 10 g_attn, 11 g_mlp,
+ * 12 g_final).  Synchronous. */
+specedge_status specedge_debug_weight_rows(specedge_model* model, int32_t tensor, int32_t layer,
+                                           int32_t row0, int32_t nrows, uint16_t* dst_host);
+/* Cached K or V (kv_sel 0/1) of positions [pos0, pos0+n) of a session, layer `layer`, as bf16
+ * bits [n][n_kv][head_dim] into host memory.  Synchronous. */
+specedge_status specedge_debug_read_kv(specedge_kvpool* pool, int32_t handle, int32_t layer,
+                                       int32_t kv_sel, int32_t pos0, int32_t n,
+                                       uint16_t* dst_host);
+/* Run the tcgen05 GEMM alone: out[r][m] = sum_k X[r][k] * W[m][k] (bf16 in, fp32 out), all
+ * device pointers, row-major.  M, K multiples of 64 (M tile zero-padded), R >= 1. */
+specedge_status specedge_debug_gemm(const uint16_t* W, const uint16_t* X, float* out, int32_t M,
+                                    int32_t R, int32_t K, void* stream);
+/* Run the LM-head GEMM (same tcgen05 kernel, fp32-store epilogue) on the final-norm hidden
+ * states left in the workspace by the last verify of (num_requests, R): writes fp32 logits
+ * [R][V] to logits_dev.  Test-only; the verify path itself never materialises logits. */
+specedge_status specedge_debug_last_logits(specedge_model* model, void* workspace,
+                                           size_t ws_bytes, int32_t num_requests, int32_t R,
+                                           float* logits_dev, void* stream);
+/* Tree-masked attention kernel alone on caller data (all device): q [S][G][hd] bf16 for one
+ * request and one kv head, prefix k/v [L][hd] bf16, tree k/v [S][hd] bf16, anc [S-1] uint64
+ * (ancestor-or-self masks over nodes); writes o [S][G][hd] fp32 (normalised). */
+specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_prefix,
+                                         const uint16_t* v_prefix, const uint16_t* k_tree,
+                                         const uint16_t* v_tree, const uint64_t* anc, int32_t S,
+                                         int32_t G, int32_t head_dim, int32_t L,
+                                         int32_t n_splits, float* o, void* workspace,
+                                         size_t ws_bytes, void* stream);
+
+/* Number of kernels the last verify_batch call launched (host counter, for the benchmark's
+ * gpu_launches field). */
+int32_t specedge_last_launch_count(void);
+
+/* ---- per-kernel timing (benchmark instrumentation) ----
+ * When enabled, verify_batch records a CUDA event pair on `stream` around every kernel it
+ * launches (stream-ordered, no host sync).  specedge_kernel_times synchronises on the recorded
+ * events, adds their durations to per-kind totals and clears the pending list; out_ms[k] and
+ * out_count[k] (arrays of SPECEDGE_KERNEL_KINDS) receive the totals since the last reset.
+ * Kinds: 0 prep, 1 embed, 2 rmsnorm, 3 gemm_qkv, 4 attention, 5 attn_combine, 6 gemm_o,
+ * 7 gemm_gateup, 8 gemm_down, 9 gemm_lmhead, 10 lm_reduce, 11 walk, 12 commit. */
+#define SPECEDGE_KERNEL_KINDS 13
+specedge_status specedge_set_kernel_timing(int32_t enable);
+specedge_status specedge_kernel_times(float* out_ms, int32_t* out_count, int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECEDGE_H_ */

@@ -7,6 +7,11 @@ decoder here is the Llama/Qwen3 family layout (SURVEY amb. A13-A16): RMSNorm -> 
 GQA attention -> O-proj + residual -> RMSNorm -> SwiGLU MLP + residual, final RMSNorm, untied
 LM head, no biases, QK-norm off.
 
+Storage points (reading R-precision, revising SURVEY amb. A12): bf16 for weights,
+embeddings, every GEMM input operand (normed h, q, O, M, final-norm output), cached K (post-RoPE)
+and V; the residual stream x is kept unrounded (the GPU keeps it in fp32), because rounding it to
+bf16 amplifies arithmetic-order noise past the north_star logit tolerance (tests/notes in DESIGN).
+
 Two independent ways of running it live here:
   * `tree_forward`   - SURVEY §8(c) O2: all S = N+1 slots of a draft tree at once; slot s
                        attends to the cached prefix, the root and its own ancestors-or-self;
@@ -179,10 +184,10 @@ def _post_attn(W: Weights, l, x, o):
     s = W.shape
     Lw = W.layer(l)
     O = bf16(o.reshape(o.shape[0], -1))
-    x = bf16(x + O @ Lw["wo"].T)
+    x = x + O @ Lw["wo"].T                 # residual stream is not a GEMM operand: not rounded
     h2 = bf16(rmsnorm(x, Lw["g_mlp"], s.eps))
     M = bf16(silu(h2 @ Lw["wg"].T) * (h2 @ Lw["wu"].T))
-    return bf16(x + M @ Lw["wd"].T)
+    return x + M @ Lw["wd"].T
 
 
 def final_hidden(W: Weights, x):

@@ -1,9 +1,9 @@
 """Elementwise numerics of the target decoder, float64.
 
-Precision reading (SURVEY amb. A12; the paper states no precision anywhere, P:16/P:744 only quote
-marketing TFLOPS): tensors that live in HBM are bf16-valued (weights, embeddings, cached K
-(post-RoPE) and V, the residual stream after each add, every GEMM input operand and the
-final-norm output).  `bf16` below rounds an exact (float64) value to the nearest bf16 value,
+Precision reading (DESIGN.md R-precision, revising SURVEY amb. A12; the paper states no precision
+anywhere, P:16/P:744 only quote marketing TFLOPS): bf16-valued are weights, embeddings, cached K
+(post-RoPE) and V, every GEMM input operand and the final-norm output; the residual stream is
+not rounded.  `bf16` below rounds an exact (float64) value to the nearest bf16 value,
 ties to even.  All other arithmetic is float64.
 """
 from __future__ import annotations

@@ -177,30 +177,44 @@ def commit(session: Session, out: Outcome):
 
 
 def verify_one(W: Weights, req: Request, mode="greedy", temperature=0.0, seed=0, keep_logits=True):
-    s = W.shape
-    ses = req.session
-    root = ses.last_token if req.root_token < 0 else req.root_token
-    ctx = ses.context_len if req.context_len < 0 else req.context_len
-    rnd = ses.round if req.round < 0 else req.round
-    parent = [int(p) for p in req.parent]
-    token = [int(t) for t in req.token]
-    st = validate(parent, token, root, s.vocab, ctx, len(ses.cache))
-    if st != OK:
-        return Outcome(status=st)
-    hf, tk, tv = tree_forward(W, ses.cache, root, parent, token)
-    logits = lm_logits(W, hf)
-    scores = target_scores(logits, mode, temperature, seed, rnd, ses.session_id)
-    y = argmax_lowest(scores)
-    acc_t, acc_n, bonus = walk(parent, token, y)
-    return Outcome(OK, acc_t, acc_n, bonus, y, scores.max(axis=-1),
-                   logits if keep_logits else None, tk, tv)
+    return verify_batch(W, [req], mode, temperature, seed, auto_commit=False, keep_logits=keep_logits)[0]
 
 
 def verify_batch(W: Weights, reqs, mode="greedy", temperature=0.0, seed=0, auto_commit=True,
                  keep_logits=True):
     """A batch is a list of independent requests: no request reads another's state (amb. A4,
-    A17), so the batch result is by construction the list of solo results."""
-    outs = [verify_one(W, r, mode, temperature, seed, keep_logits) for r in reqs]
+    A17), so the batch result is by construction the list of solo results.  The LM head
+    is applied to all requests' rows in one pass over the vocabulary (same arithmetic per row)."""
+    s = W.shape
+    staged = []
+    for req in reqs:
+        ses = req.session
+        root = ses.last_token if req.root_token < 0 else req.root_token
+        ctx = ses.context_len if req.context_len < 0 else req.context_len
+        rnd = ses.round if req.round < 0 else req.round
+        parent = [int(p) for p in req.parent]
+        token = [int(t) for t in req.token]
+        st = validate(parent, token, root, s.vocab, ctx, len(ses.cache))
+        if st != OK:
+            staged.append((st, None))
+            continue
+        hf, tk, tv = tree_forward(W, ses.cache, root, parent, token)
+        staged.append((st, (parent, token, rnd, ses.session_id, hf, tk, tv)))
+    rows = [x[1][4] for x in staged if x[0] == OK]
+    logits_all = lm_logits(W, np.concatenate(rows)) if rows else None
+    outs, off = [], 0
+    for st, x in staged:
+        if st != OK:
+            outs.append(Outcome(status=st))
+            continue
+        parent, token, rnd, sid, hf, tk, tv = x
+        logits = logits_all[off:off + hf.shape[0]]
+        off += hf.shape[0]
+        scores = target_scores(logits, mode, temperature, seed, rnd, sid)
+        y = argmax_lowest(scores)
+        acc_t, acc_n, bonus = walk(parent, token, y)
+        outs.append(Outcome(OK, acc_t, acc_n, bonus, y, scores.max(axis=-1),
+                            logits if keep_logits else None, tk, tv))
     if auto_commit:
         for r, o in zip(reqs, outs):
             if o.status == OK:

@@ -1,0 +1,286 @@
+"""Thin Python API over the C ABI.  PyTorch supplies device memory and streams only; every
+step of the verify path runs in libspecedge's kernels (no CPU or torch fallback)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class Shape:
+    n_layers: int
+    d: int
+    n_heads: int
+    n_kv: int
+    head_dim: int
+    ffn: int
+    vocab: int
+    eps: float
+    rope_theta: float
+
+    @classmethod
+    def of(cls, s):
+        return cls(s.n_layers, s.d, s.n_heads, s.n_kv, s.head_dim, s.ffn, s.vocab, s.eps, s.rope_theta)
+
+
+class Model:
+    """A target decoder with synthetic weights (Philox(seed), generated on the device)."""
+
+    def __init__(self, shape, weight_seed: int, device: int = 0, max_position: int = 32768):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libspecedge needs a CUDA device (sm_100a); no fallback exists")
+        self.lib = L.load()
+        self.shape = Shape.of(shape)
+        self.device = device
+        cfg = L.ModelConfig(shape.n_layers, shape.d, shape.n_heads, shape.n_kv, shape.head_dim,
+                            shape.ffn, shape.vocab, shape.eps, shape.rope_theta, max_position)
+        h = C.c_void_p()
+        L.check(self.lib.specedge_model_create(C.byref(cfg), C.c_uint64(weight_seed), device, C.byref(h)),
+                "model_create")
+        self.h = h
+        self.max_position = max_position
+
+    def close(self):
+        if self.h:
+            self.lib.specedge_model_destroy(self.h)
+            self.h = None
+
+    def weight_rows(self, tensor: int, layer: int, row0: int, nrows: int, cols: int) -> np.ndarray:
+        out = np.empty((nrows, cols), np.uint16)
+        L.check(self.lib.specedge_debug_weight_rows(self.h, tensor, layer, row0, nrows,
+                                                    out.ctypes.data_as(C.c_void_p)), "debug_weight_rows")
+        return out
+
+    def workspace(self, max_requests: int, max_rows: int, max_context: int) -> torch.Tensor:
+        n = C.c_size_t()
+        L.check(self.lib.specedge_workspace_size(self.h, max_requests, max_rows, max_context, C.byref(n)),
+                "workspace_size")
+        return torch.empty(n.value, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+
+class KVPool:
+    def __init__(self, model: Model, num_pages: int, max_handles: int):
+        self.model = model
+        self.lib = model.lib
+        h = C.c_void_p()
+        L.check(self.lib.specedge_kvpool_create(model.h, num_pages, max_handles, C.byref(h)), "kvpool_create")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.lib.specedge_kvpool_destroy(self.h)
+            self.h = None
+
+    def alloc(self, capacity: int) -> int:
+        out = C.c_int32()
+        L.check(self.lib.specedge_kv_alloc(self.h, capacity, C.byref(out)), "kv_alloc")
+        return out.value
+
+    def free(self, handle: int):
+        L.check(self.lib.specedge_kv_free(self.h, handle), "kv_free")
+
+    def set_len(self, handles, lens, stream=None):
+        hs = np.ascontiguousarray(handles, np.int32)
+        ls = np.ascontiguousarray(lens, np.int32)
+        L.check(self.lib.specedge_kv_set_len(self.h, hs.ctypes.data_as(C.c_void_p), ls.ctypes.data_as(C.c_void_p),
+                                             len(hs), _stream(stream)), "kv_set_len")
+
+    def get_len(self, handles):
+        hs = np.ascontiguousarray(handles, np.int32)
+        out = np.empty(len(hs), np.int32)
+        L.check(self.lib.specedge_kv_get_len(self.h, hs.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p),
+                                             len(hs)), "kv_get_len")
+        return out
+
+    def fill_random(self, handle: int, n_tokens: int, seed: int, stream_id: int, stream=None):
+        L.check(self.lib.specedge_kv_fill_random(self.h, handle, n_tokens, C.c_uint64(seed), stream_id,
+                                                 _stream(stream)), "kv_fill_random")
+
+    def prefill(self, handle: int, tokens, ws: torch.Tensor, stream=None):
+        t = np.ascontiguousarray(tokens, np.int32)
+        L.check(self.lib.specedge_prefill(self.model.h, self.h, handle, t.ctypes.data_as(C.c_void_p), len(t),
+                                          _ptr(ws), ws.numel(), _stream(stream)), "prefill")
+
+    def read_kv(self, handle: int, layer: int, kv_sel: int, pos0: int, n: int) -> np.ndarray:
+        s = self.model.shape
+        out = np.empty((n, s.n_kv, s.head_dim), np.uint16)
+        L.check(self.lib.specedge_debug_read_kv(self.h, handle, layer, kv_sel, pos0, n,
+                                                out.ctypes.data_as(C.c_void_p)), "debug_read_kv")
+        return out
+
+
+@dataclass
+class Batch:
+    """Device-resident verify inputs (specedge_verify_in's arrays) plus host scalars."""
+    kv: torch.Tensor
+    context_len: torch.Tensor
+    root_token: torch.Tensor
+    session_id: torch.Tensor
+    round: torch.Tensor
+    node_offset: torch.Tensor
+    parent: torch.Tensor
+    token: torch.Tensor
+    draft_logprob: torch.Tensor
+    total_nodes: int
+    max_nodes: int
+    max_context_len: int
+
+    @property
+    def num_requests(self):
+        return int(self.kv.numel())
+
+    @property
+    def rows(self):
+        return self.total_nodes + self.num_requests
+
+    @classmethod
+    def from_host(cls, kv, context_len, root_token, session_id, rnd, trees, device="cuda",
+                  max_context_len=None, max_nodes=None):
+        from synth.trees import pack
+        off, parent, token, logprob = pack(trees)
+        dev = torch.device(device)
+        t32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.int32)).to(dev)
+        ctx = np.ascontiguousarray(context_len, np.int32)
+        return cls(t32(kv), t32(ctx), t32(root_token),
+                   torch.as_tensor(np.ascontiguousarray(session_id, np.uint64).view(np.int64)).to(dev),
+                   torch.as_tensor(np.ascontiguousarray(rnd, np.uint32).view(np.int32)).to(dev),
+                   t32(off), t32(parent if len(parent) else np.zeros(1, np.int32)),
+                   t32(token if len(token) else np.zeros(1, np.int32)),
+                   torch.as_tensor(logprob if len(logprob) else np.zeros(1, np.float32)).to(dev),
+                   int(off[-1]),
+                   int(max_nodes if max_nodes is not None else max([t.n for t in trees] + [0])),
+                   int(max_context_len if max_context_len is not None else int(ctx.max())))
+
+
+@dataclass
+class Outputs:
+    status: torch.Tensor
+    accepted_len: torch.Tensor
+    accepted_token: torch.Tensor
+    accepted_node: torch.Tensor
+    bonus: torch.Tensor
+    row_target: torch.Tensor
+    row_score: torch.Tensor
+
+    @classmethod
+    def alloc(cls, batch: Batch, device="cuda"):
+        B, T, R = batch.num_requests, max(1, batch.total_nodes), batch.rows
+        z = lambda n, dt=torch.int32: torch.full((n,), -7, dtype=dt, device=device)
+        return cls(z(B), z(B), z(T), z(T), z(B), z(R), torch.zeros(R, dtype=torch.float32, device=device))
+
+
+def _vin(batch: Batch, mode, temperature, seed, auto_commit):
+    return L.VerifyIn(batch.num_requests, batch.total_nodes, batch.max_nodes, batch.max_context_len, mode,
+                      float(temperature), C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF).value, int(auto_commit),
+                      batch.kv.data_ptr(), batch.context_len.data_ptr(), batch.root_token.data_ptr(),
+                      batch.session_id.data_ptr(), batch.round.data_ptr(), batch.node_offset.data_ptr(),
+                      batch.parent.data_ptr(), batch.token.data_ptr(), batch.draft_logprob.data_ptr())
+
+
+def _vout(o: Outputs):
+    return L.VerifyOut(o.status.data_ptr(), o.accepted_len.data_ptr(), o.accepted_token.data_ptr(),
+                       o.accepted_node.data_ptr(), o.bonus.data_ptr(),
+                       None if o.row_target is None else o.row_target.data_ptr(),
+                       None if o.row_score is None else o.row_score.data_ptr())
+
+
+def verify(model: Model, pool: KVPool, batch: Batch, ws: torch.Tensor, mode=L.GREEDY, temperature=0.0, seed=0,
+           auto_commit=True, out: Outputs | None = None, stream=None) -> Outputs:
+    out = out if out is not None else Outputs.alloc(batch, batch.kv.device)
+    vin, vout = _vin(batch, mode, temperature, seed, auto_commit), _vout(out)
+    L.check(model.lib.specedge_verify_batch(model.h, pool.h, C.byref(vin), C.byref(vout), _ptr(ws), ws.numel(),
+                                            _stream(stream)), "verify_batch")
+    return out
+
+
+def kv_commit(model: Model, pool: KVPool, batch: Batch, out: Outputs, ws: torch.Tensor, stream=None):
+    vin, vout = _vin(batch, L.GREEDY, 0.0, 0, True), _vout(out)
+    L.check(model.lib.specedge_kv_commit(model.h, pool.h, C.byref(vin), C.byref(vout), _ptr(ws), ws.numel(),
+                                         _stream(stream)), "kv_commit")
+
+
+@dataclass
+class HostBatch:
+    """Pinned host copies of a Batch's arrays for the end-to-end entry point."""
+    arrays: dict
+    total_nodes: int
+    max_nodes: int
+    max_context_len: int
+    num_requests: int
+
+    @classmethod
+    def of(cls, b: Batch):
+        a = {k: getattr(b, k).cpu().pin_memory() for k in
+             ("kv", "context_len", "root_token", "session_id", "round", "node_offset", "parent", "token",
+              "draft_logprob")}
+        return cls(a, b.total_nodes, b.max_nodes, b.max_context_len, b.num_requests)
+
+    def nbytes(self):
+        return sum(t.numel() * t.element_size() for k, t in self.arrays.items() if k != "draft_logprob")
+
+
+def verify_host(model: Model, pool: KVPool, hb: HostBatch, ws: torch.Tensor, outs: dict, mode=L.GREEDY,
+                temperature=0.0, seed=0, auto_commit=True, stream=None):
+    a = hb.arrays
+    vin = L.VerifyIn(hb.num_requests, hb.total_nodes, hb.max_nodes, hb.max_context_len, mode, float(temperature),
+                     seed, int(auto_commit), a["kv"].data_ptr(), a["context_len"].data_ptr(),
+                     a["root_token"].data_ptr(), a["session_id"].data_ptr(), a["round"].data_ptr(),
+                     a["node_offset"].data_ptr(), a["parent"].data_ptr(), a["token"].data_ptr(),
+                     a["draft_logprob"].data_ptr())
+    vout = L.VerifyOut(*(outs[k].data_ptr() for k in ("status", "accepted_len", "accepted_token",
+                                                      "accepted_node", "bonus", "row_target", "row_score")))
+    L.check(model.lib.specedge_verify_batch_host(model.h, pool.h, C.byref(vin), C.byref(vout), _ptr(ws),
+                                                 ws.numel(), _stream(stream)), "verify_batch_host")
+
+
+def host_outputs(hb: HostBatch):
+    B, T, R = hb.num_requests, max(1, hb.total_nodes), hb.total_nodes + hb.num_requests
+    z = lambda n, dt=torch.int32: torch.zeros(n, dtype=dt).pin_memory()
+    return dict(status=z(B), accepted_len=z(B), accepted_token=z(T), accepted_node=z(T), bonus=z(B),
+                row_target=z(R), row_score=z(R, torch.float32))
+
+
+def last_launch_count() -> int:
+    return int(L.load().specedge_last_launch_count())
+
+
+def debug_gemm(W: torch.Tensor, X: torch.Tensor, stream=None) -> torch.Tensor:
+    """out[r][m] = sum_k X[r,k] W[m,k] through the tcgen05 GEMM kernel (fp32 out)."""
+    M, K = W.shape
+    R = X.shape[0]
+    out = torch.empty((R, M), dtype=torch.float32, device=W.device)
+    L.check(L.load().specedge_debug_gemm(_ptr(W), _ptr(X), _ptr(out), M, R, K, _stream(stream)), "debug_gemm")
+    return out
+
+
+def debug_attention(q, k_prefix, v_prefix, k_tree, v_tree, anc, n_splits=1, stream=None):
+    """q [S][G][hd] bf16; prefix [L][hd]; tree [S][hd]; anc [S-1] int64 (uint64 bits)."""
+    S, G, hd = q.shape
+    Lc = 0 if k_prefix is None else k_prefix.shape[0]
+    o = torch.empty((S, G, hd), dtype=torch.float32, device=q.device)
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device=q.device)
+    L.check(L.load().specedge_debug_attention(_ptr(q), _ptr(k_prefix), _ptr(v_prefix), _ptr(k_tree), _ptr(v_tree),
+                                              _ptr(anc), S, G, hd, Lc, n_splits, _ptr(o), _ptr(ws), ws.numel(),
+                                              _stream(stream)), "debug_attention")
+    return o
+
+
+def debug_last_logits(model: Model, ws: torch.Tensor, batch: Batch, stream=None) -> torch.Tensor:
+    out = torch.empty((batch.rows, model.shape.vocab), dtype=torch.float32, device=ws.device)
+    L.check(model.lib.specedge_debug_last_logits(model.h, _ptr(ws), ws.numel(), batch.num_requests, batch.rows,
+                                                 _ptr(out), _stream(stream)), "debug_last_logits")
+    return out

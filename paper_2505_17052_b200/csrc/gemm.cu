@@ -1,0 +1,380 @@
+// tcgen05 / TMEM / TMA GEMM with fused epilogues for the verify step's dense contractions
+// (QKV + RoPE + tree K/V write, O-proj + residual, gate/up + SwiGLU,
+// down + residual, LM head + vocab argmax / Gumbel-max).  P:173 ("a single forward pass" over
+// all draft tokens) makes these weight-streaming GEMMs with N = R rows of the whole batch.
+//
+// Orientation ("swap-AB"): D^T[feature][row] = W[feature][:] . X[row][:].  Weights take the
+// MMA's M = 128 side (always a multiple of 128 after zero-fill), the R activation rows of the
+// batch take N = BN <= 256 (multiple of 16), so ragged small R wastes < 16 rows per tile.
+// Both operands are K-major bf16, TMA-loaded with 128B swizzle into a `stages`-deep ring;
+// one elected thread issues tcgen05.mma (fp32 accumulators in TMEM, double-buffered so the
+// epilogue of tile i overlaps the MMAs of tile i+1); four epilogue warps read TMEM with
+// tcgen05.ld and apply the fused epilogue.  Persistent grid: one CTA per SM, static stride.
+#include "common.cuh"
+#include "internal.h"
+
+#include <algorithm>
+
+namespace se {
+
+namespace {
+
+constexpr int kThreads = 192;          // warp0 TMA, warp1 MMA + TMEM alloc, warps2-5 epilogue
+constexpr int kEpiThreads = 128;
+constexpr uint32_t kABytes = 128 * 128;  // 128 rows x 64 bf16
+constexpr int kXchStride = 33;
+
+struct SmemLayout {
+  uint32_t a_off, b_off, xch_off, red_off, bar_off, total;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(int stages, int BN) {
+  SmemLayout L;
+  L.a_off = 0;
+  L.b_off = L.a_off + stages * kABytes;
+  L.xch_off = L.b_off + stages * (uint32_t)BN * 128u;
+  L.red_off = L.xch_off + 128 * kXchStride * 4;
+  L.bar_off = L.red_off + 4 * 32 * 8;
+  L.total = L.bar_off + (2 * stages + 4) * 8 + 16;
+  return L;
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+
+// Gumbel noise for (row, vocab v) — SURVEY amb. A9: key (lo32(seed) ^ round, hi32(seed)),
+// counter (v>>2, slot, lo32(session), hi32(session)), word v&3, u = ((x>>8)|1) 2^-24.
+__device__ __forceinline__ float gumbel_noise(const GemmArgs& a, int row, int v) {
+  const int req = a.row_req[row];
+  const uint32_t rnd = a.req_round[req];
+  const uint64_t ses = a.req_session[req];
+  U4 c{(uint32_t)v >> 2, (uint32_t)a.row_slot[row], (uint32_t)ses, (uint32_t)(ses >> 32)};
+  U4 r = philox4x32_10(c, a.seed_lo ^ rnd, a.seed_hi);
+  const uint32_t w = u4_word(r, v & 3);
+  const float u = (float)((w >> 8) | 1u) * 5.9604644775390625e-08f;  // exact
+  return -logf(-logf(u));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int S = a.stages, BN = a.BN;
+  const SmemLayout L = smem_layout(S, BN);
+  uint8_t* sA = smem + L.a_off;
+  uint8_t* sB = smem + L.b_off;
+  float* xch = reinterpret_cast<float*>(smem + L.xch_off);
+  float* red_v = reinterpret_cast<float*>(smem + L.red_off);
+  int* red_i = reinterpret_cast<int*>(smem + L.red_off + 4 * 32 * 4);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t b_bytes = (uint32_t)BN * 128u;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiThreads);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, (uint32_t)a.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int ntiles = a.n_tiles_m * a.n_tiles_n;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+      const uint64_t pol_x = policy_evict_last();   // activations: re-read by every m tile
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m = t / a.n_tiles_n, n = t % a.n_tiles_n;
+        for (int kb = 0; kb < a.num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], kABytes + b_bytes);
+          tma_load_2d_hint(sA + stage * kABytes, &tmA, &full[stage], kb * 64, m * 128, pol_w);
+          tma_load_2d_hint(sB + stage * b_bytes, &tmB, &full[stage], kb * 64, n * BN, pol_x);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc = umma_idesc_bf16(128, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < a.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * kABytes);
+          const uint32_t b_addr = smem_u32(sB + stage * b_bytes);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            tc_mma_f16(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32),
+                       idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    const int tl = q * 32 + lane;      // tile-local feature (TMEM lane)
+    const int et = threadIdx.x - 64;   // 0..127 epilogue thread id
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int m = t / a.n_tiles_n, n = t % a.n_tiles_n;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int feat = m * 128 + tl;
+      const int nchunks = (BN + 31) / 32;
+      for (int c = 0; c < nchunks; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+        tmem_ld_wait();
+        const int row_base = n * BN + c * 32;
+        const int ncol = min(32, BN - c * 32);
+        if constexpr (MODE == EPI_F32) {
+          if (feat < a.M) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int row = row_base + j;
+              if (j < ncol && row < a.R) a.out_f32[(size_t)row * a.ldo + feat] = __uint_as_float(v[j]);
+            }
+          }
+        } else if constexpr (MODE == EPI_RESID) {
+          if (feat < a.M) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int row = row_base + j;
+              if (j < ncol && row < a.R) {
+                float* p = a.out_f32 + (size_t)row * a.ldo + feat;   // fp32 residual stream
+                *p = *p + __uint_as_float(v[j]);
+              }
+            }
+          }
+        } else if constexpr (MODE == EPI_SWIGLU) {
+          // tile rows: lanes 0..63 = gate features m*64 + i, lanes 64..127 = up features
+#pragma unroll
+          for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
+          named_bar_sync(1, kEpiThreads);
+          const int f = et & 63, half = et >> 6;
+          const int fo = m * 64 + f;
+          for (int jj = 0; jj < 16; ++jj) {
+            const int j = half * 16 + jj;
+            const int row = row_base + j;
+            if (j < ncol && row < a.R && fo < a.M / 2) {
+              const float g = xch[f * kXchStride + j], u = xch[(f + 64) * kXchStride + j];
+              a.out_bf16[(size_t)row * a.ld_out + fo] = __float2bfloat16_rn(silu_f(g) * u);
+            }
+          }
+          named_bar_sync(1, kEpiThreads);
+        } else if constexpr (MODE == EPI_QKV) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
+          named_bar_sync(1, kEpiThreads);
+          const int hd = a.head_dim, half_hd = hd >> 1;
+          const int qd = a.n_heads * hd, kd = a.n_kv * hd;
+          if (feat < a.M) {
+            const int dim = feat % hd;
+            const bool rot = feat < qd + kd;
+            const int partner = tl + (dim < half_hd ? half_hd : -half_hd);
+            const int fi = dim % half_hd;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int row = row_base + j;
+              if (j >= ncol || row >= a.R) continue;
+              float x = __uint_as_float(v[j]);
+              if (rot) {
+                const int pos = a.row_pos[row];
+                const float cs = a.rope_cos[(size_t)pos * half_hd + fi];
+                const float sn = a.rope_sin[(size_t)pos * half_hd + fi];
+                const float xp = xch[partner * kXchStride + j];
+                x = dim < half_hd ? (x * cs - xp * sn) : (x * cs + xp * sn);
+              }
+              const bf16 b = __float2bfloat16_rn(x);
+              if (feat < qd) {
+                a.out_bf16[(size_t)row * a.ld_out + feat] = b;
+              } else {
+                const int kvsel = feat < qd + kd ? 0 : 1;
+                const int kvh = (feat - qd - kvsel * kd) / hd;
+                a.tree_kv[((((size_t)a.layer * 2 + kvsel) * a.n_kv + kvh) * a.R_cap + row) * hd + dim] = b;
+              }
+            }
+          }
+          named_bar_sync(1, kEpiThreads);
+        } else if constexpr (MODE == EPI_ARGMAX) {
+          const bool fv = feat < a.vocab;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int row = row_base + j;
+            float s = -INFINITY;
+            if (fv && j < ncol && row < a.R) {
+              s = __uint_as_float(v[j]);
+              if (a.sample) s = s * a.inv_t + gumbel_noise(a, row, feat);
+            }
+            xch[tl * kXchStride + j] = s;
+          }
+          named_bar_sync(1, kEpiThreads);
+          {
+            const int j = et & 31, qq = et >> 5;
+            float best = -INFINITY;
+            int bi = 0x7fffffff;
+            for (int l = 0; l < 32; ++l) {
+              const float s = xch[(qq * 32 + l) * kXchStride + j];
+              if (s > best) { best = s; bi = m * 128 + qq * 32 + l; }
+            }
+            red_v[qq * 32 + j] = best;
+            red_i[qq * 32 + j] = bi;
+          }
+          named_bar_sync(1, kEpiThreads);
+          if (et < 32) {
+            const int j = et;
+            float best = red_v[j];
+            int bi = red_i[j];
+            for (int qq = 1; qq < 4; ++qq) {
+              const float s = red_v[qq * 32 + j];
+              if (s > best) { best = s; bi = red_i[qq * 32 + j]; }
+            }
+            const int row = row_base + j;
+            if (j < ncol && row < a.R) {
+              a.part_val[(size_t)row * a.n_tiles_m + m] = best;
+              a.part_idx[(size_t)row * a.n_tiles_m + m] = bi;
+            }
+          }
+          named_bar_sync(1, kEpiThreads);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, (uint32_t)a.tmem_cols);
+  }
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+int g_num_sms = 0;
+
+template <int MODE>
+cudaError_t launch_mode(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmArgs& a,
+                        size_t smem, int grid, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k_gemm<MODE><<<grid, kThreads, smem, st>>>(tmW, tmX, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int gemm_pick_bn(int R) {
+  const int nt = (R + 255) / 256;
+  int bn = (R + nt - 1) / nt;
+  bn = (bn + 15) / 16 * 16;
+  return std::max(16, std::min(256, bn));
+}
+
+cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArgs a,
+                        cudaStream_t st, int* launches) {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  a.BN = gemm_pick_bn(a.R);
+  a.n_tiles_n = (a.R + a.BN - 1) / a.BN;
+  a.n_tiles_m = (a.M + 127) / 128;
+  a.num_kb = (a.K + 63) / 64;
+  int ncols = 32;
+  const int need = a.BN + (a.BN + 31) / 32 * 32;
+  while (ncols < need) ncols *= 2;
+  a.tmem_cols = ncols;
+  const size_t budget = 227 * 1024 - 1024;
+  int stages = 8;
+  while (stages > 2 && smem_layout(stages, a.BN).total > budget) --stages;
+  a.stages = stages;
+  const size_t smem = smem_layout(stages, a.BN).total + 1024;
+  CUtensorMap tmX;
+  if (!make_tmap_2d(&tmX, X, (uint64_t)a.R, (uint64_t)a.K, (uint32_t)a.BN)) return cudaErrorInvalidValue;
+  const int ntiles = a.n_tiles_m * a.n_tiles_n;
+  const int grid = std::min(ntiles, g_num_sms);
+  if (launches) ++*launches;
+  switch (mode) {
+    case EPI_F32: return launch_mode<EPI_F32>(tmW, tmX, a, smem, grid, st);
+    case EPI_QKV: return launch_mode<EPI_QKV>(tmW, tmX, a, smem, grid, st);
+    case EPI_RESID: return launch_mode<EPI_RESID>(tmW, tmX, a, smem, grid, st);
+    case EPI_SWIGLU: return launch_mode<EPI_SWIGLU>(tmW, tmX, a, smem, grid, st);
+    case EPI_ARGMAX: return launch_mode<EPI_ARGMAX>(tmW, tmX, a, smem, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace se

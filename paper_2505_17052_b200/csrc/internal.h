@@ -1,0 +1,201 @@
+// Internal declarations shared by the libspecedge translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <vector>
+
+#include "../../include/specedge.h"
+
+namespace se {
+
+using bf16 = __nv_bfloat16;
+
+// ---------------------------------------------------------------------------------------------
+// GEMM (tcgen05, swap-AB: weights are the MMA's M side, activation rows its N side)
+// ---------------------------------------------------------------------------------------------
+enum GemmMode : int {
+  EPI_F32 = 0,     // out_f32[row][m] = acc                       (tests, logits capture)
+  EPI_QKV = 1,     // RoPE(q,k) -> Q[row][..], tree K/V scratch   (a4)
+  EPI_RESID = 2,   // X[row][m] += acc (fp32 residual stream)     (a6, a8)
+  EPI_SWIGLU = 3,  // M[row][f] = bf16(silu(gate) * up)            (a7)
+  EPI_ARGMAX = 4,  // per (row, 128-vocab tile) max / Gumbel-max   (a9)
+};
+
+struct GemmArgs {
+  int M, R, K;            // weight rows (features), activation rows, reduction length
+  int BN, n_tiles_n, n_tiles_m, num_kb, stages, tmem_cols;
+  // EPI_F32 / EPI_RESID (fp32 residual stream)
+  float* out_f32;
+  int ldo;
+  // EPI_SWIGLU / EPI_QKV(q part)
+  bf16* out_bf16;
+  int ld_out;
+  // EPI_QKV
+  bf16* tree_kv;          // [layers][2][KV][R_cap][hd]
+  int R_cap, layer, n_heads, n_kv, head_dim;
+  const int* row_pos;
+  const float* rope_cos;  // [max_pos][hd/2]
+  const float* rope_sin;
+  // EPI_ARGMAX
+  float* part_val;        // [R][n_tiles_m]
+  int* part_idx;
+  int vocab, sample;
+  float inv_t;
+  uint32_t seed_lo, seed_hi;
+  const int* row_req;
+  const int* row_slot;
+  const uint32_t* req_round;
+  const uint64_t* req_session;
+};
+
+// Build a 2D bf16 tensor map [rows][cols] (cols contiguous), box {64, box_rows}, 128B swizzle.
+bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+int gemm_pick_bn(int R);
+cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArgs a,
+                        cudaStream_t st, int* launches);
+
+// ---------------------------------------------------------------------------------------------
+// Attention (tree-masked, paged, split-KV)
+// ---------------------------------------------------------------------------------------------
+struct AttnArgs {
+  const bf16* Q;              // [R][H*hd]
+  const bf16* pool;           // [layers][num_pages][2][KV][64][hd]
+  const int* block_table;     // [max_handles][max_pages_per_seq]
+  int max_pages_per_seq, num_pages;
+  const bf16* tree_kv;        // [layers][2][KV][R_cap][hd]
+  int R_cap, layer, H, KV, G, hd;
+  const int* req_L;
+  const int* req_h;
+  const int* req_row0;
+  const int* req_S;
+  const uint64_t* row_anc;
+  int n_splits, pages_per_split, max_rows;   // max_rows = max_S * G
+  float* opart;               // [n_splits][R][H][hd]
+  float* mpart;               // [n_splits][R][H]   (log2 domain)
+  float* lpart;
+  int R;
+  float scale_log2;
+};
+cudaError_t attention_launch(const AttnArgs& a, int B, cudaStream_t st, int* launches);
+cudaError_t attn_combine_launch(const AttnArgs& a, bf16* O, float* O_f32, cudaStream_t st,
+                                int* launches);
+int attn_pick_splits(int B, int KV, int max_pages);
+
+// ---------------------------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------------------------
+struct PrepArgs {
+  int B, V, max_nodes, max_context_len, max_handles, force_chain;
+  const int* kv;
+  const int* context_len;
+  const int* root_token;
+  const int* node_offset;
+  const int* parent;
+  const int* token;
+  const int* cache_len;
+  const int* capacity;
+  // outputs
+  int* status;
+  int* req_L;
+  int* req_h;
+  int* req_row0;
+  int* req_S;
+  int* row_tok;
+  int* row_pos;
+  int* row_req;
+  int* row_slot;
+  uint64_t* row_anc;
+};
+cudaError_t prep_launch(const PrepArgs& p, cudaStream_t st, int* launches);
+cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int d, cudaStream_t st,
+                         int* launches);
+cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* out, int R, int d, float eps,
+                           cudaStream_t st, int* launches);
+cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, int* y, float* score,
+                             int* row_target, float* row_score, cudaStream_t st, int* launches);
+struct WalkArgs {
+  int B, force_chain;
+  const int* status;
+  const int* node_offset;
+  const int* parent;
+  const int* token;
+  const int* y;
+  int* accepted_len;
+  int* accepted_token;
+  int* accepted_node;
+  int* bonus;
+};
+cudaError_t walk_launch(const WalkArgs& w, cudaStream_t st, int* launches);
+struct CommitArgs {
+  int B, layers, KV, hd, R_cap, num_pages, max_pages_per_seq;
+  int* status;
+  const int* req_L;
+  const int* req_h;
+  const int* req_row0;
+  const int* node_offset;
+  const int* accepted_len;
+  const int* accepted_node;
+  const bf16* tree_kv;
+  bf16* pool;
+  const int* block_table;
+  int* cache_len;
+};
+cudaError_t commit_launch(const CommitArgs& c, cudaStream_t st, int* launches);
+
+// weights (K12) and synthetic KV (K13)
+enum InitLayout : int { INIT_PLAIN = 0, INIT_QKV = 1, INIT_GATEUP = 2 };
+struct InitArgs {
+  bf16* dst;
+  long long rows, cols;       // physical rows/cols
+  int layout;
+  int tid0, tid1, tid2;       // tensor ids (plain: tid0; qkv: q,k,v; gateup: g,u)
+  int layer;
+  long long rows0, rows1;     // qkv: q rows, k rows; gateup: F
+  float scale0, scale1, scale2;
+  int gain;                   // 1: bf16(i24*2^-25 + 1)
+  uint32_t k0, k1;
+};
+cudaError_t init_weights_launch(const InitArgs& a, cudaStream_t st);
+cudaError_t kv_fill_launch(bf16* pool, const int* block_row, int layers, int num_pages, int KV,
+                           int hd, int n_tokens, uint32_t k0, uint32_t k1, uint32_t stream_id,
+                           cudaStream_t st);
+
+}  // namespace se
+
+// ---------------------------------------------------------------------------------------------
+// opaque handle definitions
+// ---------------------------------------------------------------------------------------------
+struct specedge_model {
+  specedge_model_config cfg;
+  int device;
+  se::bf16* embed = nullptr;
+  se::bf16* lm_head = nullptr;
+  se::bf16* g_final = nullptr;
+  struct Layer {
+    se::bf16 *wqkv, *wo, *wgu, *wd, *g_attn, *g_mlp;
+    CUtensorMap tm_qkv, tm_o, tm_gu, tm_d;
+  };
+  std::vector<Layer> layers;
+  CUtensorMap tm_lm;
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  std::vector<void*> allocs;
+  void* pinned = nullptr;       // staging for specedge_verify_batch_host
+  size_t pinned_bytes = 0;
+};
+
+struct specedge_kvpool {
+  specedge_model* model;
+  int num_pages, max_handles, max_pages_per_seq;
+  se::bf16* pages = nullptr;
+  int* block_table = nullptr;   // device [max_handles][max_pages_per_seq]
+  int* cache_len = nullptr;     // device [max_handles]
+  int* capacity = nullptr;      // device [max_handles] (0 = free handle)
+  std::vector<int> free_pages;
+  std::vector<std::vector<int>> handle_pages;
+  std::vector<int> handle_cap;  // host mirror, 0 = free
+};

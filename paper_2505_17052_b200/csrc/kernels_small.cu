@@ -1,0 +1,412 @@
+// Integer / bandwidth kernels of the verify step:
+//   K1  tree prep     (S:111 tree invariants, amb. A3-A5, A18)
+//   K2  embedding gather (a2)
+//   K3  RMSNorm       (a3, amb. A13)
+//   K9b LM-head second stage: argmax over per-tile partials (a9, ties -> lowest id)
+//   K10 accept walk   (a10; "returns both the verified tokens and one additional token")
+//   K11 KV commit     (a11; amb. A19) + length finalize
+//   K12 Philox weight init, K13 synthetic KV fill
+#include "common.cuh"
+#include "internal.h"
+
+namespace se {
+
+namespace {
+
+// ------------------------------------------------------------------------------------ K1 prep
+// One CTA (64 threads) per request.  Thread i owns node i (and i+64.. when N > 64 so every row
+// is still written for oversize trees, which are flagged E_TREE_SIZE).
+__global__ void k_prep(const __grid_constant__ PrepArgs p) {
+  const int r = blockIdx.x, i0 = threadIdx.x;
+  __shared__ int s_flags[8];
+  __shared__ int s_depth_max;
+  __shared__ int s_parent[kMaxNodes];
+  __shared__ int s_token[kMaxNodes];
+  const int n0 = p.node_offset[r];
+  const int N = p.node_offset[r + 1] - n0;
+  const int row0 = n0 + r;
+  if (i0 < 8) s_flags[i0] = 0;
+  if (i0 == 0) s_depth_max = 0;
+  for (int i = i0; i < min(N, kMaxNodes); i += blockDim.x) {
+    s_parent[i] = p.parent[n0 + i];
+    s_token[i] = p.token[n0 + i];
+  }
+  __syncthreads();
+
+  // handle: in range, allocated, not used by an earlier request of this batch
+  const int h = p.kv[r];
+  bool handle_ok = h >= 0 && h < p.max_handles && p.capacity[h] > 0;
+  if (handle_ok) {
+    for (int j = i0; j < r; j += blockDim.x)
+      if (p.kv[j] == h) atomicOr(&s_flags[0], 1);
+  }
+  const bool size_ok = N >= 0 && N <= kMaxNodes && N <= p.max_nodes;
+  // per-node checks (only meaningful when the size is ok)
+  if (size_ok) {
+    for (int i = i0; i < N; i += blockDim.x) {
+      const int par = s_parent[i];
+      if (!(par == -1 || (par >= 0 && par < i))) atomicOr(&s_flags[1], 1);
+      const int tk = s_token[i];
+      if (tk < 0 || tk >= p.V) atomicOr(&s_flags[2], 1);
+      for (int j = 0; j < i; ++j)
+        if (s_parent[j] == par && s_token[j] == tk) atomicOr(&s_flags[3], 1);
+    }
+  }
+  __syncthreads();
+  const bool tree_ok = size_ok && s_flags[1] == 0;
+  const int root = p.root_token[r];
+
+  // depth / ancestor mask by walking the parent chain (<= 64 steps)
+  __shared__ int s_depth[kMaxNodes];
+  for (int i = i0; i < N; i += blockDim.x) {
+    int depth = 1;
+    uint64_t anc = 0;
+    if (tree_ok) {
+      anc = 1ull << i;
+      int c = s_parent[i];
+      while (c >= 0) {
+        anc |= 1ull << c;
+        ++depth;
+        c = s_parent[c];
+      }
+      atomicMax(&s_depth_max, depth);
+    }
+    if (i < kMaxNodes) s_depth[i] = depth;
+    const int tk = i < kMaxNodes ? s_token[i] : p.token[n0 + i];
+    p.row_tok[row0 + 1 + i] = (tk >= 0 && tk < p.V) ? tk : 0;
+    p.row_anc[row0 + 1 + i] = anc;
+    p.row_req[row0 + 1 + i] = r;
+    p.row_slot[row0 + 1 + i] = i + 1;
+  }
+  __syncthreads();
+
+  const bool h_ok = handle_ok && s_flags[0] == 0;
+  const int L = h_ok ? p.cache_len[h] : 0;
+  for (int i = i0; i < N; i += blockDim.x) p.row_pos[row0 + 1 + i] = L + (i < kMaxNodes ? s_depth[i] : 1);
+  if (i0 == 0) {
+    int st = SPECEDGE_REQ_OK;
+    if (!h_ok) st = SPECEDGE_REQ_E_HANDLE;
+    else if (!size_ok) st = SPECEDGE_REQ_E_TREE_SIZE;
+    else if (s_flags[1]) st = SPECEDGE_REQ_E_TREE;
+    else if (s_flags[2] || root < 0 || root >= p.V) st = SPECEDGE_REQ_E_TOKEN;
+    else if (s_flags[3]) st = SPECEDGE_REQ_E_DUP_SIBLING;
+    else if (p.context_len[r] != L + 1 || p.context_len[r] > p.max_context_len) st = SPECEDGE_REQ_E_CONTEXT;
+    else if (L + s_depth_max + 1 > p.capacity[h]) st = SPECEDGE_REQ_E_KV_CAPACITY;
+    p.status[r] = st;
+    p.req_L[r] = L;
+    p.req_h[r] = h_ok ? h : 0;
+    p.req_row0[r] = row0;
+    p.req_S[r] = N + 1;
+    p.row_tok[row0] = (root >= 0 && root < p.V) ? root : 0;
+    p.row_pos[row0] = L;
+    p.row_anc[row0] = 0;
+    p.row_req[row0] = r;
+    p.row_slot[row0] = 0;
+  }
+}
+
+// ------------------------------------------------------------------------------- K2 embedding
+// X (fp32 residual stream) = E[token] (bf16 values, exact in fp32)
+__global__ void k_embed(const bf16* __restrict__ E, const int* __restrict__ row_tok, float* __restrict__ X, int d) {
+  const int row = blockIdx.x;
+  const int tok = row_tok[row];
+  const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)tok * d);
+  float4* dst = reinterpret_cast<float4*>(X + (size_t)row * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+    const uint4 u = src[i];
+    dst[2 * i] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                             __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+    dst[2 * i + 1] = make_float4(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xFFFF0000u),
+                                 __uint_as_float(u.w << 16), __uint_as_float(u.w & 0xFFFF0000u));
+  }
+}
+
+// --------------------------------------------------------------------------------- K3 RMSNorm
+// out = bf16(x * rsqrt(mean(x^2) + eps) * g), x fp32 (amb. A13)
+__global__ void k_rmsnorm(const float* __restrict__ X, const bf16* __restrict__ g, bf16* __restrict__ out,
+                          int d, float eps) {
+  const int row = blockIdx.x;
+  const float* x = X + (size_t)row * d;
+  __shared__ float red[32];
+  float ss = 0.f;
+  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+    const float4 a = *reinterpret_cast<const float4*>(x + i);
+    const float4 b = *reinterpret_cast<const float4*>(x + i + 4);
+    ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w + b.x * b.x + b.y * b.y + b.z * b.z + b.w * b.w;
+  }
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / (float)d + eps);
+  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+    const float4 a = *reinterpret_cast<const float4*>(x + i);
+    const float4 b = *reinterpret_cast<const float4*>(x + i + 4);
+    const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint4 gu = *reinterpret_cast<const uint4*>(g + i);
+    const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float lo = xv[2 * k] * inv * __uint_as_float(gw[k] << 16);
+      const float hi = xv[2 * k + 1] * inv * __uint_as_float(gw[k] & 0xFFFF0000u);
+      __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+      o[k] = *reinterpret_cast<uint32_t*>(&p);
+    }
+    *reinterpret_cast<uint4*>(out + (size_t)row * d + i) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// ----------------------------------------------------------------------- K9b argmax reduction
+// One warp per row over the per-128-vocab-tile partials.  Order (value desc, index asc).
+__global__ void k_lm_reduce(const float* __restrict__ pv, const int* __restrict__ pi, int R, int ntiles,
+                            int* __restrict__ y, float* __restrict__ score, int* __restrict__ row_target,
+                            float* __restrict__ row_score) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= R) return;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int t = lane; t < ntiles; t += 32) {
+    const float v = pv[(size_t)row * ntiles + t];
+    const int i = pi[(size_t)row * ntiles + t];
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float v = __shfl_xor_sync(0xffffffff, best, o);
+    const int i = __shfl_xor_sync(0xffffffff, bi, o);
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+  if (lane == 0) {
+    y[row] = bi;
+    score[row] = best;
+    if (row_target) row_target[row] = bi;
+    if (row_score) row_score[row] = best;
+  }
+}
+
+// ------------------------------------------------------------------------------ K10 walk
+// One warp per request; lane l examines nodes l and l+32 (N <= 64 for valid requests).
+__global__ void k_walk(const __grid_constant__ WalkArgs w) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= w.B) return;
+  const int n0 = w.node_offset[r];
+  const int N = w.node_offset[r + 1] - n0;
+  const int row0 = n0 + r;
+  if (w.status[r] != SPECEDGE_REQ_OK) {
+    if (lane == 0) {
+      w.accepted_len[r] = 0;
+      w.bonus[r] = -1;
+    }
+    return;
+  }
+  if (w.force_chain) {   // prefill: accept the whole chain
+    for (int i = lane; i < N; i += 32) {
+      w.accepted_token[n0 + i] = w.token[n0 + i];
+      w.accepted_node[n0 + i] = i;
+    }
+    if (lane == 0) {
+      w.accepted_len[r] = N;
+      w.bonus[r] = -1;
+    }
+    return;
+  }
+  int par[2], tok[2];
+  for (int k = 0; k < 2; ++k) {
+    const int i = lane + 32 * k;
+    par[k] = i < N ? w.parent[n0 + i] : -2;
+    tok[k] = i < N ? w.token[n0 + i] : -1;
+  }
+  int cur = -1, a = 0;
+  while (true) {
+    const int want = w.y[row0 + cur + 1];
+    int found = -1;
+    for (int k = 0; k < 2; ++k) {
+      const unsigned m = __ballot_sync(0xffffffff, par[k] == cur && tok[k] == want);
+      if (m && found < 0) found = (__ffs(m) - 1) + 32 * k;
+    }
+    if (found < 0) break;
+    if (lane == 0) {
+      w.accepted_token[n0 + a] = want;
+      w.accepted_node[n0 + a] = found;
+    }
+    ++a;
+    cur = found;
+  }
+  if (lane == 0) {
+    w.accepted_len[r] = a;
+    w.bonus[r] = w.y[row0 + cur + 1];
+  }
+}
+
+// ----------------------------------------------------------------------------- K11 commit
+// grid (B, layers).  Copies K/V of slot 0 and of the accepted slots (in path order) from the tree
+// scratch to cache positions L, L+1, ..., L+a.  Scratch and pages are distinct buffers, so the
+// copy has no aliasing hazard.  Only if the cached length is still the one
+// this verify saw (idempotence guard).
+__global__ void k_commit(const __grid_constant__ CommitArgs c) {
+  const int r = blockIdx.x, layer = blockIdx.y;
+  if (c.status[r] != SPECEDGE_REQ_OK) return;
+  const int h = c.req_h[r];
+  const int L = c.req_L[r];
+  if (c.cache_len[h] != L) return;
+  const int a = c.accepted_len[r];
+  const int n0 = c.node_offset[r];
+  const int row0 = c.req_row0[r];
+  const int vec_per_row = c.hd / 8;           // uint4 per head row
+  const int per_tok = 2 * c.KV * vec_per_row;
+  for (int idx = threadIdx.x; idx < (a + 1) * per_tok; idx += blockDim.x) {
+    const int j = idx / per_tok;
+    const int rem = idx % per_tok;
+    const int kvsel = rem / (c.KV * vec_per_row);
+    const int g = (rem / vec_per_row) % c.KV;
+    const int v = rem % vec_per_row;
+    const int slot = j == 0 ? 0 : c.accepted_node[n0 + j - 1] + 1;
+    const size_t src = ((((size_t)layer * 2 + kvsel) * c.KV + g) * c.R_cap + row0 + slot) * c.hd;
+    const int pos = L + j;
+    const int page = c.block_table[(size_t)h * c.max_pages_per_seq + pos / kPage];
+    const size_t dst = (((((size_t)layer * c.num_pages + page) * 2 + kvsel) * c.KV + g) * kPage + pos % kPage) * c.hd;
+    reinterpret_cast<uint4*>(c.pool + dst)[v] = reinterpret_cast<const uint4*>(c.tree_kv + src)[v];
+  }
+}
+
+__global__ void k_commit_finalize(const __grid_constant__ CommitArgs c) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= c.B || c.status[r] != SPECEDGE_REQ_OK) return;
+  const int h = c.req_h[r];
+  if (c.cache_len[h] != c.req_L[r]) {
+    c.status[r] = SPECEDGE_REQ_E_CONTEXT;   // already committed
+    return;
+  }
+  c.cache_len[h] = c.req_L[r] + c.accepted_len[r] + 1;
+}
+
+// ------------------------------------------------------------------------ K12 weight init
+// Element (lrow, col) of a logical weight = bf16(f32(i24 * scale)) with i24 from Philox counter
+// (idx >> 2, tensor_id, layer, 'WEIG'), idx = lrow * cols + col, word idx & 3 (oracle/model.py O1).
+__global__ void k_init_weights(const __grid_constant__ InitArgs a) {
+  const long long total4 = a.rows * a.cols / 4;
+  for (long long g4 = blockIdx.x * (long long)blockDim.x + threadIdx.x; g4 < total4;
+       g4 += (long long)gridDim.x * blockDim.x) {
+    const long long prow = g4 * 4 / a.cols;
+    const long long col = g4 * 4 % a.cols;
+    int tid = a.tid0;
+    long long lrow = prow;
+    float scale = a.scale0;
+    if (a.layout == INIT_QKV) {
+      if (prow < a.rows0) { tid = a.tid0; lrow = prow; scale = a.scale0; }
+      else if (prow < a.rows0 + a.rows1) { tid = a.tid1; lrow = prow - a.rows0; scale = a.scale1; }
+      else { tid = a.tid2; lrow = prow - a.rows0 - a.rows1; scale = a.scale2; }
+    } else if (a.layout == INIT_GATEUP) {
+      const long long blk = prow / 128, within = prow % 128;
+      if (within < 64) { tid = a.tid0; lrow = blk * 64 + within; scale = a.scale0; }
+      else { tid = a.tid1; lrow = blk * 64 + within - 64; scale = a.scale1; }
+    }
+    const unsigned long long idx = (unsigned long long)lrow * a.cols + col;   // multiple of 4
+    const U4 r = philox4x32_10(U4{(uint32_t)(idx >> 2), (uint32_t)tid, (uint32_t)a.layer, 0x57454947u}, a.k0, a.k1);
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+    uint16_t out[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float v;
+      if (a.gain) v = __fadd_rn(__fmul_rn(philox_i24(w[k]), 2.98023223876953125e-08f), 1.0f);
+      else v = __fmul_rn(philox_i24(w[k]), scale);
+      out[k] = f32_to_bf16_bits(v);
+    }
+    uint2 pk;
+    pk.x = (uint32_t)out[0] | ((uint32_t)out[1] << 16);
+    pk.y = (uint32_t)out[2] | ((uint32_t)out[3] << 16);
+    *reinterpret_cast<uint2*>(a.dst + prow * a.cols + col) = pk;
+  }
+}
+
+// ---------------------------------------------------------------------- K13 synthetic KV
+// element e = head*hd + j of token t: Philox counter (e>>2, t, layer*2 + kv, stream ^ 'KVFI').
+__global__ void k_kv_fill(bf16* pool, const int* __restrict__ block_row, int layers, int num_pages, int KV,
+                          int hd, int n_tokens, uint32_t k0, uint32_t k1, uint32_t stream_id) {
+  const int per_tok4 = KV * hd / 4;
+  const long long total = (long long)n_tokens * layers * 2 * per_tok4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int e4 = (int)(i % per_tok4);
+    long long rest = i / per_tok4;
+    const int kvsel = (int)(rest % 2);
+    rest /= 2;
+    const int layer = (int)(rest % layers);
+    const int t = (int)(rest / layers);
+    const U4 r = philox4x32_10(U4{(uint32_t)e4, (uint32_t)t, (uint32_t)((layer << 1) | kvsel), stream_id ^ 0x4B564649u}, k0, k1);
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+    uint16_t out[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[k] = f32_to_bf16_bits(__fmul_rn(philox_i24(w[k]), 1.1920928955078125e-07f));
+    const int e = e4 * 4;
+    const int g = e / hd, j = e % hd;
+    const int page = block_row[t / kPage];
+    const size_t dst = (((((size_t)layer * num_pages + page) * 2 + kvsel) * KV + g) * kPage + t % kPage) * hd + j;
+    uint2 pk;
+    pk.x = (uint32_t)out[0] | ((uint32_t)out[1] << 16);
+    pk.y = (uint32_t)out[2] | ((uint32_t)out[3] << 16);
+    *reinterpret_cast<uint2*>(pool + dst) = pk;
+  }
+}
+
+}  // namespace
+
+cudaError_t prep_launch(const PrepArgs& p, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  k_prep<<<p.B, 64, 0, st>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int d, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  k_embed<<<R, 128, 0, st>>>(E, row_tok, X, d);
+  return cudaGetLastError();
+}
+cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* out, int R, int d, float eps, cudaStream_t st,
+                           int* launches) {
+  if (launches) ++*launches;
+  const int threads = d >= 2048 ? 256 : (d >= 512 ? 64 : 32);
+  k_rmsnorm<<<R, threads, 0, st>>>(X, g, out, d, eps);
+  return cudaGetLastError();
+}
+cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, int* y, float* score,
+                             int* row_target, float* row_score, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  k_lm_reduce<<<(R + 3) / 4, 128, 0, st>>>(pv, pi, R, ntiles, y, score, row_target, row_score);
+  return cudaGetLastError();
+}
+cudaError_t walk_launch(const WalkArgs& w, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  k_walk<<<(w.B + 3) / 4, 128, 0, st>>>(w);
+  return cudaGetLastError();
+}
+cudaError_t commit_launch(const CommitArgs& c, cudaStream_t st, int* launches) {
+  if (launches) *launches += 2;
+  k_commit<<<dim3(c.B, c.layers), 256, 0, st>>>(c);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_commit_finalize<<<(c.B + 127) / 128, 128, 0, st>>>(c);
+  return cudaGetLastError();
+}
+cudaError_t init_weights_launch(const InitArgs& a, cudaStream_t st) {
+  const long long total4 = a.rows * a.cols / 4;
+  const int blocks = (int)std::min<long long>((total4 + 255) / 256, 148 * 16);
+  k_init_weights<<<blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t kv_fill_launch(bf16* pool, const int* block_row, int layers, int num_pages, int KV, int hd, int n_tokens,
+                           uint32_t k0, uint32_t k1, uint32_t stream_id, cudaStream_t st) {
+  const long long total = (long long)n_tokens * layers * 2 * (KV * hd / 4);
+  if (total == 0) return cudaSuccess;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+  k_kv_fill<<<blocks, 256, 0, st>>>(pool, block_row, layers, num_pages, KV, hd, n_tokens, k0, k1, stream_id);
+  return cudaGetLastError();
+}
+
+}  // namespace se

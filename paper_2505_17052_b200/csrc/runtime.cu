@@ -1,0 +1,932 @@
+// libspecedge runtime: model / KV pool / workspace management and the C ABI (include/specedge.h).
+// The verify step is a fixed stream-ordered sequence of sm_100a kernels; the host only checks
+// arguments, sizes the launches and encodes TMA descriptors.
+#include "common.cuh"
+#include "internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+using namespace se;
+
+namespace {
+
+thread_local int g_last_launches = 0;
+
+// ---- optional per-kernel event timing (bench instrumentation) ----
+enum Kind { K_PREP, K_EMBED, K_RMSNORM, K_QKV, K_ATTN, K_COMBINE, K_O, K_GU, K_DOWN, K_LM, K_LMRED, K_WALK, K_COMMIT,
+            K_NKINDS };
+struct Timing {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<int, size_t>> pending;   // (kind, index of start event)
+  double ms[K_NKINDS] = {};
+  int count[K_NKINDS] = {};
+} g_timing;
+
+cudaEvent_t timing_event() {
+  if (g_timing.used == g_timing.pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_timing.pool.push_back(e);
+  }
+  return g_timing.pool[g_timing.used++];
+}
+
+// RAII: records a start event on construction and an end event on destruction (if enabled)
+struct KTimer {
+  int kind;
+  cudaStream_t st;
+  size_t idx = 0;
+  KTimer(int k, cudaStream_t s) : kind(k), st(s) {
+    if (!g_timing.on) return;
+    idx = g_timing.used;
+    cudaEventRecord(timing_event(), st);
+  }
+  ~KTimer() {
+    if (!g_timing.on) return;
+    cudaEventRecord(timing_event(), st);
+    g_timing.pending.push_back({kind, idx});
+  }
+};
+
+#define CK(x)                                   \
+  do {                                          \
+    cudaError_t _e = (x);                       \
+    if (_e != cudaSuccess) return SPECEDGE_E_CUDA; \
+  } while (0)
+
+inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct WsLayout {
+  size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
+  size_t X, Hn, Q, O, M, tree_kv, opart, mpart, lpart, part_val, part_idx, y, score;
+  size_t stage_in, stage_out, total;
+  int B, R, n_splits_max;
+};
+
+constexpr int kMaxSplits = 8;
+
+WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
+  WsLayout w{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = al256(o + bytes);
+    return at;
+  };
+  const size_t H = c.n_heads, hd = c.head_dim, KV = c.n_kv;
+  w.req_L = take(4 * B);
+  w.req_h = take(4 * B);
+  w.req_row0 = take(4 * B);
+  w.req_S = take(4 * B);
+  w.row_tok = take(4 * R);
+  w.row_pos = take(4 * R);
+  w.row_req = take(4 * R);
+  w.row_slot = take(4 * R);
+  w.row_anc = take(8 * R);
+  w.X = take(4 * (size_t)R * c.d);   // fp32 residual stream
+  w.Hn = take(2 * (size_t)R * c.d);
+  w.Q = take(2 * (size_t)R * H * hd);
+  w.O = take(2 * (size_t)R * H * hd);
+  w.M = take(2 * (size_t)R * c.ffn);
+  w.tree_kv = take(2 * (size_t)c.n_layers * 2 * KV * R * hd);
+  w.opart = take(4 * (size_t)kMaxSplits * R * H * hd);
+  w.mpart = take(4 * (size_t)kMaxSplits * R * H);
+  w.lpart = take(4 * (size_t)kMaxSplits * R * H);
+  const size_t vt = (c.vocab + 127) / 128;
+  w.part_val = take(4 * (size_t)R * vt);
+  w.part_idx = take(4 * (size_t)R * vt);
+  w.y = take(4 * R);
+  w.score = take(4 * R);
+  // staging for the host-buffer entry point: inputs then outputs
+  w.stage_in = take((size_t)B * (4 + 4 + 4 + 8 + 4) + 4 * (B + 1) + (size_t)R * 12 + 64);
+  w.stage_out = take((size_t)B * 12 + (size_t)R * 8 + (size_t)R * 8 + 64);
+  w.total = o;
+  w.B = B;
+  w.R = R;
+  w.n_splits_max = kMaxSplits;
+  return w;
+}
+
+bool check_cfg(const specedge_model_config& c) {
+  if (c.n_layers <= 0 || c.d <= 0 || c.n_heads <= 0 || c.n_kv <= 0 || c.ffn <= 0 || c.vocab <= 0) return false;
+  if (c.n_heads % c.n_kv) return false;
+  if (!(c.head_dim == 16 || c.head_dim == 32 || c.head_dim == 64 || c.head_dim == 128)) return false;
+  if (c.d % 64 || (c.n_heads * c.head_dim) % 64 || c.ffn % 64) return false;
+  if (c.max_position <= 0) return false;
+  return true;
+}
+
+template <typename T>
+T* dalloc(specedge_model* m, size_t n) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return nullptr;
+  m->allocs.push_back(p);
+  return reinterpret_cast<T*>(p);
+}
+
+struct DevIn {
+  const int32_t *kv, *context_len, *root_token, *node_offset, *parent, *token;
+  const uint64_t* session_id;
+  const uint32_t* round;
+};
+
+struct DevOut {
+  int32_t *status, *accepted_len, *accepted_token, *accepted_node, *bonus, *row_target;
+  float* row_score;
+};
+
+specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const specedge_verify_in* in, DevIn di,
+                           DevOut dout, uint8_t* ws_base, size_t ws_bytes, cudaStream_t st, bool prefill,
+                           bool do_commit) {
+  const specedge_model_config& c = m->cfg;
+  const int B = in->num_requests, T = in->total_nodes, R = T + B;
+  const WsLayout w = ws_layout(c, B, R);
+  if (!ws_base || ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
+  uint8_t* ws = ws_base;
+  auto P = [&](size_t off) { return ws + off; };
+  int launches = 0;
+  const int R_cap = R;
+
+  PrepArgs pa{};
+  pa.B = B;
+  pa.V = c.vocab;
+  pa.max_nodes = in->max_nodes;
+  pa.max_context_len = in->max_context_len;
+  pa.max_handles = pool->max_handles;
+  pa.force_chain = prefill ? 1 : 0;
+  pa.kv = di.kv;
+  pa.context_len = di.context_len;
+  pa.root_token = di.root_token;
+  pa.node_offset = di.node_offset;
+  pa.parent = di.parent;
+  pa.token = di.token;
+  pa.cache_len = pool->cache_len;
+  pa.capacity = pool->capacity;
+  pa.status = dout.status;
+  pa.req_L = (int*)P(w.req_L);
+  pa.req_h = (int*)P(w.req_h);
+  pa.req_row0 = (int*)P(w.req_row0);
+  pa.req_S = (int*)P(w.req_S);
+  pa.row_tok = (int*)P(w.row_tok);
+  pa.row_pos = (int*)P(w.row_pos);
+  pa.row_req = (int*)P(w.row_req);
+  pa.row_slot = (int*)P(w.row_slot);
+  pa.row_anc = (uint64_t*)P(w.row_anc);
+  { KTimer _t(K_PREP, st); CK(prep_launch(pa, st, &launches)); }
+
+  float* X = (float*)P(w.X);
+  bf16* Hn = (bf16*)P(w.Hn);
+  bf16* Q = (bf16*)P(w.Q);
+  bf16* O = (bf16*)P(w.O);
+  bf16* Mb = (bf16*)P(w.M);
+  bf16* tree_kv = (bf16*)P(w.tree_kv);
+  { KTimer _t(K_EMBED, st); CK(embed_launch(m->embed, pa.row_tok, X, R, c.d, st, &launches)); }
+
+  const int hd = c.head_dim, H = c.n_heads, KV = c.n_kv, G = H / KV;
+  const int max_pages = (in->max_context_len + 63) / 64;
+  AttnArgs aa{};
+  aa.Q = Q;
+  aa.pool = pool->pages;
+  aa.block_table = pool->block_table;
+  aa.max_pages_per_seq = pool->max_pages_per_seq;
+  aa.num_pages = pool->num_pages;
+  aa.tree_kv = tree_kv;
+  aa.R_cap = R_cap;
+  aa.H = H;
+  aa.KV = KV;
+  aa.G = G;
+  aa.hd = hd;
+  aa.req_L = pa.req_L;
+  aa.req_h = pa.req_h;
+  aa.req_row0 = pa.req_row0;
+  aa.req_S = pa.req_S;
+  aa.row_anc = pa.row_anc;
+  aa.n_splits = std::min(kMaxSplits, attn_pick_splits(B, KV, max_pages));
+  aa.pages_per_split = std::max(1, (max_pages + aa.n_splits - 1) / aa.n_splits);
+  aa.n_splits = std::max(1, (max_pages + aa.pages_per_split - 1) / aa.pages_per_split);
+  aa.max_rows = (in->max_nodes + 1) * G;
+  aa.opart = (float*)P(w.opart);
+  aa.mpart = (float*)P(w.mpart);
+  aa.lpart = (float*)P(w.lpart);
+  aa.R = R;
+  aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
+
+  for (int l = 0; l < c.n_layers; ++l) {
+    const auto& Lw = m->layers[l];
+    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Lw.g_attn, Hn, R, c.d, c.eps, st, &launches)); }
+    GemmArgs g{};
+    g.M = (H + 2 * KV) * hd;
+    g.R = R;
+    g.K = c.d;
+    g.out_bf16 = Q;
+    g.ld_out = H * hd;
+    g.tree_kv = tree_kv;
+    g.R_cap = R_cap;
+    g.layer = l;
+    g.n_heads = H;
+    g.n_kv = KV;
+    g.head_dim = hd;
+    g.row_pos = pa.row_pos;
+    g.rope_cos = m->rope_cos;
+    g.rope_sin = m->rope_sin;
+    { KTimer _t(K_QKV, st); CK(gemm_launch(EPI_QKV, Lw.tm_qkv, Hn, g, st, &launches)); }
+    aa.layer = l;
+    { KTimer _t(K_ATTN, st); CK(attention_launch(aa, B, st, &launches)); }
+    { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
+    GemmArgs go{};
+    go.M = c.d;
+    go.R = R;
+    go.K = H * hd;
+    go.out_f32 = X;
+    go.ldo = c.d;
+    { KTimer _t(K_O, st); CK(gemm_launch(EPI_RESID, Lw.tm_o, O, go, st, &launches)); }
+    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Lw.g_mlp, Hn, R, c.d, c.eps, st, &launches)); }
+    GemmArgs gu{};
+    gu.M = 2 * c.ffn;
+    gu.R = R;
+    gu.K = c.d;
+    gu.out_bf16 = Mb;
+    gu.ld_out = c.ffn;
+    { KTimer _t(K_GU, st); CK(gemm_launch(EPI_SWIGLU, Lw.tm_gu, Hn, gu, st, &launches)); }
+    GemmArgs gd{};
+    gd.M = c.d;
+    gd.R = R;
+    gd.K = c.ffn;
+    gd.out_f32 = X;
+    gd.ldo = c.d;
+    { KTimer _t(K_DOWN, st); CK(gemm_launch(EPI_RESID, Lw.tm_d, Mb, gd, st, &launches)); }
+  }
+  int* y = (int*)P(w.y);
+  if (!prefill) {
+    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, m->g_final, Hn, R, c.d, c.eps, st, &launches)); }
+    GemmArgs gl{};
+    gl.M = c.vocab;
+    gl.R = R;
+    gl.K = c.d;
+    gl.part_val = (float*)P(w.part_val);
+    gl.part_idx = (int*)P(w.part_idx);
+    gl.vocab = c.vocab;
+    const bool sample = in->mode == SPECEDGE_SAMPLE_TREE && in->temperature >= 1e-6f;
+    gl.sample = sample ? 1 : 0;
+    gl.inv_t = sample ? (float)(1.0 / (double)in->temperature) : 1.0f;
+    gl.seed_lo = (uint32_t)in->seed;
+    gl.seed_hi = (uint32_t)(in->seed >> 32);
+    gl.row_req = pa.row_req;
+    gl.row_slot = pa.row_slot;
+    gl.req_round = di.round;
+    gl.req_session = di.session_id;
+    { KTimer _t(K_LM, st); CK(gemm_launch(EPI_ARGMAX, m->tm_lm, Hn, gl, st, &launches)); }
+    KTimer _tr(K_LMRED, st);
+    CK(lm_reduce_launch(gl.part_val, gl.part_idx, R, (c.vocab + 127) / 128, y, (float*)P(w.score),
+                        dout.row_target, dout.row_score, st, &launches));
+  }
+  WalkArgs wa{};
+  wa.B = B;
+  wa.force_chain = prefill ? 1 : 0;
+  wa.status = dout.status;
+  wa.node_offset = di.node_offset;
+  wa.parent = di.parent;
+  wa.token = di.token;
+  wa.y = y;
+  wa.accepted_len = dout.accepted_len;
+  wa.accepted_token = dout.accepted_token;
+  wa.accepted_node = dout.accepted_node;
+  wa.bonus = dout.bonus;
+  { KTimer _t(K_WALK, st); CK(walk_launch(wa, st, &launches)); }
+  if (do_commit) {
+    CommitArgs ca{};
+    ca.B = B;
+    ca.layers = c.n_layers;
+    ca.KV = KV;
+    ca.hd = hd;
+    ca.R_cap = R_cap;
+    ca.num_pages = pool->num_pages;
+    ca.max_pages_per_seq = pool->max_pages_per_seq;
+    ca.status = dout.status;
+    ca.req_L = pa.req_L;
+    ca.req_h = pa.req_h;
+    ca.req_row0 = pa.req_row0;
+    ca.node_offset = di.node_offset;
+    ca.accepted_len = dout.accepted_len;
+    ca.accepted_node = dout.accepted_node;
+    ca.tree_kv = tree_kv;
+    ca.pool = pool->pages;
+    ca.block_table = pool->block_table;
+    ca.cache_len = pool->cache_len;
+    KTimer _t(K_COMMIT, st);
+    CK(commit_launch(ca, st, &launches));
+  }
+  g_last_launches = launches;
+  return SPECEDGE_OK;
+}
+
+specedge_status check_in(const specedge_model* m, const specedge_kvpool* pool, const specedge_verify_in* in) {
+  if (!m || !pool || !in) return SPECEDGE_E_INVALID;
+  if (pool->model != m) return SPECEDGE_E_INVALID;
+  if (in->num_requests <= 0 || in->total_nodes < 0) return SPECEDGE_E_INVALID;
+  if (in->max_nodes < 0 || in->max_nodes > SPECEDGE_MAX_NODES) return SPECEDGE_E_INVALID;
+  if (in->max_context_len <= 0 || in->max_context_len > m->cfg.max_position) return SPECEDGE_E_INVALID;
+  if (in->mode != SPECEDGE_GREEDY && in->mode != SPECEDGE_SAMPLE_TREE) return SPECEDGE_E_INVALID;
+  if (in->mode == SPECEDGE_SAMPLE_TREE && !(in->temperature >= 0.f)) return SPECEDGE_E_INVALID;
+  if (!in->kv || !in->context_len || !in->root_token || !in->session_id || !in->round || !in->node_offset)
+    return SPECEDGE_E_INVALID;
+  if (in->total_nodes > 0 && (!in->parent || !in->token)) return SPECEDGE_E_INVALID;
+  return SPECEDGE_OK;
+}
+
+specedge_status check_out(const specedge_verify_out* out, int total_nodes) {
+  if (!out || !out->status || !out->accepted_len || !out->bonus) return SPECEDGE_E_INVALID;
+  if (total_nodes > 0 && (!out->accepted_token || !out->accepted_node)) return SPECEDGE_E_INVALID;
+  return SPECEDGE_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t weight_seed, int32_t device,
+                                      specedge_model** out) {
+  if (!cfg || !out) return SPECEDGE_E_INVALID;
+  if (!check_cfg(*cfg)) return SPECEDGE_E_UNSUPPORTED;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return SPECEDGE_E_DEVICE;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return SPECEDGE_E_DEVICE;
+  CK(cudaSetDevice(device));
+  specedge_model* m = new specedge_model();
+  m->cfg = *cfg;
+  m->device = device;
+  const auto& c = *cfg;
+  const size_t H = c.n_heads, KV = c.n_kv, hd = c.head_dim, d = c.d, F = c.ffn, V = c.vocab;
+  const uint32_t k0 = (uint32_t)weight_seed, k1 = (uint32_t)(weight_seed >> 32);
+  auto fail = [&](specedge_status s) {
+    for (void* p : m->allocs) cudaFree(p);
+    delete m;
+    return s;
+  };
+  auto sc = [](double stdv) { return (float)(stdv * std::sqrt(3.0) * std::ldexp(1.0, -23)); };
+  auto init = [&](bf16* dst, long long rows, long long cols, int layout, int t0, int t1, int t2, int layer,
+                  long long r0, long long r1, float s0, float s1, float s2, int gain) {
+    InitArgs a{};
+    a.dst = dst;
+    a.rows = rows;
+    a.cols = cols;
+    a.layout = layout;
+    a.tid0 = t0;
+    a.tid1 = t1;
+    a.tid2 = t2;
+    a.layer = layer;
+    a.rows0 = r0;
+    a.rows1 = r1;
+    a.scale0 = s0;
+    a.scale1 = s1;
+    a.scale2 = s2;
+    a.gain = gain;
+    a.k0 = k0;
+    a.k1 = k1;
+    return init_weights_launch(a, 0);
+  };
+  m->embed = dalloc<bf16>(m, V * d);
+  m->lm_head = dalloc<bf16>(m, V * d);
+  m->g_final = dalloc<bf16>(m, d);
+  if (!m->embed || !m->lm_head || !m->g_final) return fail(SPECEDGE_E_OOM);
+  if (init(m->embed, V, d, INIT_PLAIN, 1, 0, 0, 0, 0, 0, sc(1.0), 0, 0, 0) != cudaSuccess) return fail(SPECEDGE_E_CUDA);
+  if (init(m->lm_head, V, d, INIT_PLAIN, 9, 0, 0, 0, 0, 0, sc(2.0 / std::sqrt((double)d)), 0, 0, 0) != cudaSuccess)
+    return fail(SPECEDGE_E_CUDA);
+  if (init(m->g_final, 1, d, INIT_PLAIN, 12, 0, 0, 0, 0, 0, 0, 0, 0, 1) != cudaSuccess) return fail(SPECEDGE_E_CUDA);
+  m->layers.resize(c.n_layers);
+  const double s_d = 1.0 / std::sqrt((double)d), s_q = 1.0 / std::sqrt((double)(H * hd)), s_f = 1.0 / std::sqrt((double)F);
+  for (int l = 0; l < c.n_layers; ++l) {
+    auto& L = m->layers[l];
+    L.wqkv = dalloc<bf16>(m, (H + 2 * KV) * hd * d);
+    L.wo = dalloc<bf16>(m, d * H * hd);
+    L.wgu = dalloc<bf16>(m, 2 * F * d);
+    L.wd = dalloc<bf16>(m, d * F);
+    L.g_attn = dalloc<bf16>(m, d);
+    L.g_mlp = dalloc<bf16>(m, d);
+    if (!L.wqkv || !L.wo || !L.wgu || !L.wd || !L.g_attn || !L.g_mlp) return fail(SPECEDGE_E_OOM);
+    bool ok = init(L.wqkv, (H + 2 * KV) * hd, d, INIT_QKV, 2, 3, 4, l, H * hd, KV * hd, sc(s_d), sc(s_d), sc(s_d), 0) == cudaSuccess;
+    ok = ok && init(L.wo, d, H * hd, INIT_PLAIN, 5, 0, 0, l, 0, 0, sc(s_q), 0, 0, 0) == cudaSuccess;
+    ok = ok && init(L.wgu, 2 * F, d, INIT_GATEUP, 6, 7, 0, l, F, 0, sc(s_d), sc(s_d), 0, 0) == cudaSuccess;
+    ok = ok && init(L.wd, d, F, INIT_PLAIN, 8, 0, 0, l, 0, 0, sc(s_f), 0, 0, 0) == cudaSuccess;
+    ok = ok && init(L.g_attn, 1, d, INIT_PLAIN, 10, 0, 0, l, 0, 0, 0, 0, 0, 1) == cudaSuccess;
+    ok = ok && init(L.g_mlp, 1, d, INIT_PLAIN, 11, 0, 0, l, 0, 0, 0, 0, 0, 1) == cudaSuccess;
+    if (!ok) return fail(SPECEDGE_E_CUDA);
+    ok = make_tmap_2d(&L.tm_qkv, L.wqkv, (H + 2 * KV) * hd, d, 128) && make_tmap_2d(&L.tm_o, L.wo, d, H * hd, 128) &&
+         make_tmap_2d(&L.tm_gu, L.wgu, 2 * F, d, 128) && make_tmap_2d(&L.tm_d, L.wd, d, F, 128);
+    if (!ok) return fail(SPECEDGE_E_CUDA);
+  }
+  if (!make_tmap_2d(&m->tm_lm, m->lm_head, V, d, 128)) return fail(SPECEDGE_E_CUDA);
+  // RoPE table: angles in double (amb. A14), stored fp32
+  const size_t half = hd / 2;
+  std::vector<float> cs((size_t)c.max_position * half), sn((size_t)c.max_position * half);
+  for (size_t i = 0; i < half; ++i) {
+    const double inv = std::pow(c.rope_theta, -2.0 * (double)i / (double)hd);
+    for (int p = 0; p < c.max_position; ++p) {
+      const double ang = (double)p * inv;
+      cs[(size_t)p * half + i] = (float)std::cos(ang);
+      sn[(size_t)p * half + i] = (float)std::sin(ang);
+    }
+  }
+  m->rope_cos = dalloc<float>(m, cs.size());
+  m->rope_sin = dalloc<float>(m, sn.size());
+  if (!m->rope_cos || !m->rope_sin) return fail(SPECEDGE_E_OOM);
+  if (cudaMemcpy(m->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(m->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(SPECEDGE_E_CUDA);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(SPECEDGE_E_CUDA);
+  *out = m;
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_model_destroy(specedge_model* m) {
+  if (!m) return SPECEDGE_E_INVALID;
+  cudaSetDevice(m->device);
+  for (void* p : m->allocs) cudaFree(p);
+  delete m;
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_kvpool_create(specedge_model* m, int32_t num_pages, int32_t max_handles, specedge_kvpool** out) {
+  if (!m || !out || num_pages <= 0 || max_handles <= 0) return SPECEDGE_E_INVALID;
+  CK(cudaSetDevice(m->device));
+  const auto& c = m->cfg;
+  specedge_kvpool* p = new specedge_kvpool();
+  p->model = m;
+  p->num_pages = num_pages;
+  p->max_handles = max_handles;
+  p->max_pages_per_seq = (c.max_position + kPage - 1) / kPage;
+  const size_t page_elems = (size_t)c.n_layers * 2 * c.n_kv * kPage * c.head_dim;
+  bool ok = cudaMalloc(&p->pages, page_elems * num_pages * sizeof(bf16)) == cudaSuccess;
+  ok = ok && cudaMalloc(&p->block_table, sizeof(int) * (size_t)max_handles * p->max_pages_per_seq) == cudaSuccess;
+  ok = ok && cudaMalloc(&p->cache_len, sizeof(int) * max_handles) == cudaSuccess;
+  ok = ok && cudaMalloc(&p->capacity, sizeof(int) * max_handles) == cudaSuccess;
+  if (!ok) {
+    cudaFree(p->pages);
+    cudaFree(p->block_table);
+    cudaFree(p->cache_len);
+    cudaFree(p->capacity);
+    delete p;
+    return SPECEDGE_E_OOM;
+  }
+  CK(cudaMemset(p->pages, 0, page_elems * num_pages * sizeof(bf16)));
+  CK(cudaMemset(p->block_table, 0, sizeof(int) * (size_t)max_handles * p->max_pages_per_seq));
+  CK(cudaMemset(p->cache_len, 0, sizeof(int) * max_handles));
+  CK(cudaMemset(p->capacity, 0, sizeof(int) * max_handles));
+  CK(cudaDeviceSynchronize());
+  p->free_pages.resize(num_pages);
+  for (int i = 0; i < num_pages; ++i) p->free_pages[i] = num_pages - 1 - i;
+  p->handle_pages.resize(max_handles);
+  p->handle_cap.assign(max_handles, 0);
+  *out = p;
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_kvpool_destroy(specedge_kvpool* p) {
+  if (!p) return SPECEDGE_E_INVALID;
+  cudaSetDevice(p->model->device);
+  cudaFree(p->pages);
+  cudaFree(p->block_table);
+  cudaFree(p->cache_len);
+  cudaFree(p->capacity);
+  delete p;
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_kv_alloc(specedge_kvpool* p, int32_t capacity_tokens, int32_t* out_handle) {
+  if (!p || !out_handle || capacity_tokens <= 0) return SPECEDGE_E_INVALID;
+  const int need = (capacity_tokens + kPage - 1) / kPage;
+  if (need > p->max_pages_per_seq) return SPECEDGE_E_INVALID;
+  int h = -1;
+  for (int i = 0; i < p->max_handles; ++i)
+    if (p->handle_cap[i] == 0) { h = i; break; }
+  if (h < 0 || (int)p->free_pages.size() < need) return SPECEDGE_E_OOM;
+  std::vector<int> pages(need);
+  for (int i = 0; i < need; ++i) {
+    pages[i] = p->free_pages.back();
+    p->free_pages.pop_back();
+  }
+  CK(cudaSetDevice(p->model->device));
+  CK(cudaMemcpy(p->block_table + (size_t)h * p->max_pages_per_seq, pages.data(), need * sizeof(int), cudaMemcpyHostToDevice));
+  const int zero = 0;
+  CK(cudaMemcpy(p->cache_len + h, &zero, sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(p->capacity + h, &capacity_tokens, sizeof(int), cudaMemcpyHostToDevice));
+  p->handle_pages[h] = pages;
+  p->handle_cap[h] = capacity_tokens;
+  *out_handle = h;
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_kv_free(specedge_kvpool* p, int32_t h) {
+  if (!p || h < 0 || h >= p->max_handles || p->handle_cap[h] == 0) return SPECEDGE_E_INVALID;
+  for (int pg : p->handle_pages[h]) p->free_pages.push_back(pg);
+  p->handle_pages[h].clear();
+  p->handle_cap[h] = 0;
+  const int zero = 0;
+  CK(cudaSetDevice(p->model->device));
+  CK(cudaMemcpy(p->capacity + h, &zero, sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(p->cache_len + h, &zero, sizeof(int), cudaMemcpyHostToDevice));
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_kv_set_len(specedge_kvpool* p, const int32_t* handles, const int32_t* lens, int32_t n, void* stream) {
+  if (!p || !handles || !lens || n < 0) return SPECEDGE_E_INVALID;
+  for (int i = 0; i < n; ++i) {
+    const int h = handles[i];
+    if (h < 0 || h >= p->max_handles || p->handle_cap[h] == 0 || lens[i] < 0 || lens[i] > p->handle_cap[h])
+      return SPECEDGE_E_INVALID;
+  }
+  for (int i = 0; i < n; ++i)
+    CK(cudaMemcpyAsync(p->cache_len + handles[i], lens + i, sizeof(int), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_kv_get_len(specedge_kvpool* p, const int32_t* handles, int32_t* lens, int32_t n) {
+  if (!p || !handles || !lens || n < 0) return SPECEDGE_E_INVALID;
+  CK(cudaDeviceSynchronize());
+  for (int i = 0; i < n; ++i) {
+    const int h = handles[i];
+    if (h < 0 || h >= p->max_handles) return SPECEDGE_E_INVALID;
+    CK(cudaMemcpy(lens + i, p->cache_len + h, sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_kv_fill_random(specedge_kvpool* p, int32_t h, int32_t n_tokens, uint64_t seed, uint32_t stream_id,
+                                        void* stream) {
+  if (!p || h < 0 || h >= p->max_handles || p->handle_cap[h] == 0 || n_tokens < 0 || n_tokens > p->handle_cap[h])
+    return SPECEDGE_E_INVALID;
+  const auto& c = p->model->cfg;
+  CK(kv_fill_launch(p->pages, p->block_table + (size_t)h * p->max_pages_per_seq, c.n_layers, p->num_pages, c.n_kv,
+                    c.head_dim, n_tokens, (uint32_t)seed, (uint32_t)(seed >> 32), stream_id, (cudaStream_t)stream));
+  CK(cudaMemcpyAsync(p->cache_len + h, &n_tokens, sizeof(int), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_workspace_size(const specedge_model* m, int32_t max_requests, int32_t max_rows,
+                                        int32_t max_context_len, size_t* bytes) {
+  if (!m || !bytes || max_requests <= 0 || max_rows < max_requests || max_context_len <= 0) return SPECEDGE_E_INVALID;
+  *bytes = ws_layout(m->cfg, max_requests, max_rows).total;
+  return SPECEDGE_OK;
+}
+
+
+specedge_status specedge_verify_batch(specedge_model* m, specedge_kvpool* pool, const specedge_verify_in* in,
+                                      specedge_verify_out* out, void* workspace, size_t ws_bytes, void* stream) {
+  specedge_status s = check_in(m, pool, in);
+  if (s != SPECEDGE_OK) return s;
+  if ((s = check_out(out, in->total_nodes)) != SPECEDGE_OK) return s;
+  DevIn di{in->kv, in->context_len, in->root_token, in->node_offset, in->parent, in->token, in->session_id, in->round};
+  DevOut dout{out->status, out->accepted_len, out->accepted_token, out->accepted_node, out->bonus, out->row_target,
+              out->row_score};
+  return run_verify(m, pool, in, di, dout, (uint8_t*)workspace, ws_bytes, (cudaStream_t)stream, false,
+                    in->auto_commit != 0);
+}
+
+specedge_status specedge_kv_commit(specedge_model* m, specedge_kvpool* pool, const specedge_verify_in* in,
+                                   specedge_verify_out* out, void* workspace, size_t ws_bytes, void* stream) {
+  specedge_status s = check_in(m, pool, in);
+  if (s != SPECEDGE_OK) return s;
+  if ((s = check_out(out, in->total_nodes)) != SPECEDGE_OK) return s;
+  const auto& c = m->cfg;
+  const int B = in->num_requests, R = in->total_nodes + B;
+  const WsLayout w = ws_layout(c, B, R);
+  if (!workspace || ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
+  uint8_t* ws = (uint8_t*)workspace;
+  CommitArgs ca{};
+  ca.B = B;
+  ca.layers = c.n_layers;
+  ca.KV = c.n_kv;
+  ca.hd = c.head_dim;
+  ca.R_cap = R;
+  ca.num_pages = pool->num_pages;
+  ca.max_pages_per_seq = pool->max_pages_per_seq;
+  ca.status = out->status;
+  ca.req_L = (int*)(ws + w.req_L);
+  ca.req_h = (int*)(ws + w.req_h);
+  ca.req_row0 = (int*)(ws + w.req_row0);
+  ca.node_offset = in->node_offset;
+  ca.accepted_len = out->accepted_len;
+  ca.accepted_node = out->accepted_node;
+  ca.tree_kv = (bf16*)(ws + w.tree_kv);
+  ca.pool = pool->pages;
+  ca.block_table = pool->block_table;
+  ca.cache_len = pool->cache_len;
+  int launches = 0;
+  CK(commit_launch(ca, (cudaStream_t)stream, &launches));
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_verify_batch_host(specedge_model* m, specedge_kvpool* pool, const specedge_verify_in* in,
+                                           specedge_verify_out* out, void* workspace, size_t ws_bytes, void* stream) {
+  specedge_status s = check_in(m, pool, in);
+  if (s != SPECEDGE_OK) return s;
+  if ((s = check_out(out, in->total_nodes)) != SPECEDGE_OK) return s;
+  const auto& c = m->cfg;
+  const int B = in->num_requests, T = in->total_nodes, R = T + B;
+  const WsLayout w = ws_layout(c, B, R);
+  if (!workspace || ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  // pack inputs into one pinned block -> one H2D copy
+  auto a8 = [](size_t x) { return (x + 7) & ~size_t(7); };
+  size_t o_kv = 0, o_ctx = a8(o_kv + 4 * B), o_root = a8(o_ctx + 4 * B), o_round = a8(o_root + 4 * B),
+         o_ses = a8(o_round + 4 * B), o_off = a8(o_ses + 8 * B), o_par = a8(o_off + 4 * (B + 1)),
+         o_tok = a8(o_par + 4 * T), in_bytes = a8(o_tok + 4 * T);
+  size_t q_st = 0, q_al = a8(4 * B), q_bo = a8(q_al + 4 * B), q_at = a8(q_bo + 4 * B), q_an = a8(q_at + 4 * T),
+         q_rt = a8(q_an + 4 * T), q_rs = a8(q_rt + 4 * R), out_bytes = a8(q_rs + 4 * R);
+  const size_t need = in_bytes + out_bytes;
+  if (m->pinned_bytes < need) {
+    if (m->pinned) cudaFreeHost(m->pinned);
+    m->pinned = nullptr;
+    m->pinned_bytes = 0;
+    CK(cudaHostAlloc(&m->pinned, need * 2, cudaHostAllocDefault));
+    m->pinned_bytes = need * 2;
+  }
+  uint8_t* hb = (uint8_t*)m->pinned;
+  std::memcpy(hb + o_kv, in->kv, 4 * B);
+  std::memcpy(hb + o_ctx, in->context_len, 4 * B);
+  std::memcpy(hb + o_root, in->root_token, 4 * B);
+  std::memcpy(hb + o_round, in->round, 4 * B);
+  std::memcpy(hb + o_ses, in->session_id, 8 * B);
+  std::memcpy(hb + o_off, in->node_offset, 4 * (B + 1));
+  if (T) {
+    std::memcpy(hb + o_par, in->parent, 4 * T);
+    std::memcpy(hb + o_tok, in->token, 4 * T);
+  }
+  uint8_t* ws = (uint8_t*)workspace;
+  uint8_t* din = ws + w.stage_in;
+  uint8_t* dou = ws + w.stage_out;
+  CK(cudaMemcpyAsync(din, hb, in_bytes, cudaMemcpyHostToDevice, st));
+  DevIn di{(int*)(din + o_kv), (int*)(din + o_ctx), (int*)(din + o_root), (int*)(din + o_off),
+           (int*)(din + o_par), (int*)(din + o_tok), (uint64_t*)(din + o_ses), (uint32_t*)(din + o_round)};
+  DevOut dout{(int*)(dou + q_st), (int*)(dou + q_al), (int*)(dou + q_at), (int*)(dou + q_an), (int*)(dou + q_bo),
+              (int*)(dou + q_rt), (float*)(dou + q_rs)};
+  s = run_verify(m, pool, in, di, dout, ws, ws_bytes, st, false, in->auto_commit != 0);
+  if (s != SPECEDGE_OK) return s;
+  uint8_t* ho = hb + in_bytes;
+  CK(cudaMemcpyAsync(ho, dou, out_bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::memcpy(out->status, ho + q_st, 4 * B);
+  std::memcpy(out->accepted_len, ho + q_al, 4 * B);
+  std::memcpy(out->bonus, ho + q_bo, 4 * B);
+  if (T) {
+    std::memcpy(out->accepted_token, ho + q_at, 4 * T);
+    std::memcpy(out->accepted_node, ho + q_an, 4 * T);
+  }
+  if (out->row_target) std::memcpy(out->row_target, ho + q_rt, 4 * R);
+  if (out->row_score) std::memcpy(out->row_score, ho + q_rs, 4 * R);
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_prefill(specedge_model* m, specedge_kvpool* pool, int32_t h, const int32_t* tokens, int32_t n,
+                                 void* workspace, size_t ws_bytes, void* stream) {
+  if (!m || !pool || !tokens || n < 1 || h < 0 || h >= pool->max_handles || pool->handle_cap[h] == 0)
+    return SPECEDGE_E_INVALID;
+  for (int i = 0; i < n; ++i)
+    if (tokens[i] < 0 || tokens[i] >= m->cfg.vocab) return SPECEDGE_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  int L = 0;
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemcpy(&L, pool->cache_len + h, sizeof(int), cudaMemcpyDeviceToHost));
+  if (L + n - 1 > pool->handle_cap[h]) return SPECEDGE_E_INVALID;
+  int i = 0;
+  while (i < n - 1) {
+    const int cn = std::min(SPECEDGE_MAX_NODES, n - 2 - i);   // chain nodes after the root tokens[i]
+    const int B = 1, T = cn, R = T + 1;
+    const WsLayout w = ws_layout(m->cfg, B, R);
+    if (!workspace || ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
+    // host block: kv, ctx, root, round, session, node_offset[2], parent[T], token[T]
+    std::vector<int32_t> blk(8 + 2 * T, 0);
+    blk[0] = h;
+    blk[1] = L + 1;
+    blk[2] = tokens[i];
+    blk[3] = 0;
+    blk[4] = 0;
+    blk[5] = 0;            // session (u64) = 0
+    blk[6] = 0;
+    blk[7] = T;            // node_offset = {0, T} -> blk[6], blk[7]
+    for (int k = 0; k < T; ++k) {
+      blk[8 + k] = k - 1;
+      blk[8 + T + k] = tokens[i + 1 + k];
+    }
+    uint8_t* ws = (uint8_t*)workspace;
+    uint8_t* din = ws + w.stage_in;
+    uint8_t* dou = ws + w.stage_out;
+    CK(cudaMemcpyAsync(din, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, st));
+    const int32_t* d32 = (const int32_t*)din;
+    specedge_verify_in vin{};
+    vin.num_requests = 1;
+    vin.total_nodes = T;
+    vin.max_nodes = std::max(T, 0);
+    vin.max_context_len = std::min(m->cfg.max_position, L + 1);
+    vin.mode = SPECEDGE_GREEDY;
+    DevIn di{d32 + 0, d32 + 1, d32 + 2, d32 + 6, d32 + 8, d32 + 8 + T, (const uint64_t*)(d32 + 4),
+             (const uint32_t*)(d32 + 3)};
+    int32_t* o32 = (int32_t*)dou;
+    DevOut dout{o32 + 0, o32 + 1, o32 + 4, o32 + 4 + SPECEDGE_MAX_NODES, o32 + 2, nullptr, nullptr};
+    specedge_status s = run_verify(m, pool, &vin, di, dout, ws, ws_bytes, st, true, true);
+    if (s != SPECEDGE_OK) return s;
+    int status = -1;
+    CK(cudaMemcpyAsync(&status, o32, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (status != SPECEDGE_REQ_OK) return SPECEDGE_E_INVALID;
+    L += T + 1;
+    i += T + 1;
+  }
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_debug_weight_rows(specedge_model* m, int32_t tensor, int32_t layer, int32_t row0, int32_t nrows,
+                                           uint16_t* dst) {
+  if (!m || !dst || nrows < 0 || row0 < 0) return SPECEDGE_E_INVALID;
+  const auto& c = m->cfg;
+  const long long H = c.n_heads, KV = c.n_kv, hd = c.head_dim, d = c.d, F = c.ffn;
+  if ((tensor >= 2 && tensor <= 8) || tensor == 10 || tensor == 11)
+    if (layer < 0 || layer >= c.n_layers) return SPECEDGE_E_INVALID;
+  CK(cudaDeviceSynchronize());
+  for (int i = 0; i < nrows; ++i) {
+    const long long r = row0 + i;
+    const bf16* base = nullptr;
+    long long cols = d, prow = r, rows = 0;
+    switch (tensor) {
+      case 1: base = m->embed; rows = c.vocab; break;
+      case 2: base = m->layers[layer].wqkv; rows = H * hd; break;
+      case 3: base = m->layers[layer].wqkv; rows = KV * hd; prow = H * hd + r; break;
+      case 4: base = m->layers[layer].wqkv; rows = KV * hd; prow = (H + KV) * hd + r; break;
+      case 5: base = m->layers[layer].wo; rows = d; cols = H * hd; break;
+      case 6: base = m->layers[layer].wgu; rows = F; prow = (r / 64) * 128 + r % 64; break;
+      case 7: base = m->layers[layer].wgu; rows = F; prow = (r / 64) * 128 + 64 + r % 64; break;
+      case 8: base = m->layers[layer].wd; rows = d; cols = F; break;
+      case 9: base = m->lm_head; rows = c.vocab; break;
+      case 10: base = m->layers[layer].g_attn; rows = 1; break;
+      case 11: base = m->layers[layer].g_mlp; rows = 1; break;
+      case 12: base = m->g_final; rows = 1; break;
+      default: return SPECEDGE_E_INVALID;
+    }
+    if (r >= rows) return SPECEDGE_E_INVALID;
+    CK(cudaMemcpy(dst + (size_t)i * cols, base + prow * cols, cols * 2, cudaMemcpyDeviceToHost));
+  }
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_debug_read_kv(specedge_kvpool* p, int32_t h, int32_t layer, int32_t kv_sel, int32_t pos0,
+                                       int32_t n, uint16_t* dst) {
+  if (!p || !dst || h < 0 || h >= p->max_handles || p->handle_cap[h] == 0 || pos0 < 0 || n < 0 ||
+      pos0 + n > p->handle_cap[h] || kv_sel < 0 || kv_sel > 1)
+    return SPECEDGE_E_INVALID;
+  const auto& c = p->model->cfg;
+  if (layer < 0 || layer >= c.n_layers) return SPECEDGE_E_INVALID;
+  CK(cudaDeviceSynchronize());
+  for (int i = 0; i < n; ++i) {
+    const int pos = pos0 + i;
+    const int page = p->handle_pages[h][pos / kPage];
+    for (int g = 0; g < c.n_kv; ++g) {
+      const size_t off = (((((size_t)layer * p->num_pages + page) * 2 + kv_sel) * c.n_kv + g) * kPage + pos % kPage) * c.head_dim;
+      CK(cudaMemcpy(dst + ((size_t)i * c.n_kv + g) * c.head_dim, p->pages + off, c.head_dim * 2, cudaMemcpyDeviceToHost));
+    }
+  }
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_debug_gemm(const uint16_t* W, const uint16_t* X, float* out, int32_t M, int32_t R, int32_t K,
+                                    void* stream) {
+  if (!W || !X || !out || M <= 0 || R <= 0 || K <= 0 || K % 8) return SPECEDGE_E_INVALID;
+  CUtensorMap tmW;
+  if (!make_tmap_2d(&tmW, W, (uint64_t)M, (uint64_t)K, 128)) return SPECEDGE_E_CUDA;
+  GemmArgs g{};
+  g.M = M;
+  g.R = R;
+  g.K = K;
+  g.out_f32 = out;
+  g.ldo = M;
+  CK(gemm_launch(EPI_F32, tmW, X, g, (cudaStream_t)stream, nullptr));
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_debug_last_logits(specedge_model* m, void* workspace, size_t ws_bytes, int32_t B, int32_t R,
+                                           float* logits, void* stream) {
+  if (!m || !workspace || !logits || B <= 0 || R < B) return SPECEDGE_E_INVALID;
+  const WsLayout w = ws_layout(m->cfg, B, R);
+  if (ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
+  GemmArgs g{};
+  g.M = m->cfg.vocab;
+  g.R = R;
+  g.K = m->cfg.d;
+  g.out_f32 = logits;
+  g.ldo = m->cfg.vocab;
+  CK(gemm_launch(EPI_F32, m->tm_lm, (uint8_t*)workspace + w.Hn, g, (cudaStream_t)stream, nullptr));
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_prefix, const uint16_t* v_prefix,
+                                         const uint16_t* k_tree, const uint16_t* v_tree, const uint64_t* anc, int32_t S,
+                                         int32_t G, int32_t hd, int32_t L, int32_t n_splits, float* o, void* workspace,
+                                         size_t ws_bytes, void* stream) {
+  if (!q || !k_tree || !v_tree || !o || S < 1 || S > SPECEDGE_MAX_NODES + 1 || G < 1 || L < 0 ||
+      (L > 0 && (!k_prefix || !v_prefix)) || (S > 1 && !anc) || n_splits < 1 || n_splits > kMaxSplits)
+    return SPECEDGE_E_INVALID;
+  if (!(hd == 16 || hd == 32 || hd == 64 || hd == 128)) return SPECEDGE_E_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int npages = std::max(1, (L + 63) / 64);
+  size_t off = 0;
+  auto take = [&](size_t b) { size_t a = off; off = al256(off + b); return a; };
+  const size_t o_pool = take((size_t)npages * 2 * 64 * hd * 2), o_bt = take(4 * npages), o_tree = take(2 * 2 * (size_t)S * hd),
+               o_req = take(4 * 4), o_anc = take(8 * (size_t)S), o_op = take(4 * (size_t)n_splits * S * G * hd),
+               o_m = take(4 * (size_t)n_splits * S * G), o_l = take(4 * (size_t)n_splits * S * G);
+  if (!workspace || ws_bytes < off) return SPECEDGE_E_WORKSPACE;
+  uint8_t* ws = (uint8_t*)workspace;
+  bf16* pool = (bf16*)(ws + o_pool);
+  for (int p = 0; p < (L + 63) / 64; ++p) {
+    const int nt = std::min(64, L - p * 64);
+    CK(cudaMemcpyAsync(pool + ((size_t)p * 2 + 0) * 64 * hd, k_prefix + (size_t)p * 64 * hd, (size_t)nt * hd * 2,
+                       cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(pool + ((size_t)p * 2 + 1) * 64 * hd, v_prefix + (size_t)p * 64 * hd, (size_t)nt * hd * 2,
+                       cudaMemcpyDeviceToDevice, st));
+  }
+  std::vector<int> bt(npages);
+  for (int p = 0; p < npages; ++p) bt[p] = p;
+  CK(cudaMemcpyAsync(ws + o_bt, bt.data(), 4 * npages, cudaMemcpyHostToDevice, st));
+  bf16* tree = (bf16*)(ws + o_tree);
+  CK(cudaMemcpyAsync(tree, k_tree, (size_t)S * hd * 2, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(tree + (size_t)S * hd, v_tree, (size_t)S * hd * 2, cudaMemcpyDeviceToDevice, st));
+  const int req[4] = {L, 0, 0, S};   // req_L, req_h, req_row0, req_S
+  CK(cudaMemcpyAsync(ws + o_req, req, 16, cudaMemcpyHostToDevice, st));
+  const uint64_t zero = 0;
+  CK(cudaMemcpyAsync(ws + o_anc, &zero, 8, cudaMemcpyHostToDevice, st));
+  if (S > 1) CK(cudaMemcpyAsync(ws + o_anc + 8, anc, 8 * (size_t)(S - 1), cudaMemcpyDeviceToDevice, st));
+  AttnArgs a{};
+  a.Q = (const bf16*)q;
+  a.pool = pool;
+  a.block_table = (const int*)(ws + o_bt);
+  a.max_pages_per_seq = npages;
+  a.num_pages = npages;
+  a.tree_kv = tree;
+  a.R_cap = S;
+  a.layer = 0;
+  a.H = G;
+  a.KV = 1;
+  a.G = G;
+  a.hd = hd;
+  const int* rq = (const int*)(ws + o_req);
+  a.req_L = rq;
+  a.req_h = rq + 1;
+  a.req_row0 = rq + 2;
+  a.req_S = rq + 3;
+  a.row_anc = (const uint64_t*)(ws + o_anc);
+  a.pages_per_split = std::max(1, ((L + 63) / 64 + n_splits - 1) / n_splits);
+  a.n_splits = n_splits;
+  a.max_rows = S * G;
+  a.opart = (float*)(ws + o_op);
+  a.mpart = (float*)(ws + o_m);
+  a.lpart = (float*)(ws + o_l);
+  a.R = S;
+  a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
+  CK(attention_launch(a, 1, st, nullptr));
+  CK(attn_combine_launch(a, nullptr, o, st, nullptr));
+  CK(cudaStreamSynchronize(st));
+  return SPECEDGE_OK;
+}
+
+int32_t specedge_last_launch_count(void) { return g_last_launches; }
+
+specedge_status specedge_set_kernel_timing(int32_t enable) {
+  g_timing.on = enable != 0;
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_kernel_times(float* out_ms, int32_t* out_count, int32_t reset) {
+  for (auto& pr : g_timing.pending) {
+    cudaEvent_t a = g_timing.pool[pr.second], b = g_timing.pool[pr.second + 1];
+    if (cudaEventSynchronize(b) != cudaSuccess) return SPECEDGE_E_CUDA;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return SPECEDGE_E_CUDA;
+    g_timing.ms[pr.first] += ms;
+    g_timing.count[pr.first] += 1;
+  }
+  g_timing.pending.clear();
+  g_timing.used = 0;
+  for (int k = 0; k < K_NKINDS; ++k) {
+    if (out_ms) out_ms[k] = (float)g_timing.ms[k];
+    if (out_count) out_count[k] = g_timing.count[k];
+    if (reset) {
+      g_timing.ms[k] = 0;
+      g_timing.count[k] = 0;
+    }
+  }
+  return SPECEDGE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+"""Helpers for the GPU parity tests: build the same seeded state on the oracle side and on the
+library side, and compare results under SURVEY amb. A21 (exactness of acceptance outputs is
+required wherever every visited node's top-1 margin, computed from ORACLE scores, exceeds 1e-2).
+
+Inputs come only from synth/ and oracle/; nothing the CUDA path computes is fed to the oracle."""
+from __future__ import annotations
+
+import numpy as np
+
+MARGIN = 1e-2          # north_star: "bit-exact whenever top-1 logit margins exceed 1e-2"
+LOGIT_TOL = 2e-2       # north_star: "logits must agree within max-abs 2e-2 (bf16)"
+ATTN_TOL = 1e-3        # north_star: "attention outputs within 1e-3 relative (fp32 accumulate)"
+
+
+def top2_margin(scores):
+    s = np.sort(np.asarray(scores, np.float64), axis=-1)
+    return s[..., -1] - s[..., -2]
+
+
+def visited_slots(parent, acc_nodes):
+    return [0] + [n + 1 for n in acc_nodes]
+
+
+def compare_outcome(o_ref, slot_scores, gpu, r):
+    """Returns 'exact' if equal, 'exempt' if a visited node has margin <= 1e-2, else raises."""
+    margins = top2_margin(slot_scores)
+    vis = visited_slots(None, o_ref.accepted_node)
+    a = int(gpu["accepted_len"][r])
+    same = (a == o_ref.accepted_len and int(gpu["bonus"][r]) == o_ref.bonus and
+            list(gpu["accepted_token"][r][:a]) == o_ref.accepted_token and
+            list(gpu["accepted_node"][r][:a]) == o_ref.accepted_node)
+    if same:
+        return "exact"
+    if min(margins[v] for v in vis) <= MARGIN:
+        return "exempt"
+    raise AssertionError(f"request {r}: gpu (a={a}, bonus={int(gpu['bonus'][r])}) != oracle "
+                         f"(a={o_ref.accepted_len}, bonus={o_ref.bonus}) with margins "
+                         f"{[float(margins[v]) for v in vis]}")
+
+
+def split_outputs(out, batch):
+    """Device Outputs -> per-request host lists."""
+    off = batch.node_offset.cpu().numpy()
+    B = batch.num_requests
+    st = out.status.cpu().numpy()
+    al = out.accepted_len.cpu().numpy()
+    at = out.accepted_token.cpu().numpy()
+    an = out.accepted_node.cpu().numpy()
+    bo = out.bonus.cpu().numpy()
+    rt = out.row_target.cpu().numpy()
+    rs = out.row_score.cpu().numpy()
+    res = dict(status=st, accepted_len=al, bonus=bo, accepted_token=[], accepted_node=[], row_target=[],
+               row_score=[])
+    for r in range(B):
+        res["accepted_token"].append(at[off[r]:off[r + 1]])
+        res["accepted_node"].append(an[off[r]:off[r + 1]])
+        res["row_target"].append(rt[off[r] + r: off[r + 1] + r + 1])
+        res["row_score"].append(rs[off[r] + r: off[r + 1] + r + 1])
+    return res
+
+
+def bf16_bits_to_f64(u16):
+    u = np.asarray(u16, np.uint16).astype(np.uint32) << 16
+    return u.view(np.float32).astype(np.float64)

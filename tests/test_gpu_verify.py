@@ -1,0 +1,341 @@
+"""End-to-end parity of specedge_verify_batch (through the C ABI) against the oracle on the same
+seeded inputs (SURVEY §8(c) tolerances, amb. A21):
+  - acceptance outputs (accepted_len / tokens / nodes, bonus) and committed KV indices: exact
+    whenever every visited node's oracle top-1 margin exceeds 1e-2, otherwise exempt + counted;
+  - target token per slot: exact where the oracle margin exceeds 1e-2;
+  - logits: max-abs <= 2e-2 (fp32 capture of the same LM-head kernel);
+  - stochastic mode: the (stop node, bonus) law passes chi-square against the oracle's closed
+    form (O7) on V = 16.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import verify as OV  # noqa: E402
+from oracle.law import closed_form_law, slot_probs  # noqa: E402
+from oracle.model import Weights, Cache, gen_kv_fill, lm_logits, tree_forward  # noqa: E402
+from synth.configs import TINY, TINY_V16, TINY_MHA, SMALL128, LLAMA3_8B_2L  # noqa: E402
+from synth.plant import plant, draw_accept_lengths  # noqa: E402
+from synth.trees import pooled_tree, random_tree, chain_tree, Tree  # noqa: E402
+from tests.gpu_helpers import (LOGIT_TOL, MARGIN, bf16_bits_to_f64, compare_outcome,  # noqa: E402
+                               split_outputs, top2_margin)
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2505_17052_b200 import api as A
+    return A
+
+
+class Pair:
+    """The same sessions on both sides: oracle Sessions and library KV handles."""
+
+    def __init__(self, api, shape, seed, prompts, session_ids, max_nodes=64, capacity=None, num_pages=None,
+                 max_requests=None):
+        self.api, self.shape = api, shape
+        self.W = Weights(shape, seed)
+        self.model = api.Model(shape, seed, max_position=4096)
+        cap = capacity or max(len(p) for p in prompts) + 256
+        pages_per = (cap + 63) // 64
+        self.pool = api.KVPool(self.model, num_pages or pages_per * len(prompts) + 4, len(prompts) + 4)
+        B = max_requests or len(prompts)
+        self.ws = self.model.workspace(B, B * (max_nodes + 1), cap)
+        self.sessions, self.handles = [], []
+        for p, sid in zip(prompts, session_ids):
+            self.sessions.append(OV.make_session(self.W, p, sid))
+            h = self.pool.alloc(cap)
+            self.pool.prefill(h, p, self.ws)
+            self.handles.append(h)
+        torch.cuda.synchronize()
+
+    def close(self):
+        self.pool.close()
+        self.model.close()
+
+    def oracle_targets(self, idx):
+        def targets(trees):
+            return [OV.verify_one(self.W, OV.Request(self.sessions[i], t.parent, t.token), keep_logits=False).row_target
+                    for i, t in zip(idx, trees)]
+        return targets
+
+    def batch(self, idx, trees, rounds=None, max_nodes=None):
+        api = self.api
+        ses = [self.sessions[i] for i in idx]
+        return api.Batch.from_host([self.handles[i] for i in idx], [s.context_len for s in ses],
+                                   [s.last_token for s in ses], [s.session_id for s in ses],
+                                   rounds if rounds is not None else [s.round for s in ses], trees,
+                                   max_context_len=max(s.context_len for s in ses) + 8, max_nodes=max_nodes)
+
+
+def _prompts(rng, n, lens, vocab):
+    return [[int(t) for t in rng.integers(0, vocab, int(l))] for l in lens[:n]]
+
+
+def test_library_prefill_matches_oracle_cache(api):
+    rng = np.random.default_rng(101)
+    prompts = _prompts(rng, 3, [32, 70, 5], TINY.vocab)    # 70 -> two prefill chunks
+    pr = Pair(api, TINY, 1, prompts, [11, 12, 13])
+    try:
+        assert list(pr.pool.get_len(pr.handles)) == [31, 69, 4]
+        for i, s in enumerate(pr.sessions):
+            for l in range(TINY.n_layers):
+                for kv_sel, ref in ((0, s.cache.k[l]), (1, s.cache.v[l])):
+                    got = bf16_bits_to_f64(pr.pool.read_kv(pr.handles[i], l, kv_sel, 0, len(s.cache)))
+                    err = np.abs(got - ref)
+                    # bf16 storage: differences are occasional 1-ulp rounding flips of upstream values
+                    assert err.max() <= 0.05 * max(1.0, np.abs(ref).max()), (i, l, kv_sel, err.max())
+                    assert np.mean(err > 0) < 0.05
+    finally:
+        pr.close()
+
+
+@pytest.mark.parametrize("shape", [TINY, TINY_MHA, SMALL128])
+def test_verify_greedy_matches_oracle(api, shape):
+    rng = np.random.default_rng(202)
+    B = 5
+    prompts = _prompts(rng, B, [32, 40, 17, 60, 32], shape.vocab)
+    pr = Pair(api, shape, 1, prompts, list(range(100, 100 + B)))
+    try:
+        trees = [pooled_tree(rng, n, 4, 3, shape.vocab) for n in (8, 16, 1, 32, 8)]
+        trees[2] = Tree(np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.float32))  # root-only
+        a = draw_accept_lengths(rng, trees, 3.98, 1.55)
+        trees = plant(trees, pr.oracle_targets(range(B)), a, shape.vocab, rng)
+        batch = pr.batch(range(B), trees)
+        out = api.verify(pr.model, pr.pool, batch, pr.ws, auto_commit=False)
+        logits_gpu = api.debug_last_logits(pr.model, pr.ws, batch).cpu().numpy()
+        g = split_outputs(out, batch)
+        kinds = []
+        off = 0
+        for r in range(B):
+            o = OV.verify_one(pr.W, OV.Request(pr.sessions[r], trees[r].parent, trees[r].token))
+            S = trees[r].n + 1
+            lg = logits_gpu[off:off + S]
+            off += S
+            assert np.abs(lg - o.logits).max() <= LOGIT_TOL, np.abs(lg - o.logits).max()
+            assert np.abs(g["row_score"][r] - o.logits.max(-1)).max() <= LOGIT_TOL
+            m = top2_margin(o.logits)
+            sure = m > MARGIN
+            assert np.array_equal(g["row_target"][r][sure], o.row_target[sure])
+            assert g["status"][r] == 0
+            kinds.append(compare_outcome(o, o.logits, g, r))
+        assert kinds.count("exact") >= B - 1, kinds
+    finally:
+        pr.close()
+
+
+def test_iterated_verify_commit_reproduces_greedy_decoding(api):
+    """P4 on the GPU: k verify+commit steps emit the oracle's greedy continuation."""
+    rng = np.random.default_rng(303)
+    B = 3
+    prompts = _prompts(rng, B, [32, 20, 45], TINY.vocab)
+    pr = Pair(api, TINY, 1, prompts, [7, 8, 9])
+    try:
+        emitted_gpu = [[] for _ in range(B)]
+        emitted_ref = [[] for _ in range(B)]
+        exempt = 0
+        for step in range(8):
+            trees = [pooled_tree(rng, 8, 4, 3, TINY.vocab) for _ in range(B)]
+            a = draw_accept_lengths(rng, trees, 3.98, 1.55)
+            trees = plant(trees, pr.oracle_targets(range(B)), a, TINY.vocab, rng)
+            batch = pr.batch(range(B), trees)
+            out = api.verify(pr.model, pr.pool, batch, pr.ws, auto_commit=True)
+            g = split_outputs(out, batch)
+            refs = OV.verify_batch(pr.W, [OV.Request(pr.sessions[r], trees[r].parent, trees[r].token)
+                                          for r in range(B)])
+            for r in range(B):
+                kind = compare_outcome(refs[r], refs[r].logits, g, r)
+                if kind == "exempt":
+                    exempt += 1
+                    pytest.skip("near-tie on a visited node; sequences diverge legitimately")
+                emitted_gpu[r] += list(g["accepted_token"][r][:g["accepted_len"][r]]) + [int(g["bonus"][r])]
+                emitted_ref[r] += refs[r].accepted_token + [refs[r].bonus]
+            lens = pr.pool.get_len(pr.handles)
+            assert list(lens) == [len(s.cache) for s in pr.sessions]
+        assert emitted_gpu == emitted_ref
+        # the committed caches equal the oracle's (indices exact, values within bf16 rounding)
+        for r in range(B):
+            s = pr.sessions[r]
+            got = bf16_bits_to_f64(pr.pool.read_kv(pr.handles[r], 1, 0, 0, len(s.cache)))
+            assert np.abs(got - s.cache.k[1]).max() <= 0.05 * max(1.0, np.abs(s.cache.k[1]).max())
+    finally:
+        pr.close()
+
+
+def test_verify_sampled_matches_oracle_draws(api):
+    rng = np.random.default_rng(404)
+    B = 4
+    prompts = _prompts(rng, B, [32, 33, 34, 35], TINY.vocab)
+    pr = Pair(api, TINY, 3, prompts, [1 << 40, 5, 6, 7])
+    try:
+        trees = [random_tree(rng, n, TINY.vocab) for n in (8, 3, 16, 0)]
+        batch = pr.batch(range(B), trees, rounds=[3, 0, 9, 1 << 31])
+        out = api.verify(pr.model, pr.pool, batch, pr.ws, mode=1, temperature=0.7, seed=0xDEADBEEF12345,
+                         auto_commit=False)
+        g = split_outputs(out, batch)
+        for r, rnd in enumerate([3, 0, 9, 1 << 31]):
+            o = OV.verify_one(pr.W, OV.Request(pr.sessions[r], trees[r].parent, trees[r].token, round=rnd),
+                              "sample", 0.7, 0xDEADBEEF12345)
+            sc = OV.target_scores(o.logits, "sample", 0.7, 0xDEADBEEF12345, rnd, pr.sessions[r].session_id)
+            sure = top2_margin(sc) > MARGIN
+            assert np.array_equal(g["row_target"][r][sure], o.row_target[sure])
+            assert np.abs(g["row_score"][r] - sc.max(-1)).max() <= 2 * LOGIT_TOL
+            compare_outcome(o, sc, g, r)
+    finally:
+        pr.close()
+
+
+def test_errors_are_per_request_and_isolated(api):
+    rng = np.random.default_rng(505)
+    prompts = _prompts(rng, 4, [10, 10, 10, 10], TINY.vocab)
+    pr = Pair(api, TINY, 1, prompts, [1, 2, 3, 4])
+    try:
+        good = pooled_tree(rng, 6, 3, 2, TINY.vocab)
+        bad_parent = Tree(np.array([-1, 2, 0], np.int32), np.array([1, 2, 3], np.int32), np.zeros(3, np.float32))
+        dup = Tree(np.array([-1, -1], np.int32), np.array([4, 4], np.int32), np.zeros(2, np.float32))
+        bad_tok = Tree(np.array([-1], np.int32), np.array([TINY.vocab], np.int32), np.zeros(1, np.float32))
+        trees = [good, bad_parent, dup, bad_tok]
+        batch = pr.batch(range(4), trees)
+        lens0 = pr.pool.get_len(pr.handles)
+        out = api.verify(pr.model, pr.pool, batch, pr.ws, auto_commit=True)
+        g = split_outputs(out, batch)
+        assert list(g["status"]) == [0, 1, 4, 3]
+        assert list(g["bonus"][1:]) == [-1, -1, -1] and list(g["accepted_len"][1:]) == [0, 0, 0]
+        lens1 = pr.pool.get_len(pr.handles)
+        assert list(lens1[1:]) == list(lens0[1:])
+        o = OV.verify_one(pr.W, OV.Request(pr.sessions[0], good.parent, good.token))
+        assert compare_outcome(o, o.logits, g, 0) in ("exact", "exempt")
+        assert lens1[0] == lens0[0] + g["accepted_len"][0] + 1
+        # stale context length -> E_CONTEXT; duplicate handle -> E_HANDLE; idempotent commit
+        batch2 = api.Batch.from_host([pr.handles[1], pr.handles[2], pr.handles[2]], [5, int(lens1[2]) + 1,
+                                     int(lens1[2]) + 1], [1, 1, 1], [1, 2, 3], [0, 0, 0], [good, good, good])
+        out2 = api.verify(pr.model, pr.pool, batch2, pr.ws, auto_commit=False)
+        assert list(out2.status.cpu().numpy()) == [5, 0, 7]
+        api.kv_commit(pr.model, pr.pool, batch2, out2, pr.ws)
+        l_a = pr.pool.get_len([pr.handles[2]])[0]
+        api.kv_commit(pr.model, pr.pool, batch2, out2, pr.ws)        # second commit: no-op
+        assert pr.pool.get_len([pr.handles[2]])[0] == l_a
+        assert out2.status.cpu().numpy()[1] == 5
+    finally:
+        pr.close()
+
+
+def test_host_entry_point_equals_device_entry(api):
+    rng = np.random.default_rng(606)
+    prompts = _prompts(rng, 3, [20, 30, 40], TINY.vocab)
+    pr = Pair(api, TINY, 1, prompts, [1, 2, 3])
+    try:
+        trees = [pooled_tree(rng, 8, 4, 3, TINY.vocab) for _ in range(3)]
+        batch = pr.batch(range(3), trees)
+        out = api.verify(pr.model, pr.pool, batch, pr.ws, auto_commit=False)
+        hb = api.HostBatch.of(batch)
+        ho = api.host_outputs(hb)
+        api.verify_host(pr.model, pr.pool, hb, pr.ws, ho, auto_commit=False)
+        for k in ("status", "accepted_len", "bonus", "row_target"):
+            assert np.array_equal(getattr(out, k).cpu().numpy(), ho[k].numpy()), k
+        assert api.last_launch_count() > 0
+    finally:
+        pr.close()
+
+
+def _sampled_law_counts(api, n_draws, T, seed):
+    """GPU (stop, bonus) counts for one fixed tree over many rounds, V = 16."""
+    shape = TINY_V16
+    W = Weights(shape, 12)
+    parent = np.array([-1, -1, -1, 0, 0, 1, 3, 3], np.int32)
+    token = np.array([0, 1, 2, 0, 1, 0, 0, 1], np.int32)
+    B = 512
+    ctx = 9
+    # identical random-filled caches on every handle (same fill seed and stream id)
+    cache = Cache(shape)
+    for l in range(shape.n_layers):
+        cache.k[l] = gen_kv_fill(99, 0, l, 0, ctx - 1, shape.n_kv, shape.head_dim)
+        cache.v[l] = gen_kv_fill(99, 0, l, 1, ctx - 1, shape.n_kv, shape.head_dim)
+    hf, _, _ = tree_forward(W, cache, 3, parent, token)
+    logits = lm_logits(W, hf)
+    law = closed_form_law(parent, token, slot_probs(logits, T))
+    model = api.Model(shape, 12, max_position=1024)
+    pool = api.KVPool(model, B + 4, B + 4)
+    try:
+        hs = []
+        for _ in range(B):
+            h = pool.alloc(64)
+            pool.fill_random(h, ctx - 1, 99, 0)
+            hs.append(h)
+        ws = model.workspace(B, B * 9, 64)
+        tr = Tree(parent, token, np.zeros(8, np.float32))
+        counts = {}
+        for k in range(n_draws // B):
+            batch = api.Batch.from_host(hs, [ctx] * B, [3] * B, [42] * B, list(range(k * B, (k + 1) * B)),
+                                        [tr] * B, max_context_len=64)
+            out = api.verify(model, pool, batch, ws, mode=1, temperature=T, seed=seed, auto_commit=False)
+            al = out.accepted_len.cpu().numpy()
+            an = out.accepted_node.cpu().numpy().reshape(B, 8)
+            bo = out.bonus.cpu().numpy()
+            for r in range(B):
+                stop = 0 if al[r] == 0 else int(an[r][al[r] - 1]) + 1
+                counts[(stop, int(bo[r]))] = counts.get((stop, int(bo[r])), 0) + 1
+        return counts, law
+    finally:
+        pool.close()
+        model.close()
+
+
+def test_sampled_verification_law_chi_square_on_gpu(api):
+    from scipy import stats
+    n = 512 * 200
+    counts, law = _sampled_law_counts(api, n, 0.7, 5)
+    keys = sorted(law)
+    exp = np.array([law[k] * n for k in keys])
+    obs = np.array([counts.get(k, 0) for k in keys], float)
+    assert obs.sum() == n
+    big = exp >= 5
+    o = np.append(obs[big], obs[~big].sum())
+    e = np.append(exp[big], exp[~big].sum())
+    assert stats.chisquare(o, e * o.sum() / e.sum()).pvalue > 1e-3
+
+
+def test_full_width_two_layer_slice_matches_oracle(api):
+    """cfg2 widths (Llama-3-8B: d 4096, 32/8 heads, F 14336, V 128256), 16 requests x 32-node
+    trees, ~1k random-filled contexts, in the launch configuration bench.py times (only the
+    layer count is reduced so the oracle finishes).  Every slot's target token is compared."""
+    shape = LLAMA3_8B_2L
+    rng = np.random.default_rng(707)
+    B = 16
+    W = Weights(shape, 2)
+    model = api.Model(shape, 2, max_position=2048)
+    pool = api.KVPool(model, B * 22, B)
+    try:
+        ctx = rng.integers(768, 1281, B)
+        hs, sessions = [], []
+        for r in range(B):
+            h = pool.alloc(1400)
+            pool.fill_random(h, int(ctx[r]) - 1, 1234, r)
+            hs.append(h)
+            c = Cache(shape)
+            for l in range(shape.n_layers):
+                c.k[l] = gen_kv_fill(1234, r, l, 0, int(ctx[r]) - 1, shape.n_kv, shape.head_dim)
+                c.v[l] = gen_kv_fill(1234, r, l, 1, int(ctx[r]) - 1, shape.n_kv, shape.head_dim)
+            sessions.append(OV.Session(c, int(rng.integers(0, shape.vocab)), 1000 + r))
+        trees = [pooled_tree(rng, 32, 7, 4, shape.vocab) for _ in range(B)]
+        ws = model.workspace(B, B * 33, 1400)
+        batch = api.Batch.from_host(hs, [int(x) for x in ctx], [s.last_token for s in sessions],
+                                    [s.session_id for s in sessions], [0] * B, trees, max_context_len=1400)
+        out = api.verify(model, pool, batch, ws, auto_commit=False)
+        g = split_outputs(out, batch)
+        n_exempt = 0
+        refs = OV.verify_batch(W, [OV.Request(sessions[r], trees[r].parent, trees[r].token) for r in range(B)],
+                               auto_commit=False)
+        for r in range(B):
+            o = refs[r]
+            m = top2_margin(o.logits)
+            sure = m > MARGIN
+            n_exempt += int((~sure).sum())
+            assert np.array_equal(g["row_target"][r][sure], o.row_target[sure]), r
+            assert np.abs(g["row_score"][r] - o.logits.max(-1)).max() <= LOGIT_TOL
+            compare_outcome(o, o.logits, g, r)
+        assert n_exempt < 0.1 * B * 33
+    finally:
+        pool.close()
+        model.close()
