@@ -8,9 +8,10 @@ GQA attention -> O-proj + residual -> RMSNorm -> SwiGLU MLP + residual, final RM
 LM head, no biases, QK-norm off.
 
 Storage points (reading R-precision, revising SURVEY amb. A12): bf16 for weights,
-embeddings, every GEMM input operand (normed h, q, O, M, final-norm output), cached K (post-RoPE)
-and V; the residual stream x is kept unrounded (the GPU keeps it in fp32), because rounding it to
-bf16 amplifies arithmetic-order noise past the north_star logit tolerance (tests/notes in DESIGN).
+embeddings, the GEMM input operands inside the layers (normed h, q, O, M), cached K (post-RoPE)
+and V.  Unrounded: the residual stream x (the GPU keeps it in fp32) and the final-norm output
+(the GPU passes it to the LM head as a hi/lo pair of bf16 operands).  Rounding those two to bf16
+amplifies arithmetic-order noise past the north_star logit tolerance (measured).
 
 Two independent ways of running it live here:
   * `tree_forward`   - SURVEY §8(c) O2: all S = N+1 slots of a draft tree at once; slot s
@@ -191,7 +192,9 @@ def _post_attn(W: Weights, l, x, o):
 
 
 def final_hidden(W: Weights, x):
-    return bf16(rmsnorm(x, W.g_final(), W.shape.eps))
+    """Final RMSNorm output.  Not rounded: the library feeds it to the LM head as a hi/lo pair of
+    bf16 operands (hi + lo = value to ~2^-17 relative), reading R-precision."""
+    return rmsnorm(x, W.g_final(), W.shape.eps)
 
 
 def tree_depth(parent):

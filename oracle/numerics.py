@@ -2,8 +2,8 @@
 
 Precision reading (DESIGN.md R-precision, revising SURVEY amb. A12; the paper states no precision
 anywhere, P:16/P:744 only quote marketing TFLOPS): bf16-valued are weights, embeddings, cached K
-(post-RoPE) and V, every GEMM input operand and the final-norm output; the residual stream is
-not rounded.  `bf16` below rounds an exact (float64) value to the nearest bf16 value,
+(post-RoPE) and V, and the in-layer GEMM input operands (h, q, O, M); the residual stream and the
+final-norm output are not rounded.  `bf16` below rounds an exact (float64) value to the nearest bf16 value,
 ties to even.  All other arithmetic is float64.
 """
 from __future__ import annotations

@@ -167,21 +167,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ncol = min(32, BN - c * 32);
         if constexpr (MODE == EPI_F32) {
           if (feat < a.M) {
+            if (a.pair) {   // physical rows 2r, 2r+1 hold hi/lo parts of logical row r
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int row = row_base + j;
-              if (j < ncol && row < a.R) a.out_f32[(size_t)row * a.ldo + feat] = __uint_as_float(v[j]);
+              for (int j = 0; j < 32; j += 2) {
+                const int row = row_base + j;
+                if (j < ncol && row < a.R)
+                  a.out_f32[(size_t)(row >> 1) * a.ldo + feat] = __uint_as_float(v[j]) + __uint_as_float(v[j + 1]);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int row = row_base + j;
+                if (j < ncol && row < a.R) a.out_f32[(size_t)row * a.ldo + feat] = __uint_as_float(v[j]);
+              }
             }
           }
         } else if constexpr (MODE == EPI_RESID) {
           if (feat < a.M) {
+            // all 32 residual loads in flight before the first store (no load->store chains)
+            float old[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int row = row_base + j;
-              if (j < ncol && row < a.R) {
-                float* p = a.out_f32 + (size_t)row * a.ldo + feat;   // fp32 residual stream
-                *p = *p + __uint_as_float(v[j]);
-              }
+              old[j] = (j < ncol && row < a.R) ? __ldcg(a.out_f32 + (size_t)row * a.ldo + feat) : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int row = row_base + j;
+              if (j < ncol && row < a.R) a.out_f32[(size_t)row * a.ldo + feat] = old[j] + __uint_as_float(v[j]);
             }
           }
         } else if constexpr (MODE == EPI_SWIGLU) {
@@ -191,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_bar_sync(1, kEpiThreads);
           const int f = et & 63, half = et >> 6;
           const int fo = m * 64 + f;
+#pragma unroll
           for (int jj = 0; jj < 16; ++jj) {
             const int j = half * 16 + jj;
             const int row = row_base + j;
@@ -201,76 +215,105 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           named_bar_sync(1, kEpiThreads);
         } else if constexpr (MODE == EPI_QKV) {
+          int* s_pos = red_i;
 #pragma unroll
           for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
+          if (et < 32) s_pos[et] = (row_base + et < a.R) ? __ldg(a.row_pos + row_base + et) : 0;
           named_bar_sync(1, kEpiThreads);
           const int hd = a.head_dim, half_hd = hd >> 1;
           const int qd = a.n_heads * hd, kd = a.n_kv * hd;
           if (feat < a.M) {
             const int dim = feat % hd;
             const bool rot = feat < qd + kd;
-            const int partner = tl + (dim < half_hd ? half_hd : -half_hd);
+            const bool lo = dim < half_hd;
+            const int partner = tl + (lo ? half_hd : -half_hd);
             const int fi = dim % half_hd;
+            uint16_t outv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float x = __uint_as_float(v[j]);
+              if (rot) {
+                const size_t ti = (size_t)s_pos[j] * half_hd + fi;
+                const float cs = __ldg(a.rope_cos + ti), sn = __ldg(a.rope_sin + ti);
+                const float xp = xch[partner * kXchStride + j];
+                x = lo ? (x * cs - xp * sn) : (x * cs + xp * sn);
+              }
+              outv[j] = f32_to_bf16_bits(x);
+            }
+            uint16_t* dst;
+            size_t stride;
+            if (feat < qd) {
+              dst = reinterpret_cast<uint16_t*>(a.out_bf16) + feat;
+              stride = a.ld_out;
+            } else {
+              const int kvsel = feat < qd + kd ? 0 : 1;
+              const int kvh = (feat - qd - kvsel * kd) / hd;
+              dst = reinterpret_cast<uint16_t*>(a.tree_kv) +
+                    ((((size_t)a.layer * 2 + kvsel) * a.n_kv + kvh) * a.R_cap) * hd + dim;
+              stride = hd;
+            }
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int row = row_base + j;
-              if (j >= ncol || row >= a.R) continue;
-              float x = __uint_as_float(v[j]);
-              if (rot) {
-                const int pos = a.row_pos[row];
-                const float cs = a.rope_cos[(size_t)pos * half_hd + fi];
-                const float sn = a.rope_sin[(size_t)pos * half_hd + fi];
-                const float xp = xch[partner * kXchStride + j];
-                x = dim < half_hd ? (x * cs - xp * sn) : (x * cs + xp * sn);
-              }
-              const bf16 b = __float2bfloat16_rn(x);
-              if (feat < qd) {
-                a.out_bf16[(size_t)row * a.ld_out + feat] = b;
-              } else {
-                const int kvsel = feat < qd + kd ? 0 : 1;
-                const int kvh = (feat - qd - kvsel * kd) / hd;
-                a.tree_kv[((((size_t)a.layer * 2 + kvsel) * a.n_kv + kvh) * a.R_cap + row) * hd + dim] = b;
-              }
+              if (j < ncol && row < a.R) dst[(size_t)row * stride] = outv[j];
             }
           }
           named_bar_sync(1, kEpiThreads);
         } else if constexpr (MODE == EPI_ARGMAX) {
+          // a.pair: physical rows (2r, 2r+1) = hi/lo parts of logical row r -> 16 logical columns
+          const int np = a.pair ? 16 : 32;
           const bool fv = feat < a.vocab;
+          if (a.pair) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int row = row_base + j;
-            float s = -INFINITY;
-            if (fv && j < ncol && row < a.R) {
-              s = __uint_as_float(v[j]);
-              if (a.sample) s = s * a.inv_t + gumbel_noise(a, row, feat);
+            for (int jj = 0; jj < 16; ++jj) {
+              const int row = row_base + 2 * jj;
+              float s = -INFINITY;
+              if (fv && 2 * jj < ncol && row < a.R) {
+                s = __uint_as_float(v[2 * jj]) + __uint_as_float(v[2 * jj + 1]);
+                if (a.sample) s = s * a.inv_t + gumbel_noise(a, row >> 1, feat);
+              }
+              xch[tl * kXchStride + jj] = s;
             }
-            xch[tl * kXchStride + j] = s;
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              const int row = row_base + jj;
+              float s = -INFINITY;
+              if (fv && jj < ncol && row < a.R) {
+                s = __uint_as_float(v[jj]);
+                if (a.sample) s = s * a.inv_t + gumbel_noise(a, row, feat);
+              }
+              xch[tl * kXchStride + jj] = s;
+            }
           }
           named_bar_sync(1, kEpiThreads);
+          const int ngrp = 128 / np, per = 128 / ngrp;
           {
-            const int j = et & 31, qq = et >> 5;
+            const int jj = et % np, g = et / np;
             float best = -INFINITY;
             int bi = 0x7fffffff;
-            for (int l = 0; l < 32; ++l) {
-              const float s = xch[(qq * 32 + l) * kXchStride + j];
-              if (s > best) { best = s; bi = m * 128 + qq * 32 + l; }
+            for (int l = 0; l < per; ++l) {
+              const float s = xch[(g * per + l) * kXchStride + jj];
+              if (s > best) { best = s; bi = m * 128 + g * per + l; }
             }
-            red_v[qq * 32 + j] = best;
-            red_i[qq * 32 + j] = bi;
+            red_v[g * np + jj] = best;
+            red_i[g * np + jj] = bi;
           }
           named_bar_sync(1, kEpiThreads);
-          if (et < 32) {
-            const int j = et;
-            float best = red_v[j];
-            int bi = red_i[j];
-            for (int qq = 1; qq < 4; ++qq) {
-              const float s = red_v[qq * 32 + j];
-              if (s > best) { best = s; bi = red_i[qq * 32 + j]; }
+          if (et < np) {
+            const int jj = et;
+            float best = red_v[jj];
+            int bi = red_i[jj];
+            for (int g = 1; g < ngrp; ++g) {
+              const float s = red_v[g * np + jj];
+              if (s > best) { best = s; bi = red_i[g * np + jj]; }
             }
+            const int j = a.pair ? 2 * jj : jj;
             const int row = row_base + j;
             if (j < ncol && row < a.R) {
-              a.part_val[(size_t)row * a.n_tiles_m + m] = best;
-              a.part_idx[(size_t)row * a.n_tiles_m + m] = bi;
+              const int lr = a.pair ? row >> 1 : row;
+              a.part_val[(size_t)lr * a.n_tiles_m + m] = best;
+              a.part_idx[(size_t)lr * a.n_tiles_m + m] = bi;
             }
           }
           named_bar_sync(1, kEpiThreads);

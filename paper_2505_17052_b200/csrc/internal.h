@@ -28,6 +28,7 @@ enum GemmMode : int {
 struct GemmArgs {
   int M, R, K;            // weight rows (features), activation rows, reduction length
   int BN, n_tiles_n, n_tiles_m, num_kb, stages, tmem_cols;
+  int pair;               // EPI_F32/EPI_ARGMAX: rows (2r, 2r+1) are hi/lo bf16 parts of row r
   // EPI_F32 / EPI_RESID (fp32 residual stream)
   float* out_f32;
   int ldo;
@@ -114,7 +115,7 @@ cudaError_t prep_launch(const PrepArgs& p, cudaStream_t st, int* launches);
 cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int d, cudaStream_t st,
                          int* launches);
 cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* out, int R, int d, float eps,
-                           cudaStream_t st, int* launches);
+                           cudaStream_t st, int* launches, int split = 0);
 cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, int* y, float* score,
                              int* row_target, float* row_score, cudaStream_t st, int* launches);
 struct WalkArgs {

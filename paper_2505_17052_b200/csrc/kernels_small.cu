@@ -122,9 +122,11 @@ __global__ void k_embed(const bf16* __restrict__ E, const int* __restrict__ row_
 }
 
 // --------------------------------------------------------------------------------- K3 RMSNorm
-// out = bf16(x * rsqrt(mean(x^2) + eps) * g), x fp32 (amb. A13)
+// out = bf16(x * rsqrt(mean(x^2) + eps) * g), x fp32 (amb. A13).
+// split = 1 (final norm feeding the LM head): y is written as two bf16 rows, hi = bf16(y) at
+// out row 2r and lo = bf16(y - hi) at row 2r+1, so hi + lo carries y to ~2^-17 relative.
 __global__ void k_rmsnorm(const float* __restrict__ X, const bf16* __restrict__ g, bf16* __restrict__ out,
-                          int d, float eps) {
+                          int d, float eps, int split) {
   const int row = blockIdx.x;
   const float* x = X + (size_t)row * d;
   __shared__ float red[32];
@@ -150,15 +152,23 @@ __global__ void k_rmsnorm(const float* __restrict__ X, const bf16* __restrict__ 
     const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     const uint4 gu = *reinterpret_cast<const uint4*>(g + i);
     const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
-    uint32_t o[4];
+    uint32_t o[4], r[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float lo = xv[2 * k] * inv * __uint_as_float(gw[k] << 16);
-      const float hi = xv[2 * k + 1] * inv * __uint_as_float(gw[k] & 0xFFFF0000u);
-      __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+      const float y0 = xv[2 * k] * inv * __uint_as_float(gw[k] << 16);
+      const float y1 = xv[2 * k + 1] * inv * __uint_as_float(gw[k] & 0xFFFF0000u);
+      __nv_bfloat162 p = __floats2bfloat162_rn(y0, y1);
       o[k] = *reinterpret_cast<uint32_t*>(&p);
+      const float h0 = __uint_as_float(o[k] << 16), h1 = __uint_as_float(o[k] & 0xFFFF0000u);
+      __nv_bfloat162 q = __floats2bfloat162_rn(y0 - h0, y1 - h1);
+      r[k] = *reinterpret_cast<uint32_t*>(&q);
     }
-    *reinterpret_cast<uint4*>(out + (size_t)row * d + i) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (split) {
+      *reinterpret_cast<uint4*>(out + (size_t)(2 * row) * d + i) = make_uint4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<uint4*>(out + (size_t)(2 * row + 1) * d + i) = make_uint4(r[0], r[1], r[2], r[3]);
+    } else {
+      *reinterpret_cast<uint4*>(out + (size_t)row * d + i) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
   }
 }
 
@@ -369,10 +379,10 @@ cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int
   return cudaGetLastError();
 }
 cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* out, int R, int d, float eps, cudaStream_t st,
-                           int* launches) {
+                           int* launches, int split) {
   if (launches) ++*launches;
   const int threads = d >= 2048 ? 256 : (d >= 512 ? 64 : 32);
-  k_rmsnorm<<<R, threads, 0, st>>>(X, g, out, d, eps);
+  k_rmsnorm<<<R, threads, 0, st>>>(X, g, out, d, eps, split);
   return cudaGetLastError();
 }
 cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, int* y, float* score,

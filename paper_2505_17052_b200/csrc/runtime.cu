@@ -66,7 +66,7 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
   size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
-  size_t X, Hn, Q, O, M, tree_kv, opart, mpart, lpart, part_val, part_idx, y, score;
+  size_t X, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, part_val, part_idx, y, score;
   size_t stage_in, stage_out, total;
   int B, R, n_splits_max;
 };
@@ -93,6 +93,7 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.row_anc = take(8 * R);
   w.X = take(4 * (size_t)R * c.d);   // fp32 residual stream
   w.Hn = take(2 * (size_t)R * c.d);
+  w.Hf = take(2 * 2 * (size_t)R * c.d);   // final-norm output as hi/lo bf16 row pairs
   w.Q = take(2 * (size_t)R * H * hd);
   w.O = take(2 * (size_t)R * H * hd);
   w.M = take(2 * (size_t)R * c.ffn);
@@ -266,10 +267,12 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   }
   int* y = (int*)P(w.y);
   if (!prefill) {
-    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, m->g_final, Hn, R, c.d, c.eps, st, &launches)); }
+    bf16* Hf = (bf16*)P(w.Hf);
+    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, m->g_final, Hf, R, c.d, c.eps, st, &launches, 1)); }
     GemmArgs gl{};
     gl.M = c.vocab;
-    gl.R = R;
+    gl.R = 2 * R;
+    gl.pair = 1;
     gl.K = c.d;
     gl.part_val = (float*)P(w.part_val);
     gl.part_idx = (int*)P(w.part_idx);
@@ -283,7 +286,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gl.row_slot = pa.row_slot;
     gl.req_round = di.round;
     gl.req_session = di.session_id;
-    { KTimer _t(K_LM, st); CK(gemm_launch(EPI_ARGMAX, m->tm_lm, Hn, gl, st, &launches)); }
+    { KTimer _t(K_LM, st); CK(gemm_launch(EPI_ARGMAX, m->tm_lm, Hf, gl, st, &launches)); }
     KTimer _tr(K_LMRED, st);
     CK(lm_reduce_launch(gl.part_val, gl.part_idx, R, (c.vocab + 127) / 128, y, (float*)P(w.score),
                         dout.row_target, dout.row_score, st, &launches));
@@ -823,11 +826,12 @@ specedge_status specedge_debug_last_logits(specedge_model* m, void* workspace, s
   if (ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
   GemmArgs g{};
   g.M = m->cfg.vocab;
-  g.R = R;
+  g.R = 2 * R;
+  g.pair = 1;
   g.K = m->cfg.d;
   g.out_f32 = logits;
   g.ldo = m->cfg.vocab;
-  CK(gemm_launch(EPI_F32, m->tm_lm, (uint8_t*)workspace + w.Hn, g, (cudaStream_t)stream, nullptr));
+  CK(gemm_launch(EPI_F32, m->tm_lm, (uint8_t*)workspace + w.Hf, g, (cudaStream_t)stream, nullptr));
   return SPECEDGE_OK;
 }
 
