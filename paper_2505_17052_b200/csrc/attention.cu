@@ -46,12 +46,6 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
-__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
-}
 __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -347,10 +341,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   cp_async_wait_all();
 }
 
-// Merge split partials: o = sum_sp 2^(m_sp - m) o_sp / sum_sp 2^(m_sp - m) l_sp
+// Merge split partials: o = sum_sp 2^(m_sp - m) o_sp / sum_sp 2^(m_sp - m) l_sp.
+// One warp per (row, head); lanes own 4 consecutive head-dim elements (float4).
 __global__ void k_attn_combine(const __grid_constant__ AttnArgs a, bf16* __restrict__ O,
                                float* __restrict__ O_f32) {
-  const int rh = blockIdx.x;                 // row * H + head
+  const int rh = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // row * H + head
+  const int lane = threadIdx.x & 31;
+  if (rh >= a.R * a.H) return;
   const int hd = a.hd;
   const size_t stride = (size_t)a.R * a.H;
   float m = -INFINITY;
@@ -362,15 +359,26 @@ __global__ void k_attn_combine(const __grid_constant__ AttnArgs a, bf16* __restr
     if (ms != -INFINITY) l += exp2f(ms - mb) * a.lpart[sp * stride + rh];
   }
   const float inv = l > 0.f ? 1.0f / l : 0.f;
-  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
-    float acc = 0.f;
+  for (int d = lane * 4; d < hd; d += 128) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int sp = 0; sp < a.n_splits; ++sp) {
       const float ms = a.mpart[sp * stride + rh];
-      if (ms != -INFINITY) acc += exp2f(ms - mb) * a.opart[(sp * stride + rh) * hd + d];
+      if (ms == -INFINITY) continue;
+      const float w = exp2f(ms - mb) * inv;
+      const float4 v = *reinterpret_cast<const float4*>(a.opart + (sp * stride + rh) * hd + d);
+      acc.x += w * v.x;
+      acc.y += w * v.y;
+      acc.z += w * v.z;
+      acc.w += w * v.w;
     }
-    const float v = acc * inv;
-    if (O) O[(size_t)rh * hd + d] = __float2bfloat16_rn(v);
-    if (O_f32) O_f32[(size_t)rh * hd + d] = v;
+    if (O) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y), p1 = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&p0);
+      u.y = *reinterpret_cast<uint32_t*>(&p1);
+      *reinterpret_cast<uint2*>(O + (size_t)rh * hd + d) = u;
+    }
+    if (O_f32) *reinterpret_cast<float4*>(O_f32 + (size_t)rh * hd + d) = acc;
   }
 }
 
@@ -394,6 +402,16 @@ cudaError_t launch_hd(const AttnArgs& a, int B, cudaStream_t st) {
 
 }  // namespace
 
+// tcgen05 kernel: one CTA per SM (512 TMEM columns); split only when (request, kv head) items
+// leave most SMs idle.
+int attn_pick_splits_tc(int B, int KV, int max_pages) {
+  const int items = std::max(1, B * KV);
+  int ns = (148 + items / 2) / items;
+  ns = std::min(ns, 8);
+  ns = std::min(ns, std::max(1, (max_pages + 1) / 2));
+  return std::max(1, ns);
+}
+
 int attn_pick_splits(int B, int KV, int max_pages) {
   const int items = std::max(1, B * KV);
   int ns = (2 * 148 + items - 1) / items;
@@ -415,7 +433,7 @@ cudaError_t attention_launch(const AttnArgs& a, int B, cudaStream_t st, int* lau
 
 cudaError_t attn_combine_launch(const AttnArgs& a, bf16* O, float* O_f32, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
-  k_attn_combine<<<a.R * a.H, std::min(128, a.hd), 0, st>>>(a, O, O_f32);
+  k_attn_combine<<<(a.R * a.H + 7) / 8, 256, 0, st>>>(a, O, O_f32);
   return cudaGetLastError();
 }
 

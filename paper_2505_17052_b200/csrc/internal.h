@@ -85,6 +85,11 @@ cudaError_t attention_launch(const AttnArgs& a, int B, cudaStream_t st, int* lau
 cudaError_t attn_combine_launch(const AttnArgs& a, bf16* O, float* O_f32, cudaStream_t st,
                                 int* launches);
 int attn_pick_splits(int B, int KV, int max_pages);
+int attn_pick_splits_tc(int B, int KV, int max_pages);
+// tcgen05 attention (head_dim 64 / 128); with n_splits == 1 it writes the normalised output
+// directly (bf16 O and/or fp32 O_f32), otherwise (o, m, l) partials for attn_combine_launch.
+bool attention_tc_supported(int hd, int G);
+cudaError_t attention_tc_launch(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStream_t st, int* launches);
 
 // ---------------------------------------------------------------------------------------------
 // small kernels

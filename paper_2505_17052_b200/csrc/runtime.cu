@@ -210,7 +210,8 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   aa.req_row0 = pa.req_row0;
   aa.req_S = pa.req_S;
   aa.row_anc = pa.row_anc;
-  aa.n_splits = std::min(kMaxSplits, attn_pick_splits(B, KV, max_pages));
+  const bool use_tc = attention_tc_supported(hd, G);
+  aa.n_splits = std::min(kMaxSplits, use_tc ? attn_pick_splits_tc(B, KV, max_pages) : attn_pick_splits(B, KV, max_pages));
   aa.pages_per_split = std::max(1, (max_pages + aa.n_splits - 1) / aa.n_splits);
   aa.n_splits = std::max(1, (max_pages + aa.pages_per_split - 1) / aa.pages_per_split);
   aa.max_rows = (in->max_nodes + 1) * G;
@@ -240,8 +241,13 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     g.rope_sin = m->rope_sin;
     { KTimer _t(K_QKV, st); CK(gemm_launch(EPI_QKV, Lw.tm_qkv, Hn, g, st, &launches)); }
     aa.layer = l;
-    { KTimer _t(K_ATTN, st); CK(attention_launch(aa, B, st, &launches)); }
-    { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
+    if (use_tc) {
+      { KTimer _t(K_ATTN, st); CK(attention_tc_launch(aa, B, aa.n_splits == 1 ? O : nullptr, nullptr, st, &launches)); }
+      if (aa.n_splits > 1) { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
+    } else {
+      { KTimer _t(K_ATTN, st); CK(attention_launch(aa, B, st, &launches)); }
+      { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
+    }
     GemmArgs go{};
     go.M = c.d;
     go.R = R;
@@ -898,8 +904,13 @@ specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_pr
   a.lpart = (float*)(ws + o_l);
   a.R = S;
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
-  CK(attention_launch(a, 1, st, nullptr));
-  CK(attn_combine_launch(a, nullptr, o, st, nullptr));
+  if (attention_tc_supported(hd, G)) {
+    CK(attention_tc_launch(a, 1, nullptr, n_splits == 1 ? o : nullptr, st, nullptr));
+    if (n_splits > 1) CK(attn_combine_launch(a, nullptr, o, st, nullptr));
+  } else {
+    CK(attention_launch(a, 1, st, nullptr));
+    CK(attn_combine_launch(a, nullptr, o, st, nullptr));
+  }
   CK(cudaStreamSynchronize(st));
   return SPECEDGE_OK;
 }
