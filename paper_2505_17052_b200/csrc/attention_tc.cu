@@ -78,6 +78,12 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
       : "memory");
 }
 
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -213,22 +219,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the epilogue of the previous pair must have drained O before it is re-initialised
         for (int mi = 0; mi < nm; ++mi) mbar_wait(&o_empty[mi], (pr & 1) ^ 1);
         tc_fence_after();
-        for (int t = 0; t < ntiles; ++t) {
+        // S_m(t+1) is issued right behind PV_m(t) so that the softmax of tile t+1 for one M-tile
+        // overlaps the MMAs and softmax of the other (tcgen05.mma executes in issue order, so
+        // S_m(t+1) cannot overwrite P_m(t) before PV_m(t) has read it).
+        auto issue_qk = [&](int mi, uint32_t kaddr) {
+          const uint32_t qaddr = smem_u32(sQ + mi * QT_BYTES);
+          const uint32_t s_tm = tmem + mi * 256;
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16(s_tm, umma_desc_sw128(qaddr + kb * 16384 + k * 32), umma_desc_sw128(kaddr + kb * 16384 + k * 32),
+                         id_qk, (kb | k) != 0);
+          tc_commit(&s_full[mi]);
+        };
+        if (ntiles > 0) {
           mbar_wait(&kv_full[stage], phase);
           tc_fence_after();
-          const uint32_t kaddr = smem_u32(sK + stage * KT_BYTES);
+          for (int mi = 0; mi < nm; ++mi) issue_qk(mi, smem_u32(sK + stage * KT_BYTES));
+        }
+        for (int t = 0; t < ntiles; ++t) {
+          const int nstage = stage ^ 1;
+          const uint32_t nphase = phase ^ (stage == 1 ? 1u : 0u);
           const uint32_t vaddr = smem_u32(sV + stage * KT_BYTES);
-          for (int mi = 0; mi < nm; ++mi) {
-            const uint32_t qaddr = smem_u32(sQ + mi * QT_BYTES);
-            const uint32_t s_tm = tmem + mi * 256;
-#pragma unroll
-            for (int kb = 0; kb < KB; ++kb)
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                tc_mma_f16(s_tm, umma_desc_sw128(qaddr + kb * 16384 + k * 32), umma_desc_sw128(kaddr + kb * 16384 + k * 32),
-                           id_qk, (kb | k) != 0);
-            tc_commit(&s_full[mi]);
-          }
           for (int mi = 0; mi < nm; ++mi) {
             mbar_wait(&p_full[mi], sp_phase[mi]);
             sp_phase[mi] ^= 1;
@@ -242,9 +255,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_mma_ts(o_tm, pc, bd, id_pv, (t | k) != 0);       // P_hi
               tc_mma_ts(o_tm, pc + 16, bd, id_pv, 1);             // P_lo
             }
+            if (mi == nm - 1) tc_commit(&kv_empty[stage]);
+            if (t + 1 < ntiles) {
+              if (mi == 0) {
+                mbar_wait(&kv_full[nstage], nphase);
+                tc_fence_after();
+              }
+              issue_qk(mi, smem_u32(sK + nstage * KT_BYTES));
+            }
           }
-          tc_commit(&kv_empty[stage]);
-          if (++stage == 2) { stage = 0; phase ^= 1; }
+          stage = nstage;
+          phase = nphase;
         }
         for (int mi = 0; mi < nm; ++mi) tc_commit(&o_full[mi]);
         tc_commit(q_empty);
@@ -274,66 +295,81 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_phase ^= 1;
         tc_fence_after();
         const bool tree = t >= n_prefix_tiles;
-        // number of valid prefix keys in this tile
-        int kvalid = 0;
-        if (!tree) {
-          const int key0 = (p_begin + 2 * t) * 64;
-          kvalid = min(128, L - key0);
-          if (p_begin + 2 * t + 1 >= p_end) kvalid = min(kvalid, 64);
-        }
-        auto visible = [&](int key) -> bool {
-          if (!valid_row) return false;
-          if (!tree) return key < kvalid;
-          if (key >= S) return false;
-          return key == 0 || (slot > 0 && ((anc >> (key - 1)) & 1ull));
-        };
-        // pass 1: row max of this tile
-        float mx = -INFINITY;
+        // 128-bit visibility mask of this tile's keys for this row
+        uint32_t mk[4] = {0u, 0u, 0u, 0u};
+        if (valid_row) {
+          if (!tree) {
+            const int key0 = (p_begin + 2 * t) * 64;
+            int kvalid = min(128, L - key0);
+            if (p_begin + 2 * t + 1 >= p_end) kvalid = min(kvalid, 64);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(s_tm + c * 32, v);
-          tmem_ld_wait();
+            for (int w = 0; w < 4; ++w) {
+              const int n = kvalid - 32 * w;
+              mk[w] = n >= 32 ? 0xFFFFFFFFu : (n <= 0 ? 0u : ((1u << n) - 1u));
+            }
+          } else {
+            // key 0 = root, key k >= 1 = node k-1: visible iff root or ancestor-or-self of my node
+            const uint64_t lo = slot > 0 ? ((anc << 1) | 1ull) : 1ull;
+            mk[0] = (uint32_t)lo;
+            mk[1] = (uint32_t)(lo >> 32);
+            mk[2] = slot > 0 ? (uint32_t)(anc >> 63) : 0u;
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (visible(c * 32 + e)) mx = fmaxf(mx, __uint_as_float(v[e]) * sl2);
-        }
-        if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
-          const float alpha = m_used == -INFINITY ? 0.f : exp2f(m_used - mx);
-          if (t > 0 && m_used != -INFINITY) {
-            // rescale O (PV of the previous tile completed: s_full of this tile was committed after it)
-#pragma unroll
-            for (int c = 0; c < HD / 32; ++c) {
-              uint32_t ov[32];
-              tmem_ld_32x32b_x32(o_tm + c * 32, ov);
-              tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-              tmem_st_32x32b_x32(o_tm + c * 32, ov);
+            for (int w = 0; w < 4; ++w) {
+              const int n = S - 32 * w;
+              mk[w] &= n >= 32 ? 0xFFFFFFFFu : (n <= 0 ? 0u : ((1u << n) - 1u));
             }
           }
-          l *= alpha;
-          m_used = mx;
         }
-        const float mb = m_used == -INFINITY ? 0.f : m_used;
-        // pass 2: P = exp2(s*scale - m), split hi/lo, written over the S chunk it came from
+        const bool any_valid = __any_sync(0xffffffffu, (mk[0] | mk[1] | mk[2] | mk[3]) != 0u);
+        if (any_valid) {
+          // pass 1: row max of this tile
+          float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(s_tm + c * 32, v);
-          tmem_ld_wait();
-          uint32_t pk[32];
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(s_tm + c * 32, v);
+            tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const float p0 = visible(c * 32 + e) ? exp2f(__uint_as_float(v[e]) * sl2 - mb) : 0.f;
-            const float p1 = visible(c * 32 + e + 1) ? exp2f(__uint_as_float(v[e + 1]) * sl2 - mb) : 0.f;
-            l += p0 + p1;
-            const uint32_t hi = pack2(p0, p1);
-            const float h0 = __uint_as_float(hi << 16), h1 = __uint_as_float(hi & 0xFFFF0000u);
-            pk[e >> 1] = hi;
-            pk[16 + (e >> 1)] = pack2(p0 - h0, p1 - h1);
+            for (int e = 0; e < 32; ++e)
+              mx = fmaxf(mx, ((mk[c] >> e) & 1u) ? __uint_as_float(v[e]) : -INFINITY);
           }
-          tmem_st_32x32b_x32(s_tm + c * 32, pk);
+          mx *= sl2;
+          if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
+            const float alpha = m_used == -INFINITY ? 0.f : ex2f(m_used - mx);
+            if (t > 0 && m_used != -INFINITY) {
+              // rescale O (PV of tile t-1 completed: s_full of this tile was committed after it)
+#pragma unroll
+              for (int c = 0; c < HD / 32; ++c) {
+                uint32_t ov[32];
+                tmem_ld_32x32b_x32(o_tm + c * 32, ov);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+                tmem_st_32x32b_x32(o_tm + c * 32, ov);
+              }
+            }
+            l *= alpha;
+            m_used = mx;
+          }
+          const float mb = m_used == -INFINITY ? 0.f : m_used;
+          // pass 2: P = 2^(s*scale - m) split hi/lo, written over the S chunk it came from
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(s_tm + c * 32, v);
+            tmem_ld_wait();
+            uint32_t pk[32];
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const float p0 = ((mk[c] >> e) & 1u) ? ex2f(fmaf(__uint_as_float(v[e]), sl2, -mb)) : 0.f;
+              const float p1 = ((mk[c] >> (e + 1)) & 1u) ? ex2f(fmaf(__uint_as_float(v[e + 1]), sl2, -mb)) : 0.f;
+              l += p0 + p1;
+              const uint32_t hi = pack2(p0, p1);
+              pk[e >> 1] = hi;
+              pk[16 + (e >> 1)] = pack2(p0 - __uint_as_float(hi << 16), p1 - __uint_as_float(hi & 0xFFFF0000u));
+            }
+            tmem_st_32x32b_x32(s_tm + c * 32, pk);
+          }
         }
         tmem_st_wait();
         tc_fence_before();
