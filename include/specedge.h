@@ -94,7 +94,7 @@ specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t
                                       int32_t device, specedge_model** out);
 specedge_status specedge_model_destroy(specedge_model* model);
 
-/* KV page pool of `num_pages` pages x 64 tokens x all layers (bf16 K and V), zero-initialised,
+/* KV page pool of `num_pages` pages x 64 tokens x all layers (fp16 K and V), zero-initialised,
  * with room for `max_handles` sessions.  Synchronous. */
 specedge_status specedge_kvpool_create(specedge_model* model, int32_t num_pages,
                                        int32_t max_handles, specedge_kvpool** out);
@@ -113,7 +113,7 @@ specedge_status specedge_kv_set_len(specedge_kvpool* pool, const int32_t* handle
 specedge_status specedge_kv_get_len(specedge_kvpool* pool, const int32_t* handles, int32_t* lens,
                                     int32_t n);
 /* Fill positions [0, n_tokens) of a session with synthetic K/V (element =
- * bf16(int24 * 2^-23) from Philox keyed (seed, position, layer*2+kv, stream_id ^ 'KVFI')) and
+ * fp16(int24 * 2^-23) from Philox keyed (seed, position, layer*2+kv, stream_id ^ 'KVFI')) and
  * set its cached length to n_tokens.  Performance runs only; parity runs prefill for real. */
 specedge_status specedge_kv_fill_random(specedge_kvpool* pool, int32_t handle, int32_t n_tokens,
                                         uint64_t seed, uint32_t stream_id, void* stream);
@@ -194,8 +194,8 @@ specedge_status specedge_verify_batch_host(specedge_model* model, specedge_kvpoo
  * 12 g_final).  Synchronous. */
 specedge_status specedge_debug_weight_rows(specedge_model* model, int32_t tensor, int32_t layer,
                                            int32_t row0, int32_t nrows, uint16_t* dst_host);
-/* Cached K or V (kv_sel 0/1) of positions [pos0, pos0+n) of a session, layer `layer`, as bf16
- * bits [n][n_kv][head_dim] into host memory.  Synchronous. */
+/* Cached K or V (kv_sel 0/1) of positions [pos0, pos0+n) of a session, layer `layer`, as fp16
+ * bits [n][n_kv][head_dim] into host memory (the KV cache is fp16).  Synchronous. */
 specedge_status specedge_debug_read_kv(specedge_kvpool* pool, int32_t handle, int32_t layer,
                                        int32_t kv_sel, int32_t pos0, int32_t n,
                                        uint16_t* dst_host);
@@ -209,8 +209,8 @@ specedge_status specedge_debug_gemm(const uint16_t* W, const uint16_t* X, float*
 specedge_status specedge_debug_last_logits(specedge_model* model, void* workspace,
                                            size_t ws_bytes, int32_t num_requests, int32_t R,
                                            float* logits_dev, void* stream);
-/* Tree-masked attention kernel alone on caller data (all device): q [S][G][hd] bf16 for one
- * request and one kv head, prefix k/v [L][hd] bf16, tree k/v [S][hd] bf16, anc [S-1] uint64
+/* Tree-masked attention kernel alone on caller data (all device): q [S][G][hd] fp16 for one
+ * request and one kv head, prefix k/v [L][hd] fp16, tree k/v [S][hd] fp16, anc [S-1] uint64
  * (ancestor-or-self masks over nodes); writes o [S][G][hd] fp32 (normalised). */
 specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_prefix,
                                          const uint16_t* v_prefix, const uint16_t* k_tree,
@@ -229,8 +229,8 @@ int32_t specedge_last_launch_count(void);
  * events, adds their durations to per-kind totals and clears the pending list; out_ms[k] and
  * out_count[k] (arrays of SPECEDGE_KERNEL_KINDS) receive the totals since the last reset.
  * Kinds: 0 prep, 1 embed, 2 rmsnorm, 3 gemm_qkv, 4 attention, 5 attn_combine, 6 gemm_o,
- * 7 gemm_gateup, 8 gemm_down, 9 gemm_lmhead, 10 lm_reduce, 11 walk, 12 commit. */
-#define SPECEDGE_KERNEL_KINDS 13
+ * 7 gemm_gateup, 8 gemm_down, 9 gemm_lmhead, 10 lm_reduce, 11 walk, 12 commit, 13 qkv_rope. */
+#define SPECEDGE_KERNEL_KINDS 14
 specedge_status specedge_set_kernel_timing(int32_t enable);
 specedge_status specedge_kernel_times(float* out_ms, int32_t* out_count, int32_t reset);
 

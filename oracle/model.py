@@ -8,10 +8,12 @@ GQA attention -> O-proj + residual -> RMSNorm -> SwiGLU MLP + residual, final RM
 LM head, no biases, QK-norm off.
 
 Storage points (reading R-precision, revising SURVEY amb. A12): bf16 for weights,
-embeddings, the GEMM input operands inside the layers (normed h, q, O, M), cached K (post-RoPE)
-and V.  Unrounded: the residual stream x (the GPU keeps it in fp32) and the final-norm output
-(the GPU passes it to the LM head as a hi/lo pair of bf16 operands).  Rounding those two to bf16
-amplifies arithmetic-order noise past the north_star logit tolerance (measured).
+embeddings and the GEMM input operands (normed h, attention output O, MLP hidden M); fp16 for the
+attention operands q, k (post-RoPE) and v, hence the KV cache (so that softmax P can enter the PV
+product as fp16: P in bf16 breaks the 1e-3 attention tolerance).  Unrounded: the residual stream
+x (the GPU keeps it in fp32) and the final-norm output (the GPU passes it to the LM head as a
+hi/lo pair of bf16 operands); rounding those two amplifies arithmetic-order noise past the
+north_star logit tolerance (measured).
 
 Two independent ways of running it live here:
   * `tree_forward`   - SURVEY §8(c) O2: all S = N+1 slots of a draft tree at once; slot s
@@ -36,7 +38,7 @@ import math
 import numpy as np
 
 from . import philox
-from .numerics import bf16, rmsnorm, rope, silu, attention
+from .numerics import bf16, f16, rmsnorm, rope, silu, attention
 
 TENSOR_ID = dict(embed=1, wq=2, wk=3, wv=4, wo=5, wg=6, wu=7, wd=8, lm_head=9,
                  g_attn=10, g_mlp=11, g_final=12)
@@ -69,7 +71,7 @@ def gen_gain(seed, tensor, layer, d):
 
 def gen_kv_fill(seed, stream, layer, kv_sel, n_tok, n_kv, hd, tok_start=0):
     """Synthetic cached K or V rows (perf runs fill the prefix instead of
-    prefilling).  Element e = head*hd + j of token position t is bf16(f32(int24 * 2^-23)) in
+    prefilling).  Element e = head*hd + j of token position t is f16(f32(int24 * 2^-23)) in
     [-1, 1) from Philox counter (e >> 2, t, layer*2 + kv_sel, stream ^ 'KVFI'), word e & 3.
     Returns [n_tok, n_kv, hd]."""
     k0, k1 = philox.split_seed(seed)
@@ -80,7 +82,7 @@ def gen_kv_fill(seed, stream, layer, kv_sel, n_tok, n_kv, hd, tok_start=0):
     r = philox.philox4x32_10(c0, c1, (layer << 1) | kv_sel, stream ^ KVFILL_TAG, k0, k1)
     w = np.stack(r, axis=-1).reshape(n_tok, per_tok)
     v = _int24(w).astype(np.float32) * np.float32(2.0 ** -23)
-    return bf16(v.astype(np.float64)).reshape(n_tok, n_kv, hd)
+    return f16(v.astype(np.float64)).reshape(n_tok, n_kv, hd)
 
 
 class Weights:
@@ -146,7 +148,7 @@ def lm_logits(W: Weights, hf, block=16384, cache_full=True):
 
 
 # ----------------------------------------------------------------------------------------------
-# KV cache: per layer, K and V arrays [L, n_kv, hd] of bf16 values (post-RoPE K).
+# KV cache: per layer, K and V arrays [L, n_kv, hd] of fp16 values (post-RoPE K).
 # ----------------------------------------------------------------------------------------------
 class Cache:
     def __init__(self, shape):
@@ -175,9 +177,9 @@ def _qkv(W: Weights, l, x, pos):
     q = (h @ Lw["wq"].T).reshape(-1, s.n_heads, s.head_dim)
     k = (h @ Lw["wk"].T).reshape(-1, s.n_kv, s.head_dim)
     v = (h @ Lw["wv"].T).reshape(-1, s.n_kv, s.head_dim)
-    q = bf16(rope(q, pos, s.rope_theta))
-    k = bf16(rope(k, pos, s.rope_theta))
-    return q, k, bf16(v)
+    q = f16(rope(q, pos, s.rope_theta))
+    k = f16(rope(k, pos, s.rope_theta))
+    return q, k, f16(v)
 
 
 def _post_attn(W: Weights, l, x, o):

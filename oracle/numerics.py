@@ -1,9 +1,10 @@
 """Elementwise numerics of the target decoder, float64.
 
 Precision reading (DESIGN.md R-precision, revising SURVEY amb. A12; the paper states no precision
-anywhere, P:16/P:744 only quote marketing TFLOPS): bf16-valued are weights, embeddings, cached K
-(post-RoPE) and V, and the in-layer GEMM input operands (h, q, O, M); the residual stream and the
-final-norm output are not rounded.  `bf16` below rounds an exact (float64) value to the nearest bf16 value,
+anywhere, P:16/P:744 only quote marketing TFLOPS): bf16-valued are weights, embeddings and the
+GEMM input operands (normed h, attention output O, MLP hidden M); fp16-valued are the attention
+operands q, k (post-RoPE) and v, i.e. also the KV cache; the residual stream and the final-norm
+output are not rounded.  `bf16` below rounds an exact (float64) value to the nearest bf16 value,
 ties to even.  All other arithmetic is float64.
 """
 from __future__ import annotations
@@ -24,6 +25,18 @@ def bf16(x):
     spacing = np.ldexp(1.0, e)
     y = np.rint(x / spacing) * spacing
     y = np.where(np.abs(y) >= 2.0 ** 128, np.copysign(np.inf, x), y)   # overflow past bf16 max
+    return np.where(np.isfinite(x), y, x)
+
+
+def f16(x):
+    """Round to nearest IEEE binary16 (11 significant bits, subnormals below 2^-14), ties to even,
+    overflow to inf.  Same construction as `bf16`; pinned against numpy's float16 conversion."""
+    x = np.asarray(x, dtype=np.float64)
+    m, e = np.frexp(x)
+    e = np.maximum(e - 11, -24)
+    spacing = np.ldexp(1.0, e)
+    y = np.rint(x / spacing) * spacing
+    y = np.where(np.abs(y) >= 65520.0, np.copysign(np.inf, x), y)
     return np.where(np.isfinite(x), y, x)
 
 

@@ -27,7 +27,7 @@ EXPORTS = [
     "specedge_set_kernel_timing", "specedge_kernel_times",
 ]
 KERNEL_KINDS = ["prep", "embed", "rmsnorm", "gemm_qkv", "attention", "attn_combine", "gemm_o", "gemm_gateup",
-                "gemm_down", "gemm_lmhead", "lm_reduce", "walk", "commit"]
+                "gemm_down", "gemm_lmhead", "lm_reduce", "walk", "commit", "qkv_rope"]
 
 
 class ModelConfig(C.Structure):

@@ -6,8 +6,8 @@
 // from 64-token pages through the block table (split sp takes a contiguous page range), plus —
 // in the last split — the S tree slots of this step from the tree K/V scratch, where slot s sees
 // slot t iff t == 0 (root) or node t-1 is an ancestor-or-self of node s-1 (uint64 bitmask).
-// Scores fp32, online softmax in the log2 domain, P split hi+lo into two bf16 operands for the
-// PV product (P rounded to bf16 alone gives ~1.5e-3 relative error, SURVEY amb. A12).
+// Scores fp32, online softmax in the log2 domain; P enters the PV product as fp16 (q, k, v and the
+// KV cache are fp16, DESIGN.md R-precision; P in bf16 would give ~1.5e-3 relative error).
 // QK^T and PV use mma.sync m16n8k16 (16-row granularity suits the ragged S*G row counts);
 // K/V tiles are staged into XOR-swizzled shared memory with cp.async, double-buffered.
 // Partials (o, m, l) per split are merged by k_attn_combine.
@@ -46,30 +46,27 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
-__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void mma_f16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-__device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
-  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
-}
 
-// Load a [64 keys][HD] bf16 tile (rows beyond `valid` zero-filled) into swizzled smem.
+// Load a [64 keys][HD] fp16 tile (rows beyond `valid` zero-filled) into swizzled smem.
 template <int HD>
-__device__ __forceinline__ void load_tile(bf16* dst, const bf16* src, int valid, int tid, int nthreads) {
+__device__ __forceinline__ void load_tile(f16* dst, const f16* src, int valid, int tid, int nthreads) {
   constexpr int NCH = HD / 8;
   for (int i = tid; i < 64 * NCH; i += nthreads) {
     const int r = i / NCH, c = i % NCH;
     const bool ok = r < valid;
-    const bf16* s = ok ? src + (size_t)r * HD + c * 8 : src;
+    const f16* s = ok ? src + (size_t)r * HD + c * 8 : src;
     cp_async16(dst + r * HD + swz(r, c, NCH) * 8, s, ok);
   }
 }
@@ -81,10 +78,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   constexpr int KS = HD / 16;      // k16 steps over head dim
   constexpr int NT = HD / 8;       // n8 tiles over head dim
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  bf16* sQ = reinterpret_cast<bf16*>(smem_raw);                   // [max_rows_pad][HD]
+  f16* sQ = reinterpret_cast<f16*>(smem_raw);                     // [max_rows_pad][HD]
   const int rows_pad = (a.max_rows + 15) / 16 * 16;
-  bf16* sK = sQ + (size_t)rows_pad * HD;                          // [2][64][HD]
-  bf16* sV = sK + 2 * 64 * HD;                                    // [2][64][HD]
+  f16* sK = sQ + (size_t)rows_pad * HD;                           // [2][64][HD]
+  f16* sV = sK + 2 * 64 * HD;                                     // [2][64][HD]
   uint64_t* sAnc = reinterpret_cast<uint64_t*>(sV + 2 * 64 * HD); // [max_S]
 
   const int r = blockIdx.x / a.KV, g = blockIdx.x % a.KV, sp = blockIdx.y;
@@ -111,13 +108,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     const int qr = i / NCH, c = i % NCH;
     const int s = qr / G, j = qr % G;
     const bool ok = qr < rows;
-    const bf16* src = ok ? a.Q + (size_t)(row0 + s) * (a.H * HD) + (size_t)(g * G + j) * HD + c * 8 : a.Q;
+    const f16* src = ok ? a.Q + (size_t)(row0 + s) * (a.H * HD) + (size_t)(g * G + j) * HD + c * 8 : a.Q;
     cp_async16(sQ + qr * HD + swz(qr, c, NCH) * 8, src, ok);
   }
   for (int s = tid; s < S; s += nthreads) sAnc[s] = a.row_anc[row0 + s];
   cp_async_commit();
 
-  auto tile_src = [&](int t, const bf16*& ks, const bf16*& vs, int& valid, int& key0) {
+  auto tile_src = [&](int t, const f16*& ks, const f16*& vs, int& valid, int& key0) {
     if (t < n_prefix_tiles) {
       const int p = p_begin + t;
       const int page = a.block_table[(size_t)h * a.max_pages_per_seq + p];
@@ -138,7 +135,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   };
 
   if (ntiles > 0) {
-    const bf16 *ks, *vs;
+    const f16 *ks, *vs;
     int valid, key0;
     tile_src(0, ks, vs, valid, key0);
     load_tile<HD>(sK, ks, valid, tid, nthreads);
@@ -168,7 +165,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       // restart the K/V stream for the next row group
       __syncthreads();
       if (ntiles > 0) {
-        const bf16 *ks, *vs;
+        const f16 *ks, *vs;
         int valid, key0;
         tile_src(0, ks, vs, valid, key0);
         load_tile<HD>(sK, ks, valid, tid, nthreads);
@@ -180,7 +177,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     for (int t = 0; t < ntiles; ++t) {
       const int buf = t & 1;
       if (t + 1 < ntiles) {
-        const bf16 *ks, *vs;
+        const f16 *ks, *vs;
         int valid, key0;
         tile_src(t + 1, ks, vs, valid, key0);
         load_tile<HD>(sK + (buf ^ 1) * 64 * HD, ks, valid, tid, nthreads);
@@ -204,9 +201,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         if (s1 < S) anc1 = sAnc[s1];
       }
       if (active) {
-        const bf16* cK = sK + buf * 64 * HD;
-        const bf16* cV = sV + buf * 64 * HD;
-        const bf16 *ks_, *vs_;
+        const f16* cK = sK + buf * 64 * HD;
+        const f16* cV = sV + buf * 64 * HD;
+        const f16 *ks_, *vs_;
         int valid, key0;
         tile_src(t, ks_, vs_, valid, key0);
         // S = Q K^T : 16 rows x 64 keys
@@ -222,8 +219,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
             const int ch = ks * 2 + (mat & 1);
             uint32_t b0, b1, b2, b3;
             ldsm_x4(smem_u32(cK + kr * HD + swz(kr, ch, NCH) * 8), b0, b1, b2, b3);
-            mma_bf16(sc[np * 2], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b0, b1);
-            mma_bf16(sc[np * 2 + 1], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b2, b3);
+            mma_f16(sc[np * 2], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b0, b1);
+            mma_f16(sc[np * 2 + 1], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b2, b3);
           }
         }
         // mask + scale (log2 domain)
@@ -281,24 +278,14 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
           o[i][2] *= alpha[1];
           o[i][3] *= alpha[1];
         }
-        // O += P V with P = P_hi + P_lo (two bf16 operands)
+        // O += P V (P fp16)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          uint32_t ah[4], al[4];
-          {
-            const float* c0 = sc[2 * kk];
-            const float* c1 = sc[2 * kk + 1];
-            const float vals[8] = {c0[0], c0[1], c0[2], c0[3], c1[0], c1[1], c1[2], c1[3]};
-            // A regs: a0=(row,k0-1) a1=(row+8,k0-1) a2=(row,k8-9) a3=(row+8,k8-9)
-            const int idx[4][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7}};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float x0 = vals[idx[q][0]], x1 = vals[idx[q][1]];
-              ah[q] = pack_bf16(x0, x1);
-              const float2 hb = unpack_bf16(ah[q]);
-              al[q] = pack_bf16(x0 - hb.x, x1 - hb.y);
-            }
-          }
+          const float* c0 = sc[2 * kk];
+          const float* c1 = sc[2 * kk + 1];
+          // A regs: a0=(row,k0-1) a1=(row+8,k0-1) a2=(row,k8-9) a3=(row+8,k8-9)
+          const uint32_t a0 = pack_f16(c0[0], c0[1]), a1 = pack_f16(c0[2], c0[3]);
+          const uint32_t a2 = pack_f16(c1[0], c1[1]), a3 = pack_f16(c1[2], c1[3]);
 #pragma unroll
           for (int np = 0; np < NT / 2; ++np) {   // pairs of n8 dim tiles
             const int mat = lane >> 3, rr = lane & 7;
@@ -306,10 +293,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
             const int ch = np * 2 + (mat >> 1);
             uint32_t b0, b1, b2, b3;
             ldsm_x4_t(smem_u32(cV + kr * HD + swz(kr, ch, NCH) * 8), b0, b1, b2, b3);
-            mma_bf16(o[np * 2], ah[0], ah[1], ah[2], ah[3], b0, b1);
-            mma_bf16(o[np * 2], al[0], al[1], al[2], al[3], b0, b1);
-            mma_bf16(o[np * 2 + 1], ah[0], ah[1], ah[2], ah[3], b2, b3);
-            mma_bf16(o[np * 2 + 1], al[0], al[1], al[2], al[3], b2, b3);
+            mma_f16(o[np * 2], a0, a1, a2, a3, b0, b1);
+            mma_f16(o[np * 2 + 1], a0, a1, a2, a3, b2, b3);
           }
         }
       }

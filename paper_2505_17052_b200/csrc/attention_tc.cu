@@ -11,15 +11,16 @@
 //               page pool and the tree scratch), 2-stage ring
 //   warp 1      TMEM allocator + MMA issuer (one elected thread):
 //                 S_m  = Q_m K^T          kind::f16, A,B from smem (K-major), D fp32 in TMEM
-//                 O_m += P_m V            A = P from TMEM (hi and lo bf16 parts), B = V from smem
-//                                         (MN-major, 128B swizzle)
+//                 O_m += P_m V            A = P (fp16) from TMEM, B = V from smem (MN-major, 128B
+//                                         swizzle); q, k, v are fp16 (DESIGN.md R-precision)
 //   warps 2-5   softmax + epilogue of M-tile 0 (one thread = one query row: row max and sum
 //   warps 6-9   softmax + epilogue of M-tile 1   need no cross-thread reduction)
 //
 // Softmax in the log2 domain with a lazily updated running max (O is rescaled only when the max
-// grows by more than 8, exact because l uses the same max).  P is split P = P_hi + P_lo into two
-// bf16 operands, so PV carries ~16 bits of P (bf16 P alone gives ~1.5e-3 relative error,
-// SURVEY amb. A12).  TMEM: per M-tile 128 columns S (aliased by P) + HD columns O.
+// grows by more than 8, exact because l uses the same max).  P enters PV as fp16 (11-bit
+// significand: ~2e-4 relative error; bf16 P would give ~1.5e-3, SURVEY amb. A12).  The 128 scores
+// of a row stay in registers between the max and the exp pass.  TMEM: per M-tile 128 columns S
+// (P aliases its first 64) + HD columns O.
 #include "common.cuh"
 #include "internal.h"
 
@@ -44,8 +45,10 @@ __device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t smem_addr, uint3
   return d;
 }
 
-// kind::f16 idesc with B MN-major (bit 16)
-__device__ __forceinline__ uint32_t idesc_bmn(int M, int N) { return umma_idesc_bf16(M, N) | (1u << 16); }
+// kind::f16 instruction descriptor, A/B fp16 (format 0), D fp32, M x N; bmn: B MN-major (bit 16)
+__device__ __forceinline__ uint32_t idesc_f16(int M, int N, bool bmn) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24) | (bmn ? (1u << 16) : 0u);
+}
 
 __device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
@@ -57,6 +60,14 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -85,6 +96,10 @@ __device__ __forceinline__ float ex2f(float x) {
 }
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
@@ -208,8 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------------------- MMA issuer
     if (elect_one()) {
-      const uint32_t id_qk = umma_idesc_bf16(128, 128);
-      const uint32_t id_pv = idesc_bmn(128, HD);
+      const uint32_t id_qk = idesc_f16(128, 128, false);
+      const uint32_t id_pv = idesc_f16(128, HD, true);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t sp_phase[2] = {0, 0};
@@ -249,11 +264,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t p_tm = tmem + mi * 256;
             const uint32_t o_tm = tmem + mi * 256 + 128;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {   // 16 keys per k-step; P chunk c = k/2 at cols 32c
-              const uint32_t pc = p_tm + (k >> 1) * 32 + (k & 1) * 8;
+            for (int k = 0; k < 8; ++k) {   // 16 keys (8 packed fp16 columns) per k-step
               const uint64_t bd = umma_desc_mn_sw128(vaddr + k * 2048, 128 * 128);
-              tc_mma_ts(o_tm, pc, bd, id_pv, (t | k) != 0);       // P_hi
-              tc_mma_ts(o_tm, pc + 16, bd, id_pv, 1);             // P_lo
+              tc_mma_ts(o_tm, p_tm + k * 8, bd, id_pv, (t | k) != 0);
             }
             if (mi == nm - 1) tc_commit(&kv_empty[stage]);
             if (t + 1 < ntiles) {
@@ -322,53 +335,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const bool any_valid = __any_sync(0xffffffffu, (mk[0] | mk[1] | mk[2] | mk[3]) != 0u);
         if (any_valid) {
-          // pass 1: row max of this tile
+          // the whole row of 128 scores in registers
+          uint32_t sv[128];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_tm + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * c));
+          tmem_ld_wait();
+          const bool full = __all_sync(0xffffffffu, (mk[0] & mk[1] & mk[2] & mk[3]) == 0xFFFFFFFFu);
           float mx = -INFINITY;
+          if (full) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(s_tm + c * 32, v);
-            tmem_ld_wait();
+            for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
+          } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e)
-              mx = fmaxf(mx, ((mk[c] >> e) & 1u) ? __uint_as_float(v[e]) : -INFINITY);
+            for (int e = 0; e < 128; ++e)
+              mx = fmaxf(mx, ((mk[e >> 5] >> (e & 31)) & 1u) ? __uint_as_float(sv[e]) : -INFINITY);
           }
           mx *= sl2;
+          float alpha = 1.f;
+          bool rescale = false;
           if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
-            const float alpha = m_used == -INFINITY ? 0.f : ex2f(m_used - mx);
-            if (t > 0 && m_used != -INFINITY) {
-              // rescale O (PV of tile t-1 completed: s_full of this tile was committed after it)
-#pragma unroll
-              for (int c = 0; c < HD / 32; ++c) {
-                uint32_t ov[32];
-                tmem_ld_32x32b_x32(o_tm + c * 32, ov);
-                tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-                tmem_st_32x32b_x32(o_tm + c * 32, ov);
-              }
-            }
+            alpha = m_used == -INFINITY ? 0.f : ex2f(m_used - mx);
+            rescale = t > 0 && m_used != -INFINITY;
             l *= alpha;
             m_used = mx;
           }
           const float mb = m_used == -INFINITY ? 0.f : m_used;
-          // pass 2: P = 2^(s*scale - m) split hi/lo, written over the S chunk it came from
+          // P = 2^(s*scale - m) as packed fp16 pairs into the first 64 columns of this S region,
+          // 32 keys (16 columns) at a time (column 16c <= 32c: never overwrites unread scores)
+          float ls = 0.f;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(s_tm + c * 32, v);
-            tmem_ld_wait();
-            uint32_t pk[32];
+            uint32_t pk[16];
+            if (full) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const float p0 = ((mk[c] >> e) & 1u) ? ex2f(fmaf(__uint_as_float(v[e]), sl2, -mb)) : 0.f;
-              const float p1 = ((mk[c] >> (e + 1)) & 1u) ? ex2f(fmaf(__uint_as_float(v[e + 1]), sl2, -mb)) : 0.f;
-              l += p0 + p1;
-              const uint32_t hi = pack2(p0, p1);
-              pk[e >> 1] = hi;
-              pk[16 + (e >> 1)] = pack2(p0 - __uint_as_float(hi << 16), p1 - __uint_as_float(hi & 0xFFFF0000u));
+              for (int e = 0; e < 32; e += 2) {
+                const float p0 = ex2f(fmaf(__uint_as_float(sv[32 * c + e]), sl2, -mb));
+                const float p1 = ex2f(fmaf(__uint_as_float(sv[32 * c + e + 1]), sl2, -mb));
+                ls += p0 + p1;
+                pk[e >> 1] = pack2(p0, p1);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                const float p0 = ((mk[c] >> e) & 1u) ? ex2f(fmaf(__uint_as_float(sv[32 * c + e]), sl2, -mb)) : 0.f;
+                const float p1 = ((mk[c] >> (e + 1)) & 1u) ? ex2f(fmaf(__uint_as_float(sv[32 * c + e + 1]), sl2, -mb)) : 0.f;
+                ls += p0 + p1;
+                pk[e >> 1] = pack2(p0, p1);
+              }
             }
-            tmem_st_32x32b_x32(s_tm + c * 32, pk);
+            tmem_st_32x32b_x16(s_tm + 16 * c, pk);
+          }
+          l += ls;
+          if (rescale) {
+            // O *= alpha before PV of this tile (PV of tile t-1 is complete: s_full of this tile
+            // was committed after it)
+#pragma unroll 1
+            for (int c = 0; c < HD / 32; ++c) {
+              uint32_t ov[32];
+              tmem_ld_32x32b_x32(o_tm + c * 32, ov);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+              tmem_st_32x32b_x32(o_tm + c * 32, ov);
+            }
           }
         }
         tmem_st_wait();
@@ -392,10 +421,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint4* dst = reinterpret_cast<uint4*>(ta.O + rh * HD + c * 32);
 #pragma unroll
               for (int e = 0; e < 32; e += 8)
-                dst[e / 8] = make_uint4(pack2(__uint_as_float(ov[e]) * inv, __uint_as_float(ov[e + 1]) * inv),
-                                        pack2(__uint_as_float(ov[e + 2]) * inv, __uint_as_float(ov[e + 3]) * inv),
-                                        pack2(__uint_as_float(ov[e + 4]) * inv, __uint_as_float(ov[e + 5]) * inv),
-                                        pack2(__uint_as_float(ov[e + 6]) * inv, __uint_as_float(ov[e + 7]) * inv));
+                dst[e / 8] = make_uint4(pack2_bf16(__uint_as_float(ov[e]) * inv, __uint_as_float(ov[e + 1]) * inv),
+                                        pack2_bf16(__uint_as_float(ov[e + 2]) * inv, __uint_as_float(ov[e + 3]) * inv),
+                                        pack2_bf16(__uint_as_float(ov[e + 4]) * inv, __uint_as_float(ov[e + 5]) * inv),
+                                        pack2_bf16(__uint_as_float(ov[e + 6]) * inv, __uint_as_float(ov[e + 7]) * inv));
             }
             if (ta.O_f32) {
               float4* dst = reinterpret_cast<float4*>(ta.O_f32 + rh * HD + c * 32);
@@ -448,7 +477,7 @@ bool tmap_rows(CUtensorMap* m, const void* base, uint64_t rows, int hd) {
   cuuint64_t strides[1] = {(cuuint64_t)hd * 2};
   cuuint32_t box[2] = {64, 64};
   cuuint32_t estr[2] = {1, 1};
-  return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -458,7 +487,7 @@ bool tmap_q(CUtensorMap* m, const void* base, uint64_t R, int H, int hd, int G, 
   cuuint64_t strides[2] = {(cuuint64_t)hd * 2, (cuuint64_t)H * hd * 2};
   cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)spm};
   cuuint32_t estr[3] = {1, 1, 1};
-  return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+  return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

@@ -1,6 +1,8 @@
 // tcgen05 / TMEM / TMA GEMM with fused epilogues for the verify step's dense contractions
-// (QKV + RoPE + tree K/V write, O-proj + residual, gate/up + SwiGLU,
-// down + residual, LM head + vocab argmax / Gumbel-max).  P:173 ("a single forward pass" over
+// (QKV, O-proj, gate/up + SwiGLU, down, LM head + vocab argmax /
+// Gumbel-max).  QKV / O / down store fp32 per-K-split partials; RoPE + K/V scatter and the residual
+// add are applied by the following elementwise kernels (kernels_small.cu), which sum the splits in
+// a fixed order (deterministic).  P:173 ("a single forward pass" over
 // all draft tokens) makes these weight-streaming GEMMs with N = R rows of the whole batch.
 //
 // Orientation ("swap-AB"): D^T[feature][row] = W[feature][:] . X[row][:].  Weights take the
@@ -97,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int ntiles = a.n_tiles_m * a.n_tiles_n;
+  const int nunits = ntiles * a.splits;   // work unit = (tile, K split)
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
@@ -105,9 +108,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_x = policy_evict_last();   // activations: re-read by every m tile
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int t = u / a.splits, sk = u % a.splits;
         const int m = t / a.n_tiles_n, n = t % a.n_tiles_n;
-        for (int kb = 0; kb < a.num_kb; ++kb) {
+        const int kb0 = sk * a.kb_per_split, kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], kABytes + b_bytes);
           tma_load_2d_hint(sA + stage * kABytes, &tmA, &full[stage], kb * 64, m * 128, pol_w);
@@ -123,13 +128,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+        const int sk = u % a.splits;
+        const int kb0 = sk * a.kb_per_split, kb1 = min(a.num_kb, kb0 + a.kb_per_split);
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < a.num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * kABytes);
@@ -137,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             tc_mma_f16(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32),
-                       idesc, (kb | k) != 0);
+                       idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           tc_commit(&empty[stage]);
           if (++stage == S) { stage = 0; phase ^= 1; }
@@ -151,7 +158,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tl = q * 32 + lane;      // tile-local feature (TMEM lane)
     const int et = threadIdx.x - 64;   // 0..127 epilogue thread id
     int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+      const int t = u / a.splits, sk = u % a.splits;
       const int m = t / a.n_tiles_n, n = t % a.n_tiles_n;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
@@ -175,26 +183,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                   a.out_f32[(size_t)(row >> 1) * a.ldo + feat] = __uint_as_float(v[j]) + __uint_as_float(v[j + 1]);
               }
             } else {
+              float* out = a.out_f32 + (size_t)sk * a.split_stride;   // K-split sk's partial
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
                 const int row = row_base + j;
-                if (j < ncol && row < a.R) a.out_f32[(size_t)row * a.ldo + feat] = __uint_as_float(v[j]);
+                if (j < ncol && row < a.R) out[(size_t)row * a.ldo + feat] = __uint_as_float(v[j]);
               }
-            }
-          }
-        } else if constexpr (MODE == EPI_RESID) {
-          if (feat < a.M) {
-            // all 32 residual loads in flight before the first store (no load->store chains)
-            float old[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int row = row_base + j;
-              old[j] = (j < ncol && row < a.R) ? __ldcg(a.out_f32 + (size_t)row * a.ldo + feat) : 0.f;
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int row = row_base + j;
-              if (j < ncol && row < a.R) a.out_f32[(size_t)row * a.ldo + feat] = old[j] + __uint_as_float(v[j]);
             }
           }
         } else if constexpr (MODE == EPI_SWIGLU) {
@@ -211,51 +205,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j < ncol && row < a.R && fo < a.M / 2) {
               const float g = xch[f * kXchStride + j], u = xch[(f + 64) * kXchStride + j];
               a.out_bf16[(size_t)row * a.ld_out + fo] = __float2bfloat16_rn(silu_f(g) * u);
-            }
-          }
-          named_bar_sync(1, kEpiThreads);
-        } else if constexpr (MODE == EPI_QKV) {
-          int* s_pos = red_i;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
-          if (et < 32) s_pos[et] = (row_base + et < a.R) ? __ldg(a.row_pos + row_base + et) : 0;
-          named_bar_sync(1, kEpiThreads);
-          const int hd = a.head_dim, half_hd = hd >> 1;
-          const int qd = a.n_heads * hd, kd = a.n_kv * hd;
-          if (feat < a.M) {
-            const int dim = feat % hd;
-            const bool rot = feat < qd + kd;
-            const bool lo = dim < half_hd;
-            const int partner = tl + (lo ? half_hd : -half_hd);
-            const int fi = dim % half_hd;
-            uint16_t outv[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              float x = __uint_as_float(v[j]);
-              if (rot) {
-                const size_t ti = (size_t)s_pos[j] * half_hd + fi;
-                const float cs = __ldg(a.rope_cos + ti), sn = __ldg(a.rope_sin + ti);
-                const float xp = xch[partner * kXchStride + j];
-                x = lo ? (x * cs - xp * sn) : (x * cs + xp * sn);
-              }
-              outv[j] = f32_to_bf16_bits(x);
-            }
-            uint16_t* dst;
-            size_t stride;
-            if (feat < qd) {
-              dst = reinterpret_cast<uint16_t*>(a.out_bf16) + feat;
-              stride = a.ld_out;
-            } else {
-              const int kvsel = feat < qd + kd ? 0 : 1;
-              const int kvh = (feat - qd - kvsel * kd) / hd;
-              dst = reinterpret_cast<uint16_t*>(a.tree_kv) +
-                    ((((size_t)a.layer * 2 + kvsel) * a.n_kv + kvh) * a.R_cap) * hd + dim;
-              stride = hd;
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int row = row_base + j;
-              if (j < ncol && row < a.R) dst[(size_t)row * stride] = outv[j];
             }
           }
           named_bar_sync(1, kEpiThreads);
@@ -348,6 +297,7 @@ PFN_encodeTiled get_encode() {
 }
 
 int g_num_sms = 0;
+thread_local int g_last_splits = 1;
 
 template <int MODE>
 cudaError_t launch_mode(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmArgs& a,
@@ -377,6 +327,8 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+int gemm_splits_last() { return g_last_splits; }
 
 int gemm_pick_bn(int R) {
   const int nt = (R + 255) / 256;
@@ -408,12 +360,21 @@ cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArg
   CUtensorMap tmX;
   if (!make_tmap_2d(&tmX, X, (uint64_t)a.R, (uint64_t)a.K, (uint32_t)a.BN)) return cudaErrorInvalidValue;
   const int ntiles = a.n_tiles_m * a.n_tiles_n;
-  const int grid = std::min(ntiles, g_num_sms);
+  // K-split (EPI_F32 only, caller provides max_splits slices of split_stride floats): give every
+  // CTA >= 2 units so the epilogue of one overlaps the MMAs of the next, and fill the SMs.
+  a.splits = 1;
+  if (mode == EPI_F32 && !a.pair && a.max_splits > 1 && ntiles < g_num_sms * 3 / 2) {
+    int sp = (2 * g_num_sms + ntiles / 2) / ntiles;
+    sp = std::min(sp, a.max_splits);
+    while (sp > 1 && a.num_kb / sp < 8) --sp;
+    a.splits = std::max(1, sp);
+  }
+  a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
+  g_last_splits = a.splits;
+  const int grid = std::min(ntiles * a.splits, g_num_sms);
   if (launches) ++*launches;
   switch (mode) {
     case EPI_F32: return launch_mode<EPI_F32>(tmW, tmX, a, smem, grid, st);
-    case EPI_QKV: return launch_mode<EPI_QKV>(tmW, tmX, a, smem, grid, st);
-    case EPI_RESID: return launch_mode<EPI_RESID>(tmW, tmX, a, smem, grid, st);
     case EPI_SWIGLU: return launch_mode<EPI_SWIGLU>(tmW, tmX, a, smem, grid, st);
     case EPI_ARGMAX: return launch_mode<EPI_ARGMAX>(tmW, tmX, a, smem, grid, st);
   }

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 #include <stddef.h>
 #include <vector>
@@ -13,14 +14,13 @@
 namespace se {
 
 using bf16 = __nv_bfloat16;
+using f16 = __half;   // attention operands q, k, v and the KV cache
 
 // ---------------------------------------------------------------------------------------------
 // GEMM (tcgen05, swap-AB: weights are the MMA's M side, activation rows its N side)
 // ---------------------------------------------------------------------------------------------
 enum GemmMode : int {
-  EPI_F32 = 0,     // out_f32[row][m] = acc                       (tests, logits capture)
-  EPI_QKV = 1,     // RoPE(q,k) -> Q[row][..], tree K/V scratch   (a4)
-  EPI_RESID = 2,   // X[row][m] += acc (fp32 residual stream)     (a6, a8)
+  EPI_F32 = 0,     // out_f32[split][row][m] = partial acc (a4 QKV, a6 O, a8 down; logits capture)
   EPI_SWIGLU = 3,  // M[row][f] = bf16(silu(gate) * up)            (a7)
   EPI_ARGMAX = 4,  // per (row, 128-vocab tile) max / Gumbel-max   (a9)
 };
@@ -29,6 +29,8 @@ struct GemmArgs {
   int M, R, K;            // weight rows (features), activation rows, reduction length
   int BN, n_tiles_n, n_tiles_m, num_kb, stages, tmem_cols;
   int pair;               // EPI_F32/EPI_ARGMAX: rows (2r, 2r+1) are hi/lo bf16 parts of row r
+  int splits, kb_per_split, max_splits;   // K-split (EPI_F32): slice sk at out_f32 + sk*split_stride
+  size_t split_stride;
   // EPI_F32 / EPI_RESID (fp32 residual stream)
   float* out_f32;
   int ldo;
@@ -56,6 +58,7 @@ struct GemmArgs {
 // Build a 2D bf16 tensor map [rows][cols] (cols contiguous), box {64, box_rows}, 128B swizzle.
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 int gemm_pick_bn(int R);
+int gemm_splits_last();   // K-splits chosen by the last gemm_launch on this thread
 cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArgs a,
                         cudaStream_t st, int* launches);
 
@@ -63,11 +66,11 @@ cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArg
 // Attention (tree-masked, paged, split-KV)
 // ---------------------------------------------------------------------------------------------
 struct AttnArgs {
-  const bf16* Q;              // [R][H*hd]
-  const bf16* pool;           // [layers][num_pages][2][KV][64][hd]
+  const f16* Q;               // [R][H*hd]
+  const f16* pool;            // [layers][num_pages][2][KV][64][hd]
   const int* block_table;     // [max_handles][max_pages_per_seq]
   int max_pages_per_seq, num_pages;
-  const bf16* tree_kv;        // [layers][2][KV][R_cap][hd]
+  const f16* tree_kv;         // [layers][2][KV][R_cap][hd]
   int R_cap, layer, H, KV, G, hd;
   const int* req_L;
   const int* req_h;
@@ -119,8 +122,24 @@ struct PrepArgs {
 cudaError_t prep_launch(const PrepArgs& p, cudaStream_t st, int* launches);
 cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int d, cudaStream_t st,
                          int* launches);
-cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* out, int R, int d, float eps,
-                           cudaStream_t st, int* launches, int split = 0);
+// x = X + sum_s Y[s] (s < nY, fixed order; X updated in place), out = bf16(rmsnorm(x) * g);
+// split = 1 writes out as hi/lo bf16 row pairs (LM-head input).
+cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, const bf16* g, bf16* out,
+                           int R, int d, float eps, cudaStream_t st, int* launches, int split = 0);
+// Q / tree K/V from the QKV GEMM's fp32 split partials: sum splits, RoPE(q, k) at row_pos,
+// bf16 round, scatter
+struct RopeArgs {
+  const float* Y;
+  int nY;
+  size_t y_stride;
+  int R, H, KV, hd, layer, R_cap;
+  const int* row_pos;
+  const float* rope_cos;
+  const float* rope_sin;
+  f16* Q;
+  f16* tree_kv;
+};
+cudaError_t qkv_rope_launch(const RopeArgs& r, cudaStream_t st, int* launches);
 cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, int* y, float* score,
                              int* row_target, float* row_score, cudaStream_t st, int* launches);
 struct WalkArgs {
@@ -145,8 +164,8 @@ struct CommitArgs {
   const int* node_offset;
   const int* accepted_len;
   const int* accepted_node;
-  const bf16* tree_kv;
-  bf16* pool;
+  const f16* tree_kv;
+  f16* pool;
   const int* block_table;
   int* cache_len;
 };
@@ -166,7 +185,7 @@ struct InitArgs {
   uint32_t k0, k1;
 };
 cudaError_t init_weights_launch(const InitArgs& a, cudaStream_t st);
-cudaError_t kv_fill_launch(bf16* pool, const int* block_row, int layers, int num_pages, int KV,
+cudaError_t kv_fill_launch(f16* pool, const int* block_row, int layers, int num_pages, int KV,
                            int hd, int n_tokens, uint32_t k0, uint32_t k1, uint32_t stream_id,
                            cudaStream_t st);
 
@@ -197,7 +216,7 @@ struct specedge_model {
 struct specedge_kvpool {
   specedge_model* model;
   int num_pages, max_handles, max_pages_per_seq;
-  se::bf16* pages = nullptr;
+  se::f16* pages = nullptr;     // [layers][num_pages][2][KV][64][hd] fp16
   int* block_table = nullptr;   // device [max_handles][max_pages_per_seq]
   int* cache_len = nullptr;     // device [max_handles]
   int* capacity = nullptr;      // device [max_handles] (0 = free handle)

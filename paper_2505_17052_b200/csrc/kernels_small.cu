@@ -122,52 +122,127 @@ __global__ void k_embed(const bf16* __restrict__ E, const int* __restrict__ row_
 }
 
 // --------------------------------------------------------------------------------- K3 RMSNorm
-// out = bf16(x * rsqrt(mean(x^2) + eps) * g), x fp32 (amb. A13).
-// split = 1 (final norm feeding the LM head): y is written as two bf16 rows, hi = bf16(y) at
-// out row 2r and lo = bf16(y - hi) at row 2r+1, so hi + lo carries y to ~2^-17 relative.
-__global__ void k_rmsnorm(const float* __restrict__ X, const bf16* __restrict__ g, bf16* __restrict__ out,
-                          int d, float eps, int split) {
+// Residual add + RMSNorm (amb. A13): x = X + Y[0] + ... + Y[nY-1] (the O-proj / down GEMM's K-split
+// partials, summed in this fixed order), X = x (fp32 residual stream), out = bf16(x * rsqrt(mean(x^2)
+// + eps) * g).  split = 1 (final norm feeding the LM head): y is written as two bf16 rows, hi =
+// bf16(y) at out row 2r and lo = bf16(y - hi) at row 2r+1, so hi + lo carries y to ~2^-17.
+template <int NY>
+__global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const float* __restrict__ Y, size_t y_stride,
+                                                  const bf16* __restrict__ g, bf16* __restrict__ out, int d, float eps,
+                                                  int split) {
+  // blockDim.x = d / 16: each thread owns 16 consecutive elements, kept in registers across passes
   const int row = blockIdx.x;
-  const float* x = X + (size_t)row * d;
+  const int i = threadIdx.x * 16;
+  float* x = X + (size_t)row * d + i;
   __shared__ float red[32];
-  float ss = 0.f;
-  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
-    const float4 a = *reinterpret_cast<const float4*>(x + i);
-    const float4 b = *reinterpret_cast<const float4*>(x + i + 4);
-    ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w + b.x * b.x + b.y * b.y + b.z * b.z + b.w * b.w;
-  }
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
-    if (threadIdx.x == 0) red[0] = v;
-  }
-  __syncthreads();
-  const float inv = rsqrtf(red[0] / (float)d + eps);
-  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
-    const float4 a = *reinterpret_cast<const float4*>(x + i);
-    const float4 b = *reinterpret_cast<const float4*>(x + i + 4);
-    const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    const uint4 gu = *reinterpret_cast<const uint4*>(g + i);
-    const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
-    uint32_t o[4], r[4];
+  float xv[16];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float y0 = xv[2 * k] * inv * __uint_as_float(gw[k] << 16);
-      const float y1 = xv[2 * k + 1] * inv * __uint_as_float(gw[k] & 0xFFFF0000u);
-      __nv_bfloat162 p = __floats2bfloat162_rn(y0, y1);
-      o[k] = *reinterpret_cast<uint32_t*>(&p);
-      const float h0 = __uint_as_float(o[k] << 16), h1 = __uint_as_float(o[k] & 0xFFFF0000u);
-      __nv_bfloat162 q = __floats2bfloat162_rn(y0 - h0, y1 - h1);
-      r[k] = *reinterpret_cast<uint32_t*>(&q);
+  for (int k = 0; k < 4; ++k) {
+    const float4 a = *reinterpret_cast<const float4*>(x + 4 * k);
+    xv[4 * k] = a.x; xv[4 * k + 1] = a.y; xv[4 * k + 2] = a.z; xv[4 * k + 3] = a.w;
+  }
+  if constexpr (NY > 0) {
+    float4 yv[NY][4];
+#pragma unroll
+    for (int s = 0; s < NY; ++s)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        yv[s][k] = __ldcs(reinterpret_cast<const float4*>(Y + s * y_stride + (size_t)row * d + i + 4 * k));
+#pragma unroll
+    for (int s = 0; s < NY; ++s)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        xv[4 * k] += yv[s][k].x; xv[4 * k + 1] += yv[s][k].y; xv[4 * k + 2] += yv[s][k].z; xv[4 * k + 3] += yv[s][k].w;
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<float4*>(x + 4 * k) = make_float4(xv[4 * k], xv[4 * k + 1], xv[4 * k + 2], xv[4 * k + 3]);
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) ss += xv[k] * xv[k];
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o, 32);
+  const int nw = (blockDim.x + 31) >> 5;
+  if (nw > 1) {
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float v = threadIdx.x < nw ? red[threadIdx.x] : 0.f;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+      if (threadIdx.x == 0) red[0] = v;
     }
-    if (split) {
-      *reinterpret_cast<uint4*>(out + (size_t)(2 * row) * d + i) = make_uint4(o[0], o[1], o[2], o[3]);
-      *reinterpret_cast<uint4*>(out + (size_t)(2 * row + 1) * d + i) = make_uint4(r[0], r[1], r[2], r[3]);
+    __syncthreads();
+    ss = red[0];
+  }
+  const float inv = rsqrtf(ss / (float)d + eps);
+  const uint4* gp = reinterpret_cast<const uint4*>(g + i);
+  uint32_t o[8], r[8];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint4 gu = gp[k];
+    const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float y0 = xv[8 * k + 2 * q] * inv * __uint_as_float(gw[q] << 16);
+      const float y1 = xv[8 * k + 2 * q + 1] * inv * __uint_as_float(gw[q] & 0xFFFF0000u);
+      __nv_bfloat162 p = __floats2bfloat162_rn(y0, y1);
+      o[4 * k + q] = *reinterpret_cast<uint32_t*>(&p);
+      const float h0 = __uint_as_float(o[4 * k + q] << 16), h1 = __uint_as_float(o[4 * k + q] & 0xFFFF0000u);
+      __nv_bfloat162 pq = __floats2bfloat162_rn(y0 - h0, y1 - h1);
+      r[4 * k + q] = *reinterpret_cast<uint32_t*>(&pq);
+    }
+  }
+  if (split) {
+    uint4* dh = reinterpret_cast<uint4*>(out + (size_t)(2 * row) * d + i);
+    uint4* dl = reinterpret_cast<uint4*>(out + (size_t)(2 * row + 1) * d + i);
+    dh[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    dh[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    dl[0] = make_uint4(r[0], r[1], r[2], r[3]);
+    dl[1] = make_uint4(r[4], r[5], r[6], r[7]);
+  } else {
+    uint4* dh = reinterpret_cast<uint4*>(out + (size_t)row * d + i);
+    dh[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    dh[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+
+// ------------------------------------------------------------------------- K4b QKV RoPE/scatter
+// One CTA per row.  Work item e < (H+KV)*hd/2: rotate-half pair (i, i+hd/2) of q head (or k head)
+// e / (hd/2) at position row_pos (amb. A14); e >= that: one v element.  Splits summed in order.
+__global__ void k_qkv_rope(const __grid_constant__ RopeArgs r) {
+  const int row = blockIdx.y;
+  const int hd = r.hd, half = hd >> 1;
+  const int qkv = (r.H + 2 * r.KV) * hd;
+  const int npair = (r.H + r.KV) * half;
+  const int pos = r.row_pos[row];
+  const float* y = r.Y + (size_t)row * qkv;
+  auto ysum = [&](int f) {
+    float v = y[f];
+    for (int s = 1; s < r.nY; ++s) v += y[s * r.y_stride + f];
+    return v;
+  };
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npair + r.KV * hd; e += gridDim.x * blockDim.x) {
+    if (e < npair) {
+      const int head = e / half, i = e % half;
+      const int f1 = head * hd + i;
+      const float x1 = ysum(f1), x2 = ysum(f1 + half);
+      const float cs = r.rope_cos[(size_t)pos * half + i], sn = r.rope_sin[(size_t)pos * half + i];
+      const f16 o1 = __float2half_rn(x1 * cs - x2 * sn);
+      const f16 o2 = __float2half_rn(x2 * cs + x1 * sn);
+      if (head < r.H) {
+        r.Q[(size_t)row * r.H * hd + f1] = o1;
+        r.Q[(size_t)row * r.H * hd + f1 + half] = o2;
+      } else {
+        const int kvh = head - r.H;
+        f16* dst = r.tree_kv + ((((size_t)r.layer * 2 + 0) * r.KV + kvh) * r.R_cap + row) * hd;
+        dst[i] = o1;
+        dst[i + half] = o2;
+      }
     } else {
-      *reinterpret_cast<uint4*>(out + (size_t)row * d + i) = make_uint4(o[0], o[1], o[2], o[3]);
+      const int ve = e - npair;
+      const int kvh = ve / hd, dd = ve % hd;
+      const float x = ysum((r.H + r.KV) * hd + ve);
+      r.tree_kv[((((size_t)r.layer * 2 + 1) * r.KV + kvh) * r.R_cap + row) * hd + dd] = __float2half_rn(x);
     }
   }
 }
@@ -338,7 +413,7 @@ __global__ void k_init_weights(const __grid_constant__ InitArgs a) {
 
 // ---------------------------------------------------------------------- K13 synthetic KV
 // element e = head*hd + j of token t: Philox counter (e>>2, t, layer*2 + kv, stream ^ 'KVFI').
-__global__ void k_kv_fill(bf16* pool, const int* __restrict__ block_row, int layers, int num_pages, int KV,
+__global__ void k_kv_fill(f16* pool, const int* __restrict__ block_row, int layers, int num_pages, int KV,
                           int hd, int n_tokens, uint32_t k0, uint32_t k1, uint32_t stream_id) {
   const int per_tok4 = KV * hd / 4;
   const long long total = (long long)n_tokens * layers * 2 * per_tok4;
@@ -354,7 +429,7 @@ __global__ void k_kv_fill(bf16* pool, const int* __restrict__ block_row, int lay
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
     uint16_t out[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) out[k] = f32_to_bf16_bits(__fmul_rn(philox_i24(w[k]), 1.1920928955078125e-07f));
+    for (int k = 0; k < 4; ++k) out[k] = __half_as_ushort(__float2half_rn(__fmul_rn(philox_i24(w[k]), 1.1920928955078125e-07f)));
     const int e = e4 * 4;
     const int g = e / hd, j = e % hd;
     const int page = block_row[t / kPage];
@@ -378,11 +453,24 @@ cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int
   k_embed<<<R, 128, 0, st>>>(E, row_tok, X, d);
   return cudaGetLastError();
 }
-cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* out, int R, int d, float eps, cudaStream_t st,
-                           int* launches, int split) {
+cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, const bf16* g, bf16* out, int R, int d,
+                           float eps, cudaStream_t st, int* launches, int split) {
   if (launches) ++*launches;
-  const int threads = d >= 2048 ? 256 : (d >= 512 ? 64 : 32);
-  k_rmsnorm<<<R, threads, 0, st>>>(X, g, out, d, eps, split);
+  const int threads = d / 16;   // d % 64 == 0 (checked at model creation), <= 1024
+  switch (nY) {
+    case 0: k_rmsnorm<0><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
+    case 1: k_rmsnorm<1><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
+    case 2: k_rmsnorm<2><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
+    case 3: k_rmsnorm<3><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
+    case 4: k_rmsnorm<4><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+cudaError_t qkv_rope_launch(const RopeArgs& r, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  const int items = (r.H + r.KV) * (r.hd / 2) + r.KV * r.hd;
+  k_qkv_rope<<<dim3((items + 127) / 128, r.R), 128, 0, st>>>(r);
   return cudaGetLastError();
 }
 cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, int* y, float* score,
@@ -410,7 +498,7 @@ cudaError_t init_weights_launch(const InitArgs& a, cudaStream_t st) {
   k_init_weights<<<blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
-cudaError_t kv_fill_launch(bf16* pool, const int* block_row, int layers, int num_pages, int KV, int hd, int n_tokens,
+cudaError_t kv_fill_launch(f16* pool, const int* block_row, int layers, int num_pages, int KV, int hd, int n_tokens,
                            uint32_t k0, uint32_t k1, uint32_t stream_id, cudaStream_t st) {
   const long long total = (long long)n_tokens * layers * 2 * (KV * hd / 4);
   if (total == 0) return cudaSuccess;

@@ -20,7 +20,7 @@ thread_local int g_last_launches = 0;
 
 // ---- optional per-kernel event timing (bench instrumentation) ----
 enum Kind { K_PREP, K_EMBED, K_RMSNORM, K_QKV, K_ATTN, K_COMBINE, K_O, K_GU, K_DOWN, K_LM, K_LMRED, K_WALK, K_COMMIT,
-            K_NKINDS };
+            K_ROPE, K_NKINDS };
 struct Timing {
   bool on = false;
   std::vector<cudaEvent_t> pool;
@@ -66,12 +66,13 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
   size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
-  size_t X, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, part_val, part_idx, y, score;
+  size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, part_val, part_idx, y, score;
   size_t stage_in, stage_out, total;
   int B, R, n_splits_max;
 };
 
 constexpr int kMaxSplits = 8;
+constexpr int kGemmSplits = 4;
 
 WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   WsLayout w{};
@@ -92,6 +93,8 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.row_slot = take(4 * R);
   w.row_anc = take(8 * R);
   w.X = take(4 * (size_t)R * c.d);   // fp32 residual stream
+  // fp32 K-split partials of the QKV / O / down GEMMs: [kGemmSplits][R][max(qkv, d)]
+  w.Y = take(4 * (size_t)kGemmSplits * R * std::max((size_t)(H + 2 * KV) * hd, (size_t)c.d));
   w.Hn = take(2 * (size_t)R * c.d);
   w.Hf = take(2 * 2 * (size_t)R * c.d);   // final-norm output as hi/lo bf16 row pairs
   w.Q = take(2 * (size_t)R * H * hd);
@@ -120,7 +123,7 @@ bool check_cfg(const specedge_model_config& c) {
   if (c.n_layers <= 0 || c.d <= 0 || c.n_heads <= 0 || c.n_kv <= 0 || c.ffn <= 0 || c.vocab <= 0) return false;
   if (c.n_heads % c.n_kv) return false;
   if (!(c.head_dim == 16 || c.head_dim == 32 || c.head_dim == 64 || c.head_dim == 128)) return false;
-  if (c.d % 64 || (c.n_heads * c.head_dim) % 64 || c.ffn % 64) return false;
+  if (c.d % 64 || (c.n_heads * c.head_dim) % 64 || c.ffn % 64 || c.d > 16384) return false;
   if (c.max_position <= 0) return false;
   return true;
 }
@@ -185,10 +188,10 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
 
   float* X = (float*)P(w.X);
   bf16* Hn = (bf16*)P(w.Hn);
-  bf16* Q = (bf16*)P(w.Q);
+  f16* Q = (f16*)P(w.Q);
   bf16* O = (bf16*)P(w.O);
   bf16* Mb = (bf16*)P(w.M);
-  bf16* tree_kv = (bf16*)P(w.tree_kv);
+  f16* tree_kv = (f16*)P(w.tree_kv);
   { KTimer _t(K_EMBED, st); CK(embed_launch(m->embed, pa.row_tok, X, R, c.d, st, &launches)); }
 
   const int hd = c.head_dim, H = c.n_heads, KV = c.n_kv, G = H / KV;
@@ -221,25 +224,43 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   aa.R = R;
   aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
 
+  float* Y = (float*)P(w.Y);
+  const size_t y_stride = (size_t)R * std::max((H + 2 * KV) * hd, c.d);
+  int pendingY = 0;   // K-split partials of the last down-proj not yet added to X
+  auto f32_gemm = [&](int kind, const CUtensorMap& tm, const void* Xin, int Mrows, int K) -> int {
+    GemmArgs g{};
+    g.M = Mrows;
+    g.R = R;
+    g.K = K;
+    g.out_f32 = Y;
+    g.ldo = Mrows;
+    g.max_splits = kGemmSplits;
+    g.split_stride = y_stride;
+    KTimer _t(kind, st);
+    if (gemm_launch(EPI_F32, tm, Xin, g, st, &launches) != cudaSuccess) return -1;
+    return gemm_splits_last();
+  };
   for (int l = 0; l < c.n_layers; ++l) {
     const auto& Lw = m->layers[l];
-    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Lw.g_attn, Hn, R, c.d, c.eps, st, &launches)); }
-    GemmArgs g{};
-    g.M = (H + 2 * KV) * hd;
-    g.R = R;
-    g.K = c.d;
-    g.out_bf16 = Q;
-    g.ld_out = H * hd;
-    g.tree_kv = tree_kv;
-    g.R_cap = R_cap;
-    g.layer = l;
-    g.n_heads = H;
-    g.n_kv = KV;
-    g.head_dim = hd;
-    g.row_pos = pa.row_pos;
-    g.rope_cos = m->rope_cos;
-    g.rope_sin = m->rope_sin;
-    { KTimer _t(K_QKV, st); CK(gemm_launch(EPI_QKV, Lw.tm_qkv, Hn, g, st, &launches)); }
+    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Y, pendingY, y_stride, Lw.g_attn, Hn, R, c.d, c.eps, st, &launches)); }
+    const int sq = f32_gemm(K_QKV, Lw.tm_qkv, Hn, (H + 2 * KV) * hd, c.d);
+    if (sq < 0) return SPECEDGE_E_CUDA;
+    RopeArgs ra{};
+    ra.Y = Y;
+    ra.nY = sq;
+    ra.y_stride = y_stride;
+    ra.R = R;
+    ra.H = H;
+    ra.KV = KV;
+    ra.hd = hd;
+    ra.layer = l;
+    ra.R_cap = R_cap;
+    ra.row_pos = pa.row_pos;
+    ra.rope_cos = m->rope_cos;
+    ra.rope_sin = m->rope_sin;
+    ra.Q = Q;
+    ra.tree_kv = tree_kv;
+    { KTimer _t(K_ROPE, st); CK(qkv_rope_launch(ra, st, &launches)); }
     aa.layer = l;
     if (use_tc) {
       { KTimer _t(K_ATTN, st); CK(attention_tc_launch(aa, B, aa.n_splits == 1 ? O : nullptr, nullptr, st, &launches)); }
@@ -248,14 +269,9 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
       { KTimer _t(K_ATTN, st); CK(attention_launch(aa, B, st, &launches)); }
       { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
     }
-    GemmArgs go{};
-    go.M = c.d;
-    go.R = R;
-    go.K = H * hd;
-    go.out_f32 = X;
-    go.ldo = c.d;
-    { KTimer _t(K_O, st); CK(gemm_launch(EPI_RESID, Lw.tm_o, O, go, st, &launches)); }
-    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Lw.g_mlp, Hn, R, c.d, c.eps, st, &launches)); }
+    const int so = f32_gemm(K_O, Lw.tm_o, O, c.d, H * hd);
+    if (so < 0) return SPECEDGE_E_CUDA;
+    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Y, so, y_stride, Lw.g_mlp, Hn, R, c.d, c.eps, st, &launches)); }
     GemmArgs gu{};
     gu.M = 2 * c.ffn;
     gu.R = R;
@@ -263,18 +279,13 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gu.out_bf16 = Mb;
     gu.ld_out = c.ffn;
     { KTimer _t(K_GU, st); CK(gemm_launch(EPI_SWIGLU, Lw.tm_gu, Hn, gu, st, &launches)); }
-    GemmArgs gd{};
-    gd.M = c.d;
-    gd.R = R;
-    gd.K = c.ffn;
-    gd.out_f32 = X;
-    gd.ldo = c.d;
-    { KTimer _t(K_DOWN, st); CK(gemm_launch(EPI_RESID, Lw.tm_d, Mb, gd, st, &launches)); }
+    pendingY = f32_gemm(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn);
+    if (pendingY < 0) return SPECEDGE_E_CUDA;
   }
   int* y = (int*)P(w.y);
   if (!prefill) {
     bf16* Hf = (bf16*)P(w.Hf);
-    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, m->g_final, Hf, R, c.d, c.eps, st, &launches, 1)); }
+    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Y, pendingY, y_stride, m->g_final, Hf, R, c.d, c.eps, st, &launches, 1)); }
     GemmArgs gl{};
     gl.M = c.vocab;
     gl.R = 2 * R;
@@ -630,7 +641,7 @@ specedge_status specedge_kv_commit(specedge_model* m, specedge_kvpool* pool, con
   ca.node_offset = in->node_offset;
   ca.accepted_len = out->accepted_len;
   ca.accepted_node = out->accepted_node;
-  ca.tree_kv = (bf16*)(ws + w.tree_kv);
+  ca.tree_kv = (f16*)(ws + w.tree_kv);
   ca.pool = pool->pages;
   ca.block_table = pool->block_table;
   ca.cache_len = pool->cache_len;
@@ -858,7 +869,7 @@ specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_pr
                o_m = take(4 * (size_t)n_splits * S * G), o_l = take(4 * (size_t)n_splits * S * G);
   if (!workspace || ws_bytes < off) return SPECEDGE_E_WORKSPACE;
   uint8_t* ws = (uint8_t*)workspace;
-  bf16* pool = (bf16*)(ws + o_pool);
+  f16* pool = (f16*)(ws + o_pool);
   for (int p = 0; p < (L + 63) / 64; ++p) {
     const int nt = std::min(64, L - p * 64);
     CK(cudaMemcpyAsync(pool + ((size_t)p * 2 + 0) * 64 * hd, k_prefix + (size_t)p * 64 * hd, (size_t)nt * hd * 2,
@@ -869,7 +880,7 @@ specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_pr
   std::vector<int> bt(npages);
   for (int p = 0; p < npages; ++p) bt[p] = p;
   CK(cudaMemcpyAsync(ws + o_bt, bt.data(), 4 * npages, cudaMemcpyHostToDevice, st));
-  bf16* tree = (bf16*)(ws + o_tree);
+  f16* tree = (f16*)(ws + o_tree);
   CK(cudaMemcpyAsync(tree, k_tree, (size_t)S * hd * 2, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(tree + (size_t)S * hd, v_tree, (size_t)S * hd * 2, cudaMemcpyDeviceToDevice, st));
   const int req[4] = {L, 0, 0, S};   // req_L, req_h, req_row0, req_S
@@ -878,7 +889,7 @@ specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_pr
   CK(cudaMemcpyAsync(ws + o_anc, &zero, 8, cudaMemcpyHostToDevice, st));
   if (S > 1) CK(cudaMemcpyAsync(ws + o_anc + 8, anc, 8 * (size_t)(S - 1), cudaMemcpyDeviceToDevice, st));
   AttnArgs a{};
-  a.Q = (const bf16*)q;
+  a.Q = (const f16*)q;
   a.pool = pool;
   a.block_table = (const int*)(ws + o_bt);
   a.max_pages_per_seq = npages;

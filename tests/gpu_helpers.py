@@ -62,3 +62,7 @@ def split_outputs(out, batch):
 def bf16_bits_to_f64(u16):
     u = np.asarray(u16, np.uint16).astype(np.uint32) << 16
     return u.view(np.float32).astype(np.float64)
+
+
+def f16_bits_to_f64(u16):
+    return np.asarray(u16, np.uint16).view(np.float16).astype(np.float64)

@@ -9,7 +9,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from oracle.model import gen_matrix, gen_gain, Weights  # noqa: E402
-from oracle.numerics import attention, bf16  # noqa: E402
+from oracle.numerics import attention, bf16, f16  # noqa: E402
 from synth.configs import TINY, LLAMA3_8B_2L, SMALL128  # noqa: E402
 from tests.gpu_helpers import ATTN_TOL, bf16_bits_to_f64  # noqa: E402
 
@@ -23,6 +23,11 @@ def api():
 def _rand_bf16(rng, shape, scale=1.0):
     x = bf16(rng.standard_normal(shape) * scale).astype(np.float32)
     return torch.from_numpy(x).to(torch.bfloat16).cuda()
+
+
+def _rand_f16(rng, shape, scale=1.0):
+    x = f16(rng.standard_normal(shape) * scale).astype(np.float32)
+    return torch.from_numpy(x).to(torch.float16).cuda()
 
 
 # ------------------------------------------------------------------ K12: bit-identical weights
@@ -93,11 +98,11 @@ def test_tree_attention_matches_oracle(api, hd, G, L, N, splits):
     rng = np.random.default_rng(hd + G + L + N)
     S = N + 1
     tree = random_tree(rng, N, 1000)
-    q = _rand_bf16(rng, (S, G, hd))
-    kp = _rand_bf16(rng, (max(L, 1), hd))[:L] if L else None
-    vp = _rand_bf16(rng, (max(L, 1), hd))[:L] if L else None
-    kt = _rand_bf16(rng, (S, hd))
-    vt = _rand_bf16(rng, (S, hd))
+    q = _rand_f16(rng, (S, G, hd))          # attention operands are fp16 (DESIGN R-precision)
+    kp = _rand_f16(rng, (max(L, 1), hd))[:L] if L else None
+    vp = _rand_f16(rng, (max(L, 1), hd))[:L] if L else None
+    kt = _rand_f16(rng, (S, hd))
+    vt = _rand_f16(rng, (S, hd))
     anc = np.array(_anc_masks(tree.parent), dtype=np.uint64).view(np.int64)
     anc_t = torch.from_numpy(anc).cuda() if N else torch.zeros(1, dtype=torch.int64, device="cuda")
     o = api.debug_attention(q, kp, vp, kt, vt, anc_t, n_splits=splits).cpu().numpy().astype(np.float64)

@@ -19,7 +19,7 @@ from oracle.model import Weights, Cache, gen_kv_fill, lm_logits, tree_forward  #
 from synth.configs import TINY, TINY_V16, TINY_MHA, SMALL128, LLAMA3_8B_2L  # noqa: E402
 from synth.plant import plant, draw_accept_lengths  # noqa: E402
 from synth.trees import pooled_tree, random_tree, chain_tree, Tree  # noqa: E402
-from tests.gpu_helpers import (LOGIT_TOL, MARGIN, bf16_bits_to_f64, compare_outcome,  # noqa: E402
+from tests.gpu_helpers import (LOGIT_TOL, MARGIN, f16_bits_to_f64, compare_outcome,  # noqa: E402
                                split_outputs, top2_margin)
 
 
@@ -82,9 +82,9 @@ def test_library_prefill_matches_oracle_cache(api):
         for i, s in enumerate(pr.sessions):
             for l in range(TINY.n_layers):
                 for kv_sel, ref in ((0, s.cache.k[l]), (1, s.cache.v[l])):
-                    got = bf16_bits_to_f64(pr.pool.read_kv(pr.handles[i], l, kv_sel, 0, len(s.cache)))
+                    got = f16_bits_to_f64(pr.pool.read_kv(pr.handles[i], l, kv_sel, 0, len(s.cache)))
                     err = np.abs(got - ref)
-                    # bf16 storage: differences are occasional 1-ulp rounding flips of upstream values
+                    # fp16 storage: differences are occasional 1-ulp rounding flips of upstream values
                     assert err.max() <= 0.05 * max(1.0, np.abs(ref).max()), (i, l, kv_sel, err.max())
                     assert np.mean(err > 0) < 0.05
     finally:
@@ -154,10 +154,10 @@ def test_iterated_verify_commit_reproduces_greedy_decoding(api):
             lens = pr.pool.get_len(pr.handles)
             assert list(lens) == [len(s.cache) for s in pr.sessions]
         assert emitted_gpu == emitted_ref
-        # the committed caches equal the oracle's (indices exact, values within bf16 rounding)
+        # the committed caches equal the oracle's (indices exact, values within fp16 rounding)
         for r in range(B):
             s = pr.sessions[r]
-            got = bf16_bits_to_f64(pr.pool.read_kv(pr.handles[r], 1, 0, 0, len(s.cache)))
+            got = f16_bits_to_f64(pr.pool.read_kv(pr.handles[r], 1, 0, 0, len(s.cache)))
             assert np.abs(got - s.cache.k[1]).max() <= 0.05 * max(1.0, np.abs(s.cache.k[1]).max())
     finally:
         pr.close()

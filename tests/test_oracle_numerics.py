@@ -7,7 +7,7 @@ import pytest
 import torch
 
 from oracle import philox
-from oracle.numerics import bf16, rmsnorm, rope, attention, softmax, silu
+from oracle.numerics import bf16, f16, rmsnorm, rope, attention, softmax, silu
 from oracle.model import gen_matrix, gen_gain, gen_kv_fill, Weights
 from synth.configs import TINY
 
@@ -48,6 +48,18 @@ def test_bf16_matches_torch_rne():
     x = np.concatenate([x, ties, -ties, np.float32([0.0, -0.0, 1.0, 3.0e38])])
     ref = torch.from_numpy(x).to(torch.bfloat16).to(torch.float64).numpy()
     got = bf16(x.astype(np.float64))
+    assert np.array_equal(got, ref)
+
+
+def test_f16_matches_numpy_rne():
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.standard_normal(200000) * s for s in (1e-6, 1e-3, 1.0, 1e3, 3e4)])
+    # exact ties between fp16 neighbours and subnormals / overflow edges
+    h = rng.integers(0, 0x7BFF, 20000).astype(np.uint16).view(np.float16).astype(np.float64)
+    h2 = (rng.integers(0, 0x7BFF, 20000).astype(np.uint16) + 1).view(np.float16).astype(np.float64)
+    x = np.concatenate([x, (h + h2) / 2, -(h + h2) / 2, [0.0, 65504.0, 65519.0, 65520.0, 2.0 ** -25, 3 * 2.0 ** -26]])
+    ref = x.astype(np.float16).astype(np.float64)
+    got = f16(x)
     assert np.array_equal(got, ref)
 
 
