@@ -39,6 +39,22 @@ def _dist():
     return world, rank, local
 
 
+def reduce_max(value: float, dist=None, device=None) -> float:
+    """Max of a per-rank timing over all ranks (the contract's max-over-ranks clock)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def box_throughput(world: int, tokens_per_step_per_rank: int, steps: int, max_ms: float) -> float:
+    """Whole-box verified tokens/s: every rank verifies its own replica's batch each step (weak
+    scaling), the window is the slowest rank's."""
+    return world * tokens_per_step_per_rank * steps / (max_ms / 1e3)
+
+
 def _peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -206,11 +222,24 @@ def run_gpu(args, world, rank, local):
         step()
     torch.cuda.synchronize()
     tokens_per_step = int(sum(a + 1 for a in st["accepted"]))
-    # ---- timed region: K steps, per-step CUDA events, per-kernel events inside the library
     import ctypes as C
     nk = len(api.L.KERNEL_KINDS)
+    kinds = api.L.KERNEL_KINDS
+    # ---- calibration pass (untimed): per-kernel event timing of every kind, to find the kernel
+    # with the largest share of the step and to report the per-kernel table
     lib.specedge_kernel_times(None, None, 1)
-    lib.specedge_set_kernel_timing(1)
+    lib.specedge_set_kernel_timing(-1)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    lib.specedge_set_kernel_timing(0)
+    cal_ms = (C.c_float * nk)()
+    cal_cnt = (C.c_int32 * nk)()
+    lib.specedge_kernel_times(cal_ms, cal_cnt, 1)
+    dom = max(range(nk), key=lambda i: cal_ms[i])
+    # ---- timed region: K steps, per-step CUDA events; only the dominant kernel kind is wrapped
+    # in events (its launch durations feed the roofline), so instrumentation stays ~1-2% of a step
+    lib.specedge_set_kernel_timing(1 << dom)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     if dist:
         dist.barrier()
@@ -230,11 +259,8 @@ def run_gpu(args, world, rank, local):
     lib.specedge_kernel_times(kms, kcnt, 1)
     acc = outs.accepted_len.cpu().numpy()
     assert int((acc + 1).sum()) == tokens_per_step, "accepted counts changed between steps"
-    if dist:
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * tokens_per_step * args.steps / (total_ms / 1e3)
+    total_ms = reduce_max(total_ms, dist, f"cuda:{local}")
+    value = box_throughput(world, tokens_per_step, args.steps, total_ms)
 
     # ---- end-to-end through the host-buffer C-ABI entry point (copies inside the timed region)
     hb = api.HostBatch.of(batch)
@@ -253,19 +279,15 @@ def run_gpu(args, world, rank, local):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([e2e_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = reduce_max(e2e_ms, dist, f"cuda:{local}")
     e2e_tokens = int((ho["accepted_len"].numpy() + 1).sum())
     B, T, R = hb.num_requests, hb.total_nodes, hb.total_nodes + hb.num_requests
     h2d = hb.nbytes()
     d2h = 4 * (3 * B + 2 * T + 2 * R)
 
-    # ---- roofline of the dominant kernel (largest share of the timed step)
-    kinds = api.L.KERNEL_KINDS
+    # ---- roofline of the dominant kernel (largest share of the step), timed in the timed region
     share = {kinds[i]: float(kms[i]) for i in range(nk)}
-    dom = max(share, key=share.get)
+    dom = kinds[dom]
     work = algorithmic_work(wl, st)
     peaks = _peaks()
     roof = None
@@ -290,8 +312,9 @@ def run_gpu(args, world, rank, local):
                         frac=round(ach / peak, 4), traffic=traffic,
                         algorithmic_bytes_per_launch=w["bytes"], launch_ms=round(per_launch_ms, 4),
                         peak_source="MEASURED_PEAKS.json hbm_gbs")
-    kernel_table = {kinds[i]: dict(ms_per_step=round(float(kms[i]) / args.steps, 4), launches=int(kcnt[i]) // args.steps)
-                    for i in range(nk) if kcnt[i]}
+    kernel_table = {kinds[i]: dict(ms_per_step=round(float(cal_ms[i]) / args.steps, 4),
+                                   launches=int(cal_cnt[i]) // args.steps)
+                    for i in range(nk) if cal_cnt[i]}
     for k, w in work.items():
         if k in kernel_table and kernel_table[k]["launches"]:
             per = kernel_table[k]["ms_per_step"] / kernel_table[k]["launches"] / 1e3
@@ -315,8 +338,11 @@ def run_gpu(args, world, rank, local):
                    "parallelism": f"replicas x{world}"},
         "p50_ms": round(statistics.median(step_ms), 4), "p90_ms": round(float(np.quantile(step_ms, 0.9)), 4),
         "rows_per_s": round(world * st["R"] * args.steps / (total_ms / 1e3), 1),
-        "roofline": roof, "kernels": kernel_table,
-        "e2e": {"value": round(world * e2e_tokens * args.steps / (e2e_ms / 1e3), 1), "unit": UNIT,
+        "roofline": roof,
+        "kernels": kernel_table,
+        "kernels_note": "per-kernel ms from an event-instrumented calibration pass of the same steps "
+                        "(each event pair adds a few us of stream time; small kernels read high)",
+        "e2e": {"value": round(box_throughput(world, e2e_tokens, args.steps, e2e_ms), 1), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches), "clocks": clk.result(),
     }

@@ -224,8 +224,9 @@ specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_pr
 int32_t specedge_last_launch_count(void);
 
 /* ---- per-kernel timing (benchmark instrumentation) ----
- * When enabled, verify_batch records a CUDA event pair on `stream` around every kernel it
- * launches (stream-ordered, no host sync).  specedge_kernel_times synchronises on the recorded
+ * enable: 0 off, -1 every kernel kind, > 0 bitmask of kinds (bit k = kind k).  When enabled,
+ * verify_batch records a CUDA event pair on `stream` around every launch of a selected kind
+ * (stream-ordered, no host sync; each pair costs a few microseconds of stream time).  specedge_kernel_times synchronises on the recorded
  * events, adds their durations to per-kind totals and clears the pending list; out_ms[k] and
  * out_count[k] (arrays of SPECEDGE_KERNEL_KINDS) receive the totals since the last reset.
  * Kinds: 0 prep, 1 embed, 2 rmsnorm, 3 gemm_qkv, 4 attention, 5 attn_combine, 6 gemm_o,

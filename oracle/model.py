@@ -40,6 +40,18 @@ import numpy as np
 from . import philox
 from .numerics import bf16, f16, rmsnorm, rope, silu, attention
 
+# Matmul arithmetic of the oracle.  float64 is the reference; tests switch it to float32 (same
+# storage contract) to measure the oracle's own arithmetic-noise floor, against which the
+# library's floating-point agreement is calibrated.
+MATMUL_DTYPE = np.float64
+
+
+def _mm(a, b):
+    if MATMUL_DTYPE == np.float64:
+        return a @ b
+    return (a.astype(MATMUL_DTYPE) @ b.astype(MATMUL_DTYPE)).astype(np.float64)
+
+
 TENSOR_ID = dict(embed=1, wq=2, wk=3, wv=4, wo=5, wg=6, wu=7, wd=8, lm_head=9,
                  g_attn=10, g_mlp=11, g_final=12)
 WEIGHT_TAG = 0x57454947  # 'WEIG'
@@ -139,11 +151,11 @@ def lm_logits(W: Weights, hf, block=16384, cache_full=True):
     """logits = hf . Wlm^T (float64, never rounded; SURVEY §8(c) O2 last line)."""
     s = W.shape
     if cache_full and s.vocab <= 65536:
-        return hf @ W.lm_head().T
+        return _mm(hf, W.lm_head().T)
     out = np.empty((hf.shape[0], s.vocab))
     for v0 in range(0, s.vocab, block):
         nv = min(block, s.vocab - v0)
-        out[:, v0:v0 + nv] = hf @ W.lm_head_block(v0, nv).T
+        out[:, v0:v0 + nv] = _mm(hf, W.lm_head_block(v0, nv).T)
     return out
 
 
@@ -174,9 +186,9 @@ def _qkv(W: Weights, l, x, pos):
     s = W.shape
     Lw = W.layer(l)
     h = bf16(rmsnorm(x, Lw["g_attn"], s.eps))
-    q = (h @ Lw["wq"].T).reshape(-1, s.n_heads, s.head_dim)
-    k = (h @ Lw["wk"].T).reshape(-1, s.n_kv, s.head_dim)
-    v = (h @ Lw["wv"].T).reshape(-1, s.n_kv, s.head_dim)
+    q = _mm(h, Lw["wq"].T).reshape(-1, s.n_heads, s.head_dim)
+    k = _mm(h, Lw["wk"].T).reshape(-1, s.n_kv, s.head_dim)
+    v = _mm(h, Lw["wv"].T).reshape(-1, s.n_kv, s.head_dim)
     q = f16(rope(q, pos, s.rope_theta))
     k = f16(rope(k, pos, s.rope_theta))
     return q, k, f16(v)
@@ -187,10 +199,10 @@ def _post_attn(W: Weights, l, x, o):
     s = W.shape
     Lw = W.layer(l)
     O = bf16(o.reshape(o.shape[0], -1))
-    x = x + O @ Lw["wo"].T                 # residual stream is not a GEMM operand: not rounded
+    x = x + _mm(O, Lw["wo"].T)             # residual stream is not a GEMM operand: not rounded
     h2 = bf16(rmsnorm(x, Lw["g_mlp"], s.eps))
-    M = bf16(silu(h2 @ Lw["wg"].T) * (h2 @ Lw["wu"].T))
-    return x + M @ Lw["wd"].T
+    M = bf16(silu(_mm(h2, Lw["wg"].T)) * _mm(h2, Lw["wu"].T))
+    return x + _mm(M, Lw["wd"].T)
 
 
 def final_hidden(W: Weights, x):

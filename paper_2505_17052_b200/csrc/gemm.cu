@@ -16,6 +16,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace se {
 
@@ -54,6 +55,108 @@ __device__ __forceinline__ float gumbel_noise(const GemmArgs& a, int row, int v)
   const uint32_t w = u4_word(r, v & 3);
   const float u = (float)((w >> 8) | 1u) * 5.9604644775390625e-08f;  // exact
   return -logf(-logf(u));
+}
+
+// Epilogue of one 32-column chunk of a 128-feature accumulator tile.  v[j] = D[feature][row]
+// for feature = m128*128 + tl (tl = TMEM lane) and row = row_base + j, j < ncol.
+template <int MODE>
+__device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)[32], int m128, int tl, int et,
+                                          int row_base, int ncol, int sk, float* xch, float* red_v, int* red_i) {
+    const int feat = m128 * 128 + tl;
+    if constexpr (MODE == EPI_F32) {
+      if (feat < a.M) {
+        if (a.pair) {   // physical rows 2r, 2r+1 hold hi/lo parts of logical row r
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const int row = row_base + j;
+            if (j < ncol && row < a.R)
+              a.out_f32[(size_t)(row >> 1) * a.ldo + feat] = __uint_as_float(v[j]) + __uint_as_float(v[j + 1]);
+          }
+        } else {
+          float* out = a.out_f32 + (size_t)sk * a.split_stride;   // K-split sk's partial
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int row = row_base + j;
+            if (j < ncol && row < a.R) out[(size_t)row * a.ldo + feat] = __uint_as_float(v[j]);
+          }
+        }
+      }
+    } else if constexpr (MODE == EPI_SWIGLU) {
+      // tile rows: lanes 0..63 = gate features m*64 + i, lanes 64..127 = up features
+#pragma unroll
+      for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
+      named_bar_sync(1, kEpiThreads);
+      const int f = et & 63, half = et >> 6;
+      const int fo = m128 * 64 + f;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int j = half * 16 + jj;
+        const int row = row_base + j;
+        if (j < ncol && row < a.R && fo < a.M / 2) {
+          const float g = xch[f * kXchStride + j], u = xch[(f + 64) * kXchStride + j];
+          a.out_bf16[(size_t)row * a.ld_out + fo] = __float2bfloat16_rn(silu_f(g) * u);
+        }
+      }
+      named_bar_sync(1, kEpiThreads);
+    } else if constexpr (MODE == EPI_ARGMAX) {
+      // a.pair: physical rows (2r, 2r+1) = hi/lo parts of logical row r -> 16 logical columns
+      const int np = a.pair ? 16 : 32;
+      const bool fv = feat < a.vocab;
+      if (a.pair) {
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int row = row_base + 2 * jj;
+          float s = -INFINITY;
+          if (fv && 2 * jj < ncol && row < a.R) {
+            s = __uint_as_float(v[2 * jj]) + __uint_as_float(v[2 * jj + 1]);
+            if (a.sample) s = s * a.inv_t + gumbel_noise(a, row >> 1, feat);
+          }
+          xch[tl * kXchStride + jj] = s;
+        }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          const int row = row_base + jj;
+          float s = -INFINITY;
+          if (fv && jj < ncol && row < a.R) {
+            s = __uint_as_float(v[jj]);
+            if (a.sample) s = s * a.inv_t + gumbel_noise(a, row, feat);
+          }
+          xch[tl * kXchStride + jj] = s;
+        }
+      }
+      named_bar_sync(1, kEpiThreads);
+      const int ngrp = 128 / np, per = 128 / ngrp;
+      {
+        const int jj = et % np, g = et / np;
+        float best = -INFINITY;
+        int bi = 0x7fffffff;
+        for (int l = 0; l < per; ++l) {
+          const float s = xch[(g * per + l) * kXchStride + jj];
+          if (s > best) { best = s; bi = m128 * 128 + g * per + l; }
+        }
+        red_v[g * np + jj] = best;
+        red_i[g * np + jj] = bi;
+      }
+      named_bar_sync(1, kEpiThreads);
+      if (et < np) {
+        const int jj = et;
+        float best = red_v[jj];
+        int bi = red_i[jj];
+        for (int g = 1; g < ngrp; ++g) {
+          const float s = red_v[g * np + jj];
+          if (s > best) { best = s; bi = red_i[g * np + jj]; }
+        }
+        const int j = a.pair ? 2 * jj : jj;
+        const int row = row_base + j;
+        if (j < ncol && row < a.R) {
+          const int lr = a.pair ? row >> 1 : row;
+          a.part_val[(size_t)lr * a.ntm128 + m128] = best;
+          a.part_idx[(size_t)lr * a.ntm128 + m128] = bi;
+        }
+      }
+      named_bar_sync(1, kEpiThreads);
+    }
 }
 
 template <int MODE>
@@ -165,7 +268,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int feat = m * 128 + tl;
       const int nchunks = (BN + 31) / 32;
       for (int c = 0; c < nchunks; ++c) {
         uint32_t v[32];
@@ -173,100 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         const int row_base = n * BN + c * 32;
         const int ncol = min(32, BN - c * 32);
-        if constexpr (MODE == EPI_F32) {
-          if (feat < a.M) {
-            if (a.pair) {   // physical rows 2r, 2r+1 hold hi/lo parts of logical row r
-#pragma unroll
-              for (int j = 0; j < 32; j += 2) {
-                const int row = row_base + j;
-                if (j < ncol && row < a.R)
-                  a.out_f32[(size_t)(row >> 1) * a.ldo + feat] = __uint_as_float(v[j]) + __uint_as_float(v[j + 1]);
-              }
-            } else {
-              float* out = a.out_f32 + (size_t)sk * a.split_stride;   // K-split sk's partial
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const int row = row_base + j;
-                if (j < ncol && row < a.R) out[(size_t)row * a.ldo + feat] = __uint_as_float(v[j]);
-              }
-            }
-          }
-        } else if constexpr (MODE == EPI_SWIGLU) {
-          // tile rows: lanes 0..63 = gate features m*64 + i, lanes 64..127 = up features
-#pragma unroll
-          for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
-          named_bar_sync(1, kEpiThreads);
-          const int f = et & 63, half = et >> 6;
-          const int fo = m * 64 + f;
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            const int j = half * 16 + jj;
-            const int row = row_base + j;
-            if (j < ncol && row < a.R && fo < a.M / 2) {
-              const float g = xch[f * kXchStride + j], u = xch[(f + 64) * kXchStride + j];
-              a.out_bf16[(size_t)row * a.ld_out + fo] = __float2bfloat16_rn(silu_f(g) * u);
-            }
-          }
-          named_bar_sync(1, kEpiThreads);
-        } else if constexpr (MODE == EPI_ARGMAX) {
-          // a.pair: physical rows (2r, 2r+1) = hi/lo parts of logical row r -> 16 logical columns
-          const int np = a.pair ? 16 : 32;
-          const bool fv = feat < a.vocab;
-          if (a.pair) {
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-              const int row = row_base + 2 * jj;
-              float s = -INFINITY;
-              if (fv && 2 * jj < ncol && row < a.R) {
-                s = __uint_as_float(v[2 * jj]) + __uint_as_float(v[2 * jj + 1]);
-                if (a.sample) s = s * a.inv_t + gumbel_noise(a, row >> 1, feat);
-              }
-              xch[tl * kXchStride + jj] = s;
-            }
-          } else {
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              const int row = row_base + jj;
-              float s = -INFINITY;
-              if (fv && jj < ncol && row < a.R) {
-                s = __uint_as_float(v[jj]);
-                if (a.sample) s = s * a.inv_t + gumbel_noise(a, row, feat);
-              }
-              xch[tl * kXchStride + jj] = s;
-            }
-          }
-          named_bar_sync(1, kEpiThreads);
-          const int ngrp = 128 / np, per = 128 / ngrp;
-          {
-            const int jj = et % np, g = et / np;
-            float best = -INFINITY;
-            int bi = 0x7fffffff;
-            for (int l = 0; l < per; ++l) {
-              const float s = xch[(g * per + l) * kXchStride + jj];
-              if (s > best) { best = s; bi = m * 128 + g * per + l; }
-            }
-            red_v[g * np + jj] = best;
-            red_i[g * np + jj] = bi;
-          }
-          named_bar_sync(1, kEpiThreads);
-          if (et < np) {
-            const int jj = et;
-            float best = red_v[jj];
-            int bi = red_i[jj];
-            for (int g = 1; g < ngrp; ++g) {
-              const float s = red_v[g * np + jj];
-              if (s > best) { best = s; bi = red_i[g * np + jj]; }
-            }
-            const int j = a.pair ? 2 * jj : jj;
-            const int row = row_base + j;
-            if (j < ncol && row < a.R) {
-              const int lr = a.pair ? row >> 1 : row;
-              a.part_val[(size_t)lr * a.n_tiles_m + m] = best;
-              a.part_idx[(size_t)lr * a.n_tiles_m + m] = bi;
-            }
-          }
-          named_bar_sync(1, kEpiThreads);
-        }
+        epi_chunk<MODE>(a, v, m, tl, et, row_base, ncol, sk, xch, red_v, red_i);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -276,6 +285,189 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, (uint32_t)a.tmem_cols);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a 256-feature x BN tile.
+// CTA r loads weight rows [256p + 128r, +128) and activation rows [n*BN + r*BN/2, +BN/2) of each
+// 64-deep k-block; the leader issues M=256 tcgen05.mma that read both CTAs' shared memory, so each
+// SM receives 16 KB + BN*64 B per k-block instead of 16 KB + BN*128 B (operand delivery is the
+// bottleneck of these skinny GEMMs).  Each CTA's TMEM holds its 128 features.
+// ------------------------------------------------------------------------------------------
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;   // shared::cluster address of the leader's copy
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* m, uint64_t* leader_bar, int c0, int c1,
+                                                uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(leader_bar) & kPeerMask), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_2sm(uint32_t* smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = a.stages, BN = a.BN, HB = BN / 2;
+  const SmemLayout L = smem_layout(S, HB);
+  uint8_t* sA = smem + L.a_off;
+  uint8_t* sB = smem + L.b_off;
+  float* xch = reinterpret_cast<float*>(smem + L.xch_off);
+  float* red_v = reinterpret_cast<float*>(smem + L.red_off);
+  int* red_i = reinterpret_cast<int*>(smem + L.red_off + 4 * 32 * 4);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t b_bytes = (uint32_t)HB * 128u;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 2);         // one arrival per CTA (leader's carries the tx bytes)
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiThreads);   // epilogue threads of both CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_2sm(tmem_slot, (uint32_t)a.tmem_cols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int ntiles = a.n_tiles_m * a.n_tiles_n;   // n_tiles_m counts 256-feature pairs here
+  const int nunits = ntiles * a.splits;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cl; u < nunits; u += ncl) {
+        const int t = u / a.splits, sk = u % a.splits;
+        const int p = t / a.n_tiles_n, n = t % a.n_tiles_n;
+        const int kb0 = sk * a.kb_per_split, kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + b_bytes));
+          else mbar_arrive_leader(&full[stage]);
+          tma_load_2d_2sm(sA + stage * kABytes, &tmA, &full[stage], kb * 64, p * 256 + (int)rank * 128, pol_w);
+          tma_load_2d_2sm(sB + stage * b_bytes, &tmB, &full[stage], kb * 64, n * BN + (int)rank * HB, pol_x);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && elect_one()) {
+      const uint32_t idesc = umma_idesc_bf16(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int u = cl; u < nunits; u += ncl, ++it) {
+        const int sk = u % a.splits;
+        const int kb0 = sk * a.kb_per_split, kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * kABytes);
+          const uint32_t b_addr = smem_u32(sB + stage * b_bytes);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc_mma_f16_2sm(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
+                           (kb > kb0 || k > 0) ? 1u : 0u);
+          tc_commit_2sm_mc(&empty[stage]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_2sm_mc(&tfull[acc]);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int tl = q * 32 + lane;
+    const int et = threadIdx.x - 64;
+    int it = 0;
+    for (int u = cl; u < nunits; u += ncl, ++it) {
+      const int t = u / a.splits, sk = u % a.splits;
+      const int p = t / a.n_tiles_n, n = t % a.n_tiles_n;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int nchunks = (BN + 31) / 32;
+      for (int c = 0; c < nchunks; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+        tmem_ld_wait();
+        const int row_base = n * BN + c * 32;
+        const int ncol = min(32, BN - c * 32);
+        epi_chunk<MODE>(a, v, 2 * p + (int)rank, tl, et, row_base, ncol, sk, xch, red_v, red_i);
+      }
+      tc_fence_before();
+      mbar_arrive_leader(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, (uint32_t)a.tmem_cols);
   }
 }
 
@@ -313,6 +505,20 @@ cudaError_t launch_mode(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
   return cudaGetLastError();
 }
 
+template <int MODE>
+cudaError_t launch_mode2(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmArgs& a,
+                         size_t smem, int grid, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k_gemm2<MODE><<<grid, kThreads, smem, st>>>(tmW, tmX, a);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
@@ -337,6 +543,52 @@ int gemm_pick_bn(int R) {
   return std::max(16, std::min(256, bn));
 }
 
+namespace {
+bool g_force_single = false;
+
+cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, GemmArgs a, cudaStream_t st,
+                             int* launches) {
+  const int HB = a.BN / 2;
+  int ncols = 32;
+  const int need = a.BN + (a.BN + 31) / 32 * 32;
+  while (ncols < need) ncols *= 2;
+  a.tmem_cols = ncols;
+  const size_t budget = 227 * 1024 - 1024;
+  int stages = 10;
+  while (stages > 2 && smem_layout(stages, HB).total > budget) --stages;
+  a.stages = stages;
+  const size_t smem = smem_layout(stages, HB).total + 1024;
+  CUtensorMap tmX;
+  if (!make_tmap_2d(&tmX, X, (uint64_t)a.R, (uint64_t)a.K, (uint32_t)HB)) return cudaErrorInvalidValue;
+  const int n_pairs = (a.M + 255) / 256;
+  const int ntiles = n_pairs * a.n_tiles_n;
+  const int nclusters = g_num_sms / 2;
+  a.splits = 1;
+  static const int env_max = getenv("SPECEDGE_MAX_SPLITS") ? atoi(getenv("SPECEDGE_MAX_SPLITS")) : 0;
+  if (env_max > 0) a.max_splits = std::min(a.max_splits, env_max);
+  if (mode == EPI_F32 && !a.pair && a.max_splits > 1 && ntiles < nclusters * 3 / 2) {
+    int sp = (2 * nclusters + ntiles / 2) / ntiles;
+    sp = std::min(sp, a.max_splits);
+    while (sp > 1 && a.num_kb / sp < 8) --sp;
+    a.splits = std::max(1, sp);
+  }
+  a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
+  g_last_splits = a.splits;
+  GemmArgs b = a;
+  b.n_tiles_m = n_pairs;      // the kernel iterates 256-feature pairs
+  const int grid = 2 * std::min(ntiles * a.splits, nclusters);
+  if (launches) ++*launches;
+  switch (mode) {
+    case EPI_F32: return launch_mode2<EPI_F32>(tmW, tmX, b, smem, grid, st);
+    case EPI_SWIGLU: return launch_mode2<EPI_SWIGLU>(tmW, tmX, b, smem, grid, st);
+    case EPI_ARGMAX: return launch_mode2<EPI_ARGMAX>(tmW, tmX, b, smem, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
+void gemm_force_single(bool on) { g_force_single = on; }
+
 cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArgs a,
                         cudaStream_t st, int* launches) {
   if (g_num_sms == 0) {
@@ -347,7 +599,13 @@ cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArg
   a.BN = gemm_pick_bn(a.R);
   a.n_tiles_n = (a.R + a.BN - 1) / a.BN;
   a.n_tiles_m = (a.M + 127) / 128;
+  a.ntm128 = a.n_tiles_m;
   a.num_kb = (a.K + 63) / 64;
+  // CTA pairs whenever the weight side has >= 2 128-row tiles (the pair needs BN/2 rows per CTA
+  // aligned to 8 rows: BN is a multiple of 16)
+  static const bool env_single = getenv("SPECEDGE_GEMM_SINGLE") && getenv("SPECEDGE_GEMM_SINGLE")[0] == '1';
+  const bool pair_mode = !g_force_single && !env_single && a.n_tiles_m >= 2;
+  if (pair_mode) return gemm_launch_pair(mode, tmW, X, a, st, launches);
   int ncols = 32;
   const int need = a.BN + (a.BN + 31) / 32 * 32;
   while (ncols < need) ncols *= 2;

@@ -28,6 +28,7 @@ enum GemmMode : int {
 struct GemmArgs {
   int M, R, K;            // weight rows (features), activation rows, reduction length
   int BN, n_tiles_n, n_tiles_m, num_kb, stages, tmem_cols;
+  int ntm128;             // 128-feature tiles (stride of the ARGMAX partials)
   int pair;               // EPI_F32/EPI_ARGMAX: rows (2r, 2r+1) are hi/lo bf16 parts of row r
   int splits, kb_per_split, max_splits;   // K-split (EPI_F32): slice sk at out_f32 + sk*split_stride
   size_t split_stride;
@@ -59,6 +60,7 @@ struct GemmArgs {
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 int gemm_pick_bn(int R);
 int gemm_splits_last();   // K-splits chosen by the last gemm_launch on this thread
+void gemm_force_single(bool on);   // tests/probes: disable the CTA-pair kernel
 cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArgs a,
                         cudaStream_t st, int* launches);
 

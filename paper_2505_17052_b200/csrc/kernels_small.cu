@@ -207,43 +207,54 @@ __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const f
 }
 
 // ------------------------------------------------------------------------- K4b QKV RoPE/scatter
-// One CTA per row.  Work item e < (H+KV)*hd/2: rotate-half pair (i, i+hd/2) of q head (or k head)
-// e / (hd/2) at position row_pos (amb. A14); e >= that: one v element.  Splits summed in order.
+// One thread per 4 consecutive rotate-half pairs (i..i+3, i+hd/2..i+hd/2+3) of one q or k head at
+// position row_pos (amb. A14), or per 4 consecutive v elements; float4 loads of every K-split
+// partial (summed in split order), fp16 stores.
 __global__ void k_qkv_rope(const __grid_constant__ RopeArgs r) {
   const int row = blockIdx.y;
-  const int hd = r.hd, half = hd >> 1;
+  const int hd = r.hd, half = hd >> 1, hq = half >> 2;    // 4-pair groups per head
   const int qkv = (r.H + 2 * r.KV) * hd;
-  const int npair = (r.H + r.KV) * half;
-  const int pos = r.row_pos[row];
+  const int ngroups = (r.H + r.KV) * hq;
+  const int nv4 = r.KV * hd / 4;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ngroups + nv4) return;
   const float* y = r.Y + (size_t)row * qkv;
-  auto ysum = [&](int f) {
-    float v = y[f];
-    for (int s = 1; s < r.nY; ++s) v += y[s * r.y_stride + f];
+  auto ld4 = [&](int f) {
+    float4 v = __ldcs(reinterpret_cast<const float4*>(y + f));
+    for (int s = 1; s < r.nY; ++s) {
+      const float4 w = __ldcs(reinterpret_cast<const float4*>(y + s * r.y_stride + f));
+      v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+    }
     return v;
   };
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npair + r.KV * hd; e += gridDim.x * blockDim.x) {
-    if (e < npair) {
-      const int head = e / half, i = e % half;
-      const int f1 = head * hd + i;
-      const float x1 = ysum(f1), x2 = ysum(f1 + half);
-      const float cs = r.rope_cos[(size_t)pos * half + i], sn = r.rope_sin[(size_t)pos * half + i];
-      const f16 o1 = __float2half_rn(x1 * cs - x2 * sn);
-      const f16 o2 = __float2half_rn(x2 * cs + x1 * sn);
-      if (head < r.H) {
-        r.Q[(size_t)row * r.H * hd + f1] = o1;
-        r.Q[(size_t)row * r.H * hd + f1 + half] = o2;
-      } else {
-        const int kvh = head - r.H;
-        f16* dst = r.tree_kv + ((((size_t)r.layer * 2 + 0) * r.KV + kvh) * r.R_cap + row) * hd;
-        dst[i] = o1;
-        dst[i + half] = o2;
-      }
+  auto st4 = [](f16* dst, float a, float b, float c, float d) {
+    __half2 p0 = __floats2half2_rn(a, b), p1 = __floats2half2_rn(c, d);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&p0);
+    u.y = *reinterpret_cast<uint32_t*>(&p1);
+    *reinterpret_cast<uint2*>(dst) = u;
+  };
+  if (e < ngroups) {
+    const int head = e / hq, i = (e % hq) * 4;
+    const int f1 = head * hd + i;
+    const float4 x1 = ld4(f1), x2 = ld4(f1 + half);
+    const int pos = r.row_pos[row];
+    const float4 c = *reinterpret_cast<const float4*>(r.rope_cos + (size_t)pos * half + i);
+    const float4 sn = *reinterpret_cast<const float4*>(r.rope_sin + (size_t)pos * half + i);
+    f16* dst;
+    if (head < r.H) {
+      dst = r.Q + (size_t)row * r.H * hd + head * hd;
     } else {
-      const int ve = e - npair;
-      const int kvh = ve / hd, dd = ve % hd;
-      const float x = ysum((r.H + r.KV) * hd + ve);
-      r.tree_kv[((((size_t)r.layer * 2 + 1) * r.KV + kvh) * r.R_cap + row) * hd + dd] = __float2half_rn(x);
+      dst = r.tree_kv + ((((size_t)r.layer * 2 + 0) * r.KV + (head - r.H)) * r.R_cap + row) * hd;
     }
+    st4(dst + i, x1.x * c.x - x2.x * sn.x, x1.y * c.y - x2.y * sn.y, x1.z * c.z - x2.z * sn.z, x1.w * c.w - x2.w * sn.w);
+    st4(dst + i + half, x2.x * c.x + x1.x * sn.x, x2.y * c.y + x1.y * sn.y, x2.z * c.z + x1.z * sn.z,
+        x2.w * c.w + x1.w * sn.w);
+  } else {
+    const int ve = (e - ngroups) * 4;
+    const int kvh = ve / hd, dd = ve % hd;
+    const float4 x = ld4((r.H + r.KV) * hd + ve);
+    st4(r.tree_kv + ((((size_t)r.layer * 2 + 1) * r.KV + kvh) * r.R_cap + row) * hd + dd, x.x, x.y, x.z, x.w);
   }
 }
 
@@ -469,7 +480,7 @@ cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, co
 }
 cudaError_t qkv_rope_launch(const RopeArgs& r, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
-  const int items = (r.H + r.KV) * (r.hd / 2) + r.KV * r.hd;
+  const int items = (r.H + r.KV) * (r.hd / 8) + r.KV * r.hd / 4;   // head_dim >= 16
   k_qkv_rope<<<dim3((items + 127) / 128, r.R), 128, 0, st>>>(r);
   return cudaGetLastError();
 }

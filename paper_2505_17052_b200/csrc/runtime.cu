@@ -23,6 +23,7 @@ enum Kind { K_PREP, K_EMBED, K_RMSNORM, K_QKV, K_ATTN, K_COMBINE, K_O, K_GU, K_D
             K_ROPE, K_NKINDS };
 struct Timing {
   bool on = false;
+  uint32_t mask = 0;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
   std::vector<std::pair<int, size_t>> pending;   // (kind, index of start event)
@@ -44,13 +45,15 @@ struct KTimer {
   int kind;
   cudaStream_t st;
   size_t idx = 0;
+  bool active = false;
   KTimer(int k, cudaStream_t s) : kind(k), st(s) {
-    if (!g_timing.on) return;
+    active = g_timing.on && ((g_timing.mask >> k) & 1u);
+    if (!active) return;
     idx = g_timing.used;
     cudaEventRecord(timing_event(), st);
   }
   ~KTimer() {
-    if (!g_timing.on) return;
+    if (!active) return;
     cudaEventRecord(timing_event(), st);
     g_timing.pending.push_back({kind, idx});
   }
@@ -930,6 +933,7 @@ int32_t specedge_last_launch_count(void) { return g_last_launches; }
 
 specedge_status specedge_set_kernel_timing(int32_t enable) {
   g_timing.on = enable != 0;
+  g_timing.mask = enable < 0 ? 0xFFFFFFFFu : (uint32_t)enable;
   return SPECEDGE_OK;
 }
 
