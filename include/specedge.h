@@ -125,9 +125,9 @@ specedge_status specedge_workspace_size(const specedge_model* model, int32_t max
                                         size_t* bytes);
 
 /* Prefill (outside the measured path): run the decoder over host tokens[0..n-2] of a
- * session whose cached length is 0 and cache their K/V (chunked causal chain verification on
- * the same kernels).  tokens[n-1] becomes the first root.  Stream-ordered; the host array is
- * copied before return. */
+ * session and append their K/V to its cache (chunked causal chain verification on the same
+ * kernels; chunks of up to 65 rows, fewer if the workspace is smaller).  tokens[n-1] becomes the
+ * next root.  Synchronous (checks each chunk's status); E_INVALID on a bad token or handle. */
 specedge_status specedge_prefill(specedge_model* model, specedge_kvpool* pool, int32_t handle,
                                  const int32_t* tokens_host, int32_t n, void* workspace,
                                  size_t ws_bytes, void* stream);

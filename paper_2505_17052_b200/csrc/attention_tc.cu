@@ -25,13 +25,16 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace se {
 
 namespace {
 
-constexpr int kWarps = 10;
+constexpr int kWarps = 10;      // producer, MMA, 8 softmax/epilogue warps (2 per TMEM lane quarter)
 constexpr int kThreads = kWarps * 32;
+constexpr int kStages = 3;      // K/V ring depth (128-key tiles)
 
 // UMMA smem descriptor for an MN-major operand, 128B swizzle: SBO = 1024 B between 8-row
 // (K) groups, LBO = stride between 64-element MN atoms.
@@ -95,6 +98,12 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -109,7 +118,13 @@ struct TcArgs {
   bf16* O;          // final output when n_splits == 1 (normalised, bf16) else nullptr
   float* O_f32;     // optional fp32 normalised output (debug) when n_splits == 1
   int slots_per_mt; // floor(128 / G)
+  unsigned long long* trace;   // debug: per-phase clock64 stamps of CTA 0 (nullptr in production)
 };
+
+#define TRACE(slot)                                                                   \
+  do {                                                                                \
+    if (ta.trace && blockIdx.x == 0 && blockIdx.y == 0) ta.trace[(slot)] = clock64(); \
+  } while (0)
 
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -118,23 +133,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int KB = HD / 64;                  // 64-element hd blocks
   constexpr uint32_t QT_BYTES = 128 * HD * 2;  // one M-tile of Q
   constexpr uint32_t KT_BYTES = 128 * HD * 2;  // one 128-key tile of K (or V)
+  constexpr int NST = kStages;
   const AttnArgs& a = ta.a;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                              // [2][KB][128 rows][128 B]
-  uint8_t* sK = sQ + 2 * QT_BYTES;                 // [2 stages][KB][128 keys][128 B]
-  uint8_t* sV = sK + 2 * KT_BYTES;                 // [2 stages][KB][128 keys][128 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * KT_BYTES);
-  uint64_t* q_full = bars;          // [1]
-  uint64_t* q_empty = bars + 1;     // [1]
-  uint64_t* kv_full = bars + 2;     // [2]
-  uint64_t* kv_empty = bars + 4;    // [2]
-  uint64_t* s_full = bars + 6;      // [2]
-  uint64_t* p_full = bars + 8;      // [2]
-  uint64_t* o_full = bars + 10;     // [2]
-  uint64_t* o_empty = bars + 12;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
-  uint64_t* s_anc = reinterpret_cast<uint64_t*>(bars + 16);   // [65]
+  // Q + 3 K/V stages take 224 KB of the 227 KB: the 1024-B alignment SW128 needs comes from the
+  // dynamic-smem base itself (no static smem in this kernel); checked below.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  uint8_t* sQ = smem;                              // [KB][128 rows][128 B]
+  uint8_t* sK = sQ + QT_BYTES;                     // [NST][KB][128 keys][128 B]
+  uint8_t* sV = sK + NST * KT_BYTES;               // [NST][KB][128 keys][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NST * KT_BYTES);
+  uint64_t* q_full = bars;              // [1]
+  uint64_t* q_empty = bars + 1;         // [1]
+  uint64_t* kv_full = bars + 2;         // [NST]
+  uint64_t* kv_empty = kv_full + NST;   // [NST]
+  uint64_t* s_full = kv_empty + NST;    // [2 streams][2 buffers]  S_h(t) in buffer t&1
+  uint64_t* p_full = s_full + 4;        // [2][2]
+  uint64_t* pv_done = p_full + 4;       // [2][2]  PV_h(t) complete
+  uint64_t* o_full = pv_done + 4;       // [1]
+  uint64_t* o_empty = o_full + 1;       // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+  uint64_t* s_anc = reinterpret_cast<uint64_t*>(o_empty + 3);  // [66]
+  float* s_ml = reinterpret_cast<float*>(s_anc + 66);          // [2 streams][m,l][128 rows]
 
   const int r = blockIdx.x / a.KV, g = blockIdx.x % a.KV, sp = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -144,29 +164,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int row0 = a.req_row0[r];
   const int h = a.req_h[r];
   const int spm = ta.slots_per_mt;
-  const int n_mt = (S + spm - 1) / spm;
+  const int n_mt = (S + spm - 1) / spm;        // passes: one 128-row M-tile each
   const int npages = (L + 63) / 64;
   const int p_begin = sp * a.pages_per_split;
   const int p_end = min(npages, p_begin + a.pages_per_split);
   const int n_prefix_tiles = max(0, (p_end - p_begin + 1) / 2);
   const bool has_tree = sp == a.n_splits - 1;
   const int ntiles = n_prefix_tiles + (has_tree ? 1 : 0);
-  const int n_pairs = (n_mt + 1) / 2;
+  // KV tile visited at step t of pass mt: odd passes walk backwards (tree tile first), so they
+  // start on the tiles the previous pass left in L2
+  auto tile_of = [&](int mt, int t) {
+    if (!(mt & 1)) return t;
+    if (has_tree && t == 0) return n_prefix_tiles;
+    return n_prefix_tiles - 1 - (t - (has_tree ? 1 : 0));
+  };
 
   if (threadIdx.x == 0) {
+    if (smem_u32(smem_raw) & 1023u) __trap();
     tma_prefetch(&tmQ);
     tma_prefetch(&tmPool);
     tma_prefetch(&tmTree);
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 128);
+      mbar_init(&pv_done[i], 1);
     }
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 256);
     fence_barrier_init();
   }
   for (int s = threadIdx.x; s < S && s <= kMaxNodes; s += blockDim.x) s_anc[s] = a.row_anc[row0 + s];
@@ -174,183 +204,220 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // TMEM columns: stream h owns S buffers [128h, 128h+64) and [128h+64, 128h+128) and the O
+  // accumulator [256+128h, 256+128h+HD)
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(322);
 
   if (warp == 0) {
     // ------------------------------------------------------------------------- TMA producer
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int pr = 0; pr < n_pairs; ++pr) {
-        mbar_wait(q_empty, (pr & 1) ^ 1);
-        const int nm = min(2, n_mt - 2 * pr);
-        const uint32_t qbox = (uint32_t)(64 * G * spm * 2);
-        mbar_expect_tx(q_full, qbox * KB * nm);
-        for (int mi = 0; mi < nm; ++mi)
-          for (int kb = 0; kb < KB; ++kb)
-            tma_load_3d(sQ + mi * QT_BYTES + kb * 128 * 128, &tmQ, q_full, kb * 64, g * G,
-                        row0 + (2 * pr + mi) * spm);
+      const int* pages = a.block_table + (size_t)h * a.max_pages_per_seq + p_begin;
+      const int np = p_end - p_begin;
+      for (int mt = 0; mt < n_mt; ++mt) {
+        // page ids of the next prefix tile, loaded one tile ahead of their use
+        int pg0 = np > 0 ? __ldg(pages) : 0, pg1 = np > 1 ? __ldg(pages + 1) : pg0;
+        mbar_wait(q_empty, (mt & 1) ^ 1);
+        mbar_expect_tx(q_full, (uint32_t)(64 * G * spm * 2) * KB);
+        for (int kb = 0; kb < KB; ++kb) tma_load_3d(sQ + kb * 128 * 128, &tmQ, q_full, kb * 64, g * G, row0 + mt * spm);
+        const bool rev = mt & 1;   // odd passes walk the tiles backwards (L2 reuse of the last tiles)
+        if (rev && n_prefix_tiles > 0) {
+          const int tl = n_prefix_tiles - 1;
+          pg0 = __ldg(pages + 2 * tl);
+          pg1 = 2 * tl + 1 < np ? __ldg(pages + 2 * tl + 1) : pg0;
+        }
         for (int t = 0; t < ntiles; ++t) {
           mbar_wait(&kv_empty[stage], phase ^ 1);
           mbar_expect_tx(&kv_full[stage], 2 * KT_BYTES);
           uint8_t* dk = sK + stage * KT_BYTES;
           uint8_t* dv = sV + stage * KT_BYTES;
-          if (t < n_prefix_tiles) {
-            for (int half = 0; half < 2; ++half) {
-              int p = p_begin + 2 * t + half;
-              if (p >= p_end) p = p_begin + 2 * t;   // odd tail: reload a valid page, masked later
-              const int page = a.block_table[(size_t)h * a.max_pages_per_seq + p];
+          const int tt = tile_of(mt, t);
+          if (tt < n_prefix_tiles) {
+            const int cur0 = pg0, cur1 = pg1;
+            const int tn = rev ? tt - 1 : tt + 1;   // next prefix tile
+            if (tn >= 0 && tn < n_prefix_tiles) {
+              pg0 = __ldg(pages + 2 * tn);
+              pg1 = 2 * tn + 1 < np ? __ldg(pages + 2 * tn + 1) : pg0;
+            }
+            for (int hf = 0; hf < 2; ++hf) {
+              const int page = hf ? cur1 : cur0;   // odd tail: page 2t reloaded, masked later
               const int rk = (((a.layer * a.num_pages + page) * 2 + 0) * a.KV + g) * 64;
               const int rv = rk + a.KV * 64;
               for (int kb = 0; kb < KB; ++kb) {
-                tma_load_2d(dk + kb * 128 * 128 + half * 64 * 128, &tmPool, &kv_full[stage], kb * 64, rk);
-                tma_load_2d(dv + kb * 128 * 128 + half * 64 * 128, &tmPool, &kv_full[stage], kb * 64, rv);
+                tma_load_2d(dk + kb * 128 * 128 + hf * 64 * 128, &tmPool, &kv_full[stage], kb * 64, rk);
+                tma_load_2d(dv + kb * 128 * 128 + hf * 64 * 128, &tmPool, &kv_full[stage], kb * 64, rv);
               }
             }
           } else {
             const int rk = ((a.layer * 2 + 0) * a.KV + g) * a.R_cap + row0;
             const int rv = ((a.layer * 2 + 1) * a.KV + g) * a.R_cap + row0;
-            for (int half = 0; half < 2; ++half)
+            for (int hf = 0; hf < 2; ++hf)
               for (int kb = 0; kb < KB; ++kb) {
-                tma_load_2d(dk + kb * 128 * 128 + half * 64 * 128, &tmTree, &kv_full[stage], kb * 64, rk + 64 * half);
-                tma_load_2d(dv + kb * 128 * 128 + half * 64 * 128, &tmTree, &kv_full[stage], kb * 64, rv + 64 * half);
+                tma_load_2d(dk + kb * 128 * 128 + hf * 64 * 128, &tmTree, &kv_full[stage], kb * 64, rk + 64 * hf);
+                tma_load_2d(dv + kb * 128 * 128 + hf * 64 * 128, &tmTree, &kv_full[stage], kb * 64, rv + 64 * hf);
               }
           }
-          if (++stage == 2) { stage = 0; phase ^= 1; }
+          if (mt == 0) TRACE(t);
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------------- MMA issuer
     if (elect_one()) {
-      const uint32_t id_qk = idesc_f16(128, 128, false);
+      const uint32_t id_qk = idesc_f16(128, 64, false);
       const uint32_t id_pv = idesc_f16(128, HD, true);
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t sp_phase[2] = {0, 0};
-      for (int pr = 0; pr < n_pairs; ++pr) {
-        const int nm = min(2, n_mt - 2 * pr);
-        mbar_wait(q_full, pr & 1);
-        // the epilogue of the previous pair must have drained O before it is re-initialised
-        for (int mi = 0; mi < nm; ++mi) mbar_wait(&o_empty[mi], (pr & 1) ^ 1);
-        tc_fence_after();
-        // S_m(t+1) is issued right behind PV_m(t) so that the softmax of tile t+1 for one M-tile
-        // overlaps the MMAs and softmax of the other (tcgen05.mma executes in issue order, so
-        // S_m(t+1) cannot overwrite P_m(t) before PV_m(t) has read it).
-        auto issue_qk = [&](int mi, uint32_t kaddr) {
-          const uint32_t qaddr = smem_u32(sQ + mi * QT_BYTES);
-          const uint32_t s_tm = tmem + mi * 256;
+      uint32_t sfill = 0;        // S tiles filled so far per stream (all passes): buffer = sfill & 1
+      uint32_t pcons = 0;        // P tiles consumed so far per stream
+      // S_hs = Q K_hs^T for the 64 keys [64hs, 64hs+64) of the tile in stage `st`
+      auto issue_qk = [&](int st) {
+        const uint32_t qaddr = smem_u32(sQ);
+        const uint32_t kaddr = smem_u32(sK + st * KT_BYTES);
+#pragma unroll
+        for (int hs = 0; hs < 2; ++hs) {
+          const uint32_t s_tm = tmem + hs * 128 + (sfill & 1) * 64;
 #pragma unroll
           for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              tc_mma_f16(s_tm, umma_desc_sw128(qaddr + kb * 16384 + k * 32), umma_desc_sw128(kaddr + kb * 16384 + k * 32),
-                         id_qk, (kb | k) != 0);
-          tc_commit(&s_full[mi]);
-        };
+              tc_mma_f16(s_tm, umma_desc_sw128(qaddr + kb * 16384 + k * 32),
+                         umma_desc_sw128(kaddr + kb * 16384 + hs * 8192 + k * 32), id_qk, (kb | k) != 0);
+          tc_commit(&s_full[hs * 2 + (sfill & 1)]);
+        }
+        ++sfill;
+      };
+      for (int mt = 0; mt < n_mt; ++mt) {
+        mbar_wait(q_full, mt & 1);
+        mbar_wait(o_empty, (mt & 1) ^ 1);   // previous pass's O has been drained
+        tc_fence_after();
         if (ntiles > 0) {
           mbar_wait(&kv_full[stage], phase);
           tc_fence_after();
-          for (int mi = 0; mi < nm; ++mi) issue_qk(mi, smem_u32(sK + stage * KT_BYTES));
+          issue_qk(stage);
         }
         for (int t = 0; t < ntiles; ++t) {
-          const int nstage = stage ^ 1;
-          const uint32_t nphase = phase ^ (stage == 1 ? 1u : 0u);
-          const uint32_t vaddr = smem_u32(sV + stage * KT_BYTES);
-          for (int mi = 0; mi < nm; ++mi) {
-            mbar_wait(&p_full[mi], sp_phase[mi]);
-            sp_phase[mi] ^= 1;
+          int nst = stage + 1;
+          uint32_t nph = phase;
+          if (nst == NST) { nst = 0; nph ^= 1; }
+          // S(t+1) into the other S buffers while the softmax works on S(t).  In-order tcgen05
+          // execution: S(t+1) overwrites P(t-1) only after PV(t-1), issued before it, has read it.
+          if (t + 1 < ntiles) {
+            mbar_wait(&kv_full[nst], nph);
             tc_fence_after();
-            const uint32_t p_tm = tmem + mi * 256;
-            const uint32_t o_tm = tmem + mi * 256 + 128;
+            issue_qk(nst);
+          }
+          const uint32_t b = pcons & 1;
+          const uint32_t vaddr = smem_u32(sV + stage * KT_BYTES);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {   // 16 keys (8 packed fp16 columns) per k-step
-              const uint64_t bd = umma_desc_mn_sw128(vaddr + k * 2048, 128 * 128);
+          for (int hs = 0; hs < 2; ++hs) {
+            mbar_wait(&p_full[hs * 2 + b], (pcons >> 1) & 1);
+            if (mt == 0 && hs == 0) TRACE(128 + t);
+            tc_fence_after();
+            const uint32_t p_tm = tmem + hs * 128 + b * 64;
+            const uint32_t o_tm = tmem + 256 + hs * 128;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {   // 16 keys (8 packed fp16 columns) per k-step
+              const uint64_t bd = umma_desc_mn_sw128(vaddr + hs * 8192 + k * 2048, 128 * 128);
               tc_mma_ts(o_tm, p_tm + k * 8, bd, id_pv, (t | k) != 0);
             }
-            if (mi == nm - 1) tc_commit(&kv_empty[stage]);
-            if (t + 1 < ntiles) {
-              if (mi == 0) {
-                mbar_wait(&kv_full[nstage], nphase);
-                tc_fence_after();
-              }
-              issue_qk(mi, smem_u32(sK + nstage * KT_BYTES));
-            }
+            tc_commit(&pv_done[hs * 2 + b]);
           }
-          stage = nstage;
-          phase = nphase;
+          tc_commit(&kv_empty[stage]);
+          ++pcons;
+          stage = nst;
+          phase = nph;
         }
-        for (int mi = 0; mi < nm; ++mi) tc_commit(&o_full[mi]);
+        tc_commit(o_full);
         tc_commit(q_empty);
       }
     }
   } else {
     // ------------------------------------------------------------------ softmax + epilogue
-    const int wg = (warp - 2) >> 2;           // M-tile slot of this warpgroup
+    // warps 2..9: stream hs = (warp-2)/4 owns keys [64hs, 64hs+64) of every KV tile with its own
+    // running max m, sum l and accumulator O_hs (an in-CTA 2-way KV split: the two streams never
+    // synchronise per tile, so the 2 warps sharing an SM sub-partition overlap each other's
+    // TMEM/MUFU latencies).  Both streams of a row live in the same TMEM lane quarter.
+    const int hs = (warp - 2) >> 2;
     const int q = warp & 3;                   // TMEM lane quarter
     const int rl = q * 32 + lane;             // row within the M-tile (= TMEM lane)
+    const int et = threadIdx.x - 64;          // 0..255
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t s_base = tmem + hs * 128 + lane_off;
+    const uint32_t o_own = tmem + 256 + hs * 128 + lane_off;
     const float sl2 = a.scale_log2;
-    uint32_t s_phase = 0;
-    for (int pr = 0; pr < n_pairs; ++pr) {
-      const int mt = 2 * pr + wg;
-      const bool active_mt = mt < n_mt;
-      if (!active_mt) continue;
+#define FTRACE(k) \
+  do {            \
+    if (et == 0 && mt < 2 && t < 16) TRACE((mt ? 448 : 384) + 4 * t + (k)); \
+  } while (0)
+    uint32_t scons = 0;   // S tiles consumed (all passes)
+    for (int mt = 0; mt < n_mt; ++mt) {
       const int rows_mt = min(spm, S - mt * spm) * G;   // valid rows in this M-tile
       const bool valid_row = rl < rows_mt;
       const int slot = mt * spm + rl / G;
       const int j = rl % G;
       const uint64_t anc = (valid_row && slot > 0) ? s_anc[slot] : 0ull;
-      const uint32_t s_tm = tmem + wg * 256 + ((uint32_t)(q * 32) << 16);
-      const uint32_t o_tm = s_tm + 128;
       float m_used = -INFINITY, l = 0.f;
-      for (int t = 0; t < ntiles; ++t) {
-        mbar_wait(&s_full[wg], s_phase);
-        s_phase ^= 1;
+      for (int t = 0; t < ntiles; ++t, ++scons) {
+        const uint32_t b = scons & 1;
+        const uint32_t s_tm = s_base + b * 64;
+        mbar_wait(&s_full[hs * 2 + b], (scons >> 1) & 1);
+        if (mt == 0 && et == 0) TRACE(192 + t);
         tc_fence_after();
-        const bool tree = t >= n_prefix_tiles;
-        // 128-bit visibility mask of this tile's keys for this row
-        uint32_t mk[4] = {0u, 0u, 0u, 0u};
+        const int tt = tile_of(mt, t);
+        const bool tree = tt >= n_prefix_tiles;
+        // 64-bit visibility mask of my stream's keys in this tile
+        uint32_t mk[2] = {0u, 0u};
         if (valid_row) {
           if (!tree) {
-            const int key0 = (p_begin + 2 * t) * 64;
+            const int key0 = (p_begin + 2 * tt) * 64;
             int kvalid = min(128, L - key0);
-            if (p_begin + 2 * t + 1 >= p_end) kvalid = min(kvalid, 64);
+            if (p_begin + 2 * tt + 1 >= p_end) kvalid = min(kvalid, 64);
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              const int n = kvalid - 32 * w;
+            for (int w = 0; w < 2; ++w) {
+              const int n = kvalid - 64 * hs - 32 * w;
               mk[w] = n >= 32 ? 0xFFFFFFFFu : (n <= 0 ? 0u : ((1u << n) - 1u));
             }
           } else {
             // key 0 = root, key k >= 1 = node k-1: visible iff root or ancestor-or-self of my node
             const uint64_t lo = slot > 0 ? ((anc << 1) | 1ull) : 1ull;
-            mk[0] = (uint32_t)lo;
-            mk[1] = (uint32_t)(lo >> 32);
-            mk[2] = slot > 0 ? (uint32_t)(anc >> 63) : 0u;
+            const uint32_t w0 = hs ? (slot > 0 ? (uint32_t)(anc >> 63) : 0u) : (uint32_t)lo;
+            const uint32_t w1 = hs ? 0u : (uint32_t)(lo >> 32);
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              const int n = S - 32 * w;
-              mk[w] &= n >= 32 ? 0xFFFFFFFFu : (n <= 0 ? 0u : ((1u << n) - 1u));
+            for (int w = 0; w < 2; ++w) {
+              const int n = S - 64 * hs - 32 * w;
+              mk[w] = (w ? w1 : w0) & (n >= 32 ? 0xFFFFFFFFu : (n <= 0 ? 0u : ((1u << n) - 1u)));
             }
           }
         }
-        const bool any_valid = __any_sync(0xffffffffu, (mk[0] | mk[1] | mk[2] | mk[3]) != 0u);
-        if (any_valid) {
-          // the whole row of 128 scores in registers
-          uint32_t sv[128];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_tm + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * c));
+        const bool any0 = __any_sync(0xffffffffu, mk[0] != 0u);
+        const bool any1 = __any_sync(0xffffffffu, mk[1] != 0u);
+        const bool full = __all_sync(0xffffffffu, (mk[0] & mk[1]) == 0xFFFFFFFFu);
+        if (any0 || any1) {
+          uint32_t sv[64];
+          tmem_ld_32x32b_x32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
+          tmem_ld_32x32b_x32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
           tmem_ld_wait();
-          const bool full = __all_sync(0xffffffffu, (mk[0] & mk[1] & mk[2] & mk[3]) == 0xFFFFFFFFu);
-          float mx = -INFINITY;
+          FTRACE(0);
+          float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
           if (full) {
 #pragma unroll
-            for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
+            for (int e = 0; e < 64; e += 4) {
+              m0 = fmaxf(m0, __uint_as_float(sv[e]));
+              m1 = fmaxf(m1, __uint_as_float(sv[e + 1]));
+              m2 = fmaxf(m2, __uint_as_float(sv[e + 2]));
+              m3 = fmaxf(m3, __uint_as_float(sv[e + 3]));
+            }
           } else {
 #pragma unroll
-            for (int e = 0; e < 128; ++e)
-              mx = fmaxf(mx, ((mk[e >> 5] >> (e & 31)) & 1u) ? __uint_as_float(sv[e]) : -INFINITY);
+            for (int e = 0; e < 64; ++e)
+              m0 = fmaxf(m0, ((mk[e >> 5] >> (e & 31)) & 1u) ? __uint_as_float(sv[e]) : -INFINITY);
           }
-          mx *= sl2;
+          const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
+          FTRACE(1);
           float alpha = 1.f;
           bool rescale = false;
           if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
@@ -360,97 +427,127 @@ __global__ void __launch_bounds__(kThreads, 1)
             m_used = mx;
           }
           const float mb = m_used == -INFINITY ? 0.f : m_used;
-          // P = 2^(s*scale - m) as packed fp16 pairs into the first 64 columns of this S region,
-          // 32 keys (16 columns) at a time (column 16c <= 32c: never overwrites unread scores)
-          float ls = 0.f;
+          // P = 2^(s*scale - m) as packed fp16 pairs: my 64 keys -> columns [0, 32) of the buffer
+          float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < 2; ++c) {
             uint32_t pk[16];
             if (full) {
 #pragma unroll
               for (int e = 0; e < 32; e += 2) {
                 const float p0 = ex2f(fmaf(__uint_as_float(sv[32 * c + e]), sl2, -mb));
                 const float p1 = ex2f(fmaf(__uint_as_float(sv[32 * c + e + 1]), sl2, -mb));
-                ls += p0 + p1;
+                ls0 += p0;
+                ls1 += p1;
                 pk[e >> 1] = pack2(p0, p1);
               }
-            } else {
+            } else if (c ? any1 : any0) {
 #pragma unroll
               for (int e = 0; e < 32; e += 2) {
                 const float p0 = ((mk[c] >> e) & 1u) ? ex2f(fmaf(__uint_as_float(sv[32 * c + e]), sl2, -mb)) : 0.f;
                 const float p1 = ((mk[c] >> (e + 1)) & 1u) ? ex2f(fmaf(__uint_as_float(sv[32 * c + e + 1]), sl2, -mb)) : 0.f;
-                ls += p0 + p1;
+                ls0 += p0;
+                ls1 += p1;
                 pk[e >> 1] = pack2(p0, p1);
               }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) pk[e] = 0u;
             }
             tmem_st_32x32b_x16(s_tm + 16 * c, pk);
           }
-          l += ls;
-          if (rescale) {
-            // O *= alpha before PV of this tile (PV of tile t-1 is complete: s_full of this tile
-            // was committed after it)
+          l += ls0 + ls1;
+          FTRACE(2);
+          if (__any_sync(0xffffffffu, rescale)) {
+            // O_hs *= alpha: PV_hs(t-1) writes O_hs and may still be in flight -> wait for it
+            const uint32_t pb = (scons - 1) & 1;
+            mbar_wait(&pv_done[hs * 2 + pb], ((scons - 1) >> 1) & 1);
+            tc_fence_after();
+            if (rescale) {
 #pragma unroll 1
-            for (int c = 0; c < HD / 32; ++c) {
-              uint32_t ov[32];
-              tmem_ld_32x32b_x32(o_tm + c * 32, ov);
-              tmem_ld_wait();
+              for (int c = 0; c < HD / 32; ++c) {
+                uint32_t ov[32];
+                tmem_ld_32x32b_x32(o_own + c * 32, ov);
+                tmem_ld_wait();
 #pragma unroll
-              for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-              tmem_st_32x32b_x32(o_tm + c * 32, ov);
+                for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+                tmem_st_32x32b_x32(o_own + c * 32, ov);
+              }
             }
           }
+        } else {
+          // no visible key of my stream for any row of this warp: P = 0
+          uint32_t z[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) z[e] = 0u;
+          tmem_st_32x32b_x16(s_tm, z);
+          tmem_st_32x32b_x16(s_tm + 16, z);
         }
         tmem_st_wait();
+        FTRACE(3);
+        if (mt == 0 && et == 0) TRACE(256 + t);
         tc_fence_before();
-        mbar_arrive(&p_full[wg]);
+        mbar_arrive(&p_full[hs * 2 + b]);
       }
-      // epilogue: O of this M-tile
-      mbar_wait(&o_full[wg], pr & 1);
+      // epilogue: merge the two streams (m_h, l_h, O_h) of every row; warp (q, hs) writes the
+      // head-dim columns [hs*HD/2, hs*HD/2 + HD/2)
+      s_ml[hs * 256 + rl] = m_used;
+      s_ml[hs * 256 + 128 + rl] = l;
+      mbar_wait(o_full, mt & 1);
+      if (mt == 0 && et == 0) TRACE(320);
       tc_fence_after();
+      named_bar_sync(2, 256);
+      const float ma = s_ml[rl], mbv = s_ml[256 + rl];
+      const float ms = fmaxf(ma, mbv);
+      const float c0 = ma == -INFINITY ? 0.f : ex2f(ma - ms);
+      const float c1 = mbv == -INFINITY ? 0.f : ex2f(mbv - ms);
+      const float lt = s_ml[128 + rl] * c0 + s_ml[384 + rl] * c1;
       const size_t rh = (size_t)(row0 + slot) * a.H + (size_t)g * G + j;
       const bool single = a.n_splits == 1;
-      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const float inv = single ? (lt > 0.f ? 1.f / lt : 0.f) : 1.f;
+      const float f0 = c0 * inv, f1 = c1 * inv;
 #pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t ov[32];
-        tmem_ld_32x32b_x32(o_tm + c * 32, ov);
+      for (int c = 0; c < HD / 64; ++c) {
+        const int col = hs * (HD / 2) + c * 32;
+        uint32_t oa[32], ob[32];
+        tmem_ld_32x32b_x32(tmem + 256 + lane_off + col, oa);
+        tmem_ld_32x32b_x32(tmem + 384 + lane_off + col, ob);
         tmem_ld_wait();
+        float ov[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) ov[e] = __uint_as_float(oa[e]) * f0 + __uint_as_float(ob[e]) * f1;
         if (valid_row) {
           if (single) {
             if (ta.O) {
-              uint4* dst = reinterpret_cast<uint4*>(ta.O + rh * HD + c * 32);
+              uint4* dst = reinterpret_cast<uint4*>(ta.O + rh * HD + col);
 #pragma unroll
               for (int e = 0; e < 32; e += 8)
-                dst[e / 8] = make_uint4(pack2_bf16(__uint_as_float(ov[e]) * inv, __uint_as_float(ov[e + 1]) * inv),
-                                        pack2_bf16(__uint_as_float(ov[e + 2]) * inv, __uint_as_float(ov[e + 3]) * inv),
-                                        pack2_bf16(__uint_as_float(ov[e + 4]) * inv, __uint_as_float(ov[e + 5]) * inv),
-                                        pack2_bf16(__uint_as_float(ov[e + 6]) * inv, __uint_as_float(ov[e + 7]) * inv));
+                dst[e / 8] = make_uint4(pack2_bf16(ov[e], ov[e + 1]), pack2_bf16(ov[e + 2], ov[e + 3]),
+                                        pack2_bf16(ov[e + 4], ov[e + 5]), pack2_bf16(ov[e + 6], ov[e + 7]));
             }
             if (ta.O_f32) {
-              float4* dst = reinterpret_cast<float4*>(ta.O_f32 + rh * HD + c * 32);
+              float4* dst = reinterpret_cast<float4*>(ta.O_f32 + rh * HD + col);
 #pragma unroll
-              for (int e = 0; e < 32; e += 4)
-                dst[e / 4] = make_float4(__uint_as_float(ov[e]) * inv, __uint_as_float(ov[e + 1]) * inv,
-                                         __uint_as_float(ov[e + 2]) * inv, __uint_as_float(ov[e + 3]) * inv);
+              for (int e = 0; e < 32; e += 4) dst[e / 4] = make_float4(ov[e], ov[e + 1], ov[e + 2], ov[e + 3]);
             }
           } else {
-            float4* dst = reinterpret_cast<float4*>(a.opart + ((size_t)sp * a.R * a.H + rh) * HD + c * 32);
+            float4* dst = reinterpret_cast<float4*>(a.opart + ((size_t)sp * a.R * a.H + rh) * HD + col);
 #pragma unroll
-            for (int e = 0; e < 32; e += 4)
-              dst[e / 4] = make_float4(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1]), __uint_as_float(ov[e + 2]),
-                                       __uint_as_float(ov[e + 3]));
+            for (int e = 0; e < 32; e += 4) dst[e / 4] = make_float4(ov[e], ov[e + 1], ov[e + 2], ov[e + 3]);
           }
         }
       }
-      if (valid_row && !single) {
-        a.mpart[(size_t)sp * a.R * a.H + rh] = m_used;
-        a.lpart[(size_t)sp * a.R * a.H + rh] = l;
+      if (valid_row && !single && hs == 0) {
+        a.mpart[(size_t)sp * a.R * a.H + rh] = ms;
+        a.lpart[(size_t)sp * a.R * a.H + rh] = lt;
       }
       tc_fence_before();
-      mbar_arrive(&o_empty[wg]);
+      mbar_arrive(o_empty);
+      named_bar_sync(2, 256);   // s_ml reuse by the next pass
     }
   }
   __syncthreads();
+  TRACE(321);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -501,8 +598,10 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
   if (!encode_fn() || !tmap_q(&tq, a.Q, (uint64_t)a.R, a.H, HD, a.G, spm) || !tmap_rows(&tp, a.pool, pool_rows, HD) ||
       !tmap_rows(&tt, a.tree_kv, tree_rows, HD))
     return cudaErrorInvalidValue;
-  TcArgs ta{a, O, O_f32, spm};
-  const size_t smem = 1024 + 2 * (size_t)128 * HD * 2 * 3 + 16 * 8 + 66 * 8 + 64;
+  static unsigned long long* trace = nullptr;
+  if (getenv("SPECEDGE_ATTN_TRACE") && !trace) cudaMalloc(&trace, 512 * 8);
+  TcArgs ta{a, O, O_f32, spm, trace};
+  const size_t smem = (size_t)128 * HD * 2 * (1 + 2 * kStages) + 8 * 24 + 66 * 8 + 512 * 4;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_attn_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -510,11 +609,37 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
     attr = true;
   }
   dim3 grid(B * a.KV, a.n_splits);
+  if (trace) cudaMemsetAsync(trace, 0, 512 * 8, st);
   k_attn_tc<HD><<<grid, kThreads, smem, st>>>(tq, tp, tt, ta);
+  if (trace) {
+    static int calls = 0;
+    unsigned long long h[512];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+    if (++calls % 32 == 5) {   // one layer per step
+      const unsigned long long t0 = h[322];
+      auto d = [&](int i) { return h[i] ? (long long)(h[i] - t0) : -1LL; };
+      fprintf(stderr, "attn trace (cycles from start): end=%lld o_full=%lld\n", d(321), d(320));
+      for (int t = 0; t < 12; ++t)
+        fprintf(stderr, "  tile %2d: tma_issued=%7lld s_ready(wg0)=%7lld p_done(wg0)=%7lld mma_got_p0=%7lld\n", t, d(t),
+                d(192 + t), d(256 + t), d(128 + t));
+      for (int m = 0; m < 2; ++m)
+        for (int t = 0; t < 10; ++t) {
+          const int b = (m ? 448 : 384) + 4 * t;
+          fprintf(stderr, "  pass %d tile %2d: ld=%7lld bar=%7lld exp=%7lld st=%7lld\n", m, t, d(b), d(b + 1), d(b + 2),
+                  d(b + 3));
+        }
+    }
+  }
   return cudaGetLastError();
 }
 
 }  // namespace
+
+unsigned long long* attention_tc_trace_ptr() {
+  static unsigned long long* p = nullptr;
+  return p;
+}
 
 bool attention_tc_supported(int hd, int G) { return (hd == 64 || hd == 128) && G >= 1 && G <= 128; }
 

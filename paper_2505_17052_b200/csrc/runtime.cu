@@ -725,9 +725,13 @@ specedge_status specedge_prefill(specedge_model* m, specedge_kvpool* pool, int32
   CK(cudaStreamSynchronize(st));
   CK(cudaMemcpy(&L, pool->cache_len + h, sizeof(int), cudaMemcpyDeviceToHost));
   if (L + n - 1 > pool->handle_cap[h]) return SPECEDGE_E_INVALID;
+  // largest chain chunk whose (1 request, cn + 1 rows) layout fits the caller's workspace
+  int max_cn = SPECEDGE_MAX_NODES;
+  while (max_cn > 0 && ws_layout(m->cfg, 1, max_cn + 1).total > ws_bytes) --max_cn;
+  if (ws_layout(m->cfg, 1, 1).total > ws_bytes) return SPECEDGE_E_WORKSPACE;
   int i = 0;
   while (i < n - 1) {
-    const int cn = std::min(SPECEDGE_MAX_NODES, n - 2 - i);   // chain nodes after the root tokens[i]
+    const int cn = std::min(max_cn, n - 2 - i);   // chain nodes after the root tokens[i]
     const int B = 1, T = cn, R = T + 1;
     const WsLayout w = ws_layout(m->cfg, B, R);
     if (!workspace || ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
