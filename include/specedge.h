@@ -94,6 +94,29 @@ specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t
                                       int32_t device, specedge_model** out);
 specedge_status specedge_model_destroy(specedge_model* model);
 
+/* ---- tensor parallelism (SURVEY §8(a) a12, §8(e) "Tensor parallel TP = 8"; cfg4) ----
+ * One process per GPU; every rank creates its shard with the same cfg / weight_seed and the
+ * same 128-byte NCCL unique id (from specedge_tp_unique_id on one rank, broadcast by the caller).
+ * Rank k holds: q heads [k*H/tp, (k+1)*H/tp) and kv heads [k*KV/tp, ...) (head-parallel attention;
+ * the KV pool of this model stores only those kv heads), gate/up rows [k*F/tp, ...) (column
+ * parallel), the matching input columns of Wo and Wd (row parallel; their fp32 [R, d] outputs
+ * are summed over ranks by an NCCL all-reduce on the verify stream: C1 after O, C2 after down),
+ * the LM-head rows [v0, v0+vn) with vn = ceil(V/tp) (vocab parallel; the per-row (score, id)
+ * winners are all-gathered and reduced, ties -> lowest id: C3).  Embedding, norms, walk and
+ * commit are replicated.  Every shard is bit-identical to the corresponding slice of the
+ * tp_size == 1 model.  Requires n_heads, n_kv divisible by tp_size and ffn by 64*tp_size, else
+ * E_UNSUPPORTED; E_UNSUPPORTED also when libnccl.so.2 cannot be loaded.  All ranks must call
+ * every verify / prefill with identical inputs (collectives are issued in program order).
+ * Synchronous (NCCL communicator creation blocks until all ranks joined). */
+specedge_status specedge_tp_unique_id(uint8_t* nccl_id /* [128] host */);
+specedge_status specedge_model_create_tp(const specedge_model_config* cfg, uint64_t weight_seed,
+                                         int32_t device, int32_t tp_rank, int32_t tp_size,
+                                         const uint8_t* nccl_id /* [128] host, NULL iff tp_size == 1 */,
+                                         specedge_model** out);
+/* This rank's position and LM-head vocab shard [vocab0, vocab0 + vocab_n); NULL outputs skipped. */
+specedge_status specedge_model_tp_info(const specedge_model* model, int32_t* tp_rank,
+                                       int32_t* tp_size, int32_t* vocab0, int32_t* vocab_n);
+
 /* KV page pool of `num_pages` pages x 64 tokens x all layers (fp16 K and V), zero-initialised,
  * with room for `max_handles` sessions.  Synchronous. */
 specedge_status specedge_kvpool_create(specedge_model* model, int32_t num_pages,
@@ -205,7 +228,7 @@ specedge_status specedge_debug_gemm(const uint16_t* W, const uint16_t* X, float*
                                     int32_t R, int32_t K, void* stream);
 /* Run the LM-head GEMM (same tcgen05 kernel, fp32-store epilogue) on the final-norm hidden
  * states left in the workspace by the last verify of (num_requests, R): writes fp32 logits
- * [R][V] to logits_dev.  Test-only; the verify path itself never materialises logits. */
+ * [R][vocab_n] (this rank's vocab shard, all of V when tp_size == 1) to logits_dev.  Test-only; the verify path itself never materialises logits. */
 specedge_status specedge_debug_last_logits(specedge_model* model, void* workspace,
                                            size_t ws_bytes, int32_t num_requests, int32_t R,
                                            float* logits_dev, void* stream);

@@ -24,7 +24,8 @@ EXPORTS = [
     "specedge_verify_batch", "specedge_kv_commit", "specedge_verify_batch_host",
     "specedge_debug_weight_rows", "specedge_debug_read_kv", "specedge_debug_gemm",
     "specedge_debug_last_logits", "specedge_debug_attention", "specedge_last_launch_count",
-    "specedge_set_kernel_timing", "specedge_kernel_times",
+    "specedge_set_kernel_timing", "specedge_kernel_times", "specedge_tp_unique_id", "specedge_model_create_tp",
+    "specedge_model_tp_info",
 ]
 KERNEL_KINDS = ["prep", "embed", "rmsnorm", "gemm_qkv", "attention", "attn_combine", "gemm_o", "gemm_gateup",
                 "gemm_down", "gemm_lmhead", "lm_reduce", "walk", "commit", "qkv_rope"]
@@ -86,6 +87,9 @@ def load(path: str = LIB_PATH):
         "specedge_last_launch_count": [],
         "specedge_set_kernel_timing": [I32],
         "specedge_kernel_times": [P, P, I32],
+        "specedge_tp_unique_id": [P],
+        "specedge_model_create_tp": [C.POINTER(ModelConfig), U64, I32, I32, I32, P, C.POINTER(P)],
+        "specedge_model_tp_info": [P, P, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

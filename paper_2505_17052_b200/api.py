@@ -37,10 +37,21 @@ class Shape:
         return cls(s.n_layers, s.d, s.n_heads, s.n_kv, s.head_dim, s.ffn, s.vocab, s.eps, s.rope_theta)
 
 
+def tp_unique_id() -> bytes:
+    """128-byte NCCL unique id for specedge_model_create_tp (call on one rank, broadcast)."""
+    lib = L.load()
+    buf = (C.c_uint8 * 128)()
+    L.check(lib.specedge_tp_unique_id(C.cast(buf, C.c_void_p)), "tp_unique_id")
+    return bytes(buf)
+
+
 class Model:
     """A target decoder with synthetic weights (Philox(seed), generated on the device)."""
 
-    def __init__(self, shape, weight_seed: int, device: int = 0, max_position: int = 32768):
+    def __init__(self, shape, weight_seed: int, device: int = 0, max_position: int = 32768,
+                 tp_rank: int = 0, tp_size: int = 1, nccl_id: bytes | None = None):
+        """tp_size > 1: this process's tensor-parallel shard (include/specedge.h,
+        specedge_model_create_tp); every rank passes the same `nccl_id` (see tp_unique_id)."""
         if not torch.cuda.is_available():
             raise RuntimeError("libspecedge needs a CUDA device (sm_100a); no fallback exists")
         self.lib = L.load()
@@ -49,10 +60,25 @@ class Model:
         cfg = L.ModelConfig(shape.n_layers, shape.d, shape.n_heads, shape.n_kv, shape.head_dim,
                             shape.ffn, shape.vocab, shape.eps, shape.rope_theta, max_position)
         h = C.c_void_p()
-        L.check(self.lib.specedge_model_create(C.byref(cfg), C.c_uint64(weight_seed), device, C.byref(h)),
-                "model_create")
+        if tp_size == 1:
+            L.check(self.lib.specedge_model_create(C.byref(cfg), C.c_uint64(weight_seed), device, C.byref(h)),
+                    "model_create")
+        else:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("tp_size > 1 needs the 128-byte NCCL id from tp_unique_id()")
+            idb = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+            L.check(self.lib.specedge_model_create_tp(C.byref(cfg), C.c_uint64(weight_seed), device, tp_rank,
+                                                      tp_size, C.cast(idb, C.c_void_p), C.byref(h)),
+                    "model_create_tp")
         self.h = h
         self.max_position = max_position
+        self.tp_rank, self.tp_size = tp_rank, tp_size
+        v0, vn = C.c_int32(), C.c_int32()
+        L.check(self.lib.specedge_model_tp_info(h, None, None, C.byref(v0), C.byref(vn)), "model_tp_info")
+        self.vocab0, self.vocab_n = v0.value, vn.value
+        # rank-local head counts (the KV pool of this model stores n_kv_local heads)
+        self.n_heads_local = shape.n_heads // tp_size
+        self.n_kv_local = shape.n_kv // tp_size
 
     def close(self):
         if self.h:
@@ -117,7 +143,7 @@ class KVPool:
 
     def read_kv(self, handle: int, layer: int, kv_sel: int, pos0: int, n: int) -> np.ndarray:
         s = self.model.shape
-        out = np.empty((n, s.n_kv, s.head_dim), np.uint16)
+        out = np.empty((n, self.model.n_kv_local, s.head_dim), np.uint16)
         L.check(self.lib.specedge_debug_read_kv(self.h, handle, layer, kv_sel, pos0, n,
                                                 out.ctypes.data_as(C.c_void_p)), "debug_read_kv")
         return out
@@ -280,7 +306,9 @@ def debug_attention(q, k_prefix, v_prefix, k_tree, v_tree, anc, n_splits=1, stre
 
 
 def debug_last_logits(model: Model, ws: torch.Tensor, batch: Batch, stream=None) -> torch.Tensor:
-    out = torch.empty((batch.rows, model.shape.vocab), dtype=torch.float32, device=ws.device)
+    """fp32 logits of the last verify's rows over this rank's vocab shard
+    [model.vocab0, model.vocab0 + model.vocab_n) (all of V when tp_size == 1)."""
+    out = torch.empty((batch.rows, model.vocab_n), dtype=torch.float32, device=ws.device)
     L.check(model.lib.specedge_debug_last_logits(model.h, _ptr(ws), ws.numel(), batch.num_requests, batch.rows,
                                                  _ptr(out), _stream(stream)), "debug_last_logits")
     return out

@@ -109,7 +109,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           float s = -INFINITY;
           if (fv && 2 * jj < ncol && row < a.R) {
             s = __uint_as_float(v[2 * jj]) + __uint_as_float(v[2 * jj + 1]);
-            if (a.sample) s = s * a.inv_t + gumbel_noise(a, row >> 1, feat);
+            if (a.sample) s = s * a.inv_t + gumbel_noise(a, row >> 1, a.vocab_off + feat);
           }
           xch[tl * kXchStride + jj] = s;
         }
@@ -120,7 +120,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           float s = -INFINITY;
           if (fv && jj < ncol && row < a.R) {
             s = __uint_as_float(v[jj]);
-            if (a.sample) s = s * a.inv_t + gumbel_noise(a, row, feat);
+            if (a.sample) s = s * a.inv_t + gumbel_noise(a, row, a.vocab_off + feat);
           }
           xch[tl * kXchStride + jj] = s;
         }
@@ -133,7 +133,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         int bi = 0x7fffffff;
         for (int l = 0; l < per; ++l) {
           const float s = xch[(g * per + l) * kXchStride + jj];
-          if (s > best) { best = s; bi = m128 * 128 + g * per + l; }
+          if (s > best) { best = s; bi = a.vocab_off + m128 * 128 + g * per + l; }
         }
         red_v[g * np + jj] = best;
         red_i[g * np + jj] = bi;

@@ -47,7 +47,8 @@ struct GemmArgs {
   // EPI_ARGMAX
   float* part_val;        // [R][n_tiles_m]
   int* part_idx;
-  int vocab, sample;
+  int vocab, sample;      // vocab: rows of this (vocab-shard) LM head
+  int vocab_off;          // global id of local row 0 (tensor parallel vocab shard)
   float inv_t;
   uint32_t seed_lo, seed_hi;
   const int* row_req;
@@ -185,10 +186,23 @@ struct InitArgs {
   float scale0, scale1, scale2;
   int gain;                   // 1: bf16(i24*2^-25 + 1)
   uint32_t k0, k1;
+  // tensor-parallel shards: element (prow, col) of the local tensor is element
+  // (off[part] + lrow, col0 + col) of the global [*, gcols] matrix of its part
+  long long off0, off1, off2, col0, gcols;
 };
 cudaError_t init_weights_launch(const InitArgs& a, cudaStream_t st);
+
+// tensor parallelism (tp.cu): NCCL resolved at run time
+constexpr int kMaxTp = 16;
+bool tp_available();
+int tp_unique_id(uint8_t* out128);
+int tp_comm_init(void** comm, const uint8_t* id128, int rank, int size);
+void tp_comm_destroy(void* comm);
+cudaError_t tp_allreduce_f32(float* buf, size_t n, void* comm, cudaStream_t st);
+cudaError_t tp_argmax_gather(int* y, float* score, int R, float* gather, int tp, void* comm, int* row_target,
+                             float* row_score, cudaStream_t st, int* launches);
 cudaError_t kv_fill_launch(f16* pool, const int* block_row, int layers, int num_pages, int KV,
-                           int hd, int n_tokens, uint32_t k0, uint32_t k1, uint32_t stream_id,
+                           int hd, int n_tokens, uint32_t k0, uint32_t k1, uint32_t stream_id, int kv_head0,
                            cudaStream_t st);
 
 }  // namespace se
@@ -197,8 +211,14 @@ cudaError_t kv_fill_launch(f16* pool, const int* block_row, int layers, int num_
 // opaque handle definitions
 // ---------------------------------------------------------------------------------------------
 struct specedge_model {
-  specedge_model_config cfg;
+  specedge_model_config cfg;    // rank-local shapes: n_heads, n_kv, ffn are this rank's shares
+  specedge_model_config gcfg;   // global model
   int device;
+  int tp_rank = 0, tp_size = 1;
+  int v0 = 0, vl = 0;           // LM-head vocab shard [v0, v0 + vl)
+  void* nccl = nullptr;         // ncclComm_t when tp_size > 1
+  float* tp_gather = nullptr;   // [tp_size][R_max][2] (score, id) all-gather buffer
+  int tp_gather_rows = 0;
   se::bf16* embed = nullptr;
   se::bf16* lm_head = nullptr;
   se::bf16* g_final = nullptr;

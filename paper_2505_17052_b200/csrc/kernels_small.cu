@@ -393,18 +393,19 @@ __global__ void k_init_weights(const __grid_constant__ InitArgs a) {
     const long long prow = g4 * 4 / a.cols;
     const long long col = g4 * 4 % a.cols;
     int tid = a.tid0;
-    long long lrow = prow;
+    long long lrow = prow + a.off0;
     float scale = a.scale0;
     if (a.layout == INIT_QKV) {
-      if (prow < a.rows0) { tid = a.tid0; lrow = prow; scale = a.scale0; }
-      else if (prow < a.rows0 + a.rows1) { tid = a.tid1; lrow = prow - a.rows0; scale = a.scale1; }
-      else { tid = a.tid2; lrow = prow - a.rows0 - a.rows1; scale = a.scale2; }
+      if (prow < a.rows0) { tid = a.tid0; lrow = a.off0 + prow; scale = a.scale0; }
+      else if (prow < a.rows0 + a.rows1) { tid = a.tid1; lrow = a.off1 + prow - a.rows0; scale = a.scale1; }
+      else { tid = a.tid2; lrow = a.off2 + prow - a.rows0 - a.rows1; scale = a.scale2; }
     } else if (a.layout == INIT_GATEUP) {
       const long long blk = prow / 128, within = prow % 128;
-      if (within < 64) { tid = a.tid0; lrow = blk * 64 + within; scale = a.scale0; }
-      else { tid = a.tid1; lrow = blk * 64 + within - 64; scale = a.scale1; }
+      if (within < 64) { tid = a.tid0; lrow = a.off0 + blk * 64 + within; scale = a.scale0; }
+      else { tid = a.tid1; lrow = a.off0 + blk * 64 + within - 64; scale = a.scale1; }
     }
-    const unsigned long long idx = (unsigned long long)lrow * a.cols + col;   // multiple of 4
+    // global element index (multiple of 4: col0, gcols and cols are multiples of 4)
+    const unsigned long long idx = (unsigned long long)lrow * a.gcols + a.col0 + col;
     const U4 r = philox4x32_10(U4{(uint32_t)(idx >> 2), (uint32_t)tid, (uint32_t)a.layer, 0x57454947u}, a.k0, a.k1);
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
     uint16_t out[4];
@@ -425,8 +426,11 @@ __global__ void k_init_weights(const __grid_constant__ InitArgs a) {
 // ---------------------------------------------------------------------- K13 synthetic KV
 // element e = head*hd + j of token t: Philox counter (e>>2, t, layer*2 + kv, stream ^ 'KVFI').
 __global__ void k_kv_fill(f16* pool, const int* __restrict__ block_row, int layers, int num_pages, int KV,
-                          int hd, int n_tokens, uint32_t k0, uint32_t k1, uint32_t stream_id) {
+                          int hd, int n_tokens, uint32_t k0, uint32_t k1, uint32_t stream_id, int kv_head0) {
+  // kv_head0: global index of local kv head 0 (tensor-parallel pool shard); the Philox counter
+  // uses the global element index, so a shard holds exactly the global cache's values
   const int per_tok4 = KV * hd / 4;
+  const int e4_off = kv_head0 * hd / 4;
   const long long total = (long long)n_tokens * layers * 2 * per_tok4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -436,7 +440,7 @@ __global__ void k_kv_fill(f16* pool, const int* __restrict__ block_row, int laye
     rest /= 2;
     const int layer = (int)(rest % layers);
     const int t = (int)(rest / layers);
-    const U4 r = philox4x32_10(U4{(uint32_t)e4, (uint32_t)t, (uint32_t)((layer << 1) | kvsel), stream_id ^ 0x4B564649u}, k0, k1);
+    const U4 r = philox4x32_10(U4{(uint32_t)(e4 + e4_off), (uint32_t)t, (uint32_t)((layer << 1) | kvsel), stream_id ^ 0x4B564649u}, k0, k1);
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
     uint16_t out[4];
 #pragma unroll
@@ -510,11 +514,11 @@ cudaError_t init_weights_launch(const InitArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 cudaError_t kv_fill_launch(f16* pool, const int* block_row, int layers, int num_pages, int KV, int hd, int n_tokens,
-                           uint32_t k0, uint32_t k1, uint32_t stream_id, cudaStream_t st) {
+                           uint32_t k0, uint32_t k1, uint32_t stream_id, int kv_head0, cudaStream_t st) {
   const long long total = (long long)n_tokens * layers * 2 * (KV * hd / 4);
   if (total == 0) return cudaSuccess;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-  k_kv_fill<<<blocks, 256, 0, st>>>(pool, block_row, layers, num_pages, KV, hd, n_tokens, k0, k1, stream_id);
+  k_kv_fill<<<blocks, 256, 0, st>>>(pool, block_row, layers, num_pages, KV, hd, n_tokens, k0, k1, stream_id, kv_head0);
   return cudaGetLastError();
 }
 

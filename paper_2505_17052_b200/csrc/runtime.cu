@@ -69,7 +69,7 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
   size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
-  size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, part_val, part_idx, y, score;
+  size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, part_val, part_idx, y, score, tp_gather;
   size_t stage_in, stage_out, total;
   int B, R, n_splits_max;
 };
@@ -112,6 +112,7 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.part_idx = take(4 * (size_t)R * vt);
   w.y = take(4 * R);
   w.score = take(4 * R);
+  w.tp_gather = take(8 * (size_t)(kMaxTp + 1) * R);   // TP C3: [tp][R](score, id) + own staging
   // staging for the host-buffer entry point: inputs then outputs
   w.stage_in = take((size_t)B * (4 + 4 + 4 + 8 + 4) + 4 * (B + 1) + (size_t)R * 12 + 64);
   w.stage_out = take((size_t)B * 12 + (size_t)R * 8 + (size_t)R * 8 + 64);
@@ -230,23 +231,32 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   float* Y = (float*)P(w.Y);
   const size_t y_stride = (size_t)R * std::max((H + 2 * KV) * hd, c.d);
   int pendingY = 0;   // K-split partials of the last down-proj not yet added to X
-  auto f32_gemm = [&](int kind, const CUtensorMap& tm, const void* Xin, int Mrows, int K) -> int {
+  const bool tp = m->tp_size > 1;
+  // row_parallel: O / down under TP -> one unsplit fp32 partial, summed over ranks in place (C1/C2)
+  auto f32_gemm = [&](int kind, const CUtensorMap& tm, const void* Xin, int Mrows, int K, bool row_parallel) -> int {
     GemmArgs g{};
     g.M = Mrows;
     g.R = R;
     g.K = K;
     g.out_f32 = Y;
     g.ldo = Mrows;
-    g.max_splits = kGemmSplits;
+    g.max_splits = (tp && row_parallel) ? 1 : kGemmSplits;
     g.split_stride = y_stride;
-    KTimer _t(kind, st);
-    if (gemm_launch(EPI_F32, tm, Xin, g, st, &launches) != cudaSuccess) return -1;
-    return gemm_splits_last();
+    {
+      KTimer _t(kind, st);
+      if (gemm_launch(EPI_F32, tm, Xin, g, st, &launches) != cudaSuccess) return -1;
+    }
+    const int ns = gemm_splits_last();
+    if (tp && row_parallel) {
+      if (tp_allreduce_f32(Y, (size_t)R * Mrows, m->nccl, st) != cudaSuccess) return -1;
+      ++launches;
+    }
+    return ns;
   };
   for (int l = 0; l < c.n_layers; ++l) {
     const auto& Lw = m->layers[l];
     { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Y, pendingY, y_stride, Lw.g_attn, Hn, R, c.d, c.eps, st, &launches)); }
-    const int sq = f32_gemm(K_QKV, Lw.tm_qkv, Hn, (H + 2 * KV) * hd, c.d);
+    const int sq = f32_gemm(K_QKV, Lw.tm_qkv, Hn, (H + 2 * KV) * hd, c.d, false);
     if (sq < 0) return SPECEDGE_E_CUDA;
     RopeArgs ra{};
     ra.Y = Y;
@@ -272,7 +282,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
       { KTimer _t(K_ATTN, st); CK(attention_launch(aa, B, st, &launches)); }
       { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
     }
-    const int so = f32_gemm(K_O, Lw.tm_o, O, c.d, H * hd);
+    const int so = f32_gemm(K_O, Lw.tm_o, O, c.d, H * hd, true);
     if (so < 0) return SPECEDGE_E_CUDA;
     { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Y, so, y_stride, Lw.g_mlp, Hn, R, c.d, c.eps, st, &launches)); }
     GemmArgs gu{};
@@ -282,7 +292,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gu.out_bf16 = Mb;
     gu.ld_out = c.ffn;
     { KTimer _t(K_GU, st); CK(gemm_launch(EPI_SWIGLU, Lw.tm_gu, Hn, gu, st, &launches)); }
-    pendingY = f32_gemm(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn);
+    pendingY = f32_gemm(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn, true);
     if (pendingY < 0) return SPECEDGE_E_CUDA;
   }
   int* y = (int*)P(w.y);
@@ -290,13 +300,14 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     bf16* Hf = (bf16*)P(w.Hf);
     { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Y, pendingY, y_stride, m->g_final, Hf, R, c.d, c.eps, st, &launches, 1)); }
     GemmArgs gl{};
-    gl.M = c.vocab;
+    gl.M = m->vl;   // this rank's vocab shard (all of V when tp_size == 1)
     gl.R = 2 * R;
     gl.pair = 1;
     gl.K = c.d;
     gl.part_val = (float*)P(w.part_val);
     gl.part_idx = (int*)P(w.part_idx);
-    gl.vocab = c.vocab;
+    gl.vocab = m->vl;
+    gl.vocab_off = m->v0;
     const bool sample = in->mode == SPECEDGE_SAMPLE_TREE && in->temperature >= 1e-6f;
     gl.sample = sample ? 1 : 0;
     gl.inv_t = sample ? (float)(1.0 / (double)in->temperature) : 1.0f;
@@ -308,8 +319,11 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gl.req_session = di.session_id;
     { KTimer _t(K_LM, st); CK(gemm_launch(EPI_ARGMAX, m->tm_lm, Hf, gl, st, &launches)); }
     KTimer _tr(K_LMRED, st);
-    CK(lm_reduce_launch(gl.part_val, gl.part_idx, R, (c.vocab + 127) / 128, y, (float*)P(w.score),
-                        dout.row_target, dout.row_score, st, &launches));
+    CK(lm_reduce_launch(gl.part_val, gl.part_idx, R, (m->vl + 127) / 128, y, (float*)P(w.score),
+                        tp ? nullptr : dout.row_target, tp ? nullptr : dout.row_score, st, &launches));
+    if (tp)
+      CK(tp_argmax_gather(y, (float*)P(w.score), R, (float*)P(w.tp_gather), m->tp_size, m->nccl, dout.row_target,
+                          dout.row_score, st, &launches));
   }
   WalkArgs wa{};
   wa.B = B;
@@ -380,8 +394,32 @@ extern "C" {
 
 specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t weight_seed, int32_t device,
                                       specedge_model** out) {
+  return specedge_model_create_tp(cfg, weight_seed, device, 0, 1, nullptr, out);
+}
+
+specedge_status specedge_tp_unique_id(uint8_t* id) {
+  if (!id) return SPECEDGE_E_INVALID;
+  const int r = tp_unique_id(id);
+  return r == 0 ? SPECEDGE_OK : (r == -1 ? SPECEDGE_E_UNSUPPORTED : SPECEDGE_E_CUDA);
+}
+
+specedge_status specedge_model_create_tp(const specedge_model_config* cfg, uint64_t weight_seed, int32_t device,
+                                         int32_t tp_rank, int32_t tp_size, const uint8_t* nccl_id,
+                                         specedge_model** out) {
   if (!cfg || !out) return SPECEDGE_E_INVALID;
+  if (tp_size < 1 || tp_size > kMaxTp || tp_rank < 0 || tp_rank >= tp_size) return SPECEDGE_E_INVALID;
+  if (tp_size > 1 && !nccl_id) return SPECEDGE_E_INVALID;
   if (!check_cfg(*cfg)) return SPECEDGE_E_UNSUPPORTED;
+  // head-parallel attention, column-parallel QKV / gate-up (gate-up in 64-row blocks),
+  // row-parallel O / down, vocab-parallel LM head
+  if (cfg->n_kv % tp_size || cfg->n_heads % tp_size || cfg->ffn % (64 * tp_size) || cfg->vocab < tp_size)
+    return SPECEDGE_E_UNSUPPORTED;
+  specedge_model_config lc = *cfg;
+  lc.n_heads /= tp_size;
+  lc.n_kv /= tp_size;
+  lc.ffn /= tp_size;
+  if (!check_cfg(lc)) return SPECEDGE_E_UNSUPPORTED;
+  if (tp_size > 1 && !tp_available()) return SPECEDGE_E_UNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return SPECEDGE_E_DEVICE;
   cudaDeviceProp prop;
@@ -389,20 +427,37 @@ specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t
   if (prop.major != 10) return SPECEDGE_E_DEVICE;
   CK(cudaSetDevice(device));
   specedge_model* m = new specedge_model();
-  m->cfg = *cfg;
+  m->gcfg = *cfg;
+  m->cfg = lc;
   m->device = device;
-  const auto& c = *cfg;
-  const size_t H = c.n_heads, KV = c.n_kv, hd = c.head_dim, d = c.d, F = c.ffn, V = c.vocab;
+  m->tp_rank = tp_rank;
+  m->tp_size = tp_size;
+  {
+    const int vs = (cfg->vocab + tp_size - 1) / tp_size;
+    m->v0 = std::min(cfg->vocab, tp_rank * vs);
+    m->vl = std::min(cfg->vocab, m->v0 + vs) - m->v0;
+  }
+  const auto& c = lc;   // rank-local shapes
+  const size_t H = c.n_heads, KV = c.n_kv, hd = c.head_dim, d = c.d, F = c.ffn, V = c.vocab, Vl = m->vl;
+  const size_t gH = cfg->n_heads, gF = cfg->ffn;
   const uint32_t k0 = (uint32_t)weight_seed, k1 = (uint32_t)(weight_seed >> 32);
   auto fail = [&](specedge_status s) {
     for (void* p : m->allocs) cudaFree(p);
+    if (m->nccl) tp_comm_destroy(m->nccl);
     delete m;
     return s;
   };
   auto sc = [](double stdv) { return (float)(stdv * std::sqrt(3.0) * std::ldexp(1.0, -23)); };
+  // off0..2: global row offsets of the local parts, col0/gcols: column shard of the global matrix
   auto init = [&](bf16* dst, long long rows, long long cols, int layout, int t0, int t1, int t2, int layer,
-                  long long r0, long long r1, float s0, float s1, float s2, int gain) {
+                  long long r0, long long r1, float s0, float s1, float s2, int gain, long long off0 = 0,
+                  long long off1 = 0, long long off2 = 0, long long col0 = 0, long long gcols = -1) {
     InitArgs a{};
+    a.off0 = off0;
+    a.off1 = off1;
+    a.off2 = off2;
+    a.col0 = col0;
+    a.gcols = gcols < 0 ? cols : gcols;
     a.dst = dst;
     a.rows = rows;
     a.cols = cols;
@@ -422,15 +477,16 @@ specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t
     return init_weights_launch(a, 0);
   };
   m->embed = dalloc<bf16>(m, V * d);
-  m->lm_head = dalloc<bf16>(m, V * d);
+  m->lm_head = dalloc<bf16>(m, Vl * d);
   m->g_final = dalloc<bf16>(m, d);
   if (!m->embed || !m->lm_head || !m->g_final) return fail(SPECEDGE_E_OOM);
   if (init(m->embed, V, d, INIT_PLAIN, 1, 0, 0, 0, 0, 0, sc(1.0), 0, 0, 0) != cudaSuccess) return fail(SPECEDGE_E_CUDA);
-  if (init(m->lm_head, V, d, INIT_PLAIN, 9, 0, 0, 0, 0, 0, sc(2.0 / std::sqrt((double)d)), 0, 0, 0) != cudaSuccess)
+  if (init(m->lm_head, Vl, d, INIT_PLAIN, 9, 0, 0, 0, 0, 0, sc(2.0 / std::sqrt((double)d)), 0, 0, 0, m->v0) != cudaSuccess)
     return fail(SPECEDGE_E_CUDA);
   if (init(m->g_final, 1, d, INIT_PLAIN, 12, 0, 0, 0, 0, 0, 0, 0, 0, 1) != cudaSuccess) return fail(SPECEDGE_E_CUDA);
   m->layers.resize(c.n_layers);
-  const double s_d = 1.0 / std::sqrt((double)d), s_q = 1.0 / std::sqrt((double)(H * hd)), s_f = 1.0 / std::sqrt((double)F);
+  const double s_d = 1.0 / std::sqrt((double)d), s_q = 1.0 / std::sqrt((double)(gH * hd)), s_f = 1.0 / std::sqrt((double)gF);
+  const long long rk = tp_rank;
   for (int l = 0; l < c.n_layers; ++l) {
     auto& L = m->layers[l];
     L.wqkv = dalloc<bf16>(m, (H + 2 * KV) * hd * d);
@@ -440,10 +496,12 @@ specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t
     L.g_attn = dalloc<bf16>(m, d);
     L.g_mlp = dalloc<bf16>(m, d);
     if (!L.wqkv || !L.wo || !L.wgu || !L.wd || !L.g_attn || !L.g_mlp) return fail(SPECEDGE_E_OOM);
-    bool ok = init(L.wqkv, (H + 2 * KV) * hd, d, INIT_QKV, 2, 3, 4, l, H * hd, KV * hd, sc(s_d), sc(s_d), sc(s_d), 0) == cudaSuccess;
-    ok = ok && init(L.wo, d, H * hd, INIT_PLAIN, 5, 0, 0, l, 0, 0, sc(s_q), 0, 0, 0) == cudaSuccess;
-    ok = ok && init(L.wgu, 2 * F, d, INIT_GATEUP, 6, 7, 0, l, F, 0, sc(s_d), sc(s_d), 0, 0) == cudaSuccess;
-    ok = ok && init(L.wd, d, F, INIT_PLAIN, 8, 0, 0, l, 0, 0, sc(s_f), 0, 0, 0) == cudaSuccess;
+    bool ok = init(L.wqkv, (H + 2 * KV) * hd, d, INIT_QKV, 2, 3, 4, l, H * hd, KV * hd, sc(s_d), sc(s_d), sc(s_d), 0,
+                   rk * H * hd, rk * KV * hd, rk * KV * hd) == cudaSuccess;
+    ok = ok && init(L.wo, d, H * hd, INIT_PLAIN, 5, 0, 0, l, 0, 0, sc(s_q), 0, 0, 0, 0, 0, 0, rk * H * hd,
+                    (long long)gH * hd) == cudaSuccess;
+    ok = ok && init(L.wgu, 2 * F, d, INIT_GATEUP, 6, 7, 0, l, F, 0, sc(s_d), sc(s_d), 0, 0, rk * F) == cudaSuccess;
+    ok = ok && init(L.wd, d, F, INIT_PLAIN, 8, 0, 0, l, 0, 0, sc(s_f), 0, 0, 0, 0, 0, 0, rk * F, (long long)gF) == cudaSuccess;
     ok = ok && init(L.g_attn, 1, d, INIT_PLAIN, 10, 0, 0, l, 0, 0, 0, 0, 0, 1) == cudaSuccess;
     ok = ok && init(L.g_mlp, 1, d, INIT_PLAIN, 11, 0, 0, l, 0, 0, 0, 0, 0, 1) == cudaSuccess;
     if (!ok) return fail(SPECEDGE_E_CUDA);
@@ -451,7 +509,7 @@ specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t
          make_tmap_2d(&L.tm_gu, L.wgu, 2 * F, d, 128) && make_tmap_2d(&L.tm_d, L.wd, d, F, 128);
     if (!ok) return fail(SPECEDGE_E_CUDA);
   }
-  if (!make_tmap_2d(&m->tm_lm, m->lm_head, V, d, 128)) return fail(SPECEDGE_E_CUDA);
+  if (!make_tmap_2d(&m->tm_lm, m->lm_head, Vl, d, 128)) return fail(SPECEDGE_E_CUDA);
   // RoPE table: angles in double (amb. A14), stored fp32
   const size_t half = hd / 2;
   std::vector<float> cs((size_t)c.max_position * half), sn((size_t)c.max_position * half);
@@ -470,13 +528,25 @@ specedge_status specedge_model_create(const specedge_model_config* cfg, uint64_t
       cudaMemcpy(m->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(SPECEDGE_E_CUDA);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(SPECEDGE_E_CUDA);
+  if (tp_size > 1 && tp_comm_init(&m->nccl, nccl_id, tp_rank, tp_size) != 0) return fail(SPECEDGE_E_CUDA);
   *out = m;
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_model_tp_info(const specedge_model* m, int32_t* tp_rank, int32_t* tp_size, int32_t* vocab0,
+                                       int32_t* vocab_n) {
+  if (!m) return SPECEDGE_E_INVALID;
+  if (tp_rank) *tp_rank = m->tp_rank;
+  if (tp_size) *tp_size = m->tp_size;
+  if (vocab0) *vocab0 = m->v0;
+  if (vocab_n) *vocab_n = m->vl;
   return SPECEDGE_OK;
 }
 
 specedge_status specedge_model_destroy(specedge_model* m) {
   if (!m) return SPECEDGE_E_INVALID;
   cudaSetDevice(m->device);
+  if (m->nccl) tp_comm_destroy(m->nccl);
   for (void* p : m->allocs) cudaFree(p);
   delete m;
   return SPECEDGE_OK;
@@ -593,7 +663,8 @@ specedge_status specedge_kv_fill_random(specedge_kvpool* p, int32_t h, int32_t n
     return SPECEDGE_E_INVALID;
   const auto& c = p->model->cfg;
   CK(kv_fill_launch(p->pages, p->block_table + (size_t)h * p->max_pages_per_seq, c.n_layers, p->num_pages, c.n_kv,
-                    c.head_dim, n_tokens, (uint32_t)seed, (uint32_t)(seed >> 32), stream_id, (cudaStream_t)stream));
+                    c.head_dim, n_tokens, (uint32_t)seed, (uint32_t)(seed >> 32), stream_id, p->model->tp_rank * c.n_kv,
+                    (cudaStream_t)stream));
   CK(cudaMemcpyAsync(p->cache_len + h, &n_tokens, sizeof(int), cudaMemcpyHostToDevice, (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   return SPECEDGE_OK;
@@ -849,12 +920,12 @@ specedge_status specedge_debug_last_logits(specedge_model* m, void* workspace, s
   const WsLayout w = ws_layout(m->cfg, B, R);
   if (ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
   GemmArgs g{};
-  g.M = m->cfg.vocab;
+  g.M = m->vl;   // this rank's vocab shard
   g.R = 2 * R;
   g.pair = 1;
   g.K = m->cfg.d;
   g.out_f32 = logits;
-  g.ldo = m->cfg.vocab;
+  g.ldo = m->vl;
   CK(gemm_launch(EPI_F32, m->tm_lm, (uint8_t*)workspace + w.Hf, g, (cudaStream_t)stream, nullptr));
   return SPECEDGE_OK;
 }

@@ -1,0 +1,122 @@
+// Tensor parallelism for the verify step (SURVEY §8(a) a12, §8(e) "Tensor parallel TP = 8"):
+// head-parallel attention, column-parallel QKV / gate-up, row-parallel O / down followed by a
+// sum all-reduce of the fp32 [R, d] residual update (C1, C2), vocab-parallel LM head followed by
+// an all-gather of the per-row (score, id) winners (C3) and a replicated final argmax.
+//
+// NCCL is resolved at run time (dlopen of libnccl.so.2, the copy torch has already loaded when it
+// is in the process), so libspecedge.so has no link-time NCCL dependency and TP = 1 never touches
+// it.  All collectives are enqueued on the verify stream; every rank issues them in the same order.
+#include "common.cuh"
+#include "internal.h"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+
+namespace se {
+
+namespace {
+
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (api.tried) return api;
+  api.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+  if (!h) return api;
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+  api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+  api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.AllGather;
+  return api;
+}
+
+// C3 reduction: per row, the best (score, id) over the tp_size vocab shards; ties -> lowest id
+// (amb. A7).  g = [tp][R][2] floats, id stored as int bits.
+__global__ void k_tp_argmax(const float* __restrict__ g, int tp, int R, int* __restrict__ y, float* __restrict__ score,
+                            int* __restrict__ row_target, float* __restrict__ row_score) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= R) return;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int k = 0; k < tp; ++k) {
+    const float v = g[((size_t)k * R + row) * 2];
+    const int i = __float_as_int(g[((size_t)k * R + row) * 2 + 1]);
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+  y[row] = bi;
+  score[row] = best;
+  if (row_target) row_target[row] = bi;
+  if (row_score) row_score[row] = best;
+}
+
+__global__ void k_tp_pack(const int* __restrict__ y, const float* __restrict__ score, int R, float* __restrict__ out) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= R) return;
+  out[2 * row] = score[row];
+  out[2 * row + 1] = __int_as_float(y[row]);
+}
+
+}  // namespace
+
+bool tp_available() { return nccl().ok; }
+
+int tp_unique_id(uint8_t* out128) {
+  NcclApi& n = nccl();
+  if (!n.ok) return -1;
+  ncclUniqueId id;
+  if (n.GetUniqueId(&id) != ncclSuccess) return -2;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, 128);
+  return 0;
+}
+
+int tp_comm_init(void** comm, const uint8_t* id128, int rank, int size) {
+  NcclApi& n = nccl();
+  if (!n.ok) return -1;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, 128);
+  ncclComm_t c = nullptr;
+  if (n.CommInitRank(&c, size, id, rank) != ncclSuccess) return -2;
+  *comm = c;
+  return 0;
+}
+
+void tp_comm_destroy(void* comm) {
+  if (comm && nccl().ok) nccl().CommDestroy(reinterpret_cast<ncclComm_t>(comm));
+}
+
+// C1 / C2: in-place fp32 sum of the [R, d] residual updates of all ranks
+cudaError_t tp_allreduce_f32(float* buf, size_t n, void* comm, cudaStream_t st) {
+  if (nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, reinterpret_cast<ncclComm_t>(comm), st) != ncclSuccess)
+    return cudaErrorUnknown;
+  return cudaSuccess;
+}
+
+// C3: gather every rank's per-row winner and reduce to the global target token
+cudaError_t tp_argmax_gather(int* y, float* score, int R, float* gather, int tp, void* comm, int* row_target,
+                             float* row_score, cudaStream_t st, int* launches) {
+  float* mine = gather + (size_t)tp * R * 2;   // staging after the gather area
+  k_tp_pack<<<(R + 127) / 128, 128, 0, st>>>(y, score, R, mine);
+  if (launches) *launches += 2;
+  if (nccl().AllGather(mine, gather, (size_t)R * 2, ncclFloat32, reinterpret_cast<ncclComm_t>(comm), st) !=
+      ncclSuccess)
+    return cudaErrorUnknown;
+  k_tp_argmax<<<(R + 127) / 128, 128, 0, st>>>(gather, tp, R, y, score, row_target, row_score);
+  return cudaGetLastError();
+}
+
+}  // namespace se

@@ -1,0 +1,157 @@
+"""Tensor-parallel verify (SURVEY §8(a) a12, §8(e) TP regime; P14 "TP = k == TP = 1"): two
+processes, one GPU each, run the same verify through specedge_model_create_tp shards with the
+NCCL collectives C1/C2 (all-reduce after O and down) and C3 (all-gather of per-row winners).
+Checked against the oracle exactly as the TP = 1 parity tests are (tests/test_gpu_verify.py):
+concatenated vocab-shard logits within the derived tolerance, per-slot targets exact where the
+oracle margin allows, acceptance outputs exact (or margin-exempt), and the committed KV of each
+rank's kv-head shard equal to the oracle cache slice.  Needs >= 2 GPUs (gpurun --gpus 2)."""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import verify as OV  # noqa: E402
+from oracle.model import Weights  # noqa: E402
+from synth.configs import SMALL128  # noqa: E402
+from synth.plant import plant, draw_accept_lengths  # noqa: E402
+from synth.trees import pooled_tree  # noqa: E402
+from tests.gpu_helpers import MARGIN, check_logits, compare_outcome, f16_bits_to_f64, top2_margin  # noqa: E402
+
+SEED = 7
+TP = 2
+
+
+def _needs_gpus(n):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+
+
+def _setup(seed=SEED):
+    """Host-side inputs shared by every rank and the oracle (a pure function of the seed)."""
+    shape = SMALL128
+    rng = np.random.default_rng(909)
+    B = 4
+    prompts = [[int(t) for t in rng.integers(0, shape.vocab, n)] for n in (40, 75, 17, 64)]
+    W = Weights(shape, seed)
+    sessions = [OV.make_session(W, p, 300 + i) for i, p in enumerate(prompts)]
+    trees = [pooled_tree(rng, n, 4, 3, shape.vocab) for n in (8, 32, 16, 4)]
+    a = draw_accept_lengths(rng, trees, 3.98, 1.55)
+
+    def targets(trs):
+        return [OV.verify_one(W, OV.Request(sessions[i], t.parent, t.token), keep_logits=False).row_target
+                for i, t in enumerate(trs)]
+    trees = plant(trees, targets, a, shape.vocab, rng)
+    return shape, W, prompts, sessions, trees
+
+
+def _worker(rank, nccl_id, mode, temperature, q):
+    try:
+        torch.cuda.set_device(rank)
+        from paper_2505_17052_b200 import api
+        shape, W, prompts, sessions, trees = _setup()
+        model = api.Model(shape, SEED, device=rank, max_position=4096, tp_rank=rank, tp_size=TP, nccl_id=nccl_id)
+        cap = max(len(p) for p in prompts) + 256
+        pool = api.KVPool(model, ((cap + 63) // 64) * len(prompts) + 4, len(prompts) + 4)
+        B = len(prompts)
+        ws = model.workspace(B, B * 65, cap)
+        handles = []
+        for p in prompts:
+            h = pool.alloc(cap)
+            pool.prefill(h, p, ws)
+            handles.append(h)
+        batch = api.Batch.from_host(handles, [s.context_len for s in sessions], [s.last_token for s in sessions],
+                                    [s.session_id for s in sessions], [s.round for s in sessions], trees,
+                                    max_context_len=max(s.context_len for s in sessions) + 8)
+        mode_c = api.L.GREEDY if mode == "greedy" else api.L.SAMPLE_TREE
+        out = api.verify(model, pool, batch, ws, mode=mode_c, temperature=temperature, seed=SEED, auto_commit=True)
+        logits = api.debug_last_logits(model, ws, batch).cpu().numpy()
+        torch.cuda.synchronize()
+        res = dict(status=out.status.cpu().numpy(), accepted_len=out.accepted_len.cpu().numpy(),
+                   accepted_token=out.accepted_token.cpu().numpy(), accepted_node=out.accepted_node.cpu().numpy(),
+                   bonus=out.bonus.cpu().numpy(), row_target=out.row_target.cpu().numpy(),
+                   row_score=out.row_score.cpu().numpy(), logits=logits, vocab0=model.vocab0,
+                   lens=pool.get_len(handles))
+        # committed K/V of this rank's kv-head shard, every layer
+        res["kv"] = [[pool.read_kv(h, l, sel, 0, int(res["lens"][i])) for l in range(shape.n_layers)
+                      for sel in (0, 1)] for i, h in enumerate(handles)]
+        pool.close()
+        model.close()
+        q.put((rank, res))
+    except Exception as e:  # surfaced by the parent
+        import traceback
+        q.put((rank, RuntimeError(f"rank {rank}: {e}\n{traceback.format_exc()}")))
+
+
+def _run_tp(mode, temperature):
+    import torch.multiprocessing as mp
+    from paper_2505_17052_b200 import api
+    nccl_id = api.tp_unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, nccl_id, mode, temperature, q)) for r in range(TP)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(TP):
+        r, v = q.get(timeout=600)
+        if isinstance(v, Exception):
+            raise v
+        res[r] = v
+    for p in procs:
+        p.join(timeout=60)
+    return res
+
+
+@pytest.mark.parametrize("mode,temperature", [("greedy", 0.0), ("sample", 1.0)])
+def test_tp2_verify_matches_oracle(mode, temperature):
+    _needs_gpus(TP)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    res = _run_tp(mode, temperature)
+    shape, W, prompts, sessions, trees = _setup()
+    B = len(prompts)
+    refs = OV.verify_batch(W, [OV.Request(sessions[r], trees[r].parent, trees[r].token) for r in range(B)],
+                           mode=mode, temperature=temperature, seed=SEED, auto_commit=True)
+    # replicated outputs: identical on every rank
+    for k in ("status", "accepted_len", "accepted_token", "accepted_node", "bonus", "row_target", "row_score"):
+        assert np.array_equal(res[0][k], res[1][k]), k
+    # vocab shards concatenate to the full logits
+    assert res[0]["vocab0"] == 0 and res[1]["vocab0"] == res[0]["logits"].shape[1]
+    logits = np.concatenate([res[0]["logits"], res[1]["logits"]], axis=1)
+    ref_logits = np.concatenate([o.logits for o in refs])
+    dl = check_logits(logits, ref_logits)
+    g = res[0]
+    noff = np.cumsum([0] + [t.n for t in trees])
+    gr = dict(accepted_len=g["accepted_len"], bonus=g["bonus"],
+              accepted_token=[g["accepted_token"][noff[r]:noff[r + 1]] for r in range(B)],
+              accepted_node=[g["accepted_node"][noff[r]:noff[r + 1]] for r in range(B)])
+    off_rows = 0
+    kinds = []
+    for r in range(B):
+        o = refs[r]
+        S = trees[r].n + 1
+        eps = float(dl[off_rows:off_rows + S].max())
+        # the oracle committed (round advanced): score with the round the verify used
+        scores = OV.target_scores(o.logits, mode, temperature, SEED, sessions[r].round - 1, sessions[r].session_id)
+        sure = top2_margin(scores) > max(MARGIN, 2 * eps / (temperature if temperature else 1.0))
+        assert np.array_equal(g["row_target"][off_rows:off_rows + S][sure], o.row_target[sure]), r
+        kinds.append(compare_outcome(o, scores, gr, r, eps / (temperature if temperature else 1.0)))
+        off_rows += S
+    assert kinds.count("exact") >= B - 1, kinds
+    # committed KV: each rank holds kv heads [rank*KV/TP, (rank+1)*KV/TP) of the oracle cache
+    kvl = shape.n_kv // TP
+    for r in range(B):
+        if kinds[r] != "exact":
+            continue
+        ses = sessions[r]
+        assert int(g["lens"][r]) == len(ses.cache)
+        for rank in range(TP):
+            for l in range(shape.n_layers):
+                for sel, ref in ((0, ses.cache.k[l]), (1, ses.cache.v[l])):
+                    got = f16_bits_to_f64(res[rank]["kv"][r][2 * l + sel])
+                    want = ref[:, rank * kvl:(rank + 1) * kvl]
+                    num = np.linalg.norm((got - want).reshape(len(want), -1), axis=1)
+                    den = np.linalg.norm(want.reshape(len(want), -1), axis=1)
+                    assert (num / np.maximum(den, 1e-30)).max() <= 2e-2, (r, rank, l, sel)

@@ -54,6 +54,16 @@ def test_api_errors_without_device(libpath):
     assert lib.specedge_verify_batch(None, None, None, None, None, 0, None) == _lib.E_INVALID
     bad = _lib.ModelConfig(2, 64, 4, 2, 24, 256, 256, 1e-6, 1e4, 128)   # head_dim 24 unsupported
     assert lib.specedge_model_create(ctypes.byref(bad), 1, 0, ctypes.byref(out)) == _lib.E_UNSUPPORTED
+    # tensor-parallel shards: rank/size/id checks, divisibility of heads / ffn
+    ok = _lib.ModelConfig(2, 512, 8, 2, 128, 1024, 2048, 1e-5, 5e5, 128)
+    nid = (ctypes.c_uint8 * 128)()
+    create_tp = lib.specedge_model_create_tp
+    assert create_tp(ctypes.byref(ok), 1, 0, 2, 2, ctypes.cast(nid, ctypes.c_void_p), ctypes.byref(out)) == _lib.E_INVALID
+    assert create_tp(ctypes.byref(ok), 1, 0, 0, 2, None, ctypes.byref(out)) == _lib.E_INVALID
+    assert create_tp(ctypes.byref(ok), 1, 0, 0, 0, None, ctypes.byref(out)) == _lib.E_INVALID
+    assert create_tp(ctypes.byref(ok), 1, 0, 0, 4, ctypes.cast(nid, ctypes.c_void_p), ctypes.byref(out)) == \
+        _lib.E_UNSUPPORTED   # n_kv = 2 not divisible by 4
+    assert lib.specedge_model_tp_info(None, None, None, None, None) == _lib.E_INVALID
 
 
 def test_product_never_imports_oracle():
