@@ -9,6 +9,10 @@ cached lengths so every step sees identical inputs.  Multi-GPU: one process per 
 independent replica with its own 16 requests (weak scaling, no collective on the data path;
 SURVEY §8(e) replicas).
 
+--workload cfg4: Llama-3-70B-shaped, ONE tensor-parallel model over all ranks (specedge_model_create_tp,
+NCCL all-reduce after O and down, all-gather of the vocab-shard argmax), 32 requests x
+64-node trees for the whole box, ctx U[3072, 5120]; `value` is the box's tokens/s ("strong").
+
 --impl reference: the CPU oracle (oracle/, numpy float64) on the box's host cores, on a bounded
 sample of the same workload, extrapolated to the metric's unit (this tier's reference arm).
 """
@@ -126,14 +130,22 @@ def contexts(wl, rank):
     return [int(x) for x in rng.integers(wl.ctx_lo, wl.ctx_hi + 1, wl.n_requests)]
 
 
-def setup_gpu(wl, rank, device):
+def setup_gpu(wl, rank, device, tp=None):
+    """tp = (tp_rank, tp_size, nccl_id): every rank builds the SAME requests (data rank 0) on its
+    tensor-parallel shard of one model; otherwise rank r builds its own replica's requests."""
     import torch
     from paper_2505_17052_b200 import api
     from synth.plant import plant, draw_accept_lengths
     shape = wl.shape
+    if tp is not None:
+        rank = 0   # one request set for the whole box
     ctx = contexts(wl, rank)
     max_ctx = max(ctx) + wl.n_nodes + 64
-    model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64)
+    if tp is None:
+        model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64)
+    else:
+        model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64, tp_rank=tp[0],
+                          tp_size=tp[1], nccl_id=tp[2])
     pages = sum((c + wl.n_nodes + 2 + 63) // 64 for c in ctx) + 8
     pool = api.KVPool(model, pages, wl.n_requests + 2)
     handles = []
@@ -175,11 +187,12 @@ def setup_gpu(wl, rank, device):
                 trees=trees, planted=accept, accepted=got, R=R)
 
 
-def algorithmic_work(wl, st):
-    """Algorithmic flops and bytes per launch of each kernel kind."""
+def algorithmic_work(wl, st, tp=1):
+    """Algorithmic flops and bytes per launch of each kernel kind, per rank: under
+    tensor parallelism every kernel works on its 1/tp shard (heads, ffn, vocab)."""
     s = wl.shape
     R = st["R"]
-    hd, H, KV, d, F, V = s.head_dim, s.n_heads, s.n_kv, s.d, s.ffn, s.vocab
+    hd, H, KV, d, F, V = s.head_dim, s.n_heads // tp, s.n_kv // tp, s.d, s.ffn // tp, -(-s.vocab // tp)
     qkv = (H + 2 * KV) * hd
     gemms = {
         "gemm_qkv": (qkv, d), "gemm_o": (d, H * hd), "gemm_gateup": (2 * F, d), "gemm_down": (d, F),
@@ -205,7 +218,15 @@ def run_gpu(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    st = setup_gpu(wl, rank, local)
+    tp = None
+    if wl.tp:
+        if world < 2:
+            raise SystemExit(f"{wl.name} is tensor parallel: run it under torchrun with --nproc-per-node >= 2")
+        from paper_2505_17052_b200 import api as _api
+        obj = [_api.tp_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        tp = (rank, world, obj[0])
+    st = setup_gpu(wl, rank, local, tp)
     api, model, pool, ws, batch = st["api"], st["model"], st["pool"], st["ws"], st["batch"]
     lib = model.lib
     handles, L0 = st["handles"], [c - 1 for c in st["ctx"]]
@@ -260,7 +281,8 @@ def run_gpu(args, world, rank, local):
     acc = outs.accepted_len.cpu().numpy()
     assert int((acc + 1).sum()) == tokens_per_step, "accepted counts changed between steps"
     total_ms = reduce_max(total_ms, dist, f"cuda:{local}")
-    value = box_throughput(world, tokens_per_step, args.steps, total_ms)
+    replicas = 1 if tp else world   # TP: one model (one request set) spans the box
+    value = box_throughput(replicas, tokens_per_step, args.steps, total_ms)
 
     # ---- end-to-end through the host-buffer C-ABI entry point (copies inside the timed region)
     hb = api.HostBatch.of(batch)
@@ -288,7 +310,7 @@ def run_gpu(args, world, rank, local):
     # ---- roofline of the dominant kernel (largest share of the step), timed in the timed region
     share = {kinds[i]: float(kms[i]) for i in range(nk)}
     dom = kinds[dom]
-    work = algorithmic_work(wl, st)
+    work = algorithmic_work(wl, st, world if tp else 1)
     peaks = _peaks()
     roof = None
     if dom in work:
@@ -325,24 +347,28 @@ def run_gpu(args, world, rank, local):
             dist.barrier()
             dist.destroy_process_group()
         return
+    sh = wl.shape
+    weight_gb = 2.0 * sh.n_layers * ((sh.n_heads + 2 * sh.n_kv) * sh.head_dim * sh.d + sh.d * sh.n_heads * sh.head_dim +
+                                     3 * sh.ffn * sh.d) / (world if tp else 1) / 1e9 + 2.0 * sh.vocab * sh.d / (world if tp else 1) / 1e9
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"{wl.name}: {wl.shape.name}-shaped random-init, {wl.n_requests} requests x "
                                f"{wl.n_nodes}-node trees (D={wl.depth}, b={wl.branching}), ctx U[{wl.ctx_lo},"
                                f"{wl.ctx_hi}], {wl.mode}",
-                   "requests_per_gpu": wl.n_requests, "rows_per_step": st["R"], "tokens_per_step_per_gpu": tokens_per_step,
+                   ("requests_per_box" if tp else "requests_per_gpu"): wl.n_requests, "rows_per_step": st["R"],
+                   ("tokens_per_step_per_box" if tp else "tokens_per_step_per_gpu"): tokens_per_step,
                    "planted_tokens_per_verify": round(tokens_per_step / wl.n_requests, 3),
-                   "l2": "inputs larger than L2 (16 GB of weights streamed every step)",
-                   "parallelism": f"replicas x{world}"},
+                   "l2": f"inputs larger than L2 ({weight_gb:.1f} GB of weights per GPU streamed every step)",
+                   "parallelism": f"tp{world}" if tp else f"replicas x{world}"},
         "p50_ms": round(statistics.median(step_ms), 4), "p90_ms": round(float(np.quantile(step_ms, 0.9)), 4),
-        "rows_per_s": round(world * st["R"] * args.steps / (total_ms / 1e3), 1),
+        "rows_per_s": round(replicas * st["R"] * args.steps / (total_ms / 1e3), 1),
         "roofline": roof,
         "kernels": kernel_table,
         "kernels_note": "per-kernel ms from an event-instrumented calibration pass of the same steps "
                         "(each event pair adds a few us of stream time; small kernels read high)",
-        "e2e": {"value": round(box_throughput(world, e2e_tokens, args.steps, e2e_ms), 1), "unit": UNIT,
+        "e2e": {"value": round(box_throughput(replicas, e2e_tokens, args.steps, e2e_ms), 1), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches), "clocks": clk.result(),
     }
