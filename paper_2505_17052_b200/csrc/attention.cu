@@ -394,8 +394,6 @@ int attn_pick_splits_tc(int B, int KV, int max_pages) {
   int ns = (148 + items / 2) / items;
   ns = std::min(ns, 8);
   ns = std::min(ns, std::max(1, (max_pages + 1) / 2));
-  // the split's page ids are staged in shared memory next to a 3-stage K/V ring: <= 224 pages
-  ns = std::max(ns, (max_pages + 223) / 224);
   return std::max(1, ns);
 }
 

@@ -2,29 +2,38 @@
 // masking for each token sequence in the batch ... without cross-sequence interference").
 //
 // One CTA per (request r, kv head g, split sp).  Query rows of the item are the request's S slots
-// x the G query heads sharing kv head g (row = s*G + j); they are cut into M-tiles of
-// G*floor(128/G) rows, processed two at a time.  Keys stream in tiles of 128 (two 64-token pages
-// of the paged cache, then — in the last split — one tile of the S tree slots from the tree K/V
-// scratch, masked by the uint64 ancestor-or-self bitmask).
+// x the G query heads sharing kv head g (row = s*G + j), cut into 128-row M-tiles of
+// G*floor(128/G) rows.  Keys stream in 64-key sub-tiles (one page of the paged cache each, then —
+// in the last split — the S tree slots from the tree K/V scratch, masked by the uint64
+// ancestor-or-self bitmask) through a 5-stage TMA ring.
 //
-//   warp 0      TMA producer: Q tiles (3-D map over Q[R][H][hd]), K/V tiles (2-D maps over the
-//               page pool and the tree scratch), 2-stage ring
-//   warp 1      TMEM allocator + MMA issuer (one elected thread):
-//                 S_m  = Q_m K^T          kind::f16, A,B from smem (K-major), D fp32 in TMEM
-//                 O_m += P_m V            A = P (fp16) from TMEM, B = V from smem (MN-major, 128B
-//                                         swizzle); q, k, v are fp16 (DESIGN.md R-precision)
-//   warps 2-5   softmax + epilogue of M-tile 0 (one thread = one query row: row max and sum
-//   warps 6-9   softmax + epilogue of M-tile 1   need no cross-thread reduction)
+// Two "units" share the CTA; a unit = one softmax warpgroup + its TMEM (two 64-column S buffers
+// + a 128-column O accumulator).  A pass streams the KV once:
+//   pair pass   (>= 2 M-tiles left): unit u owns M-tile 2p+u and consumes every sub-tile, so two
+//               M-tiles share one KV read (cfg2's 132 rows = 1 pass instead of 2);
+//   single pass (last M-tile alone): both units work on the same M-tile, unit u taking sub-tiles
+//               j = u mod 2 with its own running max / sum / O (an in-CTA 2-way KV split), merged
+//               in the epilogue.
+// Within a unit, S is double-buffered at sub-tile granularity: while the warps turn S(k) into P(k),
+// the tensor core computes S(k+1); S(k+2) overwrites P(k) right after PV(k) (in-order tcgen05).
+//
+//   warp 0      TMA producer: Q tiles (3-D map over Q[R][H][hd]), K/V sub-tiles (2-D maps)
+//   warp 1      TMEM allocator + MMA issuer of unit 0; warp 10: MMA issuer of unit 1 (one elected
+//               thread each, so one unit's barrier waits never delay the other's issue):
+//                 S_u  = Q_u K^T      kind::f16, M=128 N=64, A,B from smem (K-major, SW128)
+//                 O_u += P_u V        A = P (fp16) from TMEM, B = V from smem (MN-major, SW128)
+//   warps 2-5   unit 0 softmax + epilogue (one thread = one query row: no cross-thread reduction)
+//   warps 6-9   unit 1 softmax + epilogue
 //
 // Softmax in the log2 domain with a lazily updated running max (O is rescaled only when the max
 // grows by more than 8, exact because l uses the same max).  P enters PV as fp16 (11-bit
-// significand: ~2e-4 relative error; bf16 P would give ~1.5e-3, SURVEY amb. A12).  The 128 scores
-// of a row stay in registers between the max and the exp pass.  TMEM: per M-tile 128 columns S
-// (P aliases its first 64) + HD columns O.
+// significand: ~2e-4 relative error; bf16 P would give ~1.5e-3, SURVEY amb. A12); q, k, v are fp16
+// (DESIGN.md R-precision).
 #include "common.cuh"
 #include "internal.h"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -32,9 +41,10 @@ namespace se {
 
 namespace {
 
-constexpr int kWarps = 10;      // producer, MMA, 8 softmax/epilogue warps (2 per TMEM lane quarter)
+constexpr int kWarps = 11;      // producer, MMA (unit 0), 2 units x 4 softmax/epilogue warps, MMA (unit 1)
 constexpr int kThreads = kWarps * 32;
-constexpr int kStages = 3;      // K/V ring depth (128-key tiles)
+constexpr int kStages = 5;      // K/V ring depth (64-key sub-tiles)
+constexpr int kPrefetchDefault = 0;   // L2 prefetch distance (sub-tiles) ahead of the ring; env SPECEDGE_ATTN_PREFETCH
 
 // UMMA smem descriptor for an MN-major operand, 128B swizzle: SBO = 1024 B between 8-row
 // (K) groups, LBO = stride between 64-element MN atoms.
@@ -82,6 +92,18 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
@@ -98,6 +120,12 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -112,43 +140,44 @@ struct TcArgs {
   bf16* O;          // final output when n_splits == 1 (normalised, bf16) else nullptr
   float* O_f32;     // optional fp32 normalised output (debug) when n_splits == 1
   int slots_per_mt; // floor(128 / G)
-  unsigned long long* trace;   // debug: per-phase clock64 stamps of CTA 0 (nullptr in production)
+  int prefetch;     // L2 prefetch distance in sub-tiles (0: off)
+  unsigned long long* trace;   // debug (env SPECEDGE_ATTN_TRACE): clock64 stamps of CTA 0, else null
 };
 
-#define TRACE(slot)                                                                   \
-  do {                                                                                \
-    if (ta.trace && blockIdx.x == 0 && blockIdx.y == 0) ta.trace[(slot)] = clock64(); \
+#define TRACE(i)                                                                                  \
+  do {                                                                                            \
+    if (ta.trace && blockIdx.x == 0 && blockIdx.y == 0 && (i) < 1024) ta.trace[(i)] = clock64(); \
   } while (0)
 
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmPool,
+    k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQ2,
+              const __grid_constant__ CUtensorMap tmQ4, const __grid_constant__ CUtensorMap tmPool,
               const __grid_constant__ CUtensorMap tmTree, const __grid_constant__ TcArgs ta) {
-  constexpr int KB = HD / 64;                  // 64-element hd blocks
-  constexpr uint32_t QT_BYTES = 128 * HD * 2;  // one M-tile of Q
-  constexpr uint32_t KT_BYTES = 128 * HD * 2;  // one 128-key tile of K (or V)
+  constexpr int KB = HD / 64;                       // 64-element hd blocks
+  constexpr uint32_t QT_BYTES = 128 * HD * 2;       // one 128-row M-tile of Q
+  constexpr uint32_t PG_BYTES = 64 * HD * 2;        // K (or V) of one 64-key sub-tile
   constexpr int NST = kStages;
   const AttnArgs& a = ta.a;
-  // Q + 3 K/V stages take 224 KB of the 227 KB: the 1024-B alignment SW128 needs comes from the
-  // dynamic-smem base itself (no static smem in this kernel); checked below.
+  // 2 Q tiles + 5 K/V sub-tile stages = 224 KB of the 227 KB: the 1024-B alignment SW128 needs
+  // comes from the dynamic-smem base itself (no static smem in this kernel); checked below.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw;
-  uint8_t* sQ = smem;                              // [KB][128 rows][128 B]
-  uint8_t* sK = sQ + QT_BYTES;                     // [NST][KB][128 keys][128 B]
-  uint8_t* sV = sK + NST * KT_BYTES;               // [NST][KB][128 keys][128 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NST * KT_BYTES);
+  uint8_t* sQ = smem_raw;                           // [2 units][KB][128 rows][128 B]
+  uint8_t* sK = sQ + 2 * QT_BYTES;                  // [NST][KB][64 keys][128 B]
+  uint8_t* sV = sK + NST * PG_BYTES;                // [NST][KB][64 keys][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NST * PG_BYTES);
   uint64_t* q_full = bars;              // [1]
   uint64_t* q_empty = bars + 1;         // [1]
   uint64_t* kv_full = bars + 2;         // [NST]
   uint64_t* kv_empty = kv_full + NST;   // [NST]
-  uint64_t* s_full = kv_empty + NST;    // [2 streams][2 buffers]  S_h(t) in buffer t&1
+  uint64_t* s_full = kv_empty + NST;    // [2 units][2 buffers]
   uint64_t* p_full = s_full + 4;        // [2][2]
-  uint64_t* pv_done = p_full + 4;       // [2][2]  PV_h(t) complete
+  uint64_t* pv_done = p_full + 4;       // [2][2]
   uint64_t* o_full = pv_done + 4;       // [1]
   uint64_t* o_empty = o_full + 1;       // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
   uint64_t* s_anc = reinterpret_cast<uint64_t*>(o_empty + 3);  // [66]
-  float* s_ml = reinterpret_cast<float*>(s_anc + 66);          // [2 streams][m,l][128 rows]
+  float* s_ml = reinterpret_cast<float*>(s_anc + 66);          // [2 units][m, l][128 rows]
 
   const int r = blockIdx.x / a.KV, g = blockIdx.x % a.KV, sp = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -158,38 +187,53 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int row0 = a.req_row0[r];
   const int h = a.req_h[r];
   const int spm = ta.slots_per_mt;
-  const int n_mt = (S + spm - 1) / spm;        // passes: one 128-row M-tile each
+  const int n_mt = (S + spm - 1) / spm;        // 128-row M-tiles
+  const int n_pass = (n_mt + 1) / 2;           // pass p: M-tiles 2p, 2p+1 ("pair") or the last one alone
   const int npages = (L + 63) / 64;
   const int p_begin = sp * a.pages_per_split;
   const int p_end = min(npages, p_begin + a.pages_per_split);
-  const int n_prefix_tiles = max(0, (p_end - p_begin + 1) / 2);
+  const int npg = max(0, p_end - p_begin);
   const bool has_tree = sp == a.n_splits - 1;
-  const int ntiles = n_prefix_tiles + (has_tree ? 1 : 0);
-  // KV tile visited at step t of pass mt: odd passes walk backwards (tree tile first), so they
-  // start on the tiles the previous pass left in L2
-  auto tile_of = [&](int mt, int t) {
-    if (!(mt & 1)) return t;
-    if (has_tree && t == 0) return n_prefix_tiles;
-    return n_prefix_tiles - 1 - (t - (has_tree ? 1 : 0));
+  const int ntree = has_tree ? (S > 64 ? 2 : 1) : 0;
+  const int nsub = npg + ntree;                // 64-key sub-tiles per pass
+  // sub-tile visited at step j of pass p: odd passes walk backwards (tree first) so they start on
+  // what the previous pass left in L2.  Returns 0..npg-1 for pages, npg + h for tree half h.
+  auto sub_of = [&](int p, int j) { return (p & 1) ? nsub - 1 - j : j; };
+  auto pair_pass = [&](int p) { return 2 * p + 1 < n_mt; };
+  // unit u's k-th sub-tile in pass p: pair pass -> every sub-tile (unit u = M-tile 2p+u);
+  // single pass -> the two units split the sub-tiles of one M-tile (unit u takes j = 2k+u)
+  auto nsub_u = [&](int p, int u) { return pair_pass(p) ? nsub : (nsub - u + 1) / 2; };
+  auto j_of = [&](int p, int u, int k) { return pair_pass(p) ? k : 2 * k + u; };
+  // M-tile of unit u in pass p and its row replication: a tile of <= floor(32/G) slots is loaded
+  // 4 times (one copy per TMEM lane quarter), <= floor(64/G) slots twice.  Replica r of a unit
+  // sees only keys [r*64/Rf, (r+1)*64/Rf) of every sub-tile with its own running max / sum / O,
+  // so a small tail tile (cfg2: 4 rows) spreads its softmax over all four SM sub-partitions
+  // instead of doubling one of them; replicas are merged in the epilogue.
+  auto mt_of = [&](int p, int u) { return pair_pass(p) ? 2 * p + u : 2 * p; };
+  auto rep_of = [&](int p, int u) {
+    const int slots = min(spm, S - mt_of(p, u) * spm);
+    return slots <= 32 / G ? 4 : (slots <= 64 / G ? 2 : 1);
   };
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem_raw) & 1023u) __trap();
     tma_prefetch(&tmQ);
+    tma_prefetch(&tmQ2);
+    tma_prefetch(&tmQ4);
     tma_prefetch(&tmPool);
     tma_prefetch(&tmTree);
     mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    mbar_init(q_empty, 2);   // one commit per MMA issuer
     for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&kv_empty[i], 2);
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&pv_done[i], 1);
     }
-    mbar_init(o_full, 1);
+    mbar_init(o_full, 2);
     mbar_init(o_empty, 256);
     fence_barrier_init();
   }
@@ -198,10 +242,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  // TMEM columns: stream h owns S buffers [128h, 128h+64) and [128h+64, 128h+128) and the O
-  // accumulator [256+128h, 256+128h+HD)
+  // TMEM columns: unit u owns S buffers [256u, 256u+64) and [256u+64, 256u+128) (P aliases the
+  // first 32 columns of its buffer) and the O accumulator [256u+128, 256u+128+HD)
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) TRACE(322);
+  if (threadIdx.x == 0) TRACE(1000);
+  // one 32-column chunk of an output row: normalised bf16 (+ optional fp32) when the KV is not
+  // split, else the unnormalised fp32 partial (the combine kernel merges splits with m, l)
+  auto store_out = [&](size_t rh, int col, const float (&ov)[32], float, float) {
+    if (a.n_splits == 1) {
+      if (ta.O) {
+        uint4* dst = reinterpret_cast<uint4*>(ta.O + rh * HD + col);
+#pragma unroll
+        for (int e = 0; e < 32; e += 8)
+          dst[e / 8] = make_uint4(pack2_bf16(ov[e], ov[e + 1]), pack2_bf16(ov[e + 2], ov[e + 3]),
+                                  pack2_bf16(ov[e + 4], ov[e + 5]), pack2_bf16(ov[e + 6], ov[e + 7]));
+      }
+      if (ta.O_f32) {
+        float4* dst = reinterpret_cast<float4*>(ta.O_f32 + rh * HD + col);
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) dst[e / 4] = make_float4(ov[e], ov[e + 1], ov[e + 2], ov[e + 3]);
+      }
+    } else {
+      float4* dst = reinterpret_cast<float4*>(a.opart + ((size_t)sp * a.R * a.H + rh) * HD + col);
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) dst[e / 4] = make_float4(ov[e], ov[e + 1], ov[e + 2], ov[e + 3]);
+    }
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------------------- TMA producer
@@ -209,268 +275,292 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int* pages = a.block_table + (size_t)h * a.max_pages_per_seq + p_begin;
-      const int np = p_end - p_begin;
-      for (int mt = 0; mt < n_mt; ++mt) {
-        // page ids of the next prefix tile, loaded one tile ahead of their use
-        int pg0 = np > 0 ? __ldg(pages) : 0, pg1 = np > 1 ? __ldg(pages + 1) : pg0;
-        mbar_wait(q_empty, (mt & 1) ^ 1);
-        mbar_expect_tx(q_full, (uint32_t)(64 * G * spm * 2) * KB);
-        for (int kb = 0; kb < KB; ++kb) tma_load_3d(sQ + kb * 128 * 128, &tmQ, q_full, kb * 64, g * G, row0 + mt * spm);
-        const bool rev = mt & 1;   // odd passes walk the tiles backwards (L2 reuse of the last tiles)
-        if (rev && n_prefix_tiles > 0) {
-          const int tl = n_prefix_tiles - 1;
-          pg0 = __ldg(pages + 2 * tl);
-          pg1 = 2 * tl + 1 < np ? __ldg(pages + 2 * tl + 1) : pg0;
+      for (int p = 0; p < n_pass; ++p) {
+        const int nq = pair_pass(p) ? 2 : 1;
+        mbar_wait(q_empty, (p & 1) ^ 1);
+        uint32_t qbytes = 0;
+        for (int u = 0; u < nq; ++u) qbytes += (uint32_t)rep_of(p, u) * (128 / rep_of(p, u) / G) * G * 128 * KB;
+        mbar_expect_tx(q_full, qbytes);
+        for (int u = 0; u < nq; ++u) {
+          const int rf = rep_of(p, u);
+          const CUtensorMap* tq = rf == 4 ? &tmQ4 : (rf == 2 ? &tmQ2 : &tmQ);
+          for (int rr = 0; rr < rf; ++rr)
+            for (int kb = 0; kb < KB; ++kb)
+              tma_load_3d(sQ + u * QT_BYTES + kb * 128 * 128 + rr * (128 / rf) * 128, tq, q_full, kb * 64, g * G,
+                          row0 + mt_of(p, u) * spm);
         }
-        for (int t = 0; t < ntiles; ++t) {
-          mbar_wait(&kv_empty[stage], phase ^ 1);
-          mbar_expect_tx(&kv_full[stage], 2 * KT_BYTES);
-          uint8_t* dk = sK + stage * KT_BYTES;
-          uint8_t* dv = sV + stage * KT_BYTES;
-          const int tt = tile_of(mt, t);
-          if (tt < n_prefix_tiles) {
-            const int cur0 = pg0, cur1 = pg1;
-            const int tn = rev ? tt - 1 : tt + 1;   // next prefix tile
-            if (tn >= 0 && tn < n_prefix_tiles) {
-              pg0 = __ldg(pages + 2 * tn);
-              pg1 = 2 * tn + 1 < np ? __ldg(pages + 2 * tn + 1) : pg0;
-            }
-            for (int hf = 0; hf < 2; ++hf) {
-              const int page = hf ? cur1 : cur0;   // odd tail: page 2t reloaded, masked later
-              const int rk = (((a.layer * a.num_pages + page) * 2 + 0) * a.KV + g) * 64;
-              const int rv = rk + a.KV * 64;
-              for (int kb = 0; kb < KB; ++kb) {
-                tma_load_2d(dk + kb * 128 * 128 + hf * 64 * 128, &tmPool, &kv_full[stage], kb * 64, rk);
-                tma_load_2d(dv + kb * 128 * 128 + hf * 64 * 128, &tmPool, &kv_full[stage], kb * 64, rv);
-              }
-            }
-          } else {
-            const int rk = ((a.layer * 2 + 0) * a.KV + g) * a.R_cap + row0;
-            const int rv = ((a.layer * 2 + 1) * a.KV + g) * a.R_cap + row0;
-            for (int hf = 0; hf < 2; ++hf)
-              for (int kb = 0; kb < KB; ++kb) {
-                tma_load_2d(dk + kb * 128 * 128 + hf * 64 * 128, &tmTree, &kv_full[stage], kb * 64, rk + 64 * hf);
-                tma_load_2d(dv + kb * 128 * 128 + hf * 64 * 128, &tmTree, &kv_full[stage], kb * 64, rv + 64 * hf);
-              }
+        int next_page = nsub > 0 && sub_of(p, 0) < npg ? __ldg(pages + sub_of(p, 0)) : 0;
+        // L2 prefetch of the pages kPrefetch sub-tiles ahead of the ring: the ring holds only a few
+        // sub-tiles in flight, so HBM latency would otherwise bound the per-SM stream rate
+        auto prefetch = [&](int jj) {
+          if (jj >= nsub) return;
+          const int sjj = sub_of(p, jj);
+          if (sjj >= npg) return;
+          const int rk = (((a.layer * a.num_pages + __ldg(pages + sjj)) * 2 + 0) * a.KV + g) * 64;
+          for (int kb = 0; kb < KB; ++kb) {
+            tma_prefetch_l2_2d(&tmPool, kb * 64, rk);
+            tma_prefetch_l2_2d(&tmPool, kb * 64, rk + a.KV * 64);
           }
-          if (mt == 0) TRACE(t);
+        };
+        const int kPrefetch = ta.prefetch;
+        for (int jj = 0; jj < kPrefetch; ++jj) prefetch(jj);
+        for (int j = 0; j < nsub; ++j) {
+          if (kPrefetch) prefetch(j + kPrefetch);
+          const int sj = sub_of(p, j);
+          const int page = next_page;   // page ids are read one sub-tile ahead of their use
+          if (j + 1 < nsub && sub_of(p, j + 1) < npg) next_page = __ldg(pages + sub_of(p, j + 1));
+          mbar_wait(&kv_empty[stage], phase ^ 1);
+          mbar_expect_tx(&kv_full[stage], 2 * PG_BYTES);
+          uint8_t* dk = sK + stage * PG_BYTES;
+          uint8_t* dv = sV + stage * PG_BYTES;
+          int rk, rv;
+          const CUtensorMap* tm;
+          if (sj < npg) {
+            rk = (((a.layer * a.num_pages + page) * 2 + 0) * a.KV + g) * 64;
+            rv = rk + a.KV * 64;
+            tm = &tmPool;
+          } else {
+            const int th = sj - npg;
+            rk = ((a.layer * 2 + 0) * a.KV + g) * a.R_cap + row0 + 64 * th;
+            rv = ((a.layer * 2 + 1) * a.KV + g) * a.R_cap + row0 + 64 * th;
+            tm = &tmTree;
+          }
+          for (int kb = 0; kb < KB; ++kb) {
+            tma_load_2d(dk + kb * 64 * 128, tm, &kv_full[stage], kb * 64, rk);
+            tma_load_2d(dv + kb * 64 * 128, tm, &kv_full[stage], kb * 64, rv);
+          }
+          if (p == 0) TRACE(j);
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------------------- MMA issuer
+  } else if (warp == 1 || warp == kWarps - 1) {
+    // ------------------------------------------------------------------------- MMA issuers
+    // one issuing thread per unit (warp 1: unit 0, last warp: unit 1), so neither unit's QK/PV
+    // issue waits behind the other's barriers; per unit the tcgen05 ops stay in program order.
+    const int u = warp == 1 ? 0 : 1;
     if (elect_one()) {
       const uint32_t id_qk = idesc_f16(128, 64, false);
       const uint32_t id_pv = idesc_f16(128, HD, true);
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t sfill = 0;        // S tiles filled so far per stream (all passes): buffer = sfill & 1
-      uint32_t pcons = 0;        // P tiles consumed so far per stream
-      // S_hs = Q K_hs^T for the 64 keys [64hs, 64hs+64) of the tile in stage `st`
-      auto issue_qk = [&](int st) {
-        const uint32_t qaddr = smem_u32(sQ);
-        const uint32_t kaddr = smem_u32(sK + st * KT_BYTES);
-#pragma unroll
-        for (int hs = 0; hs < 2; ++hs) {
-          const uint32_t s_tm = tmem + hs * 128 + (sfill & 1) * 64;
+      uint32_t sub_base = 0;           // sub-tiles streamed before this pass (ring position)
+      uint32_t kc = 0;                 // this unit's sub-tiles consumed (all passes): buffer kc & 1
+      for (int p = 0; p < n_pass; ++p) {
+        const bool pr = pair_pass(p);
+        const int nk = nsub_u(p, u);
+        mbar_wait(q_full, p & 1);
+        tc_fence_after();
+        // QK of this unit's k-th sub-tile of the pass into S buffer (kc + k) & 1
+        auto issue_qk = [&](int k) {
+          const uint32_t gi = sub_base + (uint32_t)j_of(p, u, k);
+          mbar_wait(&kv_full[gi % NST], (gi / NST) & 1);
+          tc_fence_after();
+          const uint32_t qaddr = smem_u32(sQ + (pr ? u : 0) * QT_BYTES);
+          const uint32_t kaddr = smem_u32(sK + (gi % NST) * PG_BYTES);
+          const uint32_t b = (kc + k) & 1;
+          const uint32_t s_tm = tmem + u * 256 + b * 64;
 #pragma unroll
           for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc_mma_f16(s_tm, umma_desc_sw128(qaddr + kb * 16384 + k * 32),
-                         umma_desc_sw128(kaddr + kb * 16384 + hs * 8192 + k * 32), id_qk, (kb | k) != 0);
-          tc_commit(&s_full[hs * 2 + (sfill & 1)]);
-        }
-        ++sfill;
-      };
-      for (int mt = 0; mt < n_mt; ++mt) {
-        mbar_wait(q_full, mt & 1);
-        mbar_wait(o_empty, (mt & 1) ^ 1);   // previous pass's O has been drained
-        tc_fence_after();
-        if (ntiles > 0) {
-          mbar_wait(&kv_full[stage], phase);
+            for (int kk = 0; kk < 4; ++kk)
+              tc_mma_f16(s_tm, umma_desc_sw128(qaddr + kb * 16384 + kk * 32),
+                         umma_desc_sw128(kaddr + kb * 8192 + kk * 32), id_qk, (kb | kk) != 0);
+          tc_commit(&s_full[u * 2 + b]);
+          if (k == nk - 1) tc_commit(q_empty);   // last QK of the pass: Q may be reloaded
+        };
+        for (int k = 0; k < 2 && k < nk; ++k) issue_qk(k);
+        if (nk == 0) tc_commit(q_empty);
+        for (int k = 0; k < nk; ++k) {
+          const uint32_t kg = kc + k;
+          const uint32_t b = kg & 1;
+          mbar_wait(&p_full[u * 2 + b], (kg >> 1) & 1);
+          if (k == 0) mbar_wait(o_empty, (p & 1) ^ 1);   // the previous pass's O has been drained
           tc_fence_after();
-          issue_qk(stage);
-        }
-        for (int t = 0; t < ntiles; ++t) {
-          int nst = stage + 1;
-          uint32_t nph = phase;
-          if (nst == NST) { nst = 0; nph ^= 1; }
-          // S(t+1) into the other S buffers while the softmax works on S(t).  In-order tcgen05
-          // execution: S(t+1) overwrites P(t-1) only after PV(t-1), issued before it, has read it.
-          if (t + 1 < ntiles) {
-            mbar_wait(&kv_full[nst], nph);
-            tc_fence_after();
-            issue_qk(nst);
-          }
-          const uint32_t b = pcons & 1;
-          const uint32_t vaddr = smem_u32(sV + stage * KT_BYTES);
+          const uint32_t gi = sub_base + (uint32_t)j_of(p, u, k);
+          const uint32_t vaddr = smem_u32(sV + (gi % NST) * PG_BYTES);
+          const uint32_t p_tm = tmem + u * 256 + b * 64;
+          const uint32_t o_tm = tmem + u * 256 + 128;
 #pragma unroll
-          for (int hs = 0; hs < 2; ++hs) {
-            mbar_wait(&p_full[hs * 2 + b], (pcons >> 1) & 1);
-            if (mt == 0 && hs == 0) TRACE(128 + t);
-            tc_fence_after();
-            const uint32_t p_tm = tmem + hs * 128 + b * 64;
-            const uint32_t o_tm = tmem + 256 + hs * 128;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {   // 16 keys (8 packed fp16 columns) per k-step
-              const uint64_t bd = umma_desc_mn_sw128(vaddr + hs * 8192 + k * 2048, 128 * 128);
-              tc_mma_ts(o_tm, p_tm + k * 8, bd, id_pv, (t | k) != 0);
-            }
-            tc_commit(&pv_done[hs * 2 + b]);
+          for (int kk = 0; kk < 4; ++kk) {   // 16 keys (8 packed fp16 columns) per k-step
+            const uint64_t bd = umma_desc_mn_sw128(vaddr + kk * 2048, 64 * 128);
+            tc_mma_ts(o_tm, p_tm + kk * 8, bd, id_pv, (k | kk) != 0);
           }
-          tc_commit(&kv_empty[stage]);
-          ++pcons;
-          stage = nst;
-          phase = nph;
+          tc_commit(&pv_done[u * 2 + b]);
+          // kv_empty takes 2 arrivals per use: one per unit in a pair pass, both from the only
+          // reader in a single pass
+          tc_commit(&kv_empty[gi % NST]);
+          if (!pr) tc_commit(&kv_empty[gi % NST]);
+          // S buffer b takes sub-tile k+2 (in-order execution: after PV(k) has read P(k))
+          if (k + 2 < nk) issue_qk(k + 2);
         }
         tc_commit(o_full);
-        tc_commit(q_empty);
+        kc += nk;
+        sub_base += nsub;
       }
     }
   } else {
     // ------------------------------------------------------------------ softmax + epilogue
-    // warps 2..9: stream hs = (warp-2)/4 owns keys [64hs, 64hs+64) of every KV tile with its own
-    // running max m, sum l and accumulator O_hs (an in-CTA 2-way KV split: the two streams never
-    // synchronise per tile, so the 2 warps sharing an SM sub-partition overlap each other's
-    // TMEM/MUFU latencies).  Both streams of a row live in the same TMEM lane quarter.
-    const int hs = (warp - 2) >> 2;
+    // warps 2..9: unit u = (warp-2)/4, one thread per TMEM lane (query row or a replica of one),
+    // 64 keys per sub-tile.
+    const int u = (warp - 2) >> 2;
     const int q = warp & 3;                   // TMEM lane quarter
-    const int rl = q * 32 + lane;             // row within the M-tile (= TMEM lane)
-    const int et = threadIdx.x - 64;          // 0..255
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const uint32_t s_base = tmem + hs * 128 + lane_off;
-    const uint32_t o_own = tmem + 256 + hs * 128 + lane_off;
+    const uint32_t s_base = tmem + u * 256 + lane_off;
+    const uint32_t o_own = tmem + u * 256 + 128 + lane_off;
     const float sl2 = a.scale_log2;
-#define FTRACE(k) \
-  do {            \
-    if (et == 0 && mt < 2 && t < 16) TRACE((mt ? 448 : 384) + 4 * t + (k)); \
-  } while (0)
-    uint32_t scons = 0;   // S tiles consumed (all passes)
-    for (int mt = 0; mt < n_mt; ++mt) {
+    const bool single = a.n_splits == 1;
+    uint32_t kc = 0;   // this unit's sub-tiles consumed (all passes)
+    for (int p = 0; p < n_pass; ++p) {
+      const bool pr = pair_pass(p);
+      const int mt = mt_of(p, u);
+      const int rf = rep_of(p, u);
+      const int rrows = 128 / rf;                       // lanes per replica
+      const int rq = (q * 32) / rrows;                  // my replica
+      const int ri = q * 32 + lane - rq * rrows;        // my row within the M-tile
       const int rows_mt = min(spm, S - mt * spm) * G;   // valid rows in this M-tile
-      const bool valid_row = rl < rows_mt;
-      const int slot = mt * spm + rl / G;
-      const int j = rl % G;
+      const bool valid_row = ri < rows_mt;
+      const int slot = mt * spm + ri / G;
+      const int j = ri % G;
       const uint64_t anc = (valid_row && slot > 0) ? s_anc[slot] : 0ull;
+      // my replica's key window within every 64-key sub-tile
+      const uint64_t win = rf == 1 ? ~0ull : (((1ull << (64 / rf)) - 1ull) << (rq * (64 / rf)));
+      const int nk = nsub_u(p, u);
       float m_used = -INFINITY, l = 0.f;
-      for (int t = 0; t < ntiles; ++t, ++scons) {
-        const uint32_t b = scons & 1;
+      for (int k = 0; k < nk; ++k) {
+        const uint32_t kg = kc + k;
+        const uint32_t b = kg & 1;
         const uint32_t s_tm = s_base + b * 64;
-        mbar_wait(&s_full[hs * 2 + b], (scons >> 1) & 1);
-        if (mt == 0 && et == 0) TRACE(192 + t);
+        mbar_wait(&s_full[u * 2 + b], (kg >> 1) & 1);
+        if (p == 0 && lane == 0 && q == 0) TRACE(256 + 64 * u + k);
         tc_fence_after();
-        const int tt = tile_of(mt, t);
-        const bool tree = tt >= n_prefix_tiles;
-        // 64-bit visibility mask of my stream's keys in this tile
-        uint32_t mk[2] = {0u, 0u};
+        const int sj = sub_of(p, j_of(p, u, k));
+        // 64-bit visibility mask of the sub-tile's keys for my row
+        uint64_t mk = 0ull;
         if (valid_row) {
-          if (!tree) {
-            const int key0 = (p_begin + 2 * tt) * 64;
-            int kvalid = min(128, L - key0);
-            if (p_begin + 2 * tt + 1 >= p_end) kvalid = min(kvalid, 64);
-#pragma unroll
-            for (int w = 0; w < 2; ++w) {
-              const int n = kvalid - 64 * hs - 32 * w;
-              mk[w] = n >= 32 ? 0xFFFFFFFFu : (n <= 0 ? 0u : ((1u << n) - 1u));
-            }
+          if (sj < npg) {
+            const int kvalid = min(64, L - (p_begin + sj) * 64);
+            mk = kvalid >= 64 ? ~0ull : ((1ull << kvalid) - 1ull);
           } else {
             // key 0 = root, key k >= 1 = node k-1: visible iff root or ancestor-or-self of my node
+            const int th = sj - npg;
             const uint64_t lo = slot > 0 ? ((anc << 1) | 1ull) : 1ull;
-            const uint32_t w0 = hs ? (slot > 0 ? (uint32_t)(anc >> 63) : 0u) : (uint32_t)lo;
-            const uint32_t w1 = hs ? 0u : (uint32_t)(lo >> 32);
-#pragma unroll
-            for (int w = 0; w < 2; ++w) {
-              const int n = S - 64 * hs - 32 * w;
-              mk[w] = (w ? w1 : w0) & (n >= 32 ? 0xFFFFFFFFu : (n <= 0 ? 0u : ((1u << n) - 1u)));
-            }
+            const uint64_t hi = slot > 0 ? (anc >> 63) : 0ull;
+            const int n = S - 64 * th;   // tree keys in this half
+            mk = (th ? hi : lo) & (n >= 64 ? ~0ull : ((1ull << n) - 1ull));
           }
+          mk &= win;
         }
-        const bool any0 = __any_sync(0xffffffffu, mk[0] != 0u);
-        const bool any1 = __any_sync(0xffffffffu, mk[1] != 0u);
-        const bool full = __all_sync(0xffffffffu, (mk[0] & mk[1]) == 0xFFFFFFFFu);
-        if (any0 || any1) {
-          uint32_t sv[64];
-          tmem_ld_32x32b_x32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
-          tmem_ld_32x32b_x32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-          tmem_ld_wait();
-          FTRACE(0);
-          float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
-          if (full) {
+        const bool any = __any_sync(0xffffffffu, mk != 0ull);
+        if (any) {
+          // only my replica's key window [c0, c0 + W) is loaded, reduced and exponentiated; the
+          // other P columns of the buffer are zeroed (they hold stale scores)
+          auto body = [&](auto wc) {
+            constexpr int W = decltype(wc)::value;
+            const int c0 = W == 64 ? 0 : rq * W;
+            const uint64_t mw = mk >> c0;   // bit e <-> key c0 + e
+            const bool full = __all_sync(0xffffffffu, (W == 64 ? mk == ~0ull : (mw & ((1ull << W) - 1ull)) == ((1ull << W) - 1ull)));
+            uint32_t sv[W];
+            if constexpr (W == 16) {
+              tmem_ld_32x32b_x16(s_tm + c0, *reinterpret_cast<uint32_t(*)[16]>(sv));
+            } else {
 #pragma unroll
-            for (int e = 0; e < 64; e += 4) {
-              m0 = fmaxf(m0, __uint_as_float(sv[e]));
-              m1 = fmaxf(m1, __uint_as_float(sv[e + 1]));
-              m2 = fmaxf(m2, __uint_as_float(sv[e + 2]));
-              m3 = fmaxf(m3, __uint_as_float(sv[e + 3]));
+              for (int h = 0; h < W / 32; ++h)
+                tmem_ld_32x32b_x32(s_tm + c0 + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * h));
             }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 64; ++e)
-              m0 = fmaxf(m0, ((mk[e >> 5] >> (e & 31)) & 1u) ? __uint_as_float(sv[e]) : -INFINITY);
-          }
-          const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
-          FTRACE(1);
-          float alpha = 1.f;
-          bool rescale = false;
-          if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
-            alpha = m_used == -INFINITY ? 0.f : ex2f(m_used - mx);
-            rescale = t > 0 && m_used != -INFINITY;
-            l *= alpha;
-            m_used = mx;
-          }
-          const float mb = m_used == -INFINITY ? 0.f : m_used;
-          // P = 2^(s*scale - m) as packed fp16 pairs: my 64 keys -> columns [0, 32) of the buffer
-          float ls0 = 0.f, ls1 = 0.f;
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t pk[16];
+            tmem_ld_wait();
+            if (p == 0 && lane == 0 && q == 0 && k < 16) TRACE(512 + 64 * u + 4 * k);
+            float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
             if (full) {
 #pragma unroll
-              for (int e = 0; e < 32; e += 2) {
-                const float p0 = ex2f(fmaf(__uint_as_float(sv[32 * c + e]), sl2, -mb));
-                const float p1 = ex2f(fmaf(__uint_as_float(sv[32 * c + e + 1]), sl2, -mb));
-                ls0 += p0;
-                ls1 += p1;
-                pk[e >> 1] = pack2(p0, p1);
+              for (int e = 0; e < W; e += 4) {
+                m0 = fmaxf(m0, __uint_as_float(sv[e]));
+                m1 = fmaxf(m1, __uint_as_float(sv[e + 1]));
+                m2 = fmaxf(m2, __uint_as_float(sv[e + 2]));
+                m3 = fmaxf(m3, __uint_as_float(sv[e + 3]));
               }
-            } else if (c ? any1 : any0) {
+            } else {
+              const uint32_t mlo = (uint32_t)mw, mhi = (uint32_t)(mw >> 32);
 #pragma unroll
-              for (int e = 0; e < 32; e += 2) {
-                const float p0 = ((mk[c] >> e) & 1u) ? ex2f(fmaf(__uint_as_float(sv[32 * c + e]), sl2, -mb)) : 0.f;
-                const float p1 = ((mk[c] >> (e + 1)) & 1u) ? ex2f(fmaf(__uint_as_float(sv[32 * c + e + 1]), sl2, -mb)) : 0.f;
+              for (int e = 0; e < W; e += 2) {
+                const uint32_t wd = e < 32 ? mlo : mhi;
+                m0 = fmaxf(m0, ((wd >> (e & 31)) & 1u) ? __uint_as_float(sv[e]) : -INFINITY);
+                m1 = fmaxf(m1, ((wd >> ((e + 1) & 31)) & 1u) ? __uint_as_float(sv[e + 1]) : -INFINITY);
+              }
+            }
+            const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
+            if (p == 0 && lane == 0 && q == 0 && k < 16) TRACE(513 + 64 * u + 4 * k);
+            float alpha = 1.f;
+            bool rescale = false;
+            if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
+              alpha = m_used == -INFINITY ? 0.f : ex2f(m_used - mx);
+              rescale = k > 0 && m_used != -INFINITY;
+              l *= alpha;
+              m_used = mx;
+            }
+            const float mb = m_used == -INFINITY ? 0.f : m_used;
+            // P = 2^(s*scale - m) as packed fp16 pairs: keys c0 + e -> column (c0 + e) / 2
+            float ls0 = 0.f, ls1 = 0.f;
+            uint32_t pk[W / 2];
+            if (full) {
+#pragma unroll
+              for (int e = 0; e < W; e += 2) {
+                const float p0 = ex2f(fmaf(__uint_as_float(sv[e]), sl2, -mb));
+                const float p1 = ex2f(fmaf(__uint_as_float(sv[e + 1]), sl2, -mb));
                 ls0 += p0;
                 ls1 += p1;
                 pk[e >> 1] = pack2(p0, p1);
               }
             } else {
+              const uint32_t mlo = (uint32_t)mw, mhi = (uint32_t)(mw >> 32);
 #pragma unroll
-              for (int e = 0; e < 16; ++e) pk[e] = 0u;
-            }
-            tmem_st_32x32b_x16(s_tm + 16 * c, pk);
-          }
-          l += ls0 + ls1;
-          FTRACE(2);
-          if (__any_sync(0xffffffffu, rescale)) {
-            // O_hs *= alpha: PV_hs(t-1) writes O_hs and may still be in flight -> wait for it
-            const uint32_t pb = (scons - 1) & 1;
-            mbar_wait(&pv_done[hs * 2 + pb], ((scons - 1) >> 1) & 1);
-            tc_fence_after();
-            if (rescale) {
-#pragma unroll 1
-              for (int c = 0; c < HD / 32; ++c) {
-                uint32_t ov[32];
-                tmem_ld_32x32b_x32(o_own + c * 32, ov);
-                tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-                tmem_st_32x32b_x32(o_own + c * 32, ov);
+              for (int e = 0; e < W; e += 2) {
+                const uint32_t wd = e < 32 ? mlo : mhi;
+                const float p0 = ((wd >> (e & 31)) & 1u) ? ex2f(fmaf(__uint_as_float(sv[e]), sl2, -mb)) : 0.f;
+                const float p1 = ((wd >> ((e + 1) & 31)) & 1u) ? ex2f(fmaf(__uint_as_float(sv[e + 1]), sl2, -mb)) : 0.f;
+                ls0 += p0;
+                ls1 += p1;
+                pk[e >> 1] = pack2(p0, p1);
               }
             }
-          }
+            uint32_t z[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) z[e] = 0u;
+            if constexpr (W == 64) {
+              tmem_st_32x32b_x16(s_tm, *reinterpret_cast<uint32_t(*)[16]>(pk));
+              tmem_st_32x32b_x16(s_tm + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
+            } else if constexpr (W == 32) {   // columns [16 rq, 16 rq + 16)
+              tmem_st_32x32b_x16(s_tm + 16 * rq, *reinterpret_cast<uint32_t(*)[16]>(pk));
+              tmem_st_32x32b_x16(s_tm + 16 * (rq ^ 1), z);
+            } else {                          // columns [8 rq, 8 rq + 8)
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                tmem_st_32x32b_x8(s_tm + 8 * c, c == rq ? *reinterpret_cast<uint32_t(*)[8]>(pk)
+                                                        : *reinterpret_cast<uint32_t(*)[8]>(z));
+            }
+            l += ls0 + ls1;
+            if (p == 0 && lane == 0 && q == 0 && k < 16) TRACE(514 + 64 * u + 4 * k);
+            if (__any_sync(0xffffffffu, rescale)) {
+              // O *= alpha: PV(k-1) writes O and may still be in flight -> wait for it
+              const uint32_t pb = (kg - 1) & 1;
+              mbar_wait(&pv_done[u * 2 + pb], ((kg - 1) >> 1) & 1);
+              tc_fence_after();
+              if (rescale) {
+#pragma unroll 1
+                for (int c = 0; c < HD / 32; ++c) {
+                  uint32_t ov[32];
+                  tmem_ld_32x32b_x32(o_own + c * 32, ov);
+                  tmem_ld_wait();
+#pragma unroll
+                  for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+                  tmem_st_32x32b_x32(o_own + c * 32, ov);
+                }
+              }
+            }
+          };
+          if (rf == 1) body(std::integral_constant<int, 64>{});
+          else if (rf == 2) body(std::integral_constant<int, 32>{});
+          else body(std::integral_constant<int, 16>{});
         } else {
-          // no visible key of my stream for any row of this warp: P = 0
+          // no visible key in this sub-tile for any row of this warp: P = 0
           uint32_t z[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) z[e] = 0u;
@@ -478,70 +568,147 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_32x32b_x16(s_tm + 16, z);
         }
         tmem_st_wait();
-        FTRACE(3);
-        if (mt == 0 && et == 0) TRACE(256 + t);
+        if (p == 0 && lane == 0 && q == 0) TRACE(384 + 64 * u + k);
         tc_fence_before();
-        mbar_arrive(&p_full[hs * 2 + b]);
+        mbar_arrive(&p_full[u * 2 + b]);
       }
-      // epilogue: merge the two streams (m_h, l_h, O_h) of every row; warp (q, hs) writes the
-      // head-dim columns [hs*HD/2, hs*HD/2 + HD/2)
-      s_ml[hs * 256 + rl] = m_used;
-      s_ml[hs * 256 + 128 + rl] = l;
-      mbar_wait(o_full, mt & 1);
-      if (mt == 0 && et == 0) TRACE(320);
+      kc += nk;
+      // ---- epilogue of the pass
+      mbar_wait(o_full, p & 1);
       tc_fence_after();
-      named_bar_sync(2, 256);
-      const float ma = s_ml[rl], mbv = s_ml[256 + rl];
-      const float ms = fmaxf(ma, mbv);
-      const float c0 = ma == -INFINITY ? 0.f : ex2f(ma - ms);
-      const float c1 = mbv == -INFINITY ? 0.f : ex2f(mbv - ms);
-      const float lt = s_ml[128 + rl] * c0 + s_ml[384 + rl] * c1;
       const size_t rh = (size_t)(row0 + slot) * a.H + (size_t)g * G + j;
-      const bool single = a.n_splits == 1;
-      const float inv = single ? (lt > 0.f ? 1.f / lt : 0.f) : 1.f;
-      const float f0 = c0 * inv, f1 = c1 * inv;
+      const int rf_any = max(rep_of(p, 0), pr ? rep_of(p, 1) : 1);
+      if (rf == 1) {
+        s_ml[u * 256 + q * 32 + lane] = m_used;
+        s_ml[u * 256 + 128 + q * 32 + lane] = l;
+      }
+      if (rf > 1) {
+        // partial (m, l, O) of every replica (of both units in a single pass) -> the K/V ring,
+        // idle now: a replicated tile is always the last M-tile, so this is the last pass and
+        // o_full says every MMA reading the ring has completed
+        const int np_ = pr ? rf : 2 * rf;
+        const int pidx = (pr ? 0 : u) * rf + rq;
+        constexpr int PS = HD + 4;                        // padded row stride (floats)
+        float* part = reinterpret_cast<float*>(sK);       // [np_][rrows][PS]
+        float* pm = part + (size_t)np_ * rrows * PS;      // [np_][rrows]
+        float* pl = pm + np_ * rrows;
+        pm[pidx * rrows + ri] = m_used;
+        pl[pidx * rrows + ri] = l;
+        float* dst = part + ((size_t)pidx * rrows + ri) * PS;
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld_32x32b_x32(o_own + c * 32, ov);
+          tmem_ld_wait();
+          if (valid_row && m_used != -INFINITY) {
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
-        const int col = hs * (HD / 2) + c * 32;
-        uint32_t oa[32], ob[32];
-        tmem_ld_32x32b_x32(tmem + 256 + lane_off + col, oa);
-        tmem_ld_32x32b_x32(tmem + 384 + lane_off + col, ob);
-        tmem_ld_wait();
-        float ov[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) ov[e] = __uint_as_float(oa[e]) * f0 + __uint_as_float(ob[e]) * f1;
-        if (valid_row) {
-          if (single) {
-            if (ta.O) {
-              uint4* dst = reinterpret_cast<uint4*>(ta.O + rh * HD + col);
-#pragma unroll
-              for (int e = 0; e < 32; e += 8)
-                dst[e / 8] = make_uint4(pack2_bf16(ov[e], ov[e + 1]), pack2_bf16(ov[e + 2], ov[e + 3]),
-                                        pack2_bf16(ov[e + 4], ov[e + 5]), pack2_bf16(ov[e + 6], ov[e + 7]));
-            }
-            if (ta.O_f32) {
-              float4* dst = reinterpret_cast<float4*>(ta.O_f32 + rh * HD + col);
-#pragma unroll
-              for (int e = 0; e < 32; e += 4) dst[e / 4] = make_float4(ov[e], ov[e + 1], ov[e + 2], ov[e + 3]);
-            }
-          } else {
-            float4* dst = reinterpret_cast<float4*>(a.opart + ((size_t)sp * a.R * a.H + rh) * HD + col);
-#pragma unroll
-            for (int e = 0; e < 32; e += 4) dst[e / 4] = make_float4(ov[e], ov[e + 1], ov[e + 2], ov[e + 3]);
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(dst + c * 32 + e) =
+                  make_float4(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1]), __uint_as_float(ov[e + 2]),
+                              __uint_as_float(ov[e + 3]));
           }
         }
       }
-      if (valid_row && !single && hs == 0) {
-        a.mpart[(size_t)sp * a.R * a.H + rh] = ms;
-        a.lpart[(size_t)sp * a.R * a.H + rh] = lt;
+      named_bar_sync(2, 256);
+      if (rf == 1) {
+        float ms, lt, f0, f1;
+        int c_lo, c_hi;
+        const int rl = q * 32 + lane;
+        if (pr) {   // my unit's own M-tile: all HD columns of my row
+          ms = m_used;
+          lt = l;
+          f0 = 1.f;
+          f1 = 0.f;
+          c_lo = 0;
+          c_hi = HD / 32;
+        } else {    // both units hold partial (m, l, O) of the same rows: merge, unit u writes half
+          const float ma = s_ml[rl], mbv = s_ml[256 + rl];
+          ms = fmaxf(ma, mbv);
+          f0 = ma == -INFINITY ? 0.f : ex2f(ma - ms);
+          f1 = mbv == -INFINITY ? 0.f : ex2f(mbv - ms);
+          lt = s_ml[128 + rl] * f0 + s_ml[384 + rl] * f1;
+          c_lo = u * (HD / 64);
+          c_hi = c_lo + HD / 64;
+        }
+        const float inv = single ? (lt > 0.f ? 1.f / lt : 0.f) : 1.f;
+        f0 *= inv;
+        f1 *= inv;
+#pragma unroll 1
+        for (int c = c_lo; c < c_hi; ++c) {
+          const int col = c * 32;
+          uint32_t oa[32];
+          float ov[32];
+          tmem_ld_32x32b_x32((pr ? o_own : tmem + 128 + lane_off) + col, oa);
+          tmem_ld_wait();
+          // a unit without any visible key (or without sub-tiles) has factor 0 and an O that
+          // was never written: select instead of multiplying so stale TMEM cannot inject NaN
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] = f0 != 0.f ? __uint_as_float(oa[e]) * f0 : 0.f;
+          if (!pr) {
+            tmem_ld_32x32b_x32(tmem + 384 + lane_off + col, oa);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] = f1 != 0.f ? fmaf(__uint_as_float(oa[e]), f1, ov[e]) : ov[e];
+          }
+          if (valid_row) store_out(rh, col, ov, ms, lt);
+        }
+        if (valid_row && !single && (pr || u == 0)) {
+          a.mpart[(size_t)sp * a.R * a.H + rh] = ms;
+          a.lpart[(size_t)sp * a.R * a.H + rh] = lt;
+        }
+      } else {
+        // merge the replicas: the unit's (pair pass) or both units' (single pass) threads
+        // cooperate over (row, 32-column chunk) items of the tile
+        const int np_ = pr ? rf : 2 * rf;
+        constexpr int PS = HD + 4;
+        const float* part = reinterpret_cast<const float*>(sK);
+        const float* pm = part + (size_t)np_ * rrows * PS;
+        const float* pl = pm + np_ * rrows;
+        const int nthr = pr ? 128 : 256;
+        const int tid = pr ? q * 32 + lane : (u * 128 + q * 32 + lane);
+        const int items = rows_mt * (HD / 32);
+        for (int it = tid; it < items; it += nthr) {
+          const int row = it / (HD / 32), col = (it % (HD / 32)) * 32;
+          float ms = -INFINITY;
+          for (int pp = 0; pp < np_; ++pp) ms = fmaxf(ms, pm[pp * rrows + row]);
+          float lt = 0.f, ov[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] = 0.f;
+          for (int pp = 0; pp < np_; ++pp) {
+            const float mp = pm[pp * rrows + row];
+            if (mp == -INFINITY) continue;
+            const float f = ex2f(mp - ms);
+            lt += pl[pp * rrows + row] * f;
+            const float* src = part + ((size_t)pp * rrows + row) * PS + col;
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              const float4 v = *reinterpret_cast<const float4*>(src + e);
+              ov[e] = fmaf(v.x, f, ov[e]);
+              ov[e + 1] = fmaf(v.y, f, ov[e + 1]);
+              ov[e + 2] = fmaf(v.z, f, ov[e + 2]);
+              ov[e + 3] = fmaf(v.w, f, ov[e + 3]);
+            }
+          }
+          const float inv = single ? (lt > 0.f ? 1.f / lt : 0.f) : 1.f;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] *= inv;
+          const int rslot = mt * spm + row / G;
+          const size_t rrh = (size_t)(row0 + rslot) * a.H + (size_t)g * G + row % G;
+          store_out(rrh, col, ov, ms, lt);
+          if (!single && col == 0) {
+            a.mpart[(size_t)sp * a.R * a.H + rrh] = ms;
+            a.lpart[(size_t)sp * a.R * a.H + rrh] = lt;
+          }
+        }
       }
+      (void)rf_any;
       tc_fence_before();
       mbar_arrive(o_empty);
-      named_bar_sync(2, 256);   // s_ml reuse by the next pass
+      named_bar_sync(2, 256);   // s_ml / ring reuse by the next pass
     }
   }
   __syncthreads();
-  TRACE(321);
+  if (threadIdx.x == 0) TRACE(1001);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -589,13 +756,21 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
   const int spm = 128 / a.G;
   const uint64_t pool_rows = (uint64_t)(a.layer + 1) * a.num_pages * 2 * a.KV * 64;
   const uint64_t tree_rows = (uint64_t)(a.layer + 1) * 2 * a.KV * a.R_cap;
+  // replicated loads of small tail tiles: boxes of floor(64/G) / floor(32/G) slots (a tile is
+  // replicated only when it fits its box; the max(1, .) maps are valid but unused)
+  CUtensorMap tq2, tq4;
   if (!encode_fn() || !tmap_q(&tq, a.Q, (uint64_t)a.R, a.H, HD, a.G, spm) || !tmap_rows(&tp, a.pool, pool_rows, HD) ||
       !tmap_rows(&tt, a.tree_kv, tree_rows, HD))
     return cudaErrorInvalidValue;
+  if (!tmap_q(&tq2, a.Q, (uint64_t)a.R, a.H, HD, a.G, std::max(1, 64 / a.G)) ||
+      !tmap_q(&tq4, a.Q, (uint64_t)a.R, a.H, HD, a.G, std::max(1, 32 / a.G)))
+    return cudaErrorInvalidValue;
+  static const int pf = getenv("SPECEDGE_ATTN_PREFETCH") ? atoi(getenv("SPECEDGE_ATTN_PREFETCH")) : kPrefetchDefault;
   static unsigned long long* trace = nullptr;
-  if (getenv("SPECEDGE_ATTN_TRACE") && !trace) cudaMalloc(&trace, 512 * 8);
-  TcArgs ta{a, O, O_f32, spm, trace};
-  const size_t smem = (size_t)128 * HD * 2 * (1 + 2 * kStages) + 8 * 24 + 66 * 8 + 512 * 4;
+  if (getenv("SPECEDGE_ATTN_TRACE") && !trace) cudaMalloc(&trace, 1024 * 8);
+  TcArgs ta{a, O, O_f32, spm, pf, trace};
+  if (trace) cudaMemsetAsync(trace, 0, 1024 * 8, st);
+  const size_t smem = (size_t)2 * 128 * HD * 2 + (size_t)kStages * 2 * 64 * HD * 2 + 8 * 24 + 66 * 8 + 512 * 4;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_attn_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -603,37 +778,26 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
     attr = true;
   }
   dim3 grid(B * a.KV, a.n_splits);
-  if (trace) cudaMemsetAsync(trace, 0, 512 * 8, st);
-  k_attn_tc<HD><<<grid, kThreads, smem, st>>>(tq, tp, tt, ta);
+  k_attn_tc<HD><<<grid, kThreads, smem, st>>>(tq, tq2, tq4, tp, tt, ta);
   if (trace) {
     static int calls = 0;
-    unsigned long long h[512];
-    cudaStreamSynchronize(st);
-    cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
-    if (++calls % 32 == 5) {   // one layer per step
-      const unsigned long long t0 = h[322];
-      auto d = [&](int i) { return h[i] ? (long long)(h[i] - t0) : -1LL; };
-      fprintf(stderr, "attn trace (cycles from start): end=%lld o_full=%lld\n", d(321), d(320));
-      for (int t = 0; t < 12; ++t)
-        fprintf(stderr, "  tile %2d: tma_issued=%7lld s_ready(wg0)=%7lld p_done(wg0)=%7lld mma_got_p0=%7lld\n", t, d(t),
-                d(192 + t), d(256 + t), d(128 + t));
-      for (int m = 0; m < 2; ++m)
-        for (int t = 0; t < 10; ++t) {
-          const int b = (m ? 448 : 384) + 4 * t;
-          fprintf(stderr, "  pass %d tile %2d: ld=%7lld bar=%7lld exp=%7lld st=%7lld\n", m, t, d(b), d(b + 1), d(b + 2),
-                  d(b + 3));
-        }
+    if (++calls % 32 == 7) {
+      static unsigned long long hb[1024];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(hb, trace, sizeof(hb), cudaMemcpyDeviceToHost);
+      const unsigned long long t0 = hb[1000];
+      auto d = [&](int i) { return hb[i] ? (long long)(hb[i] - t0) : -1LL; };
+      fprintf(stderr, "attn trace CTA0: end=%lld\n", d(1001));
+      for (int k = 0; k < 16; ++k)
+        fprintf(stderr, " k%2d SOFTMAX u0: s=%6lld ld=%6lld max=%6lld exp=%6lld p=%6lld || u1: s=%6lld ld=%6lld max=%6lld exp=%6lld p=%6lld\n",
+                k, d(256 + k), d(512 + 4 * k), d(513 + 4 * k), d(514 + 4 * k), d(384 + k), d(320 + k), d(576 + 4 * k),
+                d(577 + 4 * k), d(578 + 4 * k), d(448 + k));
     }
   }
   return cudaGetLastError();
 }
 
 }  // namespace
-
-unsigned long long* attention_tc_trace_ptr() {
-  static unsigned long long* p = nullptr;
-  return p;
-}
 
 bool attention_tc_supported(int hd, int G) { return (hd == 64 || hd == 128) && G >= 1 && G <= 128; }
 

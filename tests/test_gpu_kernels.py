@@ -90,9 +90,15 @@ def _anc_masks(parent):
     return anc
 
 
+# tcgen05 kernel (hd 64/128) pass structure (attention_tc.cu): (128,4,1000,32,*) pair pass with a
+# 4-row tail replicated x4; (128,5,300,32,1) pair pass, 40-row tail replicated x2; (128,8,4097,64,8)
+# two pair passes + a single pass whose 8-row tile is replicated x4 (8 partials merged);
+# (128,4,500,11,1) single pass replicated x2; (128,4,700,5,2) single pass replicated x4;
+# (128,5,64,16,1) / (128,4,0,20,1) single pass without replication (2 in-CTA KV streams).
 @pytest.mark.parametrize("hd,G,L,N,splits", [(16, 2, 31, 8, 1), (128, 4, 1000, 32, 4), (128, 5, 64, 16, 1),
                                              (64, 8, 200, 64, 3), (128, 4, 0, 20, 1), (32, 1, 130, 0, 2),
-                                             (128, 8, 4097, 64, 8)])
+                                             (128, 8, 4097, 64, 8), (128, 4, 1000, 32, 1), (128, 5, 300, 32, 1),
+                                             (128, 4, 500, 11, 1), (128, 4, 700, 5, 2), (64, 4, 333, 32, 1)])
 def test_tree_attention_matches_oracle(api, hd, G, L, N, splits):
     from synth.trees import random_tree
     rng = np.random.default_rng(hd + G + L + N)
