@@ -129,7 +129,9 @@ specedge_status specedge_kv_alloc(specedge_kvpool* pool, int32_t capacity_tokens
                                   int32_t* out_handle);
 specedge_status specedge_kv_free(specedge_kvpool* pool, int32_t handle);
 /* Set the cached length of n sessions (host arrays), stream-ordered (used to rewind a session
- * between benchmark steps).  Lengths must be <= capacity. */
+ * between benchmark steps).  Lengths must be <= capacity.  The values travel as kernel
+ * parameters: the host arrays may be reused on return and the call can be captured in a CUDA
+ * graph. */
 specedge_status specedge_kv_set_len(specedge_kvpool* pool, const int32_t* handles,
                                     const int32_t* lens, int32_t n, void* stream);
 /* Read the cached lengths of n sessions into host array `lens` (synchronous). */

@@ -7,6 +7,7 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <string>
 #include <vector>
 
 #include "../../include/specedge.h"
@@ -191,6 +192,13 @@ struct InitArgs {
   long long off0, off1, off2, col0, gcols;
 };
 cudaError_t init_weights_launch(const InitArgs& a, cudaStream_t st);
+constexpr int kSetLenBatch = 128;
+struct SetLenArgs {
+  int n;
+  int handle[kSetLenBatch];
+  int len[kSetLenBatch];
+};
+cudaError_t set_len_launch(int* cache_len, const SetLenArgs& a, cudaStream_t st);
 
 // tensor parallelism (tp.cu): NCCL resolved at run time
 constexpr int kMaxTp = 16;
@@ -233,6 +241,15 @@ struct specedge_model {
   std::vector<void*> allocs;
   void* pinned = nullptr;       // staging for specedge_verify_batch_host
   size_t pinned_bytes = 0;
+  // CUDA-graph cache of whole verify steps (runtime.cu): one instantiated graph per distinct
+  // (scalars, buffers) signature, replayed on a model-owned stream ordered after the caller's
+  struct Graph {
+    std::string key;
+    cudaGraphExec_t exec;
+  };
+  std::vector<Graph> graphs;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
 };
 
 struct specedge_kvpool {

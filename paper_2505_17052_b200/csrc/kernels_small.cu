@@ -383,6 +383,13 @@ __global__ void k_commit_finalize(const __grid_constant__ CommitArgs c) {
   c.cache_len[h] = c.req_L[r] + c.accepted_len[r] + 1;
 }
 
+// cache_len[handle[i]] = len[i] for a batch of up to kSetLenBatch sessions passed by value (one
+// tiny launch, capturable in a CUDA graph; no host staging)
+__global__ void k_set_len(int* __restrict__ cache_len, const __grid_constant__ SetLenArgs a) {
+  const int i = threadIdx.x;
+  if (i < a.n) cache_len[a.handle[i]] = a.len[i];
+}
+
 // ------------------------------------------------------------------------ K12 weight init
 // Element (lrow, col) of a logical weight = bf16(f32(i24 * scale)) with i24 from Philox counter
 // (idx >> 2, tensor_id, layer, 'WEIG'), idx = lrow * cols + col, word idx & 3 (oracle/model.py O1).
@@ -505,6 +512,10 @@ cudaError_t commit_launch(const CommitArgs& c, cudaStream_t st, int* launches) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_commit_finalize<<<(c.B + 127) / 128, 128, 0, st>>>(c);
+  return cudaGetLastError();
+}
+cudaError_t set_len_launch(int* cache_len, const SetLenArgs& a, cudaStream_t st) {
+  k_set_len<<<1, kSetLenBatch, 0, st>>>(cache_len, a);
   return cudaGetLastError();
 }
 cudaError_t init_weights_launch(const InitArgs& a, cudaStream_t st) {

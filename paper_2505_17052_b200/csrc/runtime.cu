@@ -50,12 +50,19 @@ struct KTimer {
     active = g_timing.on && ((g_timing.mask >> k) & 1u);
     if (!active) return;
     idx = g_timing.used;
-    cudaEventRecord(timing_event(), st);
+    record(timing_event());
   }
   ~KTimer() {
     if (!active) return;
-    cudaEventRecord(timing_event(), st);
+    record(timing_event());
     g_timing.pending.push_back({kind, idx});
+  }
+  // under stream capture an event must be an external record node to be timed on each replay
+  void record(cudaEvent_t e) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
   }
 };
 
@@ -385,6 +392,75 @@ specedge_status check_out(const specedge_verify_out* out, int total_nodes) {
   return SPECEDGE_OK;
 }
 
+// ---- CUDA-graph replay of whole verify steps -----------------------------------------------
+// A verify step is a fixed sequence of ~8 + 8*layers launches whose parameters depend only on the
+// host scalars of specedge_verify_in and on buffer addresses.  The first call with a given
+// signature records the step (stream capture on a model-owned stream: the caller's stream may be
+// the legacy default stream, which cannot be captured) and instantiates it; every call then
+// replays it with one cudaGraphLaunch on the caller's stream.
+// Disabled by SPECEDGE_NO_GRAPH=1, while kernel timing is on, and when the caller's stream is
+// itself being captured (the plain launches then become part of the caller's graph).
+bool graphs_enabled(cudaStream_t st) {
+  static const bool off = getenv("SPECEDGE_NO_GRAPH") && getenv("SPECEDGE_NO_GRAPH")[0] == '1';
+  if (off || g_timing.on) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
+template <typename F>
+specedge_status run_graphed(specedge_model* m, const std::string& key, cudaStream_t st, F&& body) {
+  if (!m->gstream) {
+    CK(cudaStreamCreateWithFlags(&m->gstream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&m->gev_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&m->gev_out, cudaEventDisableTiming));
+  }
+  cudaGraphExec_t exec = nullptr;
+  for (size_t i = 0; i < m->graphs.size(); ++i)
+    if (m->graphs[i].key == key) {
+      exec = m->graphs[i].exec;
+      if (i) std::swap(m->graphs[i], m->graphs[0]);   // most recent first
+      break;
+    }
+  if (!exec) {
+    CK(cudaStreamBeginCapture(m->gstream, cudaStreamCaptureModeThreadLocal));
+    const specedge_status s = body(m->gstream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(m->gstream, &graph);
+    if (s != SPECEDGE_OK || e != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      return s != SPECEDGE_OK ? s : SPECEDGE_E_CUDA;
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(ei);
+    if (m->graphs.size() >= 8) {
+      cudaGraphExecDestroy(m->graphs.back().exec);
+      m->graphs.pop_back();
+    }
+    m->graphs.insert(m->graphs.begin(), specedge_model::Graph{key, exec});
+  }
+  // recorded on the model's stream (capture never executes anything), replayed on the caller's
+  CK(cudaGraphLaunch(exec, st));
+  return SPECEDGE_OK;
+}
+
+template <typename... T>
+std::string graph_key(const specedge_verify_in* in, T... extra) {
+  std::string k;
+  auto put = [&](const void* p, size_t n) { k.append(reinterpret_cast<const char*>(p), n); };
+  put(&in->num_requests, sizeof(int32_t) * 5);   // num_requests .. mode
+  put(&in->temperature, sizeof(float));
+  put(&in->seed, sizeof(uint64_t));
+  put(&in->auto_commit, sizeof(int32_t));
+  (put(&extra, sizeof(extra)), ...);
+  return k;
+}
+
 }  // namespace
 
 // =============================================================================================
@@ -547,6 +623,11 @@ specedge_status specedge_model_destroy(specedge_model* m) {
   if (!m) return SPECEDGE_E_INVALID;
   cudaSetDevice(m->device);
   if (m->nccl) tp_comm_destroy(m->nccl);
+  for (auto& g : m->graphs) cudaGraphExecDestroy(g.exec);
+  if (m->gstream) cudaStreamDestroy(m->gstream);
+  if (m->gev_in) cudaEventDestroy(m->gev_in);
+  if (m->gev_out) cudaEventDestroy(m->gev_out);
+  if (m->pinned) cudaFreeHost(m->pinned);
   for (void* p : m->allocs) cudaFree(p);
   delete m;
   return SPECEDGE_OK;
@@ -641,8 +722,16 @@ specedge_status specedge_kv_set_len(specedge_kvpool* p, const int32_t* handles, 
     if (h < 0 || h >= p->max_handles || p->handle_cap[h] == 0 || lens[i] < 0 || lens[i] > p->handle_cap[h])
       return SPECEDGE_E_INVALID;
   }
-  for (int i = 0; i < n; ++i)
-    CK(cudaMemcpyAsync(p->cache_len + handles[i], lens + i, sizeof(int), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  // lengths travel as kernel parameters (stream-ordered, graph-capturable, no host staging)
+  for (int i0 = 0; i0 < n; i0 += kSetLenBatch) {
+    SetLenArgs a{};
+    a.n = std::min(kSetLenBatch, n - i0);
+    for (int i = 0; i < a.n; ++i) {
+      a.handle[i] = handles[i0 + i];
+      a.len[i] = lens[i0 + i];
+    }
+    CK(set_len_launch(p->cache_len, a, (cudaStream_t)stream));
+  }
   return SPECEDGE_OK;
 }
 
@@ -686,8 +775,19 @@ specedge_status specedge_verify_batch(specedge_model* m, specedge_kvpool* pool, 
   DevIn di{in->kv, in->context_len, in->root_token, in->node_offset, in->parent, in->token, in->session_id, in->round};
   DevOut dout{out->status, out->accepted_len, out->accepted_token, out->accepted_node, out->bonus, out->row_target,
               out->row_score};
-  return run_verify(m, pool, in, di, dout, (uint8_t*)workspace, ws_bytes, (cudaStream_t)stream, false,
-                    in->auto_commit != 0);
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (!graphs_enabled(st))
+    return run_verify(m, pool, in, di, dout, (uint8_t*)workspace, ws_bytes, st, false, in->auto_commit != 0);
+  const std::string key = graph_key(in, (const void*)pool, workspace, ws_bytes, (const void*)in->kv,
+                                    (const void*)in->context_len, (const void*)in->root_token,
+                                    (const void*)in->node_offset, (const void*)in->parent, (const void*)in->token,
+                                    (const void*)in->session_id, (const void*)in->round, (const void*)out->status,
+                                    (const void*)out->accepted_len, (const void*)out->accepted_token,
+                                    (const void*)out->accepted_node, (const void*)out->bonus,
+                                    (const void*)out->row_target, (const void*)out->row_score, 1);
+  return run_graphed(m, key, st, [&](cudaStream_t gs) {
+    return run_verify(m, pool, in, di, dout, (uint8_t*)workspace, ws_bytes, gs, false, in->auto_commit != 0);
+  });
 }
 
 specedge_status specedge_kv_commit(specedge_model* m, specedge_kvpool* pool, const specedge_verify_in* in,
@@ -763,15 +863,24 @@ specedge_status specedge_verify_batch_host(specedge_model* m, specedge_kvpool* p
   uint8_t* ws = (uint8_t*)workspace;
   uint8_t* din = ws + w.stage_in;
   uint8_t* dou = ws + w.stage_out;
-  CK(cudaMemcpyAsync(din, hb, in_bytes, cudaMemcpyHostToDevice, st));
   DevIn di{(int*)(din + o_kv), (int*)(din + o_ctx), (int*)(din + o_root), (int*)(din + o_off),
            (int*)(din + o_par), (int*)(din + o_tok), (uint64_t*)(din + o_ses), (uint32_t*)(din + o_round)};
   DevOut dout{(int*)(dou + q_st), (int*)(dou + q_al), (int*)(dou + q_at), (int*)(dou + q_an), (int*)(dou + q_bo),
               (int*)(dou + q_rt), (float*)(dou + q_rs)};
-  s = run_verify(m, pool, in, di, dout, ws, ws_bytes, st, false, in->auto_commit != 0);
-  if (s != SPECEDGE_OK) return s;
   uint8_t* ho = hb + in_bytes;
-  CK(cudaMemcpyAsync(ho, dou, out_bytes, cudaMemcpyDeviceToHost, st));
+  // H2D of the packed inputs, the verify step, D2H of the packed outputs: one graph replay
+  auto step = [&](cudaStream_t gs) -> specedge_status {
+    CK(cudaMemcpyAsync(din, hb, in_bytes, cudaMemcpyHostToDevice, gs));
+    const specedge_status r = run_verify(m, pool, in, di, dout, ws, ws_bytes, gs, false, in->auto_commit != 0);
+    if (r != SPECEDGE_OK) return r;
+    CK(cudaMemcpyAsync(ho, dou, out_bytes, cudaMemcpyDeviceToHost, gs));
+    return SPECEDGE_OK;
+  };
+  if (graphs_enabled(st))
+    s = run_graphed(m, graph_key(in, (const void*)pool, workspace, ws_bytes, (const void*)hb, 2), st, step);
+  else
+    s = step(st);
+  if (s != SPECEDGE_OK) return s;
   CK(cudaStreamSynchronize(st));
   std::memcpy(out->status, ho + q_st, 4 * B);
   std::memcpy(out->accepted_len, ho + q_al, 4 * B);
@@ -1015,9 +1124,13 @@ specedge_status specedge_set_kernel_timing(int32_t enable) {
 specedge_status specedge_kernel_times(float* out_ms, int32_t* out_count, int32_t reset) {
   for (auto& pr : g_timing.pending) {
     cudaEvent_t a = g_timing.pool[pr.second], b = g_timing.pool[pr.second + 1];
-    if (cudaEventSynchronize(b) != cudaSuccess) return SPECEDGE_E_CUDA;
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return SPECEDGE_E_CUDA;
+    if (cudaEventSynchronize(b) != cudaSuccess || cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+      cudaGetLastError();   // do not leave the failure to the next launch check
+      g_timing.pending.clear();
+      g_timing.used = 0;
+      return SPECEDGE_E_CUDA;
+    }
     g_timing.ms[pr.first] += ms;
     g_timing.count[pr.first] += 1;
   }
