@@ -56,6 +56,7 @@ typedef struct specedge_kvpool specedge_kvpool;
 #define SPECEDGE_E_WORKSPACE (-4)    /* workspace too small for this call */
 #define SPECEDGE_E_UNSUPPORTED (-5)  /* shape outside what the kernels support */
 #define SPECEDGE_E_DEVICE (-6)       /* device is not sm_100 */
+#define SPECEDGE_E_PROTOCOL (-7)     /* scheduler: a session already has an outstanding request */
 
 /* ---- per-request status codes (device-written, out->status[r]) ---- */
 #define SPECEDGE_REQ_OK 0
@@ -259,6 +260,59 @@ int32_t specedge_last_launch_count(void);
 #define SPECEDGE_KERNEL_KINDS 14
 specedge_status specedge_set_kernel_timing(int32_t enable);
 specedge_status specedge_kernel_times(float* out_ms, int32_t* out_count, int32_t reset);
+
+/* ---- NEXT-F1: pipeline-aware verification scheduler (host only) ----
+ * PAPER.md §4.3: the server interleaves verification of many sessions and "dynamically
+ * calibrates ... draft depth" so that "server verification time ~= edge drafting time + network
+ * round-trip time"; worked depths in §5.2 (94.2 ms verify, 11 ms per draft pass ->
+ * depth 7 / 5 / 4 at RTT 15 / 40 / 50 ms).  Interface after SPEC.md S:311-383.  The scheduler is a
+ * single-threaded decision point in front of specedge_verify_batch; it never touches the GPU.
+ * Readings (DESIGN.md §4 R-sched): depth = max(1, round-half-away((verify - rtt) / draft_pass));
+ * estimates are exponentially weighted means (weight w, S:322 default 0.2) whose first observation
+ * initialises them unless a positive prior is configured; FIFO by (arrival, admission order);
+ * work-conserving plans of the oldest min(capacity, queued) requests. */
+#define SPECEDGE_TIMING_VERIFY 0       /* server verify-step time (ms) */
+#define SPECEDGE_TIMING_DRAFT_PASS 1   /* one edge draft forward pass (ms) */
+#define SPECEDGE_TIMING_RTT 2          /* network round trip (ms) */
+
+typedef struct specedge_scheduler specedge_scheduler;
+typedef struct {
+  int32_t capacity;           /* max requests per verify batch, >= 1 */
+  double ewma_weight;         /* in (0, 1] */
+  int32_t fixed_depth;        /* > 0: always this depth; 0: calibrate */
+  double init_verify_ms;      /* priors (<= 0: none, the first observation initialises) */
+  double init_draft_pass_ms;
+  double init_rtt_ms;
+} specedge_scheduler_config;
+
+typedef struct {              /* one pending verify request (host values, copied) */
+  uint64_t session_id;
+  int32_t kv_handle;
+  int32_t length;             /* committed context + draft nodes (reported as padded_len) */
+  double arrival_ms;          /* caller's clock */
+} specedge_sched_request;
+
+/* Pure depth rule; returns >= 1 (draft_pass_ms <= 0 or non-finite input -> 1). */
+int32_t specedge_calibrate_draft_depth(double verify_ms, double draft_pass_ms, double rtt_ms);
+specedge_status specedge_scheduler_create(const specedge_scheduler_config* cfg,
+                                          specedge_scheduler** out);
+specedge_status specedge_scheduler_destroy(specedge_scheduler* sched);
+/* Enqueue; E_PROTOCOL if the session is already queued or in service. */
+specedge_status specedge_scheduler_admit(specedge_scheduler* sched, const specedge_sched_request* req);
+/* Dequeue the oldest min(capacity, max_members, queued) requests into members[] (in order), set
+ * *n_members (0 when the queue is empty) and *padded_len = max member length (nullable).  The
+ * members stay outstanding until specedge_scheduler_complete. */
+specedge_status specedge_scheduler_plan(specedge_scheduler* sched, specedge_sched_request* members,
+                                        int32_t max_members, int32_t* n_members, int32_t* padded_len);
+/* A batch finished after verify_ms: its sessions may be admitted again; updates the verify estimate. */
+specedge_status specedge_scheduler_complete(specedge_scheduler* sched, const uint64_t* sessions,
+                                            int32_t n, double verify_ms);
+/* Feed a timing measurement (kind = SPECEDGE_TIMING_*). */
+specedge_status specedge_scheduler_observe(specedge_scheduler* sched, int32_t kind, double ms);
+/* Current draft depth, queue size, outstanding sessions and the three estimates (-1 = none yet);
+ * every output nullable. */
+specedge_status specedge_scheduler_state(const specedge_scheduler* sched, int32_t* depth,
+                                         int32_t* queued, int32_t* outstanding, double* estimates3);
 
 #ifdef __cplusplus
 }

@@ -10,7 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libspecedge.so")
 
 OK = 0
-E_INVALID, E_CUDA, E_OOM, E_WORKSPACE, E_UNSUPPORTED, E_DEVICE = -1, -2, -3, -4, -5, -6
+E_INVALID, E_CUDA, E_OOM, E_WORKSPACE, E_UNSUPPORTED, E_DEVICE, E_PROTOCOL = -1, -2, -3, -4, -5, -6, -7
+TIMING_VERIFY, TIMING_DRAFT_PASS, TIMING_RTT = 0, 1, 2
 REQ_OK, REQ_E_TREE, REQ_E_TREE_SIZE, REQ_E_TOKEN, REQ_E_DUP_SIBLING, REQ_E_CONTEXT, \
     REQ_E_KV_CAPACITY, REQ_E_HANDLE = range(8)
 GREEDY, SAMPLE_TREE = 0, 1
@@ -25,7 +26,9 @@ EXPORTS = [
     "specedge_debug_weight_rows", "specedge_debug_read_kv", "specedge_debug_gemm",
     "specedge_debug_last_logits", "specedge_debug_attention", "specedge_last_launch_count",
     "specedge_set_kernel_timing", "specedge_kernel_times", "specedge_tp_unique_id", "specedge_model_create_tp",
-    "specedge_model_tp_info",
+    "specedge_model_tp_info", "specedge_calibrate_draft_depth", "specedge_scheduler_create",
+    "specedge_scheduler_destroy", "specedge_scheduler_admit", "specedge_scheduler_plan",
+    "specedge_scheduler_complete", "specedge_scheduler_observe", "specedge_scheduler_state",
 ]
 KERNEL_KINDS = ["prep", "embed", "rmsnorm", "gemm_qkv", "attention", "attn_combine", "gemm_o", "gemm_gateup",
                 "gemm_down", "gemm_lmhead", "lm_reduce", "walk", "commit", "qkv_rope"]
@@ -36,6 +39,16 @@ class ModelConfig(C.Structure):
                 ("n_kv", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32),
                 ("vocab", C.c_int32), ("eps", C.c_float), ("rope_theta", C.c_double),
                 ("max_position", C.c_int32)]
+
+
+class SchedulerConfig(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("ewma_weight", C.c_double), ("fixed_depth", C.c_int32),
+                ("init_verify_ms", C.c_double), ("init_draft_pass_ms", C.c_double), ("init_rtt_ms", C.c_double)]
+
+
+class SchedRequest(C.Structure):
+    _fields_ = [("session_id", C.c_uint64), ("kv_handle", C.c_int32), ("length", C.c_int32),
+                ("arrival_ms", C.c_double)]
 
 
 class VerifyIn(C.Structure):
@@ -90,6 +103,14 @@ def load(path: str = LIB_PATH):
         "specedge_tp_unique_id": [P],
         "specedge_model_create_tp": [C.POINTER(ModelConfig), U64, I32, I32, I32, P, C.POINTER(P)],
         "specedge_model_tp_info": [P, P, P, P, P],
+        "specedge_calibrate_draft_depth": [C.c_double, C.c_double, C.c_double],
+        "specedge_scheduler_create": [C.POINTER(SchedulerConfig), C.POINTER(P)],
+        "specedge_scheduler_destroy": [P],
+        "specedge_scheduler_admit": [P, C.POINTER(SchedRequest)],
+        "specedge_scheduler_plan": [P, P, I32, C.POINTER(I32), C.POINTER(I32)],
+        "specedge_scheduler_complete": [P, P, I32, C.c_double],
+        "specedge_scheduler_observe": [P, I32, C.c_double],
+        "specedge_scheduler_state": [P, P, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

@@ -312,3 +312,58 @@ def debug_last_logits(model: Model, ws: torch.Tensor, batch: Batch, stream=None)
     L.check(model.lib.specedge_debug_last_logits(model.h, _ptr(ws), ws.numel(), batch.num_requests, batch.rows,
                                                  _ptr(out), _stream(stream)), "debug_last_logits")
     return out
+
+
+class Scheduler:
+    """NEXT-F1 pipeline-aware verification scheduler (include/specedge.h; host only, no GPU)."""
+
+    def __init__(self, capacity: int, ewma_weight: float = 0.2, fixed_depth: int = 0, init_verify_ms: float = 0.0,
+                 init_draft_pass_ms: float = 0.0, init_rtt_ms: float = 0.0):
+        self.lib = L.load()
+        cfg = L.SchedulerConfig(capacity, ewma_weight, fixed_depth, init_verify_ms, init_draft_pass_ms, init_rtt_ms)
+        h = C.c_void_p()
+        L.check(self.lib.specedge_scheduler_create(C.byref(cfg), C.byref(h)), "scheduler_create")
+        self.h = h
+        self.capacity = capacity
+
+    def close(self):
+        if self.h:
+            self.lib.specedge_scheduler_destroy(self.h)
+            self.h = None
+
+    def admit(self, session_id: int, kv_handle: int, length: int, arrival_ms: float) -> bool:
+        """False on a protocol error (the session already has an outstanding request)."""
+        r = L.SchedRequest(session_id, kv_handle, length, arrival_ms)
+        st = self.lib.specedge_scheduler_admit(self.h, C.byref(r))
+        if st == L.E_PROTOCOL:
+            return False
+        L.check(st, "scheduler_admit")
+        return True
+
+    def plan(self):
+        """-> (list of (session_id, kv_handle, length, arrival_ms), padded_len); ([], 0) if idle."""
+        buf = (L.SchedRequest * self.capacity)()
+        n, pad = C.c_int32(), C.c_int32()
+        L.check(self.lib.specedge_scheduler_plan(self.h, C.cast(buf, C.c_void_p), self.capacity, C.byref(n),
+                                                 C.byref(pad)), "scheduler_plan")
+        return [(buf[i].session_id, buf[i].kv_handle, buf[i].length, buf[i].arrival_ms) for i in range(n.value)], \
+            pad.value
+
+    def complete(self, sessions, verify_ms: float):
+        arr = (C.c_uint64 * max(1, len(sessions)))(*sessions)
+        L.check(self.lib.specedge_scheduler_complete(self.h, C.cast(arr, C.c_void_p), len(sessions), verify_ms),
+                "scheduler_complete")
+
+    def observe(self, kind: int, ms: float):
+        L.check(self.lib.specedge_scheduler_observe(self.h, kind, ms), "scheduler_observe")
+
+    def state(self):
+        d, q, o = C.c_int32(), C.c_int32(), C.c_int32()
+        est = (C.c_double * 3)()
+        L.check(self.lib.specedge_scheduler_state(self.h, C.byref(d), C.byref(q), C.byref(o),
+                                                  C.cast(est, C.c_void_p)), "scheduler_state")
+        return dict(depth=d.value, queued=q.value, outstanding=o.value, estimates=list(est))
+
+
+def calibrate_draft_depth(verify_ms: float, draft_pass_ms: float, rtt_ms: float) -> int:
+    return int(L.load().specedge_calibrate_draft_depth(verify_ms, draft_pass_ms, rtt_ms))
