@@ -74,6 +74,7 @@ __device__ __forceinline__ void load_tile(f16* dst, const f16* src, int valid, i
 template <int HD>
 __global__ void __launch_bounds__(kMaxWarps * 32)
     k_tree_attention(const __grid_constant__ AttnArgs a) {
+  pdl_begin();
   constexpr int NCH = HD / 8;      // 16-byte chunks per row
   constexpr int KS = HD / 16;      // k16 steps over head dim
   constexpr int NT = HD / 8;       // n8 tiles over head dim
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 // One warp per (row, head); lanes own 4 consecutive head-dim elements (float4).
 __global__ void k_attn_combine(const __grid_constant__ AttnArgs a, bf16* __restrict__ O,
                                float* __restrict__ O_f32) {
+  pdl_begin();
   const int rh = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // row * H + head
   const int lane = threadIdx.x & 31;
   if (rh >= a.R * a.H) return;
@@ -381,7 +383,10 @@ cudaError_t launch_hd(const AttnArgs& a, int B, cudaStream_t st) {
     attr = std::max(smem, (size_t)48 * 1024);
   }
   dim3 grid(B * a.KV, a.n_splits);
-  k_tree_attention<HD><<<grid, nwarps * 32, smem, st>>>(a);
+  {
+    cudaError_t le = launch_k(k_tree_attention<HD>, grid, dim3(nwarps * 32), smem, st, a);
+    if (le != cudaSuccess) return le;
+  }
   return cudaGetLastError();
 }
 
@@ -418,7 +423,10 @@ cudaError_t attention_launch(const AttnArgs& a, int B, cudaStream_t st, int* lau
 
 cudaError_t attn_combine_launch(const AttnArgs& a, bf16* O, float* O_f32, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
-  k_attn_combine<<<(a.R * a.H + 7) / 8, 256, 0, st>>>(a, O, O_f32);
+  {
+    cudaError_t le = launch_k(k_attn_combine, dim3((a.R * a.H + 7) / 8), dim3(256), 0, st, a, O, O_f32);
+    if (le != cudaSuccess) return le;
+  }
   return cudaGetLastError();
 }
 

@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQ2,
               const __grid_constant__ CUtensorMap tmQ4, const __grid_constant__ CUtensorMap tmPool,
               const __grid_constant__ CUtensorMap tmTree, const __grid_constant__ TcArgs ta) {
+  pdl_begin();
   constexpr int KB = HD / 64;                       // 64-element hd blocks
   constexpr uint32_t QT_BYTES = 128 * HD * 2;       // one 128-row M-tile of Q
   constexpr uint32_t PG_BYTES = 64 * HD * 2;        // K (or V) of one 64-key sub-tile
@@ -778,7 +779,10 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
     attr = true;
   }
   dim3 grid(B * a.KV, a.n_splits);
-  k_attn_tc<HD><<<grid, kThreads, smem, st>>>(tq, tq2, tq4, tp, tt, ta);
+  {
+    const cudaError_t le = launch_k(k_attn_tc<HD>, grid, dim3(kThreads), smem, st, tq, tq2, tq4, tp, tt, ta);
+    if (le != cudaSuccess) return le;
+  }
   if (trace) {
     static int calls = 0;
     if (++calls % 32 == 7) {

@@ -55,6 +55,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// Programmatic dependent launch (every verify-path kernel is launched with programmatic stream
+// serialisation, launch_k in internal.h): let the next kernel's CTAs be scheduled right away,
+// then wait until the previous kernel has completed and its writes are visible.  Must precede any
+// global-memory access of the kernel (only smem/TMEM setup may come first).
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(

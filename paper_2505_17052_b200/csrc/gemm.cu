@@ -16,6 +16,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <map>
 #include <cstdlib>
 
 namespace se {
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_begin();   // setup above overlaps the previous kernel; global reads/writes only from here
   const int ntiles = a.n_tiles_m * a.n_tiles_n;
   const int nunits = ntiles * a.splits;   // work unit = (tile, K split)
 
@@ -325,11 +327,22 @@ __device__ __forceinline__ void tc_mma_f16_2sm(uint32_t tmem_d, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar) {
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask = 3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
-      "h"((uint16_t)3)
+      "h"(mask)
+      : "memory");
+}
+// 2SM TMA load multicast to the CTAs in `mask` (same smem offset in each); every destination's
+// complete_tx goes to the barrier at leader_bar's offset in that destination's pair leader
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap* m, uint64_t* leader_bar, int c0,
+                                                   int c1, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(leader_bar) & kPeerMask), "r"(c0), "r"(c1), "h"(mask),
+      "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* smem_dst, uint32_t ncols) {
@@ -342,8 +355,11 @@ __device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr, uint32_t ncols)
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
+// Launched with clusters of 2*nc CTAs: nc CTA pairs compute the nc N-tiles of one 256-feature
+// weight tile; pair 0 loads the weight halves once and multicasts them to every pair (the
+// activation tiles differ per pair), which divides the L2->SM weight traffic by nc.
 template <int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -364,15 +380,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
+  const int NC = a.nc;
+  const int qp = (int)(rank >> 1);             // pair index in the cluster
+  const uint32_t hr = rank & 1u;               // half of the pair
+  const bool leader = hr == 0;
   const uint32_t b_bytes = (uint32_t)HB * 128u;
+  // all CTAs of the cluster / the CTAs holding weight half hr / this pair
+  const uint16_t mask_all = (uint16_t)((1u << (2 * NC)) - 1u);
+  uint16_t mask_half = 0;
+  for (int j = 0; j < NC; ++j) mask_half |= (uint16_t)(1u << (2 * j + hr));
+  const uint16_t mask_pair = (uint16_t)(3u << (2 * qp));
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 2);         // one arrival per CTA (leader's carries the tx bytes)
-      mbar_init(&empty[s], 1);
+      mbar_init(&full[s], 2);         // one arrival per CTA of the pair (leader's carries the tx)
+      mbar_init(&empty[s], NC);       // one MMA commit per pair (a stage holds multicast weights)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -385,9 +409,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int ntiles = a.n_tiles_m * a.n_tiles_n;   // n_tiles_m counts 256-feature pairs here
+  pdl_begin();   // setup above overlaps the previous kernel; global reads/writes only from here
+  // cluster work unit = (256-feature tile p, N-tile group, K-split); pair qp takes N-tile
+  // group * nc + qp (tiles past the activations read zeros and store nothing)
+  const int ntiles = a.n_tiles_m * a.n_groups;   // n_tiles_m counts 256-feature pairs here
   const int nunits = ntiles * a.splits;
-  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int cl = blockIdx.x / (2 * NC), ncl = gridDim.x / (2 * NC);
 
   if (warp == 0) {
     if (elect_one()) {
@@ -397,14 +424,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int u = cl; u < nunits; u += ncl) {
         const int t = u / a.splits, sk = u % a.splits;
-        const int p = t / a.n_tiles_n, n = t % a.n_tiles_n;
+        const int p = t / a.n_groups, n = (t % a.n_groups) * NC + qp;
         const int kb0 = sk * a.kb_per_split, kb1 = min(a.num_kb, kb0 + a.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + b_bytes));
           else mbar_arrive_leader(&full[stage]);
-          tma_load_2d_2sm(sA + stage * kABytes, &tmA, &full[stage], kb * 64, p * 256 + (int)rank * 128, pol_w);
-          tma_load_2d_2sm(sB + stage * b_bytes, &tmB, &full[stage], kb * 64, n * BN + (int)rank * HB, pol_x);
+          if (NC == 1)
+            tma_load_2d_2sm(sA + stage * kABytes, &tmA, &full[stage], kb * 64, p * 256 + (int)hr * 128, pol_w);
+          else if (qp == 0)
+            tma_load_2d_2sm_mc(sA + stage * kABytes, &tmA, &full[stage], kb * 64, p * 256 + (int)hr * 128, mask_half,
+                               pol_w);
+          tma_load_2d_2sm(sB + stage * b_bytes, &tmB, &full[stage], kb * 64, n * BN + (int)hr * HB, pol_x);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
@@ -432,10 +463,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 4; ++k)
             tc_mma_f16_2sm(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
                            (kb > kb0 || k > 0) ? 1u : 0u);
-          tc_commit_2sm_mc(&empty[stage]);
+          tc_commit_2sm_mc(&empty[stage], mask_all);   // every CTA's copy of the stage
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        tc_commit_2sm_mc(&tfull[acc]);
+        tc_commit_2sm_mc(&tfull[acc], mask_pair);
       }
     }
   } else {
@@ -445,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int it = 0;
     for (int u = cl; u < nunits; u += ncl, ++it) {
       const int t = u / a.splits, sk = u % a.splits;
-      const int p = t / a.n_tiles_n, n = t % a.n_tiles_n;
+      const int p = t / a.n_groups, n = (t % a.n_groups) * NC + qp;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -457,7 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         const int row_base = n * BN + c * 32;
         const int ncol = min(32, BN - c * 32);
-        epi_chunk<MODE>(a, v, 2 * p + (int)rank, tl, et, row_base, ncol, sk, xch, red_v, red_i);
+        epi_chunk<MODE>(a, v, 2 * p + (int)hr, tl, et, row_base, ncol, sk, xch, red_v, red_i);
       }
       tc_fence_before();
       mbar_arrive_leader(&tempty[acc]);
@@ -501,13 +532,13 @@ cudaError_t launch_mode(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_gemm<MODE><<<grid, kThreads, smem, st>>>(tmW, tmX, a);
+  const cudaError_t le = launch_k(k_gemm<MODE>, dim3(grid), dim3(kThreads), smem, st, tmW, tmX, a);
+  if (le != cudaSuccess) return le;
   return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t launch_mode2(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmArgs& a,
-                         size_t smem, int grid, cudaStream_t st) {
+cudaError_t prep_mode2() {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_gemm2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -515,7 +546,57 @@ cudaError_t launch_mode2(const CUtensorMap& tmW, const CUtensorMap& tmX, const G
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_gemm2<MODE><<<grid, kThreads, smem, st>>>(tmW, tmX, a);
+  return cudaSuccess;
+}
+
+// clusters of `csize` CTAs that can be co-resident (cached per (mode, csize, smem))
+template <int MODE>
+int max_clusters2(int csize, size_t smem) {
+  static std::map<std::pair<int, size_t>, int> cache;
+  auto key = std::make_pair(csize, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(csize * 64, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_gemm2<MODE>, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = g_num_sms / csize;
+  }
+  cache[key] = n;
+  return n;
+}
+
+template <int MODE>
+cudaError_t launch_mode2(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmArgs& a,
+                         size_t smem, int grid, cudaStream_t st) {
+  cudaError_t e = prep_mode2<MODE>();
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2 * a.nc;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  e = cudaLaunchKernelEx(&cfg, k_gemm2<MODE>, tmW, tmX, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -536,6 +617,8 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 
 int gemm_splits_last() { return g_last_splits; }
 
+// Activation-row tile: the fewest <= 256-row tiles, rows rounded up to a multiple of 16
+// (measured: 5 x 224 beats 6 x 176 for the 1056-row LM head; larger N per MMA instruction)
 int gemm_pick_bn(int R) {
   const int nt = (R + 255) / 256;
   int bn = (R + nt - 1) / nt;
@@ -561,8 +644,27 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
   CUtensorMap tmX;
   if (!make_tmap_2d(&tmX, X, (uint64_t)a.R, (uint64_t)a.K, (uint32_t)HB)) return cudaErrorInvalidValue;
   const int n_pairs = (a.M + 255) / 256;
-  const int ntiles = n_pairs * a.n_tiles_n;
-  const int nclusters = g_num_sms / 2;
+  // pairs per cluster sharing each weight tile through TMA multicast (SPECEDGE_GEMM_NC = 0: the
+  // N-tiles of one 256-feature tile, up to 4 pairs).  Off by default: measured on cfg2 it cuts
+  // the weights' L2 reads by 3x but the lock-stepped pairs and the cluster-of-6 occupancy
+  // (22 clusters = 132 SMs) make the GEMM slower (profiles/README.md); the mainloop is bound by
+  // operand delivery into shared memory, not by L2.
+  static const int env_nc = getenv("SPECEDGE_GEMM_NC") ? atoi(getenv("SPECEDGE_GEMM_NC")) : 1;
+  int nc = 1;
+  if (env_nc > 0) nc = std::min(env_nc, 4);
+  else if (a.n_tiles_n <= 4) nc = a.n_tiles_n;
+  else if (a.n_tiles_n % 3 == 0) nc = 3;
+  else if (a.n_tiles_n % 4 == 0) nc = 4;
+  else if (a.n_tiles_n % 2 == 0) nc = 2;
+  a.nc = nc;
+  a.n_groups = (a.n_tiles_n + nc - 1) / nc;
+  const int ntiles = n_pairs * a.n_groups;
+  cudaError_t pe = EPI_F32 == mode ? prep_mode2<EPI_F32>() : (mode == EPI_SWIGLU ? prep_mode2<EPI_SWIGLU>()
+                                                                                 : prep_mode2<EPI_ARGMAX>());
+  if (pe != cudaSuccess) return pe;
+  const int nclusters = mode == EPI_F32 ? max_clusters2<EPI_F32>(2 * nc, smem)
+                        : (mode == EPI_SWIGLU ? max_clusters2<EPI_SWIGLU>(2 * nc, smem)
+                                              : max_clusters2<EPI_ARGMAX>(2 * nc, smem));
   a.splits = 1;
   static const int env_max = getenv("SPECEDGE_MAX_SPLITS") ? atoi(getenv("SPECEDGE_MAX_SPLITS")) : 0;
   if (env_max > 0) a.max_splits = std::min(a.max_splits, env_max);
@@ -576,7 +678,7 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
   g_last_splits = a.splits;
   GemmArgs b = a;
   b.n_tiles_m = n_pairs;      // the kernel iterates 256-feature pairs
-  const int grid = 2 * std::min(ntiles * a.splits, nclusters);
+  const int grid = 2 * nc * std::min(ntiles * a.splits, nclusters);
   if (launches) ++*launches;
   switch (mode) {
     case EPI_F32: return launch_mode2<EPI_F32>(tmW, tmX, b, smem, grid, st);

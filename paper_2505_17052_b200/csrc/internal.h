@@ -8,11 +8,30 @@
 #include <stdint.h>
 #include <stddef.h>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/specedge.h"
 
 namespace se {
+
+// Launch (optionally with programmatic stream serialisation: kernels call pdl_begin() before any
+// global access; enabled by SPECEDGE_PDL=1).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 using bf16 = __nv_bfloat16;
 using f16 = __half;   // attention operands q, k, v and the KV cache
@@ -31,6 +50,8 @@ struct GemmArgs {
   int BN, n_tiles_n, n_tiles_m, num_kb, stages, tmem_cols;
   int ntm128;             // 128-feature tiles (stride of the ARGMAX partials)
   int pair;               // EPI_F32/EPI_ARGMAX: rows (2r, 2r+1) are hi/lo bf16 parts of row r
+  int nc;                 // CTA-pair kernel: pairs per cluster sharing one weight tile (TMA multicast)
+  int n_groups;           // CTA-pair kernel: ceil(n_tiles_n / nc)
   int splits, kb_per_split, max_splits;   // K-split (EPI_F32): slice sk at out_f32 + sk*split_stride
   size_t split_stride;
   // EPI_F32 / EPI_RESID (fp32 residual stream)

@@ -10,6 +10,12 @@
 #include "internal.h"
 
 namespace se {
+#define CK_RET(x)                 \
+  do {                            \
+    cudaError_t _e = (x);         \
+    if (_e != cudaSuccess) return _e; \
+  } while (0)
+
 
 namespace {
 
@@ -17,6 +23,7 @@ namespace {
 // One CTA (64 threads) per request.  Thread i owns node i (and i+64.. when N > 64 so every row
 // is still written for oversize trees, which are flagged E_TREE_SIZE).
 __global__ void k_prep(const __grid_constant__ PrepArgs p) {
+  pdl_begin();
   const int r = blockIdx.x, i0 = threadIdx.x;
   __shared__ int s_flags[8];
   __shared__ int s_depth_max;
@@ -108,6 +115,7 @@ __global__ void k_prep(const __grid_constant__ PrepArgs p) {
 // ------------------------------------------------------------------------------- K2 embedding
 // X (fp32 residual stream) = E[token] (bf16 values, exact in fp32)
 __global__ void k_embed(const bf16* __restrict__ E, const int* __restrict__ row_tok, float* __restrict__ X, int d) {
+  pdl_begin();
   const int row = blockIdx.x;
   const int tok = row_tok[row];
   const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)tok * d);
@@ -130,6 +138,7 @@ template <int NY>
 __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const float* __restrict__ Y, size_t y_stride,
                                                   const bf16* __restrict__ g, bf16* __restrict__ out, int d, float eps,
                                                   int split) {
+  pdl_begin();
   // blockDim.x = d / 16: each thread owns 16 consecutive elements, kept in registers across passes
   const int row = blockIdx.x;
   const int i = threadIdx.x * 16;
@@ -211,6 +220,7 @@ __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const f
 // position row_pos (amb. A14), or per 4 consecutive v elements; float4 loads of every K-split
 // partial (summed in split order), fp16 stores.
 __global__ void k_qkv_rope(const __grid_constant__ RopeArgs r) {
+  pdl_begin();
   const int row = blockIdx.y;
   const int hd = r.hd, half = hd >> 1, hq = half >> 2;    // 4-pair groups per head
   const int qkv = (r.H + 2 * r.KV) * hd;
@@ -263,6 +273,7 @@ __global__ void k_qkv_rope(const __grid_constant__ RopeArgs r) {
 __global__ void k_lm_reduce(const float* __restrict__ pv, const int* __restrict__ pi, int R, int ntiles,
                             int* __restrict__ y, float* __restrict__ score, int* __restrict__ row_target,
                             float* __restrict__ row_score) {
+  pdl_begin();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= R) return;
@@ -289,6 +300,7 @@ __global__ void k_lm_reduce(const float* __restrict__ pv, const int* __restrict_
 // ------------------------------------------------------------------------------ K10 walk
 // One warp per request; lane l examines nodes l and l+32 (N <= 64 for valid requests).
 __global__ void k_walk(const __grid_constant__ WalkArgs w) {
+  pdl_begin();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= w.B) return;
@@ -347,6 +359,7 @@ __global__ void k_walk(const __grid_constant__ WalkArgs w) {
 // copy has no aliasing hazard.  Only if the cached length is still the one
 // this verify saw (idempotence guard).
 __global__ void k_commit(const __grid_constant__ CommitArgs c) {
+  pdl_begin();
   const int r = blockIdx.x, layer = blockIdx.y;
   if (c.status[r] != SPECEDGE_REQ_OK) return;
   const int h = c.req_h[r];
@@ -373,6 +386,7 @@ __global__ void k_commit(const __grid_constant__ CommitArgs c) {
 }
 
 __global__ void k_commit_finalize(const __grid_constant__ CommitArgs c) {
+  pdl_begin();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= c.B || c.status[r] != SPECEDGE_REQ_OK) return;
   const int h = c.req_h[r];
@@ -386,6 +400,7 @@ __global__ void k_commit_finalize(const __grid_constant__ CommitArgs c) {
 // cache_len[handle[i]] = len[i] for a batch of up to kSetLenBatch sessions passed by value (one
 // tiny launch, capturable in a CUDA graph; no host staging)
 __global__ void k_set_len(int* __restrict__ cache_len, const __grid_constant__ SetLenArgs a) {
+  pdl_begin();
   const int i = threadIdx.x;
   if (i < a.n) cache_len[a.handle[i]] = a.len[i];
 }
@@ -467,12 +482,12 @@ __global__ void k_kv_fill(f16* pool, const int* __restrict__ block_row, int laye
 
 cudaError_t prep_launch(const PrepArgs& p, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
-  k_prep<<<p.B, 64, 0, st>>>(p);
+  CK_RET(launch_k(k_prep, dim3(p.B), dim3(64), 0, st, p));
   return cudaGetLastError();
 }
 cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int d, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
-  k_embed<<<R, 128, 0, st>>>(E, row_tok, X, d);
+  CK_RET(launch_k(k_embed, dim3(R), dim3(128), 0, st, E, row_tok, X, d));
   return cudaGetLastError();
 }
 cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, const bf16* g, bf16* out, int R, int d,
@@ -480,11 +495,11 @@ cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, co
   if (launches) ++*launches;
   const int threads = d / 16;   // d % 64 == 0 (checked at model creation), <= 1024
   switch (nY) {
-    case 0: k_rmsnorm<0><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
-    case 1: k_rmsnorm<1><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
-    case 2: k_rmsnorm<2><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
-    case 3: k_rmsnorm<3><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
-    case 4: k_rmsnorm<4><<<R, threads, 0, st>>>(X, Y, y_stride, g, out, d, eps, split); break;
+    case 0: CK_RET(launch_k(k_rmsnorm<0>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
+    case 1: CK_RET(launch_k(k_rmsnorm<1>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
+    case 2: CK_RET(launch_k(k_rmsnorm<2>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
+    case 3: CK_RET(launch_k(k_rmsnorm<3>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
+    case 4: CK_RET(launch_k(k_rmsnorm<4>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -492,30 +507,30 @@ cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, co
 cudaError_t qkv_rope_launch(const RopeArgs& r, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
   const int items = (r.H + r.KV) * (r.hd / 8) + r.KV * r.hd / 4;   // head_dim >= 16
-  k_qkv_rope<<<dim3((items + 127) / 128, r.R), 128, 0, st>>>(r);
+  CK_RET(launch_k(k_qkv_rope, dim3((items + 127) / 128, r.R), dim3(128), 0, st, r));
   return cudaGetLastError();
 }
 cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, int* y, float* score,
                              int* row_target, float* row_score, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
-  k_lm_reduce<<<(R + 3) / 4, 128, 0, st>>>(pv, pi, R, ntiles, y, score, row_target, row_score);
+  CK_RET(launch_k(k_lm_reduce, dim3((R + 3) / 4), dim3(128), 0, st, pv, pi, R, ntiles, y, score, row_target, row_score));
   return cudaGetLastError();
 }
 cudaError_t walk_launch(const WalkArgs& w, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
-  k_walk<<<(w.B + 3) / 4, 128, 0, st>>>(w);
+  CK_RET(launch_k(k_walk, dim3((w.B + 3) / 4), dim3(128), 0, st, w));
   return cudaGetLastError();
 }
 cudaError_t commit_launch(const CommitArgs& c, cudaStream_t st, int* launches) {
   if (launches) *launches += 2;
-  k_commit<<<dim3(c.B, c.layers), 256, 0, st>>>(c);
+  CK_RET(launch_k(k_commit, dim3(c.B, c.layers), dim3(256), 0, st, c));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_commit_finalize<<<(c.B + 127) / 128, 128, 0, st>>>(c);
+  CK_RET(launch_k(k_commit_finalize, dim3((c.B + 127) / 128), dim3(128), 0, st, c));
   return cudaGetLastError();
 }
 cudaError_t set_len_launch(int* cache_len, const SetLenArgs& a, cudaStream_t st) {
-  k_set_len<<<1, kSetLenBatch, 0, st>>>(cache_len, a);
+  CK_RET(launch_k(k_set_len, dim3(1), dim3(kSetLenBatch), 0, st, cache_len, a));
   return cudaGetLastError();
 }
 cudaError_t init_weights_launch(const InitArgs& a, cudaStream_t st) {

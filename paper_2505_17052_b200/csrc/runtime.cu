@@ -14,6 +14,13 @@
 
 using namespace se;
 
+// Programmatic dependent launch: off by default (SPECEDGE_PDL=1 enables).  Measured on cfg2
+// under graph replay it does not shorten the step (the inter-kernel gaps are already ~1 us).
+bool se::pdl_enabled() {
+  static const bool on = getenv("SPECEDGE_PDL") && getenv("SPECEDGE_PDL")[0] == '1';
+  return on;
+}
+
 namespace {
 
 thread_local int g_last_launches = 0;

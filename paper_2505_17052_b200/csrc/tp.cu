@@ -48,6 +48,7 @@ NcclApi& nccl() {
 // (amb. A7).  g = [tp][R][2] floats, id stored as int bits.
 __global__ void k_tp_argmax(const float* __restrict__ g, int tp, int R, int* __restrict__ y, float* __restrict__ score,
                             int* __restrict__ row_target, float* __restrict__ row_score) {
+  pdl_begin();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= R) return;
   float best = -INFINITY;
@@ -64,6 +65,7 @@ __global__ void k_tp_argmax(const float* __restrict__ g, int tp, int R, int* __r
 }
 
 __global__ void k_tp_pack(const int* __restrict__ y, const float* __restrict__ score, int R, float* __restrict__ out) {
+  pdl_begin();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= R) return;
   out[2 * row] = score[row];
@@ -110,12 +112,18 @@ cudaError_t tp_allreduce_f32(float* buf, size_t n, void* comm, cudaStream_t st) 
 cudaError_t tp_argmax_gather(int* y, float* score, int R, float* gather, int tp, void* comm, int* row_target,
                              float* row_score, cudaStream_t st, int* launches) {
   float* mine = gather + (size_t)tp * R * 2;   // staging after the gather area
-  k_tp_pack<<<(R + 127) / 128, 128, 0, st>>>(y, score, R, mine);
+  {
+    cudaError_t le = launch_k(k_tp_pack, dim3((R + 127) / 128), dim3(128), 0, st, y, score, R, mine);
+    if (le != cudaSuccess) return le;
+  }
   if (launches) *launches += 2;
   if (nccl().AllGather(mine, gather, (size_t)R * 2, ncclFloat32, reinterpret_cast<ncclComm_t>(comm), st) !=
       ncclSuccess)
     return cudaErrorUnknown;
-  k_tp_argmax<<<(R + 127) / 128, 128, 0, st>>>(gather, tp, R, y, score, row_target, row_score);
+  {
+    cudaError_t le = launch_k(k_tp_argmax, dim3((R + 127) / 128), dim3(128), 0, st, (const float*)gather, tp, R, y, score, row_target, row_score);
+    if (le != cudaSuccess) return le;
+  }
   return cudaGetLastError();
 }
 
