@@ -68,12 +68,23 @@ typedef struct specedge_kvpool specedge_kvpool;
                                          ("context-length mismatch -> protocol error") */
 #define SPECEDGE_REQ_E_KV_CAPACITY 6  /* cached + deepest path + 1 exceeds the handle's capacity */
 #define SPECEDGE_REQ_E_HANDLE 7       /* KV handle not allocated */
+#define SPECEDGE_REQ_E_UNSUPPORTED 8  /* SAMPLE_PQ_DENSE: the draft is not a chain */
 /* validation order (first failing check wins): HANDLE, TREE_SIZE, TREE, TOKEN, DUP_SIBLING,
    CONTEXT, KV_CAPACITY — identical to oracle/verify.py:validate for the shared codes. */
 
 /* ---- verification modes (SURVEY amb. A7-A9) ---- */
 #define SPECEDGE_GREEDY 0       /* y = argmax_v logit, ties -> lowest id */
 #define SPECEDGE_SAMPLE_TREE 1  /* y = argmax_v (logit/T + Gumbel(seed, round, session, slot, v)) */
+/* NEXT-F2: speculative sampling of a chain whose tokens the edge SAMPLED from its
+ * draft distributions q, shipped dense in verify_in.draft_q (App. B, P:766-770:
+ * Leviathan et al.).  Node i is accepted iff u(slot i) < p_i(x_i) / q_i(x_i),
+ * p_i = softmax(l / T) at slot i; the first rejection's bonus is drawn from norm(max(0, p - q))
+ * by Gumbel-max over log(max(0, p - q)), after full acceptance from p at the last slot.
+ * u(slot) = ((w >> 8) | 1) 2^-24, w = Philox4x32-10 word 0 of counter (slot, 'ACPT',
+ * lo32(session), hi32(session)), key (lo32(seed) ^ round, hi32(seed)).  Requires T >= 1e-6,
+ * draft_q != NULL and tp_size == 1 (else E_INVALID / E_UNSUPPORTED); a request whose tree is not
+ * a chain gets status REQ_E_UNSUPPORTED.  Cost: two LM-head passes (log-sum-exp, then residual). */
+#define SPECEDGE_SAMPLE_PQ_DENSE 2
 
 #define SPECEDGE_MAX_NODES 64
 #define SPECEDGE_PAGE_TOKENS 64
@@ -180,6 +191,8 @@ typedef struct {
   const int32_t* token;          /* [total_nodes] draft tokens */
   const float* draft_logprob;    /* [total_nodes] log q, nullable; unused by GREEDY and
                                     SAMPLE_TREE (SURVEY Lemma, amb. A23) */
+  const float* draft_q;          /* [total_nodes][V] fp32 draft distributions, row i = the q
+                                    node i was sampled from; SAMPLE_PQ_DENSE only, else NULL */
 } specedge_verify_in;
 
 typedef struct {                 /* device arrays, caller-allocated */
@@ -208,7 +221,8 @@ specedge_status specedge_kv_commit(specedge_model* model, specedge_kvpool* pool,
 
 /* End-to-end entry point with HOST buffers (same fields; every pointer in `in`/`out` is host
  * memory, pinned for best results).  Copies the inputs into the workspace, verifies, copies
- * the outputs back and synchronises `stream` before returning. */
+ * the outputs back and synchronises `stream` before returning.  SAMPLE_PQ_DENSE (dense q rows)
+ * is device-entry only here: E_UNSUPPORTED. */
 specedge_status specedge_verify_batch_host(specedge_model* model, specedge_kvpool* pool,
                                            const specedge_verify_in* in_host,
                                            specedge_verify_out* out_host, void* workspace,

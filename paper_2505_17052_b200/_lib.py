@@ -12,9 +12,10 @@ LIB_PATH = os.path.join(HERE, "libspecedge.so")
 OK = 0
 E_INVALID, E_CUDA, E_OOM, E_WORKSPACE, E_UNSUPPORTED, E_DEVICE, E_PROTOCOL = -1, -2, -3, -4, -5, -6, -7
 TIMING_VERIFY, TIMING_DRAFT_PASS, TIMING_RTT = 0, 1, 2
+REQ_E_UNSUPPORTED = 8
 REQ_OK, REQ_E_TREE, REQ_E_TREE_SIZE, REQ_E_TOKEN, REQ_E_DUP_SIBLING, REQ_E_CONTEXT, \
     REQ_E_KV_CAPACITY, REQ_E_HANDLE = range(8)
-GREEDY, SAMPLE_TREE = 0, 1
+GREEDY, SAMPLE_TREE, SAMPLE_PQ_DENSE = 0, 1, 2
 MAX_NODES = 64
 
 # every symbol include/specedge.h declares (tests check the .so exports all of them)
@@ -57,7 +58,8 @@ class VerifyIn(C.Structure):
                 ("seed", C.c_uint64), ("auto_commit", C.c_int32),
                 ("kv", C.c_void_p), ("context_len", C.c_void_p), ("root_token", C.c_void_p),
                 ("session_id", C.c_void_p), ("round", C.c_void_p), ("node_offset", C.c_void_p),
-                ("parent", C.c_void_p), ("token", C.c_void_p), ("draft_logprob", C.c_void_p)]
+                ("parent", C.c_void_p), ("token", C.c_void_p), ("draft_logprob", C.c_void_p),
+                ("draft_q", C.c_void_p)]
 
 
 class VerifyOut(C.Structure):

@@ -164,6 +164,7 @@ class Batch:
     total_nodes: int
     max_nodes: int
     max_context_len: int
+    draft_q: torch.Tensor | None = None   # [total_nodes, V] fp32, SAMPLE_PQ_DENSE only
 
     @property
     def num_requests(self):
@@ -214,7 +215,8 @@ def _vin(batch: Batch, mode, temperature, seed, auto_commit):
                       float(temperature), C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF).value, int(auto_commit),
                       batch.kv.data_ptr(), batch.context_len.data_ptr(), batch.root_token.data_ptr(),
                       batch.session_id.data_ptr(), batch.round.data_ptr(), batch.node_offset.data_ptr(),
-                      batch.parent.data_ptr(), batch.token.data_ptr(), batch.draft_logprob.data_ptr())
+                      batch.parent.data_ptr(), batch.token.data_ptr(), batch.draft_logprob.data_ptr(),
+                      None if batch.draft_q is None else batch.draft_q.data_ptr())
 
 
 def _vout(o: Outputs):
@@ -266,7 +268,7 @@ def verify_host(model: Model, pool: KVPool, hb: HostBatch, ws: torch.Tensor, out
                      seed, int(auto_commit), a["kv"].data_ptr(), a["context_len"].data_ptr(),
                      a["root_token"].data_ptr(), a["session_id"].data_ptr(), a["round"].data_ptr(),
                      a["node_offset"].data_ptr(), a["parent"].data_ptr(), a["token"].data_ptr(),
-                     a["draft_logprob"].data_ptr())
+                     a["draft_logprob"].data_ptr(), None)
     vout = L.VerifyOut(*(outs[k].data_ptr() for k in ("status", "accepted_len", "accepted_token",
                                                       "accepted_node", "bonus", "row_target", "row_score")))
     L.check(model.lib.specedge_verify_batch_host(model.h, pool.h, C.byref(vin), C.byref(vout), _ptr(ws),

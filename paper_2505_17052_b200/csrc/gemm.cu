@@ -99,32 +99,54 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         }
       }
       named_bar_sync(1, kEpiThreads);
-    } else if constexpr (MODE == EPI_ARGMAX) {
+    } else if constexpr (MODE == EPI_ARGMAX || MODE == EPI_PQ1 || MODE == EPI_PQ2) {
       // a.pair: physical rows (2r, 2r+1) = hi/lo parts of logical row r -> 16 logical columns
       const int np = a.pair ? 16 : 32;
       const bool fv = feat < a.vocab;
-      if (a.pair) {
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int row = row_base + 2 * jj;
-          float s = -INFINITY;
-          if (fv && 2 * jj < ncol && row < a.R) {
-            s = __uint_as_float(v[2 * jj]) + __uint_as_float(v[2 * jj + 1]);
-            if (a.sample) s = s * a.inv_t + gumbel_noise(a, row >> 1, a.vocab_off + feat);
-          }
-          xch[tl * kXchStride + jj] = s;
-        }
-      } else {
+      const int vg = a.vocab_off + feat;   // global vocab id
+      // logical row jj's logit of this thread's feature, or NaN when out of range
+      auto logit = [&](int jj, int& lrow) -> float {
+        const int j = a.pair ? 2 * jj : jj;
+        const int row = row_base + j;
+        lrow = a.pair ? row >> 1 : row;
+        if (!fv || j >= ncol || row >= a.R) return __int_as_float(0x7fc00000);
+        return a.pair ? __uint_as_float(v[2 * jj]) + __uint_as_float(v[2 * jj + 1]) : __uint_as_float(v[jj]);
+      };
+      // ---- Gumbel noise of (row, vg), precomputed for the whole [R][vocab] block by k_gumbel_fill
+      // (a full-occupancy kernel: in this 4-warp epilogue the Philox rounds would cost more than the
+      // MMA main loop hides); coalesced across the lanes' consecutive vocab ids
+      float gn[32];
+      if (MODE == EPI_PQ2 || a.sample) {
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
-          const int row = row_base + jj;
-          float s = -INFINITY;
-          if (fv && jj < ncol && row < a.R) {
-            s = __uint_as_float(v[jj]);
-            if (a.sample) s = s * a.inv_t + gumbel_noise(a, row, a.vocab_off + feat);
-          }
-          xch[tl * kXchStride + jj] = s;
+          if (jj >= np) break;
+          const int j = a.pair ? 2 * jj : jj;
+          const int row = min(row_base + j, a.R - 1);
+          gn[jj] = fv ? a.noise[(size_t)(a.pair ? row >> 1 : row) * a.vocab + feat] : 0.f;
         }
+      }
+      // ---- scores for the tile argmax
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        if (jj >= np) break;
+        int lr;
+        const float l = logit(jj, lr);
+        float sc = -INFINITY;
+        if (l == l) {
+          if constexpr (MODE == EPI_PQ2) {
+            // residual r = p - q (p = exp(l/T - lse)); Gumbel-max over log r, r > 0
+            const int qn = a.row_qnode[lr];
+            if (qn >= 0) {
+              const float pv = __expf(fmaf(l, a.inv_t, -a.lse[lr]));
+              if (vg == a.node_token[qn]) a.pchild[lr] = pv;
+              const float r = pv - a.draft_q[(size_t)qn * a.vocab_q + vg];
+              if (r > 0.f) sc = __logf(r) + gn[jj];
+            }
+          } else {
+            sc = a.sample ? l * a.inv_t + gn[jj] : l;
+          }
+        }
+        xch[tl * kXchStride + jj] = sc;
       }
       named_bar_sync(1, kEpiThreads);
       const int ngrp = 128 / np, per = 128 / ngrp;
@@ -133,8 +155,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         float best = -INFINITY;
         int bi = 0x7fffffff;
         for (int l = 0; l < per; ++l) {
-          const float s = xch[(g * per + l) * kXchStride + jj];
-          if (s > best) { best = s; bi = a.vocab_off + m128 * 128 + g * per + l; }
+          const float sc = xch[(g * per + l) * kXchStride + jj];
+          if (sc > best) { best = sc; bi = a.vocab_off + m128 * 128 + g * per + l; }
         }
         red_v[g * np + jj] = best;
         red_i[g * np + jj] = bi;
@@ -145,8 +167,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         float best = red_v[jj];
         int bi = red_i[jj];
         for (int g = 1; g < ngrp; ++g) {
-          const float s = red_v[g * np + jj];
-          if (s > best) { best = s; bi = red_i[g * np + jj]; }
+          const float sc = red_v[g * np + jj];
+          if (sc > best) { best = sc; bi = red_i[g * np + jj]; }
         }
         const int j = a.pair ? 2 * jj : jj;
         const int row = row_base + j;
@@ -157,6 +179,45 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         }
       }
       named_bar_sync(1, kEpiThreads);
+      if constexpr (MODE == EPI_PQ1) {
+        // ---- tile (max, sum exp) of l/T for the row's log-sum-exp
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          if (jj >= np) break;
+          int lr;
+          const float l = logit(jj, lr);
+          xch[tl * kXchStride + jj] = l == l ? l * a.inv_t : -INFINITY;
+        }
+        named_bar_sync(1, kEpiThreads);
+        float* red_s = reinterpret_cast<float*>(red_i);
+        {
+          const int jj = et % np, g = et / np;
+          float m = -INFINITY;
+          for (int l = 0; l < per; ++l) m = fmaxf(m, xch[(g * per + l) * kXchStride + jj]);
+          float sm = 0.f;
+          if (m > -INFINITY)
+            for (int l = 0; l < per; ++l) sm += __expf(xch[(g * per + l) * kXchStride + jj] - m);
+          red_v[g * np + jj] = m;
+          red_s[g * np + jj] = sm;
+        }
+        named_bar_sync(1, kEpiThreads);
+        if (et < np) {
+          const int jj = et;
+          float m = -INFINITY;
+          for (int g = 0; g < ngrp; ++g) m = fmaxf(m, red_v[g * np + jj]);
+          float sm = 0.f;
+          if (m > -INFINITY)
+            for (int g = 0; g < ngrp; ++g) sm += red_s[g * np + jj] * __expf(red_v[g * np + jj] - m);
+          const int j = a.pair ? 2 * jj : jj;
+          const int row = row_base + j;
+          if (j < ncol && row < a.R) {
+            const int lr = a.pair ? row >> 1 : row;
+            a.part_m[(size_t)lr * a.ntm128 + m128] = m;
+            a.part_s[(size_t)lr * a.ntm128 + m128] = sm;
+          }
+        }
+        named_bar_sync(1, kEpiThreads);
+      }
     }
 }
 
@@ -659,12 +720,17 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
   a.nc = nc;
   a.n_groups = (a.n_tiles_n + nc - 1) / nc;
   const int ntiles = n_pairs * a.n_groups;
-  cudaError_t pe = EPI_F32 == mode ? prep_mode2<EPI_F32>() : (mode == EPI_SWIGLU ? prep_mode2<EPI_SWIGLU>()
-                                                                                 : prep_mode2<EPI_ARGMAX>());
+  cudaError_t pe = cudaSuccess;
+  int nclusters = 0;
+  switch (mode) {
+    case EPI_F32: pe = prep_mode2<EPI_F32>(); nclusters = max_clusters2<EPI_F32>(2 * nc, smem); break;
+    case EPI_SWIGLU: pe = prep_mode2<EPI_SWIGLU>(); nclusters = max_clusters2<EPI_SWIGLU>(2 * nc, smem); break;
+    case EPI_ARGMAX: pe = prep_mode2<EPI_ARGMAX>(); nclusters = max_clusters2<EPI_ARGMAX>(2 * nc, smem); break;
+    case EPI_PQ1: pe = prep_mode2<EPI_PQ1>(); nclusters = max_clusters2<EPI_PQ1>(2 * nc, smem); break;
+    case EPI_PQ2: pe = prep_mode2<EPI_PQ2>(); nclusters = max_clusters2<EPI_PQ2>(2 * nc, smem); break;
+    default: return cudaErrorInvalidValue;
+  }
   if (pe != cudaSuccess) return pe;
-  const int nclusters = mode == EPI_F32 ? max_clusters2<EPI_F32>(2 * nc, smem)
-                        : (mode == EPI_SWIGLU ? max_clusters2<EPI_SWIGLU>(2 * nc, smem)
-                                              : max_clusters2<EPI_ARGMAX>(2 * nc, smem));
   a.splits = 1;
   static const int env_max = getenv("SPECEDGE_MAX_SPLITS") ? atoi(getenv("SPECEDGE_MAX_SPLITS")) : 0;
   if (env_max > 0) a.max_splits = std::min(a.max_splits, env_max);
@@ -684,6 +750,8 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
     case EPI_F32: return launch_mode2<EPI_F32>(tmW, tmX, b, smem, grid, st);
     case EPI_SWIGLU: return launch_mode2<EPI_SWIGLU>(tmW, tmX, b, smem, grid, st);
     case EPI_ARGMAX: return launch_mode2<EPI_ARGMAX>(tmW, tmX, b, smem, grid, st);
+    case EPI_PQ1: return launch_mode2<EPI_PQ1>(tmW, tmX, b, smem, grid, st);
+    case EPI_PQ2: return launch_mode2<EPI_PQ2>(tmW, tmX, b, smem, grid, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -737,6 +805,8 @@ cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArg
     case EPI_F32: return launch_mode<EPI_F32>(tmW, tmX, a, smem, grid, st);
     case EPI_SWIGLU: return launch_mode<EPI_SWIGLU>(tmW, tmX, a, smem, grid, st);
     case EPI_ARGMAX: return launch_mode<EPI_ARGMAX>(tmW, tmX, a, smem, grid, st);
+    case EPI_PQ1: return launch_mode<EPI_PQ1>(tmW, tmX, a, smem, grid, st);
+    case EPI_PQ2: return launch_mode<EPI_PQ2>(tmW, tmX, a, smem, grid, st);
   }
   return cudaErrorInvalidValue;
 }

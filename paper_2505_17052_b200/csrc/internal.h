@@ -43,6 +43,8 @@ enum GemmMode : int {
   EPI_F32 = 0,     // out_f32[split][row][m] = partial acc (a4 QKV, a6 O, a8 down; logits capture)
   EPI_SWIGLU = 3,  // M[row][f] = bf16(silu(gate) * up)            (a7)
   EPI_ARGMAX = 4,  // per (row, 128-vocab tile) max / Gumbel-max   (a9)
+  EPI_PQ1 = 5,     // NEXT-F2 pass 1: EPI_ARGMAX (Gumbel-max) + per-tile (max, sum exp) of l/T
+  EPI_PQ2 = 6,     // NEXT-F2 pass 2: per-tile Gumbel-max of log max(0, p - q) + p(child token)
 };
 
 struct GemmArgs {
@@ -77,7 +79,23 @@ struct GemmArgs {
   const int* row_slot;
   const uint32_t* req_round;
   const uint64_t* req_session;
+  // EPI_PQ1 / EPI_PQ2 (dense-q speculative sampling, SAMPLE_PQ_DENSE)
+  float* part_m;          // [R][n_tiles_m] tile max of l/T          (PQ1)
+  float* part_s;          // [R][n_tiles_m] tile sum exp(l/T - max)  (PQ1)
+  const float* lse;       // [R] log sum exp(l/T)                     (PQ2)
+  const int* row_qnode;   // [R] node drawn at this slot (its q row), -1 for the last slot
+  const int* node_token;  // [total_nodes]
+  const float* draft_q;   // [total_nodes][vocab_q] fp32
+  int vocab_q;            // row stride of draft_q (= V)
+  float* pchild;          // [R] p(child token) at this slot          (PQ2)
+  const float* noise;     // [R][vocab] Gumbel noise (sampled modes), from gumbel_fill_launch
 };
+// Gumbel noise g(seed, round, session, slot, v) for rows [0, R) x local vocab [0, vocab) (global
+// id vocab_off + v), amb. A9: Philox4x32-10 counter (v >> 2, slot, lo32(session), hi32(session)),
+// key (lo32(seed) ^ round, hi32(seed)), word v & 3, u = ((w >> 8) | 1) 2^-24, g = -log(-log u)
+cudaError_t gumbel_fill_launch(float* noise, int R, int vocab, int vocab_off, const int* row_req, const int* row_slot,
+                               const uint32_t* req_round, const uint64_t* req_session, uint32_t seed_lo,
+                               uint32_t seed_hi, cudaStream_t st, int* launches);
 
 // Build a 2D bf16 tensor map [rows][cols] (cols contiguous), box {64, box_rows}, 128B swizzle.
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
@@ -180,6 +198,34 @@ struct WalkArgs {
   int* bonus;
 };
 cudaError_t walk_launch(const WalkArgs& w, cudaStream_t st, int* launches);
+// NEXT-F2 (SAMPLE_PQ_DENSE): log-sum-exp from the PQ1 tile partials, the q row of every slot, and
+// the Leviathan walk over a sampled chain (kernels_small.cu)
+struct PqArgs {
+  int B, R, ntiles, V;
+  int* status;
+  const int* node_offset;
+  const int* parent;
+  const int* token;
+  const float* draft_q;        // [total_nodes][V]
+  const int* row_req;
+  const int* row_slot;
+  const float* part_m;         // [R][ntiles]
+  const float* part_s;
+  float* lse;                  // [R]
+  int* row_qnode;              // [R]
+  const float* pchild;         // [R]
+  const int* y;                // [R] Gumbel-max of l/T (leaf bonus)
+  const int* resid_y;          // [R] Gumbel-max of log max(0, p - q) (rejection bonus)
+  uint32_t seed_lo, seed_hi;
+  const uint32_t* req_round;
+  const uint64_t* req_session;
+  int* accepted_len;
+  int* accepted_token;
+  int* accepted_node;
+  int* bonus;
+};
+cudaError_t pq_lse_launch(const PqArgs& a, cudaStream_t st, int* launches);
+cudaError_t pq_walk_launch(const PqArgs& a, cudaStream_t st, int* launches);
 struct CommitArgs {
   int B, layers, KV, hd, R_cap, num_pages, max_pages_per_seq;
   int* status;

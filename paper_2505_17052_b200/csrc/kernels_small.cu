@@ -405,6 +405,120 @@ __global__ void k_set_len(int* __restrict__ cache_len, const __grid_constant__ S
   if (i < a.n) cache_len[a.handle[i]] = a.len[i];
 }
 
+// --------------------------------------------------------------- Gumbel noise block (a9)
+// One thread per (row, 4 consecutive vocab ids): one Philox call yields the 4 words.  The local
+// vocab offset is added to the global id; when vocab_off is not a multiple of 4 the quads straddle
+// counters, so each thread evaluates its 4 ids separately.
+__global__ void k_gumbel_fill(float* __restrict__ noise, int R, int vocab, int vocab_off, const int* __restrict__ row_req,
+                              const int* __restrict__ row_slot, const uint32_t* __restrict__ req_round,
+                              const uint64_t* __restrict__ req_session, uint32_t seed_lo, uint32_t seed_hi) {
+  pdl_begin();
+  const int nq = (vocab + 3) / 4;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)R * nq) return;
+  const int row = (int)(i / nq), q4 = (int)(i % nq);
+  const int req = row_req[row];
+  const uint64_t ses = req_session[req];
+  const uint32_t k0 = seed_lo ^ req_round[req];
+  const uint32_t slot = (uint32_t)row_slot[row];
+  float g[4];
+  if ((vocab_off & 3) == 0) {
+    const U4 w = philox4x32_10(U4{(uint32_t)((vocab_off >> 2) + q4), slot, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0,
+                               seed_hi);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float u = (float)((ws[k] >> 8) | 1u) * 5.9604644775390625e-08f;
+      g[k] = -logf(-logf(u));
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t v = (uint32_t)(vocab_off + 4 * q4 + k);
+      const U4 w = philox4x32_10(U4{v >> 2, slot, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0, seed_hi);
+      const float u = (float)((u4_word(w, (int)(v & 3)) >> 8) | 1u) * 5.9604644775390625e-08f;
+      g[k] = -logf(-logf(u));
+    }
+  }
+  float* dst = noise + (size_t)row * vocab + 4 * q4;
+  if (4 * q4 + 3 < vocab && (vocab & 3) == 0) {
+    *reinterpret_cast<float4*>(dst) = make_float4(g[0], g[1], g[2], g[3]);
+  } else {
+    for (int k = 0; k < 4 && 4 * q4 + k < vocab; ++k) dst[k] = g[k];
+  }
+}
+
+// ------------------------------------------------------- NEXT-F2 dense-q speculative sampling
+// One warp per row: lse = M + log sum_t s_t exp(m_t - M) over the PQ1 tile partials; q row of the
+// slot = the node drawn there (slot s < N: node s of a chain), -1 for the last slot.
+__global__ void k_pq_lse(const __grid_constant__ PqArgs a) {
+  pdl_begin();
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= a.R) return;
+  float m = -INFINITY;
+  for (int t = lane; t < a.ntiles; t += 32) m = fmaxf(m, a.part_m[(size_t)row * a.ntiles + t]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+  float sm = 0.f;
+  if (m > -INFINITY)
+    for (int t = lane; t < a.ntiles; t += 32)
+      sm += a.part_s[(size_t)row * a.ntiles + t] * __expf(a.part_m[(size_t)row * a.ntiles + t] - m);
+  for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffff, sm, o);
+  if (lane == 0) {
+    a.lse[row] = m + __logf(sm);
+    const int r = a.row_req[row], sl = a.row_slot[row];
+    const int n0 = a.node_offset[r], N = a.node_offset[r + 1] - n0;
+    a.row_qnode[row] = sl < N ? n0 + sl : -1;
+  }
+}
+
+// Leviathan et al. over a sampled chain (oracle/pq.py): node i (drawn from q_i) is accepted iff
+// u(slot i) < p_i(x) / q_i(x); the first rejection's bonus is the residual draw of that slot,
+// the bonus after full acceptance the Gumbel-max of p at the last slot.  u(slot): Philox word 0 of
+// counter (slot, 'ACPT', lo32(session), hi32(session)), key (lo32(seed) ^ round, hi32(seed)).
+__global__ void k_pq_walk(const __grid_constant__ PqArgs a) {
+  pdl_begin();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.B) return;
+  const int n0 = a.node_offset[r];
+  const int N = a.node_offset[r + 1] - n0;
+  const int row0 = n0 + r;
+  bool ok = a.status[r] == SPECEDGE_REQ_OK;
+  if (ok)
+    for (int i = 0; i < N; ++i)
+      if (a.parent[n0 + i] != i - 1) {   // dense-q mode verifies chains only
+        a.status[r] = SPECEDGE_REQ_E_UNSUPPORTED;
+        ok = false;
+        break;
+      }
+  if (!ok) {
+    a.accepted_len[r] = 0;
+    a.bonus[r] = -1;
+    return;
+  }
+  const uint64_t ses = a.req_session[r];
+  const uint32_t k0 = a.seed_lo ^ a.req_round[r];
+  int acc = 0, bonus = -1;
+  for (int i = 0; i < N; ++i) {
+    const int x = a.token[n0 + i];
+    const float qx = a.draft_q[(size_t)(n0 + i) * a.V + x];
+    const float ratio = qx > 0.f ? a.pchild[row0 + i] / qx : INFINITY;
+    const U4 w = philox4x32_10(U4{(uint32_t)i, 0x41435054u, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0, a.seed_hi);
+    const float u = (float)((w.x >> 8) | 1u) * 5.9604644775390625e-08f;   // exact, in (0, 1)
+    if (u < ratio) {
+      a.accepted_token[n0 + acc] = x;
+      a.accepted_node[n0 + acc] = i;
+      ++acc;
+    } else {
+      bonus = a.resid_y[row0 + i];
+      break;
+    }
+  }
+  if (acc == N) bonus = a.y[row0 + N];
+  a.accepted_len[r] = acc;
+  a.bonus[r] = bonus;
+}
+
 // ------------------------------------------------------------------------ K12 weight init
 // Element (lrow, col) of a logical weight = bf16(f32(i24 * scale)) with i24 from Philox counter
 // (idx >> 2, tensor_id, layer, 'WEIG'), idx = lrow * cols + col, word idx & 3 (oracle/model.py O1).
@@ -527,6 +641,25 @@ cudaError_t commit_launch(const CommitArgs& c, cudaStream_t st, int* launches) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CK_RET(launch_k(k_commit_finalize, dim3((c.B + 127) / 128), dim3(128), 0, st, c));
+  return cudaGetLastError();
+}
+cudaError_t gumbel_fill_launch(float* noise, int R, int vocab, int vocab_off, const int* row_req, const int* row_slot,
+                               const uint32_t* req_round, const uint64_t* req_session, uint32_t seed_lo,
+                               uint32_t seed_hi, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  const long long n = (long long)R * ((vocab + 3) / 4);
+  CK_RET(launch_k(k_gumbel_fill, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, noise, R, vocab, vocab_off,
+                  row_req, row_slot, req_round, req_session, seed_lo, seed_hi));
+  return cudaGetLastError();
+}
+cudaError_t pq_lse_launch(const PqArgs& a, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  CK_RET(launch_k(k_pq_lse, dim3((a.R + 3) / 4), dim3(128), 0, st, a));
+  return cudaGetLastError();
+}
+cudaError_t pq_walk_launch(const PqArgs& a, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  CK_RET(launch_k(k_pq_walk, dim3((a.B + 127) / 128), dim3(128), 0, st, a));
   return cudaGetLastError();
 }
 cudaError_t set_len_launch(int* cache_len, const SetLenArgs& a, cudaStream_t st) {

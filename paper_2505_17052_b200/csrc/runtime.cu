@@ -84,6 +84,8 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 struct WsLayout {
   size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
   size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, part_val, part_idx, y, score, tp_gather;
+  size_t part_m, part_s, lse, row_qnode, pchild, resid_y, resid_s;   // SAMPLE_PQ_DENSE
+  size_t noise;                                                       // [R][V] Gumbel noise (sampled modes)
   size_t stage_in, stage_out, total;
   int B, R, n_splits_max;
 };
@@ -127,6 +129,14 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.y = take(4 * R);
   w.score = take(4 * R);
   w.tp_gather = take(8 * (size_t)(kMaxTp + 1) * R);   // TP C3: [tp][R](score, id) + own staging
+  w.part_m = take(4 * (size_t)R * vt);
+  w.part_s = take(4 * (size_t)R * vt);
+  w.lse = take(4 * R);
+  w.row_qnode = take(4 * R);
+  w.pchild = take(4 * R);
+  w.resid_y = take(4 * R);
+  w.resid_s = take(4 * R);
+  w.noise = take(4 * (size_t)R * c.vocab);
   // staging for the host-buffer entry point: inputs then outputs
   w.stage_in = take((size_t)B * (4 + 4 + 4 + 8 + 4) + 4 * (B + 1) + (size_t)R * 12 + 64);
   w.stage_out = take((size_t)B * 12 + (size_t)R * 8 + (size_t)R * 8 + 64);
@@ -331,14 +341,81 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gl.row_slot = pa.row_slot;
     gl.req_round = di.round;
     gl.req_session = di.session_id;
-    { KTimer _t(K_LM, st); CK(gemm_launch(EPI_ARGMAX, m->tm_lm, Hf, gl, st, &launches)); }
-    KTimer _tr(K_LMRED, st);
-    CK(lm_reduce_launch(gl.part_val, gl.part_idx, R, (m->vl + 127) / 128, y, (float*)P(w.score),
-                        tp ? nullptr : dout.row_target, tp ? nullptr : dout.row_score, st, &launches));
-    if (tp)
-      CK(tp_argmax_gather(y, (float*)P(w.score), R, (float*)P(w.tp_gather), m->tp_size, m->nccl, dout.row_target,
-                          dout.row_score, st, &launches));
+    if (sample || in->mode == SPECEDGE_SAMPLE_PQ_DENSE) {
+      gl.noise = (float*)P(w.noise);
+      KTimer _t(K_LM, st);
+      CK(gumbel_fill_launch((float*)gl.noise, R, m->vl, m->v0, pa.row_req, pa.row_slot, di.round, di.session_id,
+                            gl.seed_lo, gl.seed_hi, st, &launches));
+    }
+    if (in->mode == SPECEDGE_SAMPLE_PQ_DENSE) {
+      // NEXT-F2: pass 1 = Gumbel-max of l/T (bonus after full acceptance) + tile (max, sum exp);
+      // pass 2 = p(child) and the Gumbel-max of log max(0, p - q) (bonus after a rejection)
+      const int vt = (m->vl + 127) / 128;
+      PqArgs pq{};
+      pq.B = B;
+      pq.R = R;
+      pq.ntiles = vt;
+      pq.V = c.vocab;
+      pq.status = dout.status;
+      pq.node_offset = di.node_offset;
+      pq.parent = di.parent;
+      pq.token = di.token;
+      pq.draft_q = in->draft_q;
+      pq.row_req = pa.row_req;
+      pq.row_slot = pa.row_slot;
+      pq.part_m = (float*)P(w.part_m);
+      pq.part_s = (float*)P(w.part_s);
+      pq.lse = (float*)P(w.lse);
+      pq.row_qnode = (int*)P(w.row_qnode);
+      pq.pchild = (float*)P(w.pchild);
+      pq.y = y;
+      pq.resid_y = (int*)P(w.resid_y);
+      pq.seed_lo = gl.seed_lo;
+      pq.seed_hi = gl.seed_hi;
+      pq.req_round = di.round;
+      pq.req_session = di.session_id;
+      pq.accepted_len = dout.accepted_len;
+      pq.accepted_token = dout.accepted_token;
+      pq.accepted_node = dout.accepted_node;
+      pq.bonus = dout.bonus;
+      gl.inv_t = (float)(1.0 / (double)in->temperature);
+      GemmArgs g1 = gl;
+      g1.sample = 1;
+      g1.part_m = (float*)pq.part_m;
+      g1.part_s = (float*)pq.part_s;
+      { KTimer _t(K_LM, st); CK(gemm_launch(EPI_PQ1, m->tm_lm, Hf, g1, st, &launches)); }
+      {
+        KTimer _tr(K_LMRED, st);
+        CK(lm_reduce_launch(gl.part_val, gl.part_idx, R, vt, y, (float*)P(w.score), dout.row_target, dout.row_score,
+                            st, &launches));
+        CK(pq_lse_launch(pq, st, &launches));
+      }
+      GemmArgs g2 = gl;
+      g2.sample = 1;
+      g2.lse = pq.lse;
+      g2.row_qnode = pq.row_qnode;
+      g2.node_token = di.token;
+      g2.draft_q = in->draft_q;
+      g2.vocab_q = c.vocab;
+      g2.pchild = (float*)pq.pchild;
+      { KTimer _t(K_LM, st); CK(gemm_launch(EPI_PQ2, m->tm_lm, Hf, g2, st, &launches)); }
+      {
+        KTimer _tr(K_LMRED, st);
+        CK(lm_reduce_launch(gl.part_val, gl.part_idx, R, vt, (int*)P(w.resid_y), (float*)P(w.resid_s), nullptr,
+                            nullptr, st, &launches));
+      }
+      { KTimer _t(K_WALK, st); CK(pq_walk_launch(pq, st, &launches)); }
+    } else {
+      { KTimer _t(K_LM, st); CK(gemm_launch(EPI_ARGMAX, m->tm_lm, Hf, gl, st, &launches)); }
+      KTimer _tr(K_LMRED, st);
+      CK(lm_reduce_launch(gl.part_val, gl.part_idx, R, (m->vl + 127) / 128, y, (float*)P(w.score),
+                          tp ? nullptr : dout.row_target, tp ? nullptr : dout.row_score, st, &launches));
+      if (tp)
+        CK(tp_argmax_gather(y, (float*)P(w.score), R, (float*)P(w.tp_gather), m->tp_size, m->nccl, dout.row_target,
+                            dout.row_score, st, &launches));
+    }
   }
+  const bool pq_walked = !prefill && in->mode == SPECEDGE_SAMPLE_PQ_DENSE;
   WalkArgs wa{};
   wa.B = B;
   wa.force_chain = prefill ? 1 : 0;
@@ -351,7 +428,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   wa.accepted_token = dout.accepted_token;
   wa.accepted_node = dout.accepted_node;
   wa.bonus = dout.bonus;
-  { KTimer _t(K_WALK, st); CK(walk_launch(wa, st, &launches)); }
+  if (!pq_walked) { KTimer _t(K_WALK, st); CK(walk_launch(wa, st, &launches)); }
   if (do_commit) {
     CommitArgs ca{};
     ca.B = B;
@@ -385,8 +462,13 @@ specedge_status check_in(const specedge_model* m, const specedge_kvpool* pool, c
   if (in->num_requests <= 0 || in->total_nodes < 0) return SPECEDGE_E_INVALID;
   if (in->max_nodes < 0 || in->max_nodes > SPECEDGE_MAX_NODES) return SPECEDGE_E_INVALID;
   if (in->max_context_len <= 0 || in->max_context_len > m->cfg.max_position) return SPECEDGE_E_INVALID;
-  if (in->mode != SPECEDGE_GREEDY && in->mode != SPECEDGE_SAMPLE_TREE) return SPECEDGE_E_INVALID;
+  if (in->mode != SPECEDGE_GREEDY && in->mode != SPECEDGE_SAMPLE_TREE && in->mode != SPECEDGE_SAMPLE_PQ_DENSE)
+    return SPECEDGE_E_INVALID;
   if (in->mode == SPECEDGE_SAMPLE_TREE && !(in->temperature >= 0.f)) return SPECEDGE_E_INVALID;
+  if (in->mode == SPECEDGE_SAMPLE_PQ_DENSE) {
+    if (!(in->temperature >= 1e-6f) || (in->total_nodes > 0 && !in->draft_q)) return SPECEDGE_E_INVALID;
+    if (m->tp_size != 1) return SPECEDGE_E_UNSUPPORTED;
+  }
   if (!in->kv || !in->context_len || !in->root_token || !in->session_id || !in->round || !in->node_offset)
     return SPECEDGE_E_INVALID;
   if (in->total_nodes > 0 && (!in->parent || !in->token)) return SPECEDGE_E_INVALID;
@@ -791,7 +873,8 @@ specedge_status specedge_verify_batch(specedge_model* m, specedge_kvpool* pool, 
                                     (const void*)in->session_id, (const void*)in->round, (const void*)out->status,
                                     (const void*)out->accepted_len, (const void*)out->accepted_token,
                                     (const void*)out->accepted_node, (const void*)out->bonus,
-                                    (const void*)out->row_target, (const void*)out->row_score, 1);
+                                    (const void*)out->row_target, (const void*)out->row_score,
+                                    (const void*)in->draft_q, 1);
   return run_graphed(m, key, st, [&](cudaStream_t gs) {
     return run_verify(m, pool, in, di, dout, (uint8_t*)workspace, ws_bytes, gs, false, in->auto_commit != 0);
   });
@@ -835,6 +918,7 @@ specedge_status specedge_verify_batch_host(specedge_model* m, specedge_kvpool* p
                                            specedge_verify_out* out, void* workspace, size_t ws_bytes, void* stream) {
   specedge_status s = check_in(m, pool, in);
   if (s != SPECEDGE_OK) return s;
+  if (in->mode == SPECEDGE_SAMPLE_PQ_DENSE) return SPECEDGE_E_UNSUPPORTED;   // dense q: device entry only
   if ((s = check_out(out, in->total_nodes)) != SPECEDGE_OK) return s;
   const auto& c = m->cfg;
   const int B = in->num_requests, T = in->total_nodes, R = T + B;
