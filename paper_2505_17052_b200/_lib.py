@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspecedge.so")
+LIB_PATH = os.environ.get("SPECEDGE_LIB") or os.path.join(HERE, "libspecedge.so")   # env: experiment builds
 
 OK = 0
 E_INVALID, E_CUDA, E_OOM, E_WORKSPACE, E_UNSUPPORTED, E_DEVICE, E_PROTOCOL = -1, -2, -3, -4, -5, -6, -7

@@ -34,15 +34,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """defines / out: experiment builds (e.g. -DSPECEDGE_EMU8=3 into a separate .so, selected at
+    load time with SPECEDGE_LIB=path); the default build writes libspecedge.so."""
+    lib = out or LIB
+    if not force and not defines and out is None and up_to_date():
         return LIB
     objs = []
     procs = []
+    tag = "" if not defines else "_" + "_".join(d.replace("=", "") for d in defines)
     for src in sources():
-        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + tag + ".o")
         objs.append(obj)
-        cmd = [NVCC] + [f for f in FLAGS if f != "-shared"] + ["-dc" if False else "-c", src, "-o", obj]
+        cmd = [NVCC] + [f for f in FLAGS if f != "-shared"] + [f"-D{d}" for d in defines] + \
+            ["-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     failed = False
     for src, p in procs:
@@ -53,14 +58,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
             failed = True
     if failed:
         raise RuntimeError("nvcc failed")
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp"] + objs + ["-ldl"]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib + ".tmp"] + objs + ["-ldl"]
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    args = sys.argv[1:]
+    defs = [a[len("--define="):] for a in args if a.startswith("--define=")]
+    outp = next((a[len("--out="):] for a in args if a.startswith("--out=")), None)
+    print(build(force="--force" in args, verbose=not defs, defines=defs, out=outp))

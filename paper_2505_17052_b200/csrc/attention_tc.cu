@@ -44,6 +44,10 @@ namespace {
 constexpr int kWarps = 11;      // producer, MMA (unit 0), 2 units x 4 softmax/epilogue warps, MMA (unit 1)
 constexpr int kThreads = kWarps * 32;
 constexpr int kStages = 5;      // K/V ring depth (64-key sub-tiles)
+#ifndef SPECEDGE_EMU8
+#define SPECEDGE_EMU8 0
+#endif
+constexpr int kEmu8 = SPECEDGE_EMU8;   // exponentials per 8 on exp2_fma (rest ex2.approx); measured no gain at 2-4 (profiles/README.md)
 constexpr int kPrefetchDefault = 0;   // L2 prefetch distance (sub-tiles) ahead of the ring; env SPECEDGE_ATTN_PREFETCH
 
 // UMMA smem descriptor for an MN-major operand, 128B swizzle: SBO = 1024 B between 8-row
@@ -118,6 +122,21 @@ __device__ __forceinline__ float ex2f(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA/ALU pipes (for x <= 8): round-to-nearest split x = n + f via the 1.5*2^23 trick,
+// degree-3 fit of 2^f on [-1/2, 1/2] (max relative error 1.1e-4, below the fp16 rounding of P),
+// exponent add for 2^n.  Used for a fraction of the softmax exponentials so that the MUFU pipe
+// (16 ex2/clk/SM on B200) is not the bound (the FA4 idea).
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -127.0f);
+  const float t = x + 12582912.0f;
+  const float nf = t - 12582912.0f;
+  const float f = x - nf;
+  float p = fmaf(f, 0.054592829f, 0.24221838f);
+  p = fmaf(p, f, 0.69336867f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 __device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* m, int c0, int c1) {
@@ -504,8 +523,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (full) {
 #pragma unroll
               for (int e = 0; e < W; e += 2) {
-                const float p0 = ex2f(fmaf(__uint_as_float(sv[e]), sl2, -mb));
-                const float p1 = ex2f(fmaf(__uint_as_float(sv[e + 1]), sl2, -mb));
+                // kEmu8 of every 8 exponentials on the FMA pipe, the rest on MUFU
+                const float x0 = fmaf(__uint_as_float(sv[e]), sl2, -mb);
+                const float x1 = fmaf(__uint_as_float(sv[e + 1]), sl2, -mb);
+                const float p0 = (e & 7) < kEmu8 ? exp2_fma(x0) : ex2f(x0);
+                const float p1 = ((e + 1) & 7) < kEmu8 ? exp2_fma(x1) : ex2f(x1);
                 ls0 += p0;
                 ls1 += p1;
                 pk[e >> 1] = pack2(p0, p1);
