@@ -130,24 +130,29 @@ def contexts(wl, rank):
     return [int(x) for x in rng.integers(wl.ctx_lo, wl.ctx_hi + 1, wl.n_requests)]
 
 
-def setup_gpu(wl, rank, device, tp=None):
+def setup_gpu(wl, rank, device, tp=None, model=None, pool=None, mb=0):
     """tp = (tp_rank, tp_size, nccl_id): every rank builds the SAME requests (data rank 0) on its
-    tensor-parallel shard of one model; otherwise rank r builds its own replica's requests."""
+    tensor-parallel shard of one model; otherwise rank r builds its own replica's requests.
+    model/pool/mb: build microbatch mb's requests on an existing model and KV pool (cfg3's A/B)."""
     import torch
     from paper_2505_17052_b200 import api
     from synth.plant import plant, draw_accept_lengths
     shape = wl.shape
     if tp is not None:
         rank = 0   # one request set for the whole box
-    ctx = contexts(wl, rank)
-    max_ctx = max(ctx) + wl.n_nodes + 64
-    if tp is None:
-        model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64)
-    else:
-        model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64, tp_rank=tp[0],
-                          tp_size=tp[1], nccl_id=tp[2])
-    pages = sum((c + wl.n_nodes + 2 + 63) // 64 for c in ctx) + 8
-    pool = api.KVPool(model, pages, wl.n_requests + 2)
+    ctx = contexts(wl, rank + 64 * mb)
+    max_ctx = max(max(contexts(wl, rank + 64 * m)) for m in range(wl.microbatches)) + wl.n_nodes + 64
+    if model is None:
+        if tp is None:
+            model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64)
+        else:
+            model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64, tp_rank=tp[0],
+                              tp_size=tp[1], nccl_id=tp[2])
+    if pool is None:
+        pages = sum((c + wl.n_nodes + 2 + 63) // 64 for m in range(wl.microbatches)
+                    for c in contexts(wl, rank + 64 * m)) + 8
+        pool = api.KVPool(model, pages, wl.microbatches * wl.n_requests + 2)
+    rank = rank + 64 * mb   # request-set seed of this microbatch
     handles = []
     for r, c in enumerate(ctx):
         h = pool.alloc(c + wl.n_nodes + 2)
@@ -227,22 +232,42 @@ def run_gpu(args, world, rank, local):
         dist.broadcast_object_list(obj, src=0)
         tp = (rank, world, obj[0])
     st = setup_gpu(wl, rank, local, tp)
+    # cfg3: further resident microbatches on the same model and KV pool (A/B)
+    mbs = [st] + [setup_gpu(wl, rank, local, tp, model=st["model"], pool=st["pool"], mb=m)
+                  for m in range(1, wl.microbatches)]
     api, model, pool, ws, batch = st["api"], st["model"], st["pool"], st["ws"], st["batch"]
     lib = model.lib
     handles, L0 = st["handles"], [c - 1 for c in st["ctx"]]
     stream = torch.cuda.current_stream()
+    for m in mbs:
+        m["outs"] = api.Outputs.alloc(m["batch"], f"cuda:{local}")
+        m["L0"] = [c - 1 for c in m["ctx"]]
+        m["stream"] = stream if len(mbs) == 1 else torch.cuda.Stream()
+
+    def verify_mb(m):
+        api.verify(model, pool, m["batch"], m["ws"], mode=m["mode"], temperature=wl.temperature,
+                   seed=wl.weight_seed, auto_commit=True, out=m["outs"])
+        pool.set_len(m["handles"], m["L0"])
 
     def step():
-        out = api.verify(model, pool, batch, ws, mode=st["mode"], temperature=wl.temperature,
-                         seed=wl.weight_seed, auto_commit=True, out=outs)
-        pool.set_len(handles, L0)
-        return out
+        if len(mbs) == 1:
+            verify_mb(st)
+            return
+        # A/B microbatches on their own streams: each is a complete verify step; issued together
+        # they fill each other's idle SMs (wave tails, attention's 128 of 148 SMs)
+        start = torch.cuda.current_stream().record_event()
+        for m in mbs:
+            m["stream"].wait_event(start)
+            with torch.cuda.stream(m["stream"]):
+                verify_mb(m)
+        for m in mbs:
+            torch.cuda.current_stream().wait_stream(m["stream"])
 
-    outs = api.Outputs.alloc(batch, f"cuda:{local}")
+    outs = st["outs"]
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    tokens_per_step = int(sum(a + 1 for a in st["accepted"]))
+    tokens_per_step = int(sum(a + 1 for m in mbs for a in m["accepted"]))
     import ctypes as C
     nk = len(api.L.KERNEL_KINDS)
     kinds = api.L.KERNEL_KINDS
@@ -262,7 +287,7 @@ def run_gpu(args, world, rank, local):
     # in events (its launch durations feed the roofline), so instrumentation stays ~1-2% of a step
     lib.specedge_set_kernel_timing(1 << dom)
     run = step
-    if not args.no_graph:
+    if not args.no_graph and len(mbs) == 1:
         # one verify step (+ the rewind kernel) captured as a CUDA graph and replayed: every launch
         # of the step is recorded once, so per-launch host overhead leaves the timed region
         graph = torch.cuda.CUDAGraph()
@@ -290,34 +315,40 @@ def run_gpu(args, world, rank, local):
     kms = (C.c_float * nk)()
     kcnt = (C.c_int32 * nk)()
     lib.specedge_kernel_times(kms, kcnt, 1)
-    acc = outs.accepted_len.cpu().numpy()
-    assert int((acc + 1).sum()) == tokens_per_step, "accepted counts changed between steps"
+    acc_all = sum(int((m["outs"].accepted_len.cpu().numpy() + 1).sum()) for m in mbs)
+    assert acc_all == tokens_per_step, "accepted counts changed between steps"
     total_ms = reduce_max(total_ms, dist, f"cuda:{local}")
     replicas = 1 if tp else world   # TP: one model (one request set) spans the box
     value = box_throughput(replicas, tokens_per_step, args.steps, total_ms)
 
-    # ---- end-to-end through the host-buffer C-ABI entry point (copies inside the timed region)
-    hb = api.HostBatch.of(batch)
-    ho = api.host_outputs(hb)
+    # ---- end-to-end through the host-buffer C-ABI entry point (copies inside the timed region);
+    # microbatches are verified one after another from the host (the synchronous public call)
+    for m in mbs:
+        m["hb"] = api.HostBatch.of(m["batch"])
+        m["ho"] = api.host_outputs(m["hb"])
+
+    def e2e_step():
+        for m in mbs:
+            api.verify_host(model, pool, m["hb"], m["ws"], m["ho"], mode=m["mode"], temperature=wl.temperature,
+                            seed=wl.weight_seed)
+            pool.set_len(m["handles"], m["L0"])
     for _ in range(2):
-        api.verify_host(model, pool, hb, ws, ho, mode=st["mode"], temperature=wl.temperature, seed=wl.weight_seed)
-        pool.set_len(handles, L0)
+        e2e_step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        api.verify_host(model, pool, hb, ws, ho, mode=st["mode"], temperature=wl.temperature, seed=wl.weight_seed)
-        pool.set_len(handles, L0)
+        e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     e2e_ms = reduce_max(e2e_ms, dist, f"cuda:{local}")
-    e2e_tokens = int((ho["accepted_len"].numpy() + 1).sum())
-    B, T, R = hb.num_requests, hb.total_nodes, hb.total_nodes + hb.num_requests
-    h2d = hb.nbytes()
-    d2h = 4 * (3 * B + 2 * T + 2 * R)
+    e2e_tokens = sum(int((m["ho"]["accepted_len"].numpy() + 1).sum()) for m in mbs)
+    h2d = sum(m["hb"].nbytes() for m in mbs)
+    d2h = sum(4 * (3 * m["hb"].num_requests + 2 * m["hb"].total_nodes + 2 * (m["hb"].total_nodes +
+                                                                          m["hb"].num_requests)) for m in mbs)
 
     # ---- roofline of the dominant kernel (largest share of the step), timed in the timed region
     share = {kinds[i]: float(kms[i]) for i in range(nk)}
@@ -366,16 +397,18 @@ def run_gpu(args, world, rank, local):
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{wl.name}: {wl.shape.name}-shaped random-init, {wl.n_requests} requests x "
+        "config": {"workload": f"{wl.name}: {wl.shape.name}-shaped random-init, "
+                               f"{(str(len(mbs)) + ' microbatches x ') if len(mbs) > 1 else ''}{wl.n_requests} requests x "
                                f"{wl.n_nodes}-node trees (D={wl.depth}, b={wl.branching}), ctx U[{wl.ctx_lo},"
                                f"{wl.ctx_hi}], {wl.mode}",
-                   ("requests_per_box" if tp else "requests_per_gpu"): wl.n_requests, "rows_per_step": st["R"],
+                   ("requests_per_box" if tp else "requests_per_gpu"): wl.n_requests * len(mbs),
+                   "microbatches": len(mbs), "rows_per_step": sum(m["R"] for m in mbs),
                    ("tokens_per_step_per_box" if tp else "tokens_per_step_per_gpu"): tokens_per_step,
-                   "planted_tokens_per_verify": round(tokens_per_step / wl.n_requests, 3),
+                   "planted_tokens_per_verify": round(tokens_per_step / (wl.n_requests * len(mbs)), 3),
                    "l2": f"inputs larger than L2 ({weight_gb:.1f} GB of weights per GPU streamed every step)",
                    "parallelism": f"tp{world}" if tp else f"replicas x{world}"},
         "p50_ms": round(statistics.median(step_ms), 4), "p90_ms": round(float(np.quantile(step_ms, 0.9)), 4),
-        "rows_per_s": round(replicas * st["R"] * args.steps / (total_ms / 1e3), 1),
+        "rows_per_s": round(replicas * sum(m["R"] for m in mbs) * args.steps / (total_ms / 1e3), 1),
         "roofline": roof,
         "kernels": kernel_table,
         "kernels_note": "per-kernel ms from an event-instrumented calibration pass of the same steps "

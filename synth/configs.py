@@ -70,11 +70,13 @@ class Workload:
     temperature: float
     real_prefill: bool    # parity configs prefill for real; perf configs random-fill KV
     tp: bool = False      # one tensor-parallel model over all ranks (cfg4) instead of per-GPU replicas
+    microbatches: int = 1  # resident request sets per GPU verified alternately (cfg3: A/B)
 
 
 CFG1 = Workload("cfg1", TINY, 1, 1, 8, 4, 3, 32, 32, 101, 3.98, 1.55, "greedy", 0.0, True)
 CFG2 = Workload("cfg2", LLAMA3_8B, 2, 16, 32, 7, 4, 768, 1280, 102, 3.98, 1.55, "greedy", 0.0, False)
-CFG3 = Workload("cfg3", QWEN3_14B, 3, 32, 32, 7, 4, 1536, 2560, 103, 4.44, 2.1, "greedy", 0.0, False)
+CFG3 = Workload("cfg3", QWEN3_14B, 3, 32, 32, 7, 4, 1536, 2560, 103, 4.44, 2.1, "greedy", 0.0, False,
+                microbatches=2)
 CFG5 = Workload("cfg5", QWEN3_14B, 5, 16, 16, 5, 4, 12288, 20480, 105, 3.98, 1.55, "sample", 1.0, False)
 # cfg4: Llama-3-70B-shaped, tensor parallel over the box's GPUs (TP = 8 in BASELINE.json; any
 # divisor of 8 heads runs), 32 requests for the whole box
