@@ -287,7 +287,7 @@ def run_gpu(args, world, rank, local):
     # in events (its launch durations feed the roofline), so instrumentation stays ~1-2% of a step
     lib.specedge_set_kernel_timing(1 << dom)
     run = step
-    if not args.no_graph and len(mbs) == 1:
+    if not args.no_graph and len(mbs) == 1 and not tp:
         # one verify step (+ the rewind kernel) captured as a CUDA graph and replayed: every launch
         # of the step is recorded once, so per-launch host overhead leaves the timed region
         graph = torch.cuda.CUDAGraph()

@@ -274,6 +274,8 @@ int tp_unique_id(uint8_t* out128);
 int tp_comm_init(void** comm, const uint8_t* id128, int rank, int size);
 void tp_comm_destroy(void* comm);
 cudaError_t tp_allreduce_f32(float* buf, size_t n, void* comm, cudaStream_t st);
+cudaError_t tp_reduce_scatter_f32(float* buf, size_t per_rank, int rank, void* comm, cudaStream_t st);
+cudaError_t tp_all_gather_bf16(bf16* buf, size_t per_rank, int rank, void* comm, cudaStream_t st);
 cudaError_t tp_argmax_gather(int* y, float* score, int R, float* gather, int tp, void* comm, int* row_target,
                              float* row_score, cudaStream_t st, int* launches);
 cudaError_t kv_fill_launch(f16* pool, const int* block_row, int layers, int num_pages, int KV,

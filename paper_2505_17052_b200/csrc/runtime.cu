@@ -111,11 +111,14 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.row_req = take(4 * R);
   w.row_slot = take(4 * R);
   w.row_anc = take(8 * R);
-  w.X = take(4 * (size_t)R * c.d);   // fp32 residual stream
-  // fp32 K-split partials of the QKV / O / down GEMMs: [kGemmSplits][R][max(qkv, d)]
-  w.Y = take(4 * (size_t)kGemmSplits * R * std::max((size_t)(H + 2 * KV) * hd, (size_t)c.d));
-  w.Hn = take(2 * (size_t)R * c.d);
-  w.Hf = take(2 * 2 * (size_t)R * c.d);   // final-norm output as hi/lo bf16 row pairs
+  // row buffers carry kMaxTp spare rows: under tensor parallelism the residual stream is
+  // row-sharded in equal chunks of ceil(R / tp) rows (reduce-scatter / all-gather)
+  const size_t Rp = (size_t)R + kMaxTp;
+  w.X = take(4 * Rp * c.d);   // fp32 residual stream
+  // fp32 K-split partials of the QKV / O / down GEMMs: [kGemmSplits][Rp][max(qkv, d)]
+  w.Y = take(4 * (size_t)kGemmSplits * Rp * std::max((size_t)(H + 2 * KV) * hd, (size_t)c.d));
+  w.Hn = take(2 * Rp * c.d);
+  w.Hf = take(2 * 2 * Rp * c.d);   // final-norm output as hi/lo bf16 row pairs
   w.Q = take(2 * (size_t)R * H * hd);
   w.O = take(2 * (size_t)R * H * hd);
   w.M = take(2 * (size_t)R * c.ffn);
@@ -220,7 +223,13 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   bf16* O = (bf16*)P(w.O);
   bf16* Mb = (bf16*)P(w.M);
   f16* tree_kv = (f16*)P(w.tree_kv);
-  { KTimer _t(K_EMBED, st); CK(embed_launch(m->embed, pa.row_tok, X, R, c.d, st, &launches)); }
+  // tensor parallel: rank k owns residual rows [k*Rl, k*Rl + nloc) (sequence-parallel residual
+  // stream: RMSNorm runs on 1/tp of the rows, C1/C2 become reduce-scatter + bf16 all-gather)
+  const bool tp = m->tp_size > 1;
+  const int Rl = tp ? (R + m->tp_size - 1) / m->tp_size : R;
+  const int r0 = tp ? m->tp_rank * Rl : 0;
+  const int nloc = std::max(0, std::min(Rl, R - r0));
+  { KTimer _t(K_EMBED, st); if (nloc) CK(embed_launch(m->embed, pa.row_tok + r0, X + (size_t)r0 * c.d, nloc, c.d, st, &launches)); }
 
   const int hd = c.head_dim, H = c.n_heads, KV = c.n_kv, G = H / KV;
   const int max_pages = (in->max_context_len + 63) / 64;
@@ -253,10 +262,9 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
 
   float* Y = (float*)P(w.Y);
-  const size_t y_stride = (size_t)R * std::max((H + 2 * KV) * hd, c.d);
+  const size_t y_stride = ((size_t)R + kMaxTp) * std::max((H + 2 * KV) * hd, c.d);
   int pendingY = 0;   // K-split partials of the last down-proj not yet added to X
-  const bool tp = m->tp_size > 1;
-  // row_parallel: O / down under TP -> one unsplit fp32 partial, summed over ranks in place (C1/C2)
+  // row_parallel: O / down under TP -> one unsplit fp32 partial, reduce-scattered over ranks (C1/C2)
   auto f32_gemm = [&](int kind, const CUtensorMap& tm, const void* Xin, int Mrows, int K, bool row_parallel) -> int {
     GemmArgs g{};
     g.M = Mrows;
@@ -272,14 +280,29 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     }
     const int ns = gemm_splits_last();
     if (tp && row_parallel) {
-      if (tp_allreduce_f32(Y, (size_t)R * Mrows, m->nccl, st) != cudaSuccess) return -1;
+      if (tp_reduce_scatter_f32(Y, (size_t)Rl * Mrows, m->tp_rank, m->nccl, st) != cudaSuccess) return -1;
       ++launches;
     }
     return ns;
   };
+  // residual add + RMSNorm of this rank's rows (all rows when tp_size == 1), then under TP the
+  // bf16 all-gather of the normalised rows for the next column-parallel GEMM
+  auto norm_rows = [&](int nY, const bf16* gain, bf16* out, int split) -> specedge_status {
+    {
+      KTimer _t(K_RMSNORM, st);
+      if (nloc)
+        CK(rmsnorm_launch(X + (size_t)r0 * c.d, Y + (size_t)r0 * c.d, nY, y_stride, gain,
+                          out + (size_t)(split ? 2 : 1) * r0 * c.d, nloc, c.d, c.eps, st, &launches, split));
+    }
+    if (tp) {
+      CK(tp_all_gather_bf16(out, (size_t)(split ? 2 : 1) * Rl * c.d, m->tp_rank, m->nccl, st));
+      ++launches;
+    }
+    return SPECEDGE_OK;
+  };
   for (int l = 0; l < c.n_layers; ++l) {
     const auto& Lw = m->layers[l];
-    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Y, pendingY, y_stride, Lw.g_attn, Hn, R, c.d, c.eps, st, &launches)); }
+    { const specedge_status ns = norm_rows(pendingY, Lw.g_attn, Hn, 0); if (ns != SPECEDGE_OK) return ns; }
     const int sq = f32_gemm(K_QKV, Lw.tm_qkv, Hn, (H + 2 * KV) * hd, c.d, false);
     if (sq < 0) return SPECEDGE_E_CUDA;
     RopeArgs ra{};
@@ -308,7 +331,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     }
     const int so = f32_gemm(K_O, Lw.tm_o, O, c.d, H * hd, true);
     if (so < 0) return SPECEDGE_E_CUDA;
-    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Y, so, y_stride, Lw.g_mlp, Hn, R, c.d, c.eps, st, &launches)); }
+    { const specedge_status ns = norm_rows(so, Lw.g_mlp, Hn, 0); if (ns != SPECEDGE_OK) return ns; }
     GemmArgs gu{};
     gu.M = 2 * c.ffn;
     gu.R = R;
@@ -322,7 +345,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   int* y = (int*)P(w.y);
   if (!prefill) {
     bf16* Hf = (bf16*)P(w.Hf);
-    { KTimer _t(K_RMSNORM, st); CK(rmsnorm_launch(X, Y, pendingY, y_stride, m->g_final, Hf, R, c.d, c.eps, st, &launches, 1)); }
+    { const specedge_status ns = norm_rows(pendingY, m->g_final, Hf, 1); if (ns != SPECEDGE_OK) return ns; }
     GemmArgs gl{};
     gl.M = m->vl;   // this rank's vocab shard (all of V when tp_size == 1)
     gl.R = 2 * R;
@@ -489,9 +512,12 @@ specedge_status check_out(const specedge_verify_out* out, int total_nodes) {
 // replays it with one cudaGraphLaunch on the caller's stream.
 // Disabled by SPECEDGE_NO_GRAPH=1, while kernel timing is on, and when the caller's stream is
 // itself being captured (the plain launches then become part of the caller's graph).
-bool graphs_enabled(cudaStream_t st) {
+bool graphs_enabled(const specedge_model* m, cudaStream_t st) {
   static const bool off = getenv("SPECEDGE_NO_GRAPH") && getenv("SPECEDGE_NO_GRAPH")[0] == '1';
-  if (off || g_timing.on) return false;
+  // tensor parallel: NCCL collectives issued earlier on another stream (prefill) make the capture
+  // of the next collective wait on an event from outside the capture on one rank only -> the
+  // ranks' collective sequences diverge; TP steps (~100 ms) gain nothing from graph replay anyway
+  if (off || g_timing.on || m->tp_size > 1) return false;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
@@ -865,7 +891,7 @@ specedge_status specedge_verify_batch(specedge_model* m, specedge_kvpool* pool, 
   DevOut dout{out->status, out->accepted_len, out->accepted_token, out->accepted_node, out->bonus, out->row_target,
               out->row_score};
   const cudaStream_t st = (cudaStream_t)stream;
-  if (!graphs_enabled(st))
+  if (!graphs_enabled(m, st))
     return run_verify(m, pool, in, di, dout, (uint8_t*)workspace, ws_bytes, st, false, in->auto_commit != 0);
   const std::string key = graph_key(in, (const void*)pool, workspace, ws_bytes, (const void*)in->kv,
                                     (const void*)in->context_len, (const void*)in->root_token,
@@ -967,7 +993,7 @@ specedge_status specedge_verify_batch_host(specedge_model* m, specedge_kvpool* p
     CK(cudaMemcpyAsync(ho, dou, out_bytes, cudaMemcpyDeviceToHost, gs));
     return SPECEDGE_OK;
   };
-  if (graphs_enabled(st))
+  if (graphs_enabled(m, st))
     s = run_graphed(m, graph_key(in, (const void*)pool, workspace, ws_bytes, (const void*)hb, 2), st, step);
   else
     s = step(st);

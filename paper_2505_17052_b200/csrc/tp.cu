@@ -26,6 +26,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -40,7 +42,9 @@ NcclApi& nccl() {
   api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
   api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
   api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
-  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.AllGather;
+  api.ReduceScatter = reinterpret_cast<decltype(api.ReduceScatter)>(dlsym(h, "ncclReduceScatter"));
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.AllGather &&
+           api.ReduceScatter;
   return api;
 }
 
@@ -104,6 +108,21 @@ void tp_comm_destroy(void* comm) {
 // C1 / C2: in-place fp32 sum of the [R, d] residual updates of all ranks
 cudaError_t tp_allreduce_f32(float* buf, size_t n, void* comm, cudaStream_t st) {
   if (nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, reinterpret_cast<ncclComm_t>(comm), st) != ncclSuccess)
+    return cudaErrorUnknown;
+  return cudaSuccess;
+}
+
+// C1 / C2 as reduce-scatter + all-gather (row-sharded residual stream): in place, rank k's chunk
+// of `per_rank` elements at buf + k * per_rank
+cudaError_t tp_reduce_scatter_f32(float* buf, size_t per_rank, int rank, void* comm, cudaStream_t st) {
+  if (nccl().ReduceScatter(buf, buf + (size_t)rank * per_rank, per_rank, ncclFloat32, ncclSum,
+                           reinterpret_cast<ncclComm_t>(comm), st) != ncclSuccess)
+    return cudaErrorUnknown;
+  return cudaSuccess;
+}
+cudaError_t tp_all_gather_bf16(bf16* buf, size_t per_rank, int rank, void* comm, cudaStream_t st) {
+  if (nccl().AllGather(buf + (size_t)rank * per_rank, buf, per_rank, ncclBfloat16, reinterpret_cast<ncclComm_t>(comm),
+                       st) != ncclSuccess)
     return cudaErrorUnknown;
   return cudaSuccess;
 }
