@@ -328,6 +328,24 @@ specedge_status specedge_scheduler_observe(specedge_scheduler* sched, int32_t ki
 specedge_status specedge_scheduler_state(const specedge_scheduler* sched, int32_t* depth,
                                          int32_t* queued, int32_t* outstanding, double* estimates3);
 
+/* ---- NEXT-F3: draft-tree builder (edge side) ----
+ * PAPER.md App. A: draft passes propose parallel candidates "pruned based on cumulative log
+ * probabilities so that the total number of tokens remains within the tree budget".  Runs `depth`
+ * passes of this model (the draft model) over the session `handle` (context_len = cached + 1,
+ * root_token = its last committed token): every frontier node proposes its top-`branching` tokens
+ * (ties: smaller id, log-softmax at T = 1), proposals are pooled with the kept nodes and the first
+ * `budget` in (-cum logprob, depth, token, insertion) order are kept (ancestor-closed), in
+ * insertion order (DESIGN.md R-draft).  Each pass is the verify path up to the
+ * final norm on a one-request tree, the LM head with an fp32 store epilogue and a top-b kernel;
+ * pruning is host code.  Outputs (host arrays of >= budget entries): parent (-1 = root child, else
+ * a smaller index), token, logprob; *n_out = node count.  Synchronous.  budget <= 64, branching <= 8,
+ * tp_size == 1; the workspace must fit (1 request, budget + 1 rows).  Does not commit anything. */
+specedge_status specedge_draft_tree(specedge_model* model, specedge_kvpool* pool, int32_t handle,
+                                    int32_t context_len, int32_t root_token, uint64_t session_id,
+                                    int32_t budget, int32_t depth, int32_t branching, void* workspace,
+                                    size_t ws_bytes, void* stream, int32_t* parent_out,
+                                    int32_t* token_out, float* logprob_out, int32_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,7 @@ EXPORTS = [
     "specedge_model_tp_info", "specedge_calibrate_draft_depth", "specedge_scheduler_create",
     "specedge_scheduler_destroy", "specedge_scheduler_admit", "specedge_scheduler_plan",
     "specedge_scheduler_complete", "specedge_scheduler_observe", "specedge_scheduler_state",
+    "specedge_draft_tree",
 ]
 KERNEL_KINDS = ["prep", "embed", "rmsnorm", "gemm_qkv", "attention", "attn_combine", "gemm_o", "gemm_gateup",
                 "gemm_down", "gemm_lmhead", "lm_reduce", "walk", "commit", "qkv_rope"]
@@ -113,6 +114,7 @@ def load(path: str = LIB_PATH):
         "specedge_scheduler_complete": [P, P, I32, C.c_double],
         "specedge_scheduler_observe": [P, I32, C.c_double],
         "specedge_scheduler_state": [P, P, P, P, P],
+        "specedge_draft_tree": [P, P, I32, I32, I32, U64, I32, I32, I32, P, SZ, P, P, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

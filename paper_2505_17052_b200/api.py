@@ -369,3 +369,20 @@ class Scheduler:
 
 def calibrate_draft_depth(verify_ms: float, draft_pass_ms: float, rtt_ms: float) -> int:
     return int(L.load().specedge_calibrate_draft_depth(verify_ms, draft_pass_ms, rtt_ms))
+
+
+def draft_tree(model: Model, pool: KVPool, handle: int, context_len: int, root_token: int, session_id: int,
+               budget: int, depth: int, branching: int, ws: torch.Tensor, stream=None):
+    """NEXT-F3: build a draft tree with this model as the draft model (include/specedge.h,
+    specedge_draft_tree).  Returns (parent, token, logprob) numpy arrays."""
+    parent = np.zeros(budget, np.int32)
+    token = np.zeros(budget, np.int32)
+    logprob = np.zeros(budget, np.float32)
+    n = C.c_int32()
+    L.check(model.lib.specedge_draft_tree(model.h, pool.h, handle, context_len, root_token,
+                                          C.c_uint64(session_id & 0xFFFFFFFFFFFFFFFF).value, budget, depth,
+                                          branching, _ptr(ws), ws.numel(), _stream(stream),
+                                          parent.ctypes.data_as(C.c_void_p), token.ctypes.data_as(C.c_void_p),
+                                          logprob.ctypes.data_as(C.c_void_p), C.byref(n)), "draft_tree")
+    k = n.value
+    return parent[:k], token[:k], logprob[:k]

@@ -225,6 +225,17 @@ struct PqArgs {
   int* bonus;
 };
 cudaError_t pq_lse_launch(const PqArgs& a, cudaStream_t st, int* launches);
+// NEXT-F3 draft-tree builder (draft.cu)
+struct DraftNode {
+  int parent, token, depth;
+  float logprob;
+  double cum;
+};
+cudaError_t topb_launch(const float* logits, int V, const int* rows, int nrows, int b, int* out_tok, float* out_lp,
+                        cudaStream_t st);
+specedge_status draft_prune(std::vector<DraftNode>& nodes, const std::vector<int>& frontier,
+                            const std::vector<int>& tok, const std::vector<float>& lp, int branching, int budget,
+                            std::vector<int>& next_frontier);
 cudaError_t pq_walk_launch(const PqArgs& a, cudaStream_t st, int* launches);
 struct CommitArgs {
   int B, layers, KV, hd, R_cap, num_pages, max_pages_per_seq;

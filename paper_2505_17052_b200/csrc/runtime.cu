@@ -178,9 +178,11 @@ struct DevOut {
   float* row_score;
 };
 
+// hidden_only (NEXT-F3 draft passes): stop after the final RMSNorm (hi/lo rows in ws Hf); no LM
+// head, walk or commit
 specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const specedge_verify_in* in, DevIn di,
                            DevOut dout, uint8_t* ws_base, size_t ws_bytes, cudaStream_t st, bool prefill,
-                           bool do_commit) {
+                           bool do_commit, bool hidden_only = false) {
   const specedge_model_config& c = m->cfg;
   const int B = in->num_requests, T = in->total_nodes, R = T + B;
   const WsLayout w = ws_layout(c, B, R);
@@ -346,6 +348,10 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   if (!prefill) {
     bf16* Hf = (bf16*)P(w.Hf);
     { const specedge_status ns = norm_rows(pendingY, m->g_final, Hf, 1); if (ns != SPECEDGE_OK) return ns; }
+    if (hidden_only) {
+      g_last_launches = launches;
+      return SPECEDGE_OK;
+    }
     GemmArgs gl{};
     gl.M = m->vl;   // this rank's vocab shard (all of V when tp_size == 1)
     gl.R = 2 * R;
@@ -1137,6 +1143,96 @@ specedge_status specedge_debug_gemm(const uint16_t* W, const uint16_t* X, float*
   g.out_f32 = out;
   g.ldo = M;
   CK(gemm_launch(EPI_F32, tmW, X, g, (cudaStream_t)stream, nullptr));
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_draft_tree(specedge_model* m, specedge_kvpool* pool, int32_t handle, int32_t context_len,
+                                    int32_t root_token, uint64_t session_id, int32_t budget, int32_t depth,
+                                    int32_t branching, void* workspace, size_t ws_bytes, void* stream,
+                                    int32_t* parent_out, int32_t* token_out, float* logprob_out, int32_t* n_out) {
+  if (!m || !pool || pool->model != m || !workspace || !parent_out || !token_out || !logprob_out || !n_out)
+    return SPECEDGE_E_INVALID;
+  if (budget < 1 || budget > SPECEDGE_MAX_NODES || depth < 1 || branching < 1 || branching > 8 ||
+      handle < 0 || handle >= pool->max_handles || context_len < 1 || root_token < 0 || root_token >= m->cfg.vocab)
+    return SPECEDGE_E_INVALID;
+  if (m->tp_size != 1) return SPECEDGE_E_UNSUPPORTED;
+  const auto& c = m->cfg;
+  const int V = c.vocab;
+  if (ws_bytes < ws_layout(c, 1, budget + 1).total) return SPECEDGE_E_WORKSPACE;
+  CK(cudaSetDevice(m->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* ws = (uint8_t*)workspace;
+  std::vector<DraftNode> nodes;
+  std::vector<int> frontier{-1};
+  for (int pass = 0; pass < depth && !frontier.empty(); ++pass) {
+    const int N = (int)nodes.size(), R = N + 1;
+    // the workspace layout of THIS pass's tree (run_verify places its buffers by (B, R)); the
+    // staging, logits and top-b buffers are regions a hidden-only forward does not touch
+    const WsLayout w = ws_layout(c, 1, R);
+    uint8_t* din = ws + w.stage_in;
+    uint8_t* dou = ws + w.stage_out;
+    int* d_rows = (int*)(ws + w.y);
+    int* d_tok = (int*)(ws + w.part_idx);
+    float* d_lp = (float*)(ws + w.part_val);
+    float* logits = (float*)(ws + w.noise);   // [R][V] fp32 (the sampled modes' noise block)
+    // inputs: kv, context_len, root_token, round, session (8 B), node_offset[2], parent[N], token[N]
+    std::vector<int32_t> h32(5 + 2 + 2 * N + 2);
+    h32[0] = handle;
+    h32[1] = context_len;
+    h32[2] = root_token;
+    h32[3] = 0;   // round
+    std::memcpy(&h32[4], &session_id, 8);
+    h32[6] = 0;
+    h32[7] = N;
+    for (int i = 0; i < N; ++i) {
+      h32[8 + i] = nodes[i].parent;
+      h32[8 + N + i] = nodes[i].token;
+    }
+    CK(cudaMemcpyAsync(din, h32.data(), h32.size() * 4, cudaMemcpyHostToDevice, st));
+    int32_t* di32 = (int32_t*)din;
+    DevIn di{di32 + 0, di32 + 1, di32 + 2, di32 + 6, di32 + 8, di32 + 8 + N, (const uint64_t*)(di32 + 4),
+             (const uint32_t*)(di32 + 3)};
+    int32_t* do32 = (int32_t*)dou;
+    DevOut dout{do32, do32 + 1, do32 + 2, do32 + 2 + std::max(N, 1), do32 + 2 + 2 * std::max(N, 1), nullptr, nullptr};
+    specedge_verify_in vin{};
+    vin.num_requests = 1;
+    vin.total_nodes = N;
+    vin.max_nodes = std::max(N, 1);
+    vin.max_context_len = context_len;
+    vin.mode = SPECEDGE_GREEDY;
+    const specedge_status s = run_verify(m, pool, &vin, di, dout, ws, ws_bytes, st, false, false, true);
+    if (s != SPECEDGE_OK) return s;
+    GemmArgs g{};
+    g.M = V;
+    g.R = 2 * R;
+    g.pair = 1;
+    g.K = c.d;
+    g.out_f32 = logits;
+    g.ldo = V;
+    CK(gemm_launch(EPI_F32, m->tm_lm, ws + w.Hf, g, st, nullptr));
+    std::vector<int> rows(frontier.size());
+    for (size_t i = 0; i < frontier.size(); ++i) rows[i] = frontier[i] < 0 ? 0 : frontier[i] + 1;   // slot
+    CK(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(topb_launch(logits, V, d_rows, (int)rows.size(), branching, d_tok, d_lp, st));
+    std::vector<int> tok(rows.size() * branching);
+    std::vector<float> lp(rows.size() * branching);
+    int32_t status = -1;
+    CK(cudaMemcpyAsync(tok.data(), d_tok, tok.size() * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(lp.data(), d_lp, lp.size() * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&status, do32, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (status != SPECEDGE_REQ_OK) return SPECEDGE_E_INVALID;   // e.g. context_len != cached + 1
+    std::vector<int> next;
+    const specedge_status ps = draft_prune(nodes, frontier, tok, lp, branching, budget, next);
+    if (ps != SPECEDGE_OK) return ps;
+    frontier.swap(next);
+  }
+  *n_out = (int32_t)nodes.size();
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    parent_out[i] = nodes[i].parent;
+    token_out[i] = nodes[i].token;
+    logprob_out[i] = nodes[i].logprob;
+  }
   return SPECEDGE_OK;
 }
 

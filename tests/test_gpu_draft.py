@@ -1,0 +1,81 @@
+"""NEXT-F3 on the GPU: specedge_draft_tree (the edge's pooled top-budget draft-tree builder on the
+verify kernels) against oracle/draft.py with the oracle's own draft model (oracle/model.py) on the
+same seeded weights and contexts.  Trees must be identical (parents, tokens) and log-probs within the
+derived logit tolerance, unless a decision of the oracle sits within the library's measured
+log-prob error (a top-`branching` cut or the budget cut closer than 2 * eps): counted as exempt."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import draft as OD  # noqa: E402
+from oracle import verify as OV  # noqa: E402
+from oracle.model import Weights  # noqa: E402
+from synth.configs import TINY, SMALL128  # noqa: E402
+from tests.gpu_helpers import LOGIT_MAX  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2505_17052_b200 import api as A
+    return A
+
+
+def _margins(lp_fn, passes, b, budget):
+    """Smallest decision margin of the oracle build: top-b cut per proposal and the budget cut."""
+    m = np.inf
+    kept, frontier = [], [()]
+    for ps in passes:
+        cand = list(kept)
+        for fp in frontier:
+            l = np.sort(lp_fn(fp))[::-1]
+            if len(l) > b:
+                m = min(m, l[b - 1] - l[b])
+            order = np.argsort(-lp_fn(fp), kind="stable")[:b]
+            cand += [fp + (int(t),) for t in order]
+        cums = sorted([sum(lp_fn(p[:k])[p[k]] for k in range(len(p))) for p in cand], reverse=True)
+        if len(cums) > budget:
+            m = min(m, cums[budget - 1] - cums[budget])
+        pth = []
+        for (pp, tt) in ps:
+            pth.append((() if pp < 0 else pth[pp]) + (tt,))
+        frontier = [p for p in pth if p not in kept]
+        kept = pth
+    return m
+
+
+@pytest.mark.parametrize("shape,budget,depth,branching", [(TINY, 8, 4, 3), (TINY, 32, 7, 4), (SMALL128, 16, 5, 2),
+                                                          (TINY, 5, 5, 1)])
+def test_draft_tree_matches_oracle(api, shape, budget, depth, branching):
+    rng = np.random.default_rng(budget + depth)
+    W = Weights(shape, 11)
+    prompts = [[int(t) for t in rng.integers(0, shape.vocab, n)] for n in (23, 40)]
+    model = api.Model(shape, 11, max_position=4096)
+    try:
+        pool = api.KVPool(model, 16, 4)
+        ws = model.workspace(1, budget + 1, 256)
+        kinds = []
+        for i, p in enumerate(prompts):
+            ses = OV.make_session(W, p, 70 + i)
+            h = pool.alloc(200)
+            pool.prefill(h, p, ws)
+            lp_fn = OD.model_lp(W, ses)
+            passes = []
+            o_par, o_tok, o_lp, o_cum = OD.build_draft_tree(lp_fn, budget, depth, branching, passes_out=passes)
+            g_par, g_tok, g_lp = api.draft_tree(model, pool, h, ses.context_len, ses.last_token, ses.session_id,
+                                                budget, depth, branching, ws)
+            same = list(g_par) == o_par and list(g_tok) == o_tok
+            if same:
+                assert np.abs(np.asarray(g_lp, np.float64) - np.asarray(o_lp)).max() <= LOGIT_MAX
+                kinds.append("exact")
+            else:
+                margin = _margins(lp_fn, passes, branching, budget)
+                assert margin <= 2 * LOGIT_MAX, (margin, list(g_tok), o_tok, list(g_par), o_par)
+                kinds.append("exempt")
+            # the builder never commits: the cache is unchanged
+            assert int(pool.get_len([h])[0]) == len(ses.cache)
+        assert kinds.count("exact") >= 1, kinds
+        pool.close()
+    finally:
+        model.close()
