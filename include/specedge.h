@@ -339,12 +339,17 @@ specedge_status specedge_scheduler_state(const specedge_scheduler* sched, int32_
  * final norm on a one-request tree, the LM head with an fp32 store epilogue and a top-b kernel;
  * pruning is host code.  Outputs (host arrays of >= budget entries): parent (-1 = root child, else
  * a smaller index), token, logprob; *n_out = node count.  Synchronous.  budget <= 64, branching <= 8,
- * tp_size == 1; the workspace must fit (1 request, budget + 1 rows).  Does not commit anything. */
+ * tp_size == 1; the workspace must fit (1 request, head_len + budget + 1 rows).  Does not commit.
+ * Proactive expansion (§4.2: the edge "continues drafting additional tokens"
+ * from the best path's leaf while the verify is in flight): head_tokens[head_len] (host, nullable
+ * when head_len = 0) is that path below the root; the subtree grows under its last token and the
+ * outputs describe the subtree only (parent -1 = child of the head; logprobs of the subtree nodes). */
 specedge_status specedge_draft_tree(specedge_model* model, specedge_kvpool* pool, int32_t handle,
                                     int32_t context_len, int32_t root_token, uint64_t session_id,
-                                    int32_t budget, int32_t depth, int32_t branching, void* workspace,
-                                    size_t ws_bytes, void* stream, int32_t* parent_out,
-                                    int32_t* token_out, float* logprob_out, int32_t* n_out);
+                                    const int32_t* head_tokens, int32_t head_len, int32_t budget,
+                                    int32_t depth, int32_t branching, void* workspace, size_t ws_bytes,
+                                    void* stream, int32_t* parent_out, int32_t* token_out,
+                                    float* logprob_out, int32_t* n_out);
 
 #ifdef __cplusplus
 }

@@ -114,7 +114,7 @@ def load(path: str = LIB_PATH):
         "specedge_scheduler_complete": [P, P, I32, C.c_double],
         "specedge_scheduler_observe": [P, I32, C.c_double],
         "specedge_scheduler_state": [P, P, P, P, P],
-        "specedge_draft_tree": [P, P, I32, I32, I32, U64, I32, I32, I32, P, SZ, P, P, P, P, P],
+        "specedge_draft_tree": [P, P, I32, I32, I32, U64, P, I32, I32, I32, I32, P, SZ, P, P, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

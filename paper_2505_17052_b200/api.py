@@ -372,15 +372,19 @@ def calibrate_draft_depth(verify_ms: float, draft_pass_ms: float, rtt_ms: float)
 
 
 def draft_tree(model: Model, pool: KVPool, handle: int, context_len: int, root_token: int, session_id: int,
-               budget: int, depth: int, branching: int, ws: torch.Tensor, stream=None):
+               budget: int, depth: int, branching: int, ws: torch.Tensor, head=(), stream=None):
     """NEXT-F3: build a draft tree with this model as the draft model (include/specedge.h,
-    specedge_draft_tree).  Returns (parent, token, logprob) numpy arrays."""
+    specedge_draft_tree); `head` (tokens below the root) = proactive expansion under that path.
+    Returns (parent, token, logprob) numpy arrays."""
     parent = np.zeros(budget, np.int32)
     token = np.zeros(budget, np.int32)
     logprob = np.zeros(budget, np.float32)
     n = C.c_int32()
+    hd = np.ascontiguousarray(head, np.int32) if len(head) else None
     L.check(model.lib.specedge_draft_tree(model.h, pool.h, handle, context_len, root_token,
-                                          C.c_uint64(session_id & 0xFFFFFFFFFFFFFFFF).value, budget, depth,
+                                          C.c_uint64(session_id & 0xFFFFFFFFFFFFFFFF).value,
+                                          None if hd is None else hd.ctypes.data_as(C.c_void_p),
+                                          0 if hd is None else len(hd), budget, depth,
                                           branching, _ptr(ws), ws.numel(), _stream(stream),
                                           parent.ctypes.data_as(C.c_void_p), token.ctypes.data_as(C.c_void_p),
                                           logprob.ctypes.data_as(C.c_void_p), C.byref(n)), "draft_tree")

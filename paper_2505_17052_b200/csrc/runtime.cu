@@ -1147,25 +1147,30 @@ specedge_status specedge_debug_gemm(const uint16_t* W, const uint16_t* X, float*
 }
 
 specedge_status specedge_draft_tree(specedge_model* m, specedge_kvpool* pool, int32_t handle, int32_t context_len,
-                                    int32_t root_token, uint64_t session_id, int32_t budget, int32_t depth,
-                                    int32_t branching, void* workspace, size_t ws_bytes, void* stream,
-                                    int32_t* parent_out, int32_t* token_out, float* logprob_out, int32_t* n_out) {
+                                    int32_t root_token, uint64_t session_id, const int32_t* head_tokens,
+                                    int32_t head_len, int32_t budget, int32_t depth, int32_t branching,
+                                    void* workspace, size_t ws_bytes, void* stream, int32_t* parent_out,
+                                    int32_t* token_out, float* logprob_out, int32_t* n_out) {
   if (!m || !pool || pool->model != m || !workspace || !parent_out || !token_out || !logprob_out || !n_out)
     return SPECEDGE_E_INVALID;
-  if (budget < 1 || budget > SPECEDGE_MAX_NODES || depth < 1 || branching < 1 || branching > 8 ||
-      handle < 0 || handle >= pool->max_handles || context_len < 1 || root_token < 0 || root_token >= m->cfg.vocab)
+  if (budget < 1 || head_len < 0 || head_len + budget > SPECEDGE_MAX_NODES || depth < 1 || branching < 1 ||
+      branching > 8 || handle < 0 || handle >= pool->max_handles || context_len < 1 || root_token < 0 ||
+      root_token >= m->cfg.vocab || (head_len > 0 && !head_tokens))
     return SPECEDGE_E_INVALID;
+  for (int i = 0; i < head_len; ++i)
+    if (head_tokens[i] < 0 || head_tokens[i] >= m->cfg.vocab) return SPECEDGE_E_INVALID;
+  const int P = head_len;   // proactive expansion: the subtree grows under this fixed chain
   if (m->tp_size != 1) return SPECEDGE_E_UNSUPPORTED;
   const auto& c = m->cfg;
   const int V = c.vocab;
-  if (ws_bytes < ws_layout(c, 1, budget + 1).total) return SPECEDGE_E_WORKSPACE;
+  if (ws_bytes < ws_layout(c, 1, P + budget + 1).total) return SPECEDGE_E_WORKSPACE;
   CK(cudaSetDevice(m->device));
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* ws = (uint8_t*)workspace;
   std::vector<DraftNode> nodes;
   std::vector<int> frontier{-1};
   for (int pass = 0; pass < depth && !frontier.empty(); ++pass) {
-    const int N = (int)nodes.size(), R = N + 1;
+    const int N = P + (int)nodes.size(), R = N + 1;   // tree = head chain ++ subtree
     // the workspace layout of THIS pass's tree (run_verify places its buffers by (B, R)); the
     // staging, logits and top-b buffers are regions a hidden-only forward does not touch
     const WsLayout w = ws_layout(c, 1, R);
@@ -1184,9 +1189,13 @@ specedge_status specedge_draft_tree(specedge_model* m, specedge_kvpool* pool, in
     std::memcpy(&h32[4], &session_id, 8);
     h32[6] = 0;
     h32[7] = N;
-    for (int i = 0; i < N; ++i) {
-      h32[8 + i] = nodes[i].parent;
-      h32[8 + N + i] = nodes[i].token;
+    for (int i = 0; i < P; ++i) {
+      h32[8 + i] = i - 1;
+      h32[8 + N + i] = head_tokens[i];
+    }
+    for (int i = 0; i < N - P; ++i) {
+      h32[8 + P + i] = nodes[i].parent < 0 ? P - 1 : P + nodes[i].parent;
+      h32[8 + N + P + i] = nodes[i].token;
     }
     CK(cudaMemcpyAsync(din, h32.data(), h32.size() * 4, cudaMemcpyHostToDevice, st));
     int32_t* di32 = (int32_t*)din;
@@ -1211,7 +1220,7 @@ specedge_status specedge_draft_tree(specedge_model* m, specedge_kvpool* pool, in
     g.ldo = V;
     CK(gemm_launch(EPI_F32, m->tm_lm, ws + w.Hf, g, st, nullptr));
     std::vector<int> rows(frontier.size());
-    for (size_t i = 0; i < frontier.size(); ++i) rows[i] = frontier[i] < 0 ? 0 : frontier[i] + 1;   // slot
+    for (size_t i = 0; i < frontier.size(); ++i) rows[i] = frontier[i] < 0 ? P : P + frontier[i] + 1;   // slot
     CK(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, st));
     CK(topb_launch(logits, V, d_rows, (int)rows.size(), branching, d_tok, d_lp, st));
     std::vector<int> tok(rows.size() * branching);

@@ -79,3 +79,36 @@ def test_draft_tree_matches_oracle(api, shape, budget, depth, branching):
         pool.close()
     finally:
         model.close()
+
+
+@pytest.mark.parametrize("shape", [TINY, SMALL128])
+def test_proactive_expansion_matches_oracle(api, shape):
+    """§4.2 proactive drafting: the subtree drafted under the best path's leaf (oracle best_path of
+    the oracle tree) equals the oracle's proactive_expand."""
+    rng = np.random.default_rng(31)
+    W = Weights(shape, 11)
+    p = [int(t) for t in rng.integers(0, shape.vocab, 30)]
+    model = api.Model(shape, 11, max_position=4096)
+    try:
+        pool = api.KVPool(model, 16, 4)
+        ws = model.workspace(1, 40, 256)
+        ses = OV.make_session(W, p, 90)
+        h = pool.alloc(200)
+        pool.prefill(h, p, ws)
+        lp_fn = OD.model_lp(W, ses)
+        par, tok, _, cum = OD.build_draft_tree(lp_fn, 12, 4, 3)
+        head = [tok[i] for i in OD.best_path(par, tok, cum)]
+        passes = []
+        o_par, o_tok, o_lp, _ = OD.build_draft_tree(lambda path: lp_fn(tuple(head) + tuple(path)), 10, 3, 2,
+                                                     passes_out=passes)
+        assert (o_par, o_tok) == tuple(list(x) for x in OD.proactive_expand(lp_fn, head, 10, 3, 2)[:2])
+        g_par, g_tok, g_lp = api.draft_tree(model, pool, h, ses.context_len, ses.last_token, ses.session_id,
+                                            10, 3, 2, ws, head=head)
+        if list(g_par) == o_par and list(g_tok) == o_tok:
+            assert np.abs(np.asarray(g_lp, np.float64) - np.asarray(o_lp)).max() <= LOGIT_MAX
+        else:
+            margin = _margins(lambda path: lp_fn(tuple(head) + tuple(path)), passes, 2, 10)
+            assert margin <= 2 * LOGIT_MAX, (margin, list(g_tok), o_tok)
+        pool.close()
+    finally:
+        model.close()
