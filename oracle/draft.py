@@ -67,6 +67,15 @@ def build_draft_tree(lp, budget, depth, branching, passes_out=None):
             [n["cum"] for n in nodes])
 
 
+def proactive_expand(lp, head_path, budget, passes, branching):
+    """§4.2 proactive drafting: `passes` draft passes rooted at the head
+    (the leaf of the best path, given as its token path below the root) with the build rule above;
+    the subtree's nodes exclude the head path itself.  Returns (parent, token, logprob, cum) of the
+    subtree, parents relative to the subtree (-1 = child of the head), cum relative to the head."""
+    head_path = tuple(head_path)
+    return build_draft_tree(lambda path: lp(head_path + tuple(path)), budget, passes, branching)
+
+
 def best_path(parent, token, cum):
     """Node indices of the best root-to-leaf path."""
     n = len(parent)
