@@ -15,6 +15,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace se {
 
@@ -337,18 +338,30 @@ __global__ void k_attn_combine(const __grid_constant__ AttnArgs a, bf16* __restr
   if (rh >= a.R * a.H) return;
   const int hd = a.hd;
   const size_t stride = (size_t)a.R * a.H;
+  int ns = a.n_splits;
+  if (a.per_req == 1) {
+    const int r = a.row_req ? a.row_req[rh / a.H] : 0;
+    const int npages = (a.req_L[r] + 63) / 64;
+    ns = max(1, (npages + a.pages_per_split - 1) / a.pages_per_split);
+    if (ns == 1) return;   // written final by the attention kernel
+  } else if (a.per_req == 2) {
+    // balanced tcgen05 attention: the kernel recorded the chunk count of every (r, g)
+    const int r = a.row_req ? a.row_req[rh / a.H] : 0;
+    ns = a.nch_tab[r * a.KV + (rh % a.H) / a.G];
+    if (ns == 1) return;
+  }
   float m = -INFINITY;
-  for (int sp = 0; sp < a.n_splits; ++sp) m = fmaxf(m, a.mpart[sp * stride + rh]);
+  for (int sp = 0; sp < ns; ++sp) m = fmaxf(m, a.mpart[sp * stride + rh]);
   const float mb = m == -INFINITY ? 0.f : m;
   float l = 0.f;
-  for (int sp = 0; sp < a.n_splits; ++sp) {
+  for (int sp = 0; sp < ns; ++sp) {
     const float ms = a.mpart[sp * stride + rh];
     if (ms != -INFINITY) l += exp2f(ms - mb) * a.lpart[sp * stride + rh];
   }
   const float inv = l > 0.f ? 1.0f / l : 0.f;
   for (int d = lane * 4; d < hd; d += 128) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int sp = 0; sp < a.n_splits; ++sp) {
+    for (int sp = 0; sp < ns; ++sp) {
       const float ms = a.mpart[sp * stride + rh];
       if (ms == -INFINITY) continue;
       const float w = exp2f(ms - mb) * inv;
@@ -392,14 +405,26 @@ cudaError_t launch_hd(const AttnArgs& a, int B, cudaStream_t st) {
 
 }  // namespace
 
-// tcgen05 kernel: one CTA per SM (512 TMEM columns); split only when (request, kv head) items
-// leave most SMs idle.
-int attn_pick_splits_tc(int B, int KV, int max_pages) {
+// tcgen05 kernel: one CTA per SM (512 TMEM columns).  Short contexts: split only when (request,
+// kv head) items leave most SMs idle.  Long contexts (>= 64 pages): cut every request's pages
+// into chunks of P pages so that the chunks fill about `waves` rounds of the 148 SMs; the
+// hardware block scheduler then balances ragged context lengths (cfg5: 192-320 pages per request
+// would otherwise leave the longest CTA running 1.25x the mean with 20 SMs idle).
+int attn_pick_chunk_tc(int B, int KV, int max_pages) {
+  static const int env_p = getenv("SPECEDGE_ATTN_CHUNK") ? atoi(getenv("SPECEDGE_ATTN_CHUNK")) : 0;
+  static const int waves = getenv("SPECEDGE_ATTN_WAVES") ? std::max(1, atoi(getenv("SPECEDGE_ATTN_WAVES"))) : 4;
+  max_pages = std::max(1, max_pages);
+  if (env_p > 0) return std::max(env_p, (max_pages + 7) / 8);
   const int items = std::max(1, B * KV);
-  int ns = (148 + items / 2) / items;
-  ns = std::min(ns, 8);
-  ns = std::min(ns, std::max(1, (max_pages + 1) / 2));
-  return std::max(1, ns);
+  if (max_pages < 64) {
+    int ns = (148 + items / 2) / items;
+    ns = std::min(ns, 8);
+    ns = std::min(ns, std::max(1, (max_pages + 1) / 2));
+    ns = std::max(1, ns);
+    return (max_pages + ns - 1) / ns;
+  }
+  const long long want = ((long long)items * max_pages + 148LL * waves - 1) / (148LL * waves);
+  return (int)std::min<long long>(max_pages, std::max<long long>({want, (max_pages + 7) / 8, 8}));
 }
 
 int attn_pick_splits(int B, int KV, int max_pages) {

@@ -43,7 +43,17 @@ namespace {
 
 constexpr int kWarps = 11;      // producer, MMA (unit 0), 2 units x 4 softmax/epilogue warps, MMA (unit 1)
 constexpr int kThreads = kWarps * 32;
-constexpr int kStages = 5;      // K/V ring depth (64-key sub-tiles)
+// K/V ring depth (64-key sub-tiles): whatever the 227 KB of shared memory leaves after NQ Q tiles
+// and ~3 KB of barriers / masks / merge scalars (hd 128: 5 stages with two Q tiles, 6 with one;
+// hd 64: 12).  The ring is the only source of memory-level parallelism: at steady state the two
+// units hold about four sub-tiles, the rest are in flight.
+constexpr int kSmemMax = 227 * 1024;
+constexpr int kSmemAux = 3 * 1024;
+__host__ __device__ constexpr int ring_stages(int hd, int nq) {
+  return (kSmemMax - kSmemAux - nq * 128 * hd * 2) / (2 * 64 * hd * 2) > 12
+             ? 12
+             : (kSmemMax - kSmemAux - nq * 128 * hd * 2) / (2 * 64 * hd * 2);
+}
 #ifndef SPECEDGE_EMU8
 #define SPECEDGE_EMU8 0
 #endif
@@ -156,8 +166,8 @@ __device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
 
 struct TcArgs {
   AttnArgs a;
-  bf16* O;          // final output when n_splits == 1 (normalised, bf16) else nullptr
-  float* O_f32;     // optional fp32 normalised output (debug) when n_splits == 1
+  bf16* O;          // final normalised output of single-chunk items (bf16), or nullptr
+  float* O_f32;     // optional fp32 normalised output (debug)
   int slots_per_mt; // floor(128 / G)
   int prefetch;     // L2 prefetch distance in sub-tiles (0: off)
   unsigned long long* trace;   // debug (env SPECEDGE_ATTN_TRACE): clock64 stamps of CTA 0, else null
@@ -168,7 +178,7 @@ struct TcArgs {
     if (ta.trace && blockIdx.x == 0 && blockIdx.y == 0 && (i) < 1024) ta.trace[(i)] = clock64(); \
   } while (0)
 
-template <int HD>
+template <int HD, int NQ>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQ2,
               const __grid_constant__ CUtensorMap tmQ4, const __grid_constant__ CUtensorMap tmPool,
@@ -177,13 +187,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int KB = HD / 64;                       // 64-element hd blocks
   constexpr uint32_t QT_BYTES = 128 * HD * 2;       // one 128-row M-tile of Q
   constexpr uint32_t PG_BYTES = 64 * HD * 2;        // K (or V) of one 64-key sub-tile
-  constexpr int NST = kStages;
+  constexpr int NST = ring_stages(HD, NQ);
   const AttnArgs& a = ta.a;
   // 2 Q tiles + 5 K/V sub-tile stages = 224 KB of the 227 KB: the 1024-B alignment SW128 needs
   // comes from the dynamic-smem base itself (no static smem in this kernel); checked below.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sQ = smem_raw;                           // [2 units][KB][128 rows][128 B]
-  uint8_t* sK = sQ + 2 * QT_BYTES;                  // [NST][KB][64 keys][128 B]
+  uint8_t* sK = sQ + NQ * QT_BYTES;                 // [NST][KB][64 keys][128 B]
   uint8_t* sV = sK + NST * PG_BYTES;                // [NST][KB][64 keys][128 B]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NST * PG_BYTES);
   uint64_t* q_full = bars;              // [1]
@@ -196,30 +206,117 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* o_full = pv_done + 4;       // [1]
   uint64_t* o_empty = o_full + 1;       // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
-  uint64_t* s_anc = reinterpret_cast<uint64_t*>(o_empty + 3);  // [66]
-  float* s_ml = reinterpret_cast<float*>(s_anc + 66);          // [2 units][m, l][128 rows]
+  // completes once per pass whose epilogue merged replicas through the K/V ring: the producer
+  // waits on it in order (it may run two passes ahead of o_empty, whose parity would alias)
+  uint64_t* scr_done = o_empty + 2;
+  float* s_ml = reinterpret_cast<float*>(o_empty + 3);          // [2 units][m, l][128 rows]
 
-  const int r = blockIdx.x / a.KV, g = blockIdx.x % a.KV, sp = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.G;
-  const int S = min(a.req_S[r], a.max_rows / G);
-  const int L = a.req_L[r];
-  const int row0 = a.req_row0[r];
-  const int h = a.req_h[r];
   const int spm = ta.slots_per_mt;
-  const int n_mt = (S + spm - 1) / spm;        // 128-row M-tiles
-  const int n_pass = (n_mt + 1) / 2;           // pass p: M-tiles 2p, 2p+1 ("pair") or the last one alone
-  const int npages = (L + 63) / 64;
-  const int p_begin = sp * a.pages_per_split;
-  const int p_end = min(npages, p_begin + a.pages_per_split);
-  const int npg = max(0, p_end - p_begin);
-  const bool has_tree = sp == a.n_splits - 1;
-  const int ntree = has_tree ? (S > 64 ? 2 : 1) : 0;
-  const int nsub = npg + ntree;                // 64-key sub-tiles per pass
+  int* s_sched = reinterpret_cast<int*>(s_ml + 512);             // [4] balanced-mode cursor
+  // ---- work items.  An item = (request r, kv head g, a range of the request's 64-key
+  // sub-tiles: pages [p_begin, p_begin + npg) then tree halves [th0, th0 + ntree)), chunk c of
+  // the nch chunks of (r, g).  Static mode: the item of blockIdx (x = r*KV + g, y = chunk of
+  // pages_per_split pages, the tree in the request's last chunk).  Balanced mode (a.per_req == 2,
+  // persistent grid): the (r, g) sub-tile sequences are concatenated (r-major, then g) into W
+  // units and CTA b takes [b*Qw, (b+1)*Qw), Qw = max(ceil(W / grid), ceil(max_nsub / (n_splits -
+  // 1))) so that no (r, g) is cut into more than n_splits chunks; the pipeline (K/V ring, TMEM
+  // buffers, barrier phases) runs on across the CTA's items.
+  auto S_of = [&](int rr) { return min(a.req_S[rr], a.max_rows / G); };
+  auto nsub_of = [&](int rr) { return (a.req_L[rr] + 63) / 64 + (S_of(rr) > 64 ? 2 : 1); };
+  const bool balanced = a.per_req == 2;
+  // per-item state (set by next_item; the lambdas below read it by reference)
+  int r = 0, g = 0, c_idx = 0, nch = 1, S = 0, L = 0, row0 = 0, h = 0, n_mt = 0, n_pass = 0, npages = 0;
+  int p_begin = 0, npg = 0, th0 = 0, ntree = 0, nsub = 0;
+  bool single = true;
+  struct Cursor { int pos, end, r, base, Qw; };
+  auto set_item = [&](int rr, int gg, int j0, int j1, int cc, int nc) {
+    r = rr; g = gg; c_idx = cc; nch = nc;
+    S = S_of(r); L = a.req_L[r]; row0 = a.req_row0[r]; h = a.req_h[r];
+    n_mt = (S + spm - 1) / spm;
+    // pass p: M-tiles 2p, 2p+1 ("pair") or the last one alone; with one Q tile (NQ = 1, chosen
+    // when every request fits one M-tile) every pass is a single pass over M-tile p
+    n_pass = NQ == 2 ? (n_mt + 1) / 2 : n_mt;
+    npages = (L + 63) / 64;
+    p_begin = j0;
+    npg = max(0, min(j1, npages) - j0);
+    th0 = max(j0, npages) - npages;
+    ntree = max(0, j1 - max(j0, npages));
+    nsub = npg + ntree;
+    single = nch == 1;
+  };
+  auto cursor0 = [&]() -> Cursor {
+    if (balanced) return Cursor{(int)blockIdx.x * s_sched[0], min(s_sched[1], (int)(blockIdx.x + 1) * s_sched[0]), s_sched[2],
+                                s_sched[3], s_sched[0]};
+    return Cursor{0, 1, 0, 0, 0};
+  };
+  auto next_item = [&](Cursor& cu) -> bool {
+    if (!balanced) {
+      if (cu.pos++ != 0) return false;
+      const int rr = blockIdx.x / a.KV, gg = blockIdx.x % a.KV, sp = blockIdx.y;
+      const int np_ = (a.req_L[rr] + 63) / 64;
+      const int nc = a.per_req ? max(1, (np_ + a.pages_per_split - 1) / a.pages_per_split) : a.n_splits;
+      if (sp >= nc) return false;
+      const int j0 = sp * a.pages_per_split;
+      const int j1 = sp == nc - 1 ? nsub_of(rr) : min(np_, j0 + a.pages_per_split);
+      set_item(rr, gg, min(j0, np_), j1, sp, nc);
+      return true;
+    }
+    if (cu.pos >= cu.end || cu.r >= a.B) return false;
+    const int n = nsub_of(cu.r);
+    const int gg = (cu.pos - cu.base) / n;
+    const int o = cu.base + gg * n;
+    const int j0 = cu.pos - o, j1 = min(n, cu.end - o);
+    set_item(cu.r, gg, j0, j1, (int)blockIdx.x - o / cu.Qw, (o + n - 1) / cu.Qw - o / cu.Qw + 1);
+    cu.pos = o + j1;
+    if (cu.pos >= cu.base + a.KV * n) { cu.base += a.KV * n; ++cu.r; }
+    return true;
+  };
+  if (balanced && warp == 0) {
+    // W, max nsub, and the request holding this CTA's first unit (lane-parallel over requests)
+    int W = 0, mx = 0;
+    for (int q0 = 0; q0 < a.B; q0 += 32) {
+      const int n = q0 + lane < a.B ? nsub_of(q0 + lane) : 0;
+      W += n;
+      mx = max(mx, n);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      W += __shfl_xor_sync(0xffffffffu, W, o);
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    W *= a.KV;
+    const int Qw = max((W + (int)gridDim.x - 1) / (int)gridDim.x, (mx + a.n_splits - 2) / (a.n_splits - 1));
+    const int start = (int)blockIdx.x * Qw;
+    int base = 0, rs = a.B;
+    for (int q0 = 0; q0 < a.B && rs == a.B; q0 += 32) {
+      const int n = q0 + lane < a.B ? a.KV * nsub_of(q0 + lane) : 0;
+      int incl = n;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int excl = incl - n;
+      const unsigned hit = __ballot_sync(0xffffffffu, n > 0 && start >= base + excl && start < base + incl);
+      if (hit) {
+        const int l = __ffs(hit) - 1;
+        rs = q0 + l;
+        base += __shfl_sync(0xffffffffu, excl, l);
+      } else {
+        base += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    if (lane == 0) {
+      s_sched[0] = Qw;
+      s_sched[1] = W;
+      s_sched[2] = rs;
+      s_sched[3] = base;
+    }
+  }
   // sub-tile visited at step j of pass p: odd passes walk backwards (tree first) so they start on
-  // what the previous pass left in L2.  Returns 0..npg-1 for pages, npg + h for tree half h.
+  // what the previous pass left in L2.  Returns 0..npg-1 for pages, npg + t for tree half th0 + t.
   auto sub_of = [&](int p, int j) { return (p & 1) ? nsub - 1 - j : j; };
-  auto pair_pass = [&](int p) { return 2 * p + 1 < n_mt; };
+  auto pair_pass = [&](int p) { return NQ == 2 && 2 * p + 1 < n_mt; };
   // unit u's k-th sub-tile in pass p: pair pass -> every sub-tile (unit u = M-tile 2p+u);
   // single pass -> the two units split the sub-tiles of one M-tile (unit u takes j = 2k+u)
   auto nsub_u = [&](int p, int u) { return pair_pass(p) ? nsub : (nsub - u + 1) / 2; };
@@ -229,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // sees only keys [r*64/Rf, (r+1)*64/Rf) of every sub-tile with its own running max / sum / O,
   // so a small tail tile (cfg2: 4 rows) spreads its softmax over all four SM sub-partitions
   // instead of doubling one of them; replicas are merged in the epilogue.
-  auto mt_of = [&](int p, int u) { return pair_pass(p) ? 2 * p + u : 2 * p; };
+  auto mt_of = [&](int p, int u) { return pair_pass(p) ? 2 * p + u : (NQ == 2 ? 2 * p : p); };
   auto rep_of = [&](int p, int u) {
     const int slots = min(spm, S - mt_of(p, u) * spm);
     return slots <= 32 / G ? 4 : (slots <= 64 / G ? 2 : 1);
@@ -255,9 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(o_full, 2);
     mbar_init(o_empty, 256);
+    mbar_init(scr_done, 256);
     fence_barrier_init();
   }
-  for (int s = threadIdx.x; s < S && s <= kMaxNodes; s += blockDim.x) s_anc[s] = a.row_anc[row0 + s];
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
@@ -269,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // one 32-column chunk of an output row: normalised bf16 (+ optional fp32) when the KV is not
   // split, else the unnormalised fp32 partial (the combine kernel merges splits with m, l)
   auto store_out = [&](size_t rh, int col, const float (&ov)[32], float, float) {
-    if (a.n_splits == 1) {
+    if (single) {
       if (ta.O) {
         uint4* dst = reinterpret_cast<uint4*>(ta.O + rh * HD + col);
 #pragma unroll
@@ -283,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int e = 0; e < 32; e += 4) dst[e / 4] = make_float4(ov[e], ov[e + 1], ov[e + 2], ov[e + 3]);
       }
     } else {
-      float4* dst = reinterpret_cast<float4*>(a.opart + ((size_t)sp * a.R * a.H + rh) * HD + col);
+      float4* dst = reinterpret_cast<float4*>(a.opart + ((size_t)c_idx * a.R * a.H + rh) * HD + col);
 #pragma unroll
       for (int e = 0; e < 32; e += 4) dst[e / 4] = make_float4(ov[e], ov[e + 1], ov[e + 2], ov[e + 3]);
     }
@@ -293,11 +390,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------------------- TMA producer
     if (elect_one()) {
       int stage = 0;
-      uint32_t phase = 0;
+      uint32_t phase = 0, gp = 0;   // gp: passes over all items (barrier phases)
+      bool scratch = false;         // the last pass merges replicas through the ring (epilogue)
+      uint32_t nscr = 0;            // scr_done completions consumed
+      Cursor cu = cursor0();
+      while (next_item(cu)) {
+      if (balanced && c_idx == 0) a.nch_tab[r * a.KV + g] = nch;   // for the combine kernel
       const int* pages = a.block_table + (size_t)h * a.max_pages_per_seq + p_begin;
-      for (int p = 0; p < n_pass; ++p) {
+      for (int p = 0; p < n_pass; ++p, ++gp) {
         const int nq = pair_pass(p) ? 2 : 1;
-        mbar_wait(q_empty, (p & 1) ^ 1);
+        mbar_wait(q_empty, (gp & 1) ^ 1);
         uint32_t qbytes = 0;
         for (int u = 0; u < nq; ++u) qbytes += (uint32_t)rep_of(p, u) * (128 / rep_of(p, u) / G) * G * 128 * KB;
         mbar_expect_tx(q_full, qbytes);
@@ -309,6 +411,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_3d(sQ + u * QT_BYTES + kb * 128 * 128 + rr * (128 / rf) * 128, tq, q_full, kb * 64, g * G,
                           row0 + mt_of(p, u) * spm);
         }
+        // the previous pass's epilogue merged replicas through the K/V ring: no K/V load may land
+        // in the ring before that merge is done (o_empty of that pass)
+        if (scratch) mbar_wait(scr_done, nscr++ & 1);
+        scratch = rep_of(p, 0) > 1 || (pair_pass(p) && rep_of(p, 1) > 1);
         int next_page = nsub > 0 && sub_of(p, 0) < npg ? __ldg(pages + sub_of(p, 0)) : 0;
         // L2 prefetch of the pages kPrefetch sub-tiles ahead of the ring: the ring holds only a few
         // sub-tiles in flight, so HBM latency would otherwise bound the per-SM stream rate
@@ -340,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             rv = rk + a.KV * 64;
             tm = &tmPool;
           } else {
-            const int th = sj - npg;
+            const int th = th0 + sj - npg;
             rk = ((a.layer * 2 + 0) * a.KV + g) * a.R_cap + row0 + 64 * th;
             rv = ((a.layer * 2 + 1) * a.KV + g) * a.R_cap + row0 + 64 * th;
             tm = &tmTree;
@@ -349,9 +455,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(dk + kb * 64 * 128, tm, &kv_full[stage], kb * 64, rk);
             tma_load_2d(dv + kb * 64 * 128, tm, &kv_full[stage], kb * 64, rv);
           }
-          if (p == 0) TRACE(j);
+          if (gp == 0) TRACE(j);
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
+      }
       }
     }
   } else if (warp == 1 || warp == kWarps - 1) {
@@ -364,15 +471,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_pv = idesc_f16(128, HD, true);
       uint32_t sub_base = 0;           // sub-tiles streamed before this pass (ring position)
       uint32_t kc = 0;                 // this unit's sub-tiles consumed (all passes): buffer kc & 1
-      for (int p = 0; p < n_pass; ++p) {
+      uint32_t gp = 0;                 // passes over all items
+      Cursor cu = cursor0();
+      while (next_item(cu)) {
+      for (int p = 0; p < n_pass; ++p, ++gp) {
         const bool pr = pair_pass(p);
         const int nk = nsub_u(p, u);
-        mbar_wait(q_full, p & 1);
+        mbar_wait(q_full, gp & 1);
         tc_fence_after();
         // QK of this unit's k-th sub-tile of the pass into S buffer (kc + k) & 1
         auto issue_qk = [&](int k) {
           const uint32_t gi = sub_base + (uint32_t)j_of(p, u, k);
           mbar_wait(&kv_full[gi % NST], (gi / NST) & 1);
+          if (gp == 0 && k < 64) TRACE(640 + 64 * u + k);
           tc_fence_after();
           const uint32_t qaddr = smem_u32(sQ + (pr ? u : 0) * QT_BYTES);
           const uint32_t kaddr = smem_u32(sK + (gi % NST) * PG_BYTES);
@@ -393,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t kg = kc + k;
           const uint32_t b = kg & 1;
           mbar_wait(&p_full[u * 2 + b], (kg >> 1) & 1);
-          if (k == 0) mbar_wait(o_empty, (p & 1) ^ 1);   // the previous pass's O has been drained
+          if (k == 0) mbar_wait(o_empty, (gp & 1) ^ 1);   // the previous pass's O has been drained
           tc_fence_after();
           const uint32_t gi = sub_base + (uint32_t)j_of(p, u, k);
           const uint32_t vaddr = smem_u32(sV + (gi % NST) * PG_BYTES);
@@ -416,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         kc += nk;
         sub_base += nsub;
       }
+      }
     }
   } else {
     // ------------------------------------------------------------------ softmax + epilogue
@@ -427,9 +539,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t s_base = tmem + u * 256 + lane_off;
     const uint32_t o_own = tmem + u * 256 + 128 + lane_off;
     const float sl2 = a.scale_log2;
-    const bool single = a.n_splits == 1;
     uint32_t kc = 0;   // this unit's sub-tiles consumed (all passes)
-    for (int p = 0; p < n_pass; ++p) {
+    uint32_t gp = 0;   // passes over all items
+    Cursor cu = cursor0();
+    while (next_item(cu)) {
+    for (int p = 0; p < n_pass; ++p, ++gp) {
       const bool pr = pair_pass(p);
       const int mt = mt_of(p, u);
       const int rf = rep_of(p, u);
@@ -440,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool valid_row = ri < rows_mt;
       const int slot = mt * spm + ri / G;
       const int j = ri % G;
-      const uint64_t anc = (valid_row && slot > 0) ? s_anc[slot] : 0ull;
+      const uint64_t anc = (valid_row && slot > 0 && ntree > 0) ? __ldg(a.row_anc + row0 + slot) : 0ull;
       // my replica's key window within every 64-key sub-tile
       const uint64_t win = rf == 1 ? ~0ull : (((1ull << (64 / rf)) - 1ull) << (rq * (64 / rf)));
       const int nk = nsub_u(p, u);
@@ -450,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t b = kg & 1;
         const uint32_t s_tm = s_base + b * 64;
         mbar_wait(&s_full[u * 2 + b], (kg >> 1) & 1);
-        if (p == 0 && lane == 0 && q == 0) TRACE(256 + 64 * u + k);
+        if (gp == 0 && lane == 0 && q == 0) TRACE(256 + 64 * u + k);
         tc_fence_after();
         const int sj = sub_of(p, j_of(p, u, k));
         // 64-bit visibility mask of the sub-tile's keys for my row
@@ -461,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mk = kvalid >= 64 ? ~0ull : ((1ull << kvalid) - 1ull);
           } else {
             // key 0 = root, key k >= 1 = node k-1: visible iff root or ancestor-or-self of my node
-            const int th = sj - npg;
+            const int th = th0 + sj - npg;
             const uint64_t lo = slot > 0 ? ((anc << 1) | 1ull) : 1ull;
             const uint64_t hi = slot > 0 ? (anc >> 63) : 0ull;
             const int n = S - 64 * th;   // tree keys in this half
@@ -487,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld_32x32b_x32(s_tm + c0 + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * h));
             }
             tmem_ld_wait();
-            if (p == 0 && lane == 0 && q == 0 && k < 16) TRACE(512 + 64 * u + 4 * k);
+            if (gp == 0 && lane == 0 && q == 0 && k < 16) TRACE(512 + 64 * u + 4 * k);
             float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
             if (full) {
 #pragma unroll
@@ -507,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
-            if (p == 0 && lane == 0 && q == 0 && k < 16) TRACE(513 + 64 * u + 4 * k);
+            if (gp == 0 && lane == 0 && q == 0 && k < 16) TRACE(513 + 64 * u + 4 * k);
             float alpha = 1.f;
             bool rescale = false;
             if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
@@ -560,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                         : *reinterpret_cast<uint32_t(*)[8]>(z));
             }
             l += ls0 + ls1;
-            if (p == 0 && lane == 0 && q == 0 && k < 16) TRACE(514 + 64 * u + 4 * k);
+            if (gp == 0 && lane == 0 && q == 0 && k < 16) TRACE(514 + 64 * u + 4 * k);
             if (__any_sync(0xffffffffu, rescale)) {
               // O *= alpha: PV(k-1) writes O and may still be in flight -> wait for it
               const uint32_t pb = (kg - 1) & 1;
@@ -591,13 +705,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_32x32b_x16(s_tm + 16, z);
         }
         tmem_st_wait();
-        if (p == 0 && lane == 0 && q == 0) TRACE(384 + 64 * u + k);
+        if (gp == 0 && lane == 0 && q == 0) TRACE(384 + 64 * u + k);
         tc_fence_before();
         mbar_arrive(&p_full[u * 2 + b]);
       }
       kc += nk;
       // ---- epilogue of the pass
-      mbar_wait(o_full, p & 1);
+      mbar_wait(o_full, gp & 1);
       tc_fence_after();
       const size_t rh = (size_t)(row0 + slot) * a.H + (size_t)g * G + j;
       const int rf_any = max(rep_of(p, 0), pr ? rep_of(p, 1) : 1);
@@ -676,8 +790,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (valid_row) store_out(rh, col, ov, ms, lt);
         }
         if (valid_row && !single && (pr || u == 0)) {
-          a.mpart[(size_t)sp * a.R * a.H + rh] = ms;
-          a.lpart[(size_t)sp * a.R * a.H + rh] = lt;
+          a.mpart[(size_t)c_idx * a.R * a.H + rh] = ms;
+          a.lpart[(size_t)c_idx * a.R * a.H + rh] = lt;
         }
       } else {
         // merge the replicas: the unit's (pair pass) or both units' (single pass) threads
@@ -719,15 +833,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const size_t rrh = (size_t)(row0 + rslot) * a.H + (size_t)g * G + row % G;
           store_out(rrh, col, ov, ms, lt);
           if (!single && col == 0) {
-            a.mpart[(size_t)sp * a.R * a.H + rrh] = ms;
-            a.lpart[(size_t)sp * a.R * a.H + rrh] = lt;
+            a.mpart[(size_t)c_idx * a.R * a.H + rrh] = ms;
+            a.lpart[(size_t)c_idx * a.R * a.H + rrh] = lt;
           }
         }
       }
       (void)rf_any;
       tc_fence_before();
       mbar_arrive(o_empty);
+      if (rep_of(p, 0) > 1 || (pr && rep_of(p, 1) > 1)) mbar_arrive(scr_done);
       named_bar_sync(2, 256);   // s_ml / ring reuse by the next pass
+    }
     }
   }
   __syncthreads();
@@ -773,7 +889,7 @@ bool tmap_q(CUtensorMap* m, const void* base, uint64_t R, int H, int hd, int G, 
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int HD>
+template <int HD, int NQ>
 cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStream_t st) {
   CUtensorMap tq, tp, tt;
   const int spm = 128 / a.G;
@@ -793,16 +909,19 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
   if (getenv("SPECEDGE_ATTN_TRACE") && !trace) cudaMalloc(&trace, 1024 * 8);
   TcArgs ta{a, O, O_f32, spm, pf, trace};
   if (trace) cudaMemsetAsync(trace, 0, 1024 * 8, st);
-  const size_t smem = (size_t)2 * 128 * HD * 2 + (size_t)kStages * 2 * 64 * HD * 2 + 8 * 24 + 66 * 8 + 512 * 4;
+  constexpr int NST = ring_stages(HD, NQ);
+  const size_t smem = (size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 16;
+  static_assert((size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 16 <=
+                    (size_t)kSmemMax, "attention smem");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_attn_tc<HD, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(B * a.KV, a.n_splits);
+  const dim3 grid = a.per_req == 2 ? dim3(a.grid_ctas) : dim3(B * a.KV, a.n_splits);
   {
-    const cudaError_t le = launch_k(k_attn_tc<HD>, grid, dim3(kThreads), smem, st, tq, tq2, tq4, tp, tt, ta);
+    const cudaError_t le = launch_k(k_attn_tc<HD, NQ>, grid, dim3(kThreads), smem, st, tq, tq2, tq4, tp, tt, ta);
     if (le != cudaSuccess) return le;
   }
   if (trace) {
@@ -814,6 +933,9 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
       const unsigned long long t0 = hb[1000];
       auto d = [&](int i) { return hb[i] ? (long long)(hb[i] - t0) : -1LL; };
       fprintf(stderr, "attn trace CTA0: end=%lld\n", d(1001));
+      for (int k = 0; k < 16; ++k)
+        fprintf(stderr, " k%2d PIPE u0: load=%6lld kv=%6lld s=%6lld p=%6lld || u1: load=%6lld kv=%6lld s=%6lld p=%6lld\n", k,
+                d(2 * k), d(640 + k), d(256 + k), d(384 + k), d(2 * k + 1), d(704 + k), d(320 + k), d(448 + k));
       for (int k = 0; k < 16; ++k)
         fprintf(stderr, " k%2d SOFTMAX u0: s=%6lld ld=%6lld max=%6lld exp=%6lld p=%6lld || u1: s=%6lld ld=%6lld max=%6lld exp=%6lld p=%6lld\n",
                 k, d(256 + k), d(512 + 4 * k), d(513 + 4 * k), d(514 + 4 * k), d(384 + k), d(320 + k), d(576 + 4 * k),
@@ -829,8 +951,11 @@ bool attention_tc_supported(int hd, int G) { return (hd == 64 || hd == 128) && G
 
 cudaError_t attention_tc_launch(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
-  if (a.hd == 128) return launch_tc<128>(a, B, O, O_f32, st);
-  if (a.hd == 64) return launch_tc<64>(a, B, O, O_f32, st);
+  // one Q tile (and a deeper K/V ring) when every request's rows fit one M-tile
+  static const int force_nq = getenv("SPECEDGE_ATTN_NQ") ? atoi(getenv("SPECEDGE_ATTN_NQ")) : 0;
+  const bool one = force_nq ? force_nq == 1 : a.max_rows / a.G <= 128 / a.G;
+  if (a.hd == 128) return one ? launch_tc<128, 1>(a, B, O, O_f32, st) : launch_tc<128, 2>(a, B, O, O_f32, st);
+  if (a.hd == 64) return one ? launch_tc<64, 1>(a, B, O, O_f32, st) : launch_tc<64, 2>(a, B, O, O_f32, st);
   return cudaErrorInvalidValue;
 }
 

@@ -126,12 +126,23 @@ struct AttnArgs {
   float* lpart;
   int R;
   float scale_log2;
+  // per_req = 1 (tcgen05 path): request r has its own chunk count max(1, ceil(pages_r /
+  // pages_per_split)) <= n_splits, the tree keys go to its last chunk, and a request with one
+  // chunk is written final by the attention kernel (the combine skips its rows, via row_req;
+  // row_req == nullptr means every row belongs to request 0).  per_req = 0: every request has
+  // n_splits splits, the tree in the last one (the mma.sync kernel).
+  // per_req = 2 (tcgen05, balanced): a persistent grid of grid_ctas CTAs splits the concatenated
+  // (r, g) sub-tile sequences evenly (attention_tc.cu); chunks per (r, g) <= n_splits.
+  int per_req;
+  const int* row_req;
+  int B, grid_ctas;
+  int* nch_tab;               // per_req = 2: [B][KV] chunk counts, written by the attention kernel
 };
 cudaError_t attention_launch(const AttnArgs& a, int B, cudaStream_t st, int* launches);
 cudaError_t attn_combine_launch(const AttnArgs& a, bf16* O, float* O_f32, cudaStream_t st,
                                 int* launches);
 int attn_pick_splits(int B, int KV, int max_pages);
-int attn_pick_splits_tc(int B, int KV, int max_pages);
+int attn_pick_chunk_tc(int B, int KV, int max_pages);   // pages per chunk (per_req = 1)
 // tcgen05 attention (head_dim 64 / 128); with n_splits == 1 it writes the normalised output
 // directly (bf16 O and/or fp32 O_f32), otherwise (o, m, l) partials for attn_combine_launch.
 bool attention_tc_supported(int hd, int G);

@@ -23,6 +23,27 @@ bool se::pdl_enabled() {
 
 namespace {
 
+// Tree attention work split on the tcgen05 path: the persistent, evenly split grid
+// (attention_tc.cu, per_req = 2) for long contexts (>= kBalancedPages pages of 64 keys), else
+// one CTA per (request, kv head, chunk).  Measured (profiles/README.md): cfg5 (12k-20k
+// contexts) gains, cfg2 (1k) loses (every pass of its replicated tail tile drains the ring).
+// SPECEDGE_ATTN_BALANCED=0/1 forces either.
+bool attn_balanced(int max_pages) {
+  static const int force = getenv("SPECEDGE_ATTN_BALANCED") ? atoi(getenv("SPECEDGE_ATTN_BALANCED")) : -1;
+  static const int min_pages = getenv("SPECEDGE_ATTN_BAL_PAGES") ? atoi(getenv("SPECEDGE_ATTN_BAL_PAGES")) : 64;
+  return force >= 0 ? force == 1 : max_pages >= min_pages;
+}
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 thread_local int g_last_launches = 0;
 
 // ---- optional per-kernel event timing (bench instrumentation) ----
@@ -83,7 +104,7 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
   size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
-  size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, part_val, part_idx, y, score, tp_gather;
+  size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, attn_nch, part_val, part_idx, y, score, tp_gather;
   size_t part_m, part_s, lse, row_qnode, pchild, resid_y, resid_s;   // SAMPLE_PQ_DENSE
   size_t noise;                                                       // [R][V] Gumbel noise (sampled modes)
   size_t stage_in, stage_out, total;
@@ -126,6 +147,7 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.opart = take(4 * (size_t)kMaxSplits * R * H * hd);
   w.mpart = take(4 * (size_t)kMaxSplits * R * H);
   w.lpart = take(4 * (size_t)kMaxSplits * R * H);
+  w.attn_nch = take(4 * (size_t)B * KV);   // balanced attention: chunks per (request, kv head)
   const size_t vt = (c.vocab + 127) / 128;
   w.part_val = take(4 * (size_t)R * vt);
   w.part_idx = take(4 * (size_t)R * vt);
@@ -253,9 +275,23 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   aa.req_S = pa.req_S;
   aa.row_anc = pa.row_anc;
   const bool use_tc = attention_tc_supported(hd, G);
-  aa.n_splits = std::min(kMaxSplits, use_tc ? attn_pick_splits_tc(B, KV, max_pages) : attn_pick_splits(B, KV, max_pages));
-  aa.pages_per_split = std::max(1, (max_pages + aa.n_splits - 1) / aa.n_splits);
-  aa.n_splits = std::max(1, (max_pages + aa.pages_per_split - 1) / aa.pages_per_split);
+  aa.B = B;
+  if (use_tc && attn_balanced(max_pages)) {   // persistent grid, even split of all (r, g) sub-tiles
+    aa.per_req = 2;
+    aa.row_req = pa.row_req;
+    aa.nch_tab = (int*)P(w.attn_nch);
+    aa.grid_ctas = num_sms();
+    aa.pages_per_split = std::max(1, (max_pages + kMaxSplits - 1) / kMaxSplits);   // unused by the kernel
+  } else if (use_tc) {   // per-request chunks (attn_pick_chunk_tc caps them at 8 = kMaxSplits)
+    aa.pages_per_split = attn_pick_chunk_tc(B, KV, max_pages);
+    aa.per_req = 1;
+    aa.row_req = pa.row_req;
+  } else {
+    aa.n_splits = std::min(kMaxSplits, attn_pick_splits(B, KV, max_pages));
+    aa.pages_per_split = std::max(1, (max_pages + aa.n_splits - 1) / aa.n_splits);
+  }
+  aa.n_splits = aa.per_req == 2 ? kMaxSplits : std::max(1, (max_pages + aa.pages_per_split - 1) / aa.pages_per_split);
+  if (aa.n_splits > kMaxSplits) return SPECEDGE_E_UNSUPPORTED;
   aa.max_rows = (in->max_nodes + 1) * G;
   aa.opart = (float*)P(w.opart);
   aa.mpart = (float*)P(w.mpart);
@@ -325,7 +361,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     { KTimer _t(K_ROPE, st); CK(qkv_rope_launch(ra, st, &launches)); }
     aa.layer = l;
     if (use_tc) {
-      { KTimer _t(K_ATTN, st); CK(attention_tc_launch(aa, B, aa.n_splits == 1 ? O : nullptr, nullptr, st, &launches)); }
+      { KTimer _t(K_ATTN, st); CK(attention_tc_launch(aa, B, O, nullptr, st, &launches)); }
       if (aa.n_splits > 1) { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
     } else {
       { KTimer _t(K_ATTN, st); CK(attention_launch(aa, B, st, &launches)); }
@@ -1325,7 +1361,8 @@ specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_pr
   a.R = S;
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
   if (attention_tc_supported(hd, G)) {
-    CK(attention_tc_launch(a, 1, nullptr, n_splits == 1 ? o : nullptr, st, nullptr));
+    a.per_req = 1;   // row_req = nullptr: one request
+    CK(attention_tc_launch(a, 1, nullptr, o, st, nullptr));
     if (n_splits > 1) CK(attn_combine_launch(a, nullptr, o, st, nullptr));
   } else {
     CK(attention_launch(a, 1, st, nullptr));

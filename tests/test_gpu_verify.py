@@ -364,3 +364,52 @@ def test_full_width_two_layer_slice_matches_oracle(api):
     finally:
         pool.close()
         model.close()
+
+
+def test_long_ragged_contexts_chunked_attention_matches_oracle(api):
+    """Long contexts (>= 64 pages) switch the tcgen05 attention to per-request chunks
+    (attn_pick_chunk_tc): a 7000-token request spans 8 chunks combined by k_attn_combine, a
+    200-token one stays a single chunk written final by the attention kernel, in the same launch.
+    Random-filled caches (gen_kv_fill on the oracle side), every slot's target compared."""
+    shape = SMALL128
+    rng = np.random.default_rng(909)
+    ctx = [4500, 200, 7000, 4100, 64]
+    B = len(ctx)
+    W = Weights(shape, 3)
+    model = api.Model(shape, 3, max_position=8192)
+    pool = api.KVPool(model, sum((c + 127) // 64 for c in ctx) + 8, B)
+    try:
+        hs, sessions = [], []
+        for r in range(B):
+            h = pool.alloc(ctx[r] + 64)
+            pool.fill_random(h, ctx[r] - 1, 4321, r)
+            hs.append(h)
+            c = Cache(shape)
+            for l in range(shape.n_layers):
+                c.k[l] = gen_kv_fill(4321, r, l, 0, ctx[r] - 1, shape.n_kv, shape.head_dim)
+                c.v[l] = gen_kv_fill(4321, r, l, 1, ctx[r] - 1, shape.n_kv, shape.head_dim)
+            sessions.append(OV.Session(c, int(rng.integers(0, shape.vocab)), 2000 + r))
+        trees = [pooled_tree(rng, n, 5, 3, shape.vocab) for n in (16, 32, 8, 63, 1)]
+        ws = model.workspace(B, sum(t.n + 1 for t in trees), 7100)
+        batch = api.Batch.from_host(hs, ctx, [s.last_token for s in sessions], [s.session_id for s in sessions],
+                                    [0] * B, trees, max_context_len=7100)
+        out = api.verify(model, pool, batch, ws, auto_commit=False)
+        g = split_outputs(out, batch)
+        logits_gpu = api.debug_last_logits(model, ws, batch).cpu().numpy()
+        refs = OV.verify_batch(W, [OV.Request(sessions[r], trees[r].parent, trees[r].token) for r in range(B)],
+                               auto_commit=False)
+        ref_all = np.concatenate([o.logits for o in refs])
+        d = np.abs(logits_gpu - ref_all)
+        assert np.quantile(d, 0.999) <= LOGIT_TOL, float(np.quantile(d, 0.999))
+        off = 0
+        for r in range(B):
+            o = refs[r]
+            eps = float(d[off:off + trees[r].n + 1].max())
+            off += trees[r].n + 1
+            sure = top2_margin(o.logits) > max(MARGIN, 2 * eps)
+            assert np.array_equal(g["row_target"][r][sure], o.row_target[sure]), r
+            assert g["status"][r] == 0
+            compare_outcome(o, o.logits, g, r, eps)
+    finally:
+        pool.close()
+        model.close()
