@@ -30,7 +30,7 @@ EXPORTS = [
     "specedge_model_tp_info", "specedge_calibrate_draft_depth", "specedge_scheduler_create",
     "specedge_scheduler_destroy", "specedge_scheduler_admit", "specedge_scheduler_plan",
     "specedge_scheduler_complete", "specedge_scheduler_observe", "specedge_scheduler_state",
-    "specedge_draft_tree",
+    "specedge_draft_tree", "specedge_tp_fused_enable",
 ]
 KERNEL_KINDS = ["prep", "embed", "rmsnorm", "gemm_qkv", "attention", "attn_combine", "gemm_o", "gemm_gateup",
                 "gemm_down", "gemm_lmhead", "lm_reduce", "walk", "commit", "qkv_rope"]
@@ -106,6 +106,7 @@ def load(path: str = LIB_PATH):
         "specedge_tp_unique_id": [P],
         "specedge_model_create_tp": [C.POINTER(ModelConfig), U64, I32, I32, I32, P, C.POINTER(P)],
         "specedge_model_tp_info": [P, P, P, P, P],
+        "specedge_tp_fused_enable": [P, I32, P],
         "specedge_calibrate_draft_depth": [C.c_double, C.c_double, C.c_double],
         "specedge_scheduler_create": [C.POINTER(SchedulerConfig), C.POINTER(P)],
         "specedge_scheduler_destroy": [P],

@@ -80,6 +80,11 @@ class Model:
         self.n_heads_local = shape.n_heads // tp_size
         self.n_kv_local = shape.n_kv // tp_size
 
+    def tp_fused_enable(self, max_rows: int, stream=None):
+        """NEXT-F4: collective (every rank, same max_rows) — fuse the O / down GEMMs with the
+        reduce-scatter of their fp32 updates over NVLink peer memory (specedge_tp_fused_enable)."""
+        L.check(self.lib.specedge_tp_fused_enable(self.h, max_rows, _stream(stream)), "tp_fused_enable")
+
     def close(self):
         if self.h:
             self.lib.specedge_model_destroy(self.h)

@@ -43,20 +43,17 @@ namespace {
 
 constexpr int kWarps = 11;      // producer, MMA (unit 0), 2 units x 4 softmax/epilogue warps, MMA (unit 1)
 constexpr int kThreads = kWarps * 32;
-// K and V rings (one 64-key sub-tile of K, resp. V, per slot): whatever the 227 KB of shared
-// memory leaves after NQ Q tiles and ~3 KB of barriers / merge scalars, split 1:2 between K and V
-// (hd 128: 4 K + 8 V slots with one Q tile, 3 + 7 with two; hd 64: 8 + 16).  K is released as
-// soon as its QK has completed, V only after PV, i.e. after the softmax: separate rings keep the
-// K slots turning over and leave more of the shared memory to loads in flight — at a DRAM latency
-// of ~1.5 us under load, the bytes in flight per SM set the stream rate of a long-context CTA.
+// K/V ring depth (64-key sub-tiles): whatever the 227 KB of shared memory leaves after NQ Q tiles
+// and ~3 KB of barriers / masks / merge scalars (hd 128: 5 stages with two Q tiles, 6 with one;
+// hd 64: 12).  The ring is the only source of memory-level parallelism: at steady state the two
+// units hold about four sub-tiles, the rest are in flight.
 constexpr int kSmemMax = 227 * 1024;
 constexpr int kSmemAux = 3 * 1024;
-__host__ __device__ constexpr int ring_slots(int hd, int nq) {
-  return (kSmemMax - kSmemAux - nq * 128 * hd * 2) / (64 * hd * 2) > 24
-             ? 24
-             : (kSmemMax - kSmemAux - nq * 128 * hd * 2) / (64 * hd * 2);
+__host__ __device__ constexpr int ring_stages(int hd, int nq) {
+  return (kSmemMax - kSmemAux - nq * 128 * hd * 2) / (2 * 64 * hd * 2) > 12
+             ? 12
+             : (kSmemMax - kSmemAux - nq * 128 * hd * 2) / (2 * 64 * hd * 2);
 }
-__host__ __device__ constexpr int k_slots(int hd, int nq) { return ring_slots(hd, nq) / 3 < 2 ? 2 : ring_slots(hd, nq) / 3; }
 #ifndef SPECEDGE_EMU8
 #define SPECEDGE_EMU8 0
 #endif
@@ -190,23 +187,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int KB = HD / 64;                       // 64-element hd blocks
   constexpr uint32_t QT_BYTES = 128 * HD * 2;       // one 128-row M-tile of Q
   constexpr uint32_t PG_BYTES = 64 * HD * 2;        // K (or V) of one 64-key sub-tile
-  constexpr int NKR = k_slots(HD, NQ);                 // K ring slots
-  constexpr int NVR = ring_slots(HD, NQ) - NKR;        // V ring slots
+  constexpr int NST = ring_stages(HD, NQ);
   const AttnArgs& a = ta.a;
   // 2 Q tiles + 5 K/V sub-tile stages = 224 KB of the 227 KB: the 1024-B alignment SW128 needs
   // comes from the dynamic-smem base itself (no static smem in this kernel); checked below.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sQ = smem_raw;                           // [2 units][KB][128 rows][128 B]
-  uint8_t* sK = sQ + NQ * QT_BYTES;                 // [NKR][KB][64 keys][128 B]
-  uint8_t* sV = sK + NKR * PG_BYTES;                // [NVR][KB][64 keys][128 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NVR * PG_BYTES);
+  uint8_t* sK = sQ + NQ * QT_BYTES;                 // [NST][KB][64 keys][128 B]
+  uint8_t* sV = sK + NST * PG_BYTES;                // [NST][KB][64 keys][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NST * PG_BYTES);
   uint64_t* q_full = bars;              // [1]
   uint64_t* q_empty = bars + 1;         // [1]
-  uint64_t* k_full = bars + 2;          // [NKR]
-  uint64_t* k_empty = k_full + NKR;     // [NKR]
-  uint64_t* v_full = k_empty + NKR;     // [NVR]
-  uint64_t* v_empty = v_full + NVR;     // [NVR]
-  uint64_t* s_full = v_empty + NVR;     // [2 units][2 buffers]
+  uint64_t* kv_full = bars + 2;         // [NST]
+  uint64_t* kv_empty = kv_full + NST;   // [NST]
+  uint64_t* s_full = kv_empty + NST;    // [2 units][2 buffers]
   uint64_t* p_full = s_full + 4;        // [2][2]
   uint64_t* pv_done = p_full + 4;       // [2][2]
   uint64_t* o_full = pv_done + 4;       // [1]
@@ -347,13 +341,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmTree);
     mbar_init(q_full, 1);
     mbar_init(q_empty, 2);   // one commit per MMA issuer
-    for (int i = 0; i < NKR; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 2);
-    }
-    for (int i = 0; i < NVR; ++i) {
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 2);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 2);
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
@@ -399,8 +389,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------------------- TMA producer
     if (elect_one()) {
-      uint32_t nld = 0;             // sub-tiles loaded so far (ring positions)
-      uint32_t gp = 0;              // gp: passes over all items (barrier phases)
+      int stage = 0;
+      uint32_t phase = 0, gp = 0;   // gp: passes over all items (barrier phases)
       bool scratch = false;         // the last pass merges replicas through the ring (epilogue)
       uint32_t nscr = 0;            // scr_done completions consumed
       Cursor cu = cursor0();
@@ -445,9 +435,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int sj = sub_of(p, j);
           const int page = next_page;   // page ids are read one sub-tile ahead of their use
           if (j + 1 < nsub && sub_of(p, j + 1) < npg) next_page = __ldg(pages + sub_of(p, j + 1));
-          const uint32_t ks = nld % NKR, vs = nld % NVR;
-          uint8_t* dk = sK + ks * PG_BYTES;
-          uint8_t* dv = sV + vs * PG_BYTES;
+          mbar_wait(&kv_empty[stage], phase ^ 1);
+          mbar_expect_tx(&kv_full[stage], 2 * PG_BYTES);
+          uint8_t* dk = sK + stage * PG_BYTES;
+          uint8_t* dv = sV + stage * PG_BYTES;
           int rk, rv;
           const CUtensorMap* tm;
           if (sj < npg) {
@@ -460,14 +451,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             rv = ((a.layer * 2 + 1) * a.KV + g) * a.R_cap + row0 + 64 * th;
             tm = &tmTree;
           }
-          mbar_wait(&k_empty[ks], ((nld / NKR) & 1) ^ 1);
-          mbar_expect_tx(&k_full[ks], PG_BYTES);
-          for (int kb = 0; kb < KB; ++kb) tma_load_2d(dk + kb * 64 * 128, tm, &k_full[ks], kb * 64, rk);
-          mbar_wait(&v_empty[vs], ((nld / NVR) & 1) ^ 1);
-          mbar_expect_tx(&v_full[vs], PG_BYTES);
-          for (int kb = 0; kb < KB; ++kb) tma_load_2d(dv + kb * 64 * 128, tm, &v_full[vs], kb * 64, rv);
+          for (int kb = 0; kb < KB; ++kb) {
+            tma_load_2d(dk + kb * 64 * 128, tm, &kv_full[stage], kb * 64, rk);
+            tma_load_2d(dv + kb * 64 * 128, tm, &kv_full[stage], kb * 64, rv);
+          }
           if (gp == 0) TRACE(j);
-          ++nld;
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
       }
@@ -493,11 +482,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // QK of this unit's k-th sub-tile of the pass into S buffer (kc + k) & 1
         auto issue_qk = [&](int k) {
           const uint32_t gi = sub_base + (uint32_t)j_of(p, u, k);
-          mbar_wait(&k_full[gi % NKR], (gi / NKR) & 1);
+          mbar_wait(&kv_full[gi % NST], (gi / NST) & 1);
           if (gp == 0 && k < 64) TRACE(640 + 64 * u + k);
           tc_fence_after();
           const uint32_t qaddr = smem_u32(sQ + (pr ? u : 0) * QT_BYTES);
-          const uint32_t kaddr = smem_u32(sK + (gi % NKR) * PG_BYTES);
+          const uint32_t kaddr = smem_u32(sK + (gi % NST) * PG_BYTES);
           const uint32_t b = (kc + k) & 1;
           const uint32_t s_tm = tmem + u * 256 + b * 64;
 #pragma unroll
@@ -507,10 +496,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_mma_f16(s_tm, umma_desc_sw128(qaddr + kb * 16384 + kk * 32),
                          umma_desc_sw128(kaddr + kb * 8192 + kk * 32), id_qk, (kb | kk) != 0);
           tc_commit(&s_full[u * 2 + b]);
-          // k_empty / v_empty take 2 arrivals per use: one per unit in a pair pass, both from the
-          // only reader in a single pass
-          tc_commit(&k_empty[gi % NKR]);
-          if (!pr) tc_commit(&k_empty[gi % NKR]);
           if (k == nk - 1) tc_commit(q_empty);   // last QK of the pass: Q may be reloaded
         };
         for (int k = 0; k < 2 && k < nk; ++k) issue_qk(k);
@@ -522,9 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (k == 0) mbar_wait(o_empty, (gp & 1) ^ 1);   // the previous pass's O has been drained
           tc_fence_after();
           const uint32_t gi = sub_base + (uint32_t)j_of(p, u, k);
-          mbar_wait(&v_full[gi % NVR], (gi / NVR) & 1);
-          tc_fence_after();
-          const uint32_t vaddr = smem_u32(sV + (gi % NVR) * PG_BYTES);
+          const uint32_t vaddr = smem_u32(sV + (gi % NST) * PG_BYTES);
           const uint32_t p_tm = tmem + u * 256 + b * 64;
           const uint32_t o_tm = tmem + u * 256 + 128;
 #pragma unroll
@@ -533,8 +516,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_mma_ts(o_tm, p_tm + kk * 8, bd, id_pv, (k | kk) != 0);
           }
           tc_commit(&pv_done[u * 2 + b]);
-          tc_commit(&v_empty[gi % NVR]);
-          if (!pr) tc_commit(&v_empty[gi % NVR]);
+          // kv_empty takes 2 arrivals per use: one per unit in a pair pass, both from the only
+          // reader in a single pass
+          tc_commit(&kv_empty[gi % NST]);
+          if (!pr) tc_commit(&kv_empty[gi % NST]);
           // S buffer b takes sub-tile k+2 (in-order execution: after PV(k) has read P(k))
           if (k + 2 < nk) issue_qk(k + 2);
         }
@@ -924,9 +909,9 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
   if (getenv("SPECEDGE_ATTN_TRACE") && !trace) cudaMalloc(&trace, 1024 * 8);
   TcArgs ta{a, O, O_f32, spm, pf, trace};
   if (trace) cudaMemsetAsync(trace, 0, 1024 * 8, st);
-  constexpr int NH = ring_slots(HD, NQ);
-  const size_t smem = (size_t)NQ * 128 * HD * 2 + (size_t)NH * 64 * HD * 2 + 8 * (18 + 2 * NH) + 512 * 4 + 16;
-  static_assert((size_t)NQ * 128 * HD * 2 + (size_t)NH * 64 * HD * 2 + 8 * (18 + 2 * NH) + 512 * 4 + 16 <=
+  constexpr int NST = ring_stages(HD, NQ);
+  const size_t smem = (size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 16;
+  static_assert((size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 16 <=
                     (size_t)kSmemMax, "attention smem");
   static bool attr = false;
   if (!attr) {

@@ -73,6 +73,17 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
             if (j < ncol && row < a.R)
               a.out_f32[(size_t)(row >> 1) * a.ldo + feat] = __uint_as_float(v[j]) + __uint_as_float(v[j + 1]);
           }
+        } else if (a.tp_fused) {
+          // NEXT-F4: straight into the owning rank's receive slot (NVLink store when remote)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int row = row_base + j;
+            if (j < ncol && row < a.R) {
+              const int o = row / a.rows_per_rank;
+              a.peer_out[o][(size_t)a.tp_src * a.slot_stride + (size_t)(row - o * a.rows_per_rank) * a.ldo + feat] =
+                  __uint_as_float(v[j]);
+            }
+          }
         } else {
           float* out = a.out_f32 + (size_t)sk * a.split_stride;   // K-split sk's partial
 #pragma unroll

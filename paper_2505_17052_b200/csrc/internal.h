@@ -47,6 +47,8 @@ enum GemmMode : int {
   EPI_PQ2 = 6,     // NEXT-F2 pass 2: per-tile Gumbel-max of log max(0, p - q) + p(child token)
 };
 
+constexpr int kMaxFusedTp = 4;   // NEXT-F4: ranks of the fused GEMM -> reduce-scatter
+
 struct GemmArgs {
   int M, R, K;            // weight rows (features), activation rows, reduction length
   int BN, n_tiles_n, n_tiles_m, num_kb, stages, tmem_cols;
@@ -59,6 +61,11 @@ struct GemmArgs {
   // EPI_F32 / EPI_RESID (fp32 residual stream)
   float* out_f32;
   int ldo;
+  // EPI_F32 with tp_fused (NEXT-F4): row r goes to rank o = r / rows_per_rank, slot [tp_src] of
+  // its receive buffer: peer_out[o] + tp_src * slot_stride + (r - o * rows_per_rank) * ldo
+  int tp_fused, tp_src, rows_per_rank;
+  size_t slot_stride;
+  float* peer_out[kMaxFusedTp];
   // EPI_SWIGLU / EPI_QKV(q part)
   bf16* out_bf16;
   int ld_out;
@@ -292,6 +299,11 @@ cudaError_t set_len_launch(int* cache_len, const SetLenArgs& a, cudaStream_t st)
 // tensor parallelism (tp.cu): NCCL resolved at run time
 constexpr int kMaxTp = 16;
 bool tp_available();
+// NEXT-F4 fused GEMM -> reduce-scatter over NVLink peer memory (tp.cu)
+int tp_fused_enable(specedge_model* m, int max_rows, cudaStream_t st);
+cudaError_t tp_fused_signal(specedge_model* m, cudaStream_t st, int* launches);
+cudaError_t tp_fused_wait(specedge_model* m, cudaStream_t st, int* launches);
+void tp_fused_close(specedge_model* m);
 int tp_unique_id(uint8_t* out128);
 int tp_comm_init(void** comm, const uint8_t* id128, int rank, int size);
 void tp_comm_destroy(void* comm);
@@ -318,6 +330,17 @@ struct specedge_model {
   void* nccl = nullptr;         // ncclComm_t when tp_size > 1
   float* tp_gather = nullptr;   // [tp_size][R_max][2] (score, id) all-gather buffer
   int tp_gather_rows = 0;
+  // NEXT-F4 (tp.cu): receive buffers [2][tp][Rl][d] fp32 + flag words [tp] (this rank's), the
+  // peers' mappings, the epoch of the last signalled collective
+  int tp_fused_rows = 0;                 // capacity (rows); 0 = fused path off
+  size_t tp_fused_slot = 0;              // floats per [src] slot = Rl * d
+  float* tp_recv = nullptr;
+  float* tp_peer_recv[se::kMaxFusedTp] = {};
+  unsigned long long* tp_flags = nullptr;
+  unsigned long long** tp_peer_flags_dev = nullptr;
+  unsigned long long tp_epoch = 0;
+  int tp_fused_buf = 0;                  // receive buffer of the next collective
+  std::vector<void*> tp_ipc_opened;
   se::bf16* embed = nullptr;
   se::bf16* lm_head = nullptr;
   se::bf16* g_final = nullptr;

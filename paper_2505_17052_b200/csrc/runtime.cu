@@ -5,6 +5,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -94,10 +95,20 @@ struct KTimer {
   }
 };
 
-#define CK(x)                                   \
-  do {                                          \
-    cudaError_t _e = (x);                       \
-    if (_e != cudaSuccess) return SPECEDGE_E_CUDA; \
+// SPECEDGE_DEBUG=1: name the failing call on stderr
+thread_local int g_dbg_layer = -1;
+bool ck_debug() {
+  static const bool on = getenv("SPECEDGE_DEBUG") && getenv("SPECEDGE_DEBUG")[0] == '1';
+  return on;
+}
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    cudaError_t _e = (x);                                                                         \
+    if (_e != cudaSuccess) {                                                                      \
+      if (ck_debug()) fprintf(stderr, "libspecedge: %s:%d (layer %d) %s -> %s\n", __FILE__, __LINE__, \
+                              g_dbg_layer, #x, cudaGetErrorString(_e));                           \
+      return SPECEDGE_E_CUDA;                                                                     \
+    }                                                                                             \
   } while (0)
 
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -323,10 +334,45 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     }
     return ns;
   };
+  // NEXT-F4: row-parallel GEMM whose epilogue stores every row into its owner's receive slot
+  // over NVLink (tp.cu), then the epoch signal; the owner's norm_rows waits and sums the tp slots
+  const bool fused = tp && m->tp_fused_rows >= R && m->tp_size <= kMaxFusedTp;
+  const float* fused_src = nullptr;   // receive buffer holding the pending row-parallel partials
+  auto f32_gemm_fused = [&](int kind, const CUtensorMap& tm, const void* Xin, int Mrows, int K) -> int {
+    GemmArgs g{};
+    g.M = Mrows;
+    g.R = R;
+    g.K = K;
+    g.out_f32 = Y;
+    g.ldo = Mrows;
+    g.max_splits = 1;
+    g.split_stride = y_stride;
+    g.tp_fused = 1;
+    g.tp_src = m->tp_rank;
+    g.rows_per_rank = Rl;
+    g.slot_stride = m->tp_fused_slot;
+    const size_t boff = (size_t)m->tp_fused_buf * m->tp_size * m->tp_fused_slot;
+    for (int p = 0; p < m->tp_size; ++p) g.peer_out[p] = m->tp_peer_recv[p] + boff;
+    {
+      KTimer _t(kind, st);
+      if (gemm_launch(EPI_F32, tm, Xin, g, st, &launches) != cudaSuccess) return -1;
+    }
+    if (tp_fused_signal(m, st, &launches) != cudaSuccess) return -1;
+    fused_src = m->tp_recv + boff;
+    m->tp_fused_buf ^= 1;
+    return m->tp_size;
+  };
   // residual add + RMSNorm of this rank's rows (all rows when tp_size == 1), then under TP the
   // bf16 all-gather of the normalised rows for the next column-parallel GEMM
   auto norm_rows = [&](int nY, const bf16* gain, bf16* out, int split) -> specedge_status {
-    {
+    if (fused_src) {   // the tp slots of this rank's rows, summed in rank order
+      CK(tp_fused_wait(m, st, &launches));
+      KTimer _t(K_RMSNORM, st);
+      if (nloc)
+        CK(rmsnorm_launch(X + (size_t)r0 * c.d, fused_src, nY, m->tp_fused_slot, gain,
+                          out + (size_t)(split ? 2 : 1) * r0 * c.d, nloc, c.d, c.eps, st, &launches, split));
+      fused_src = nullptr;
+    } else {
       KTimer _t(K_RMSNORM, st);
       if (nloc)
         CK(rmsnorm_launch(X + (size_t)r0 * c.d, Y + (size_t)r0 * c.d, nY, y_stride, gain,
@@ -339,6 +385,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     return SPECEDGE_OK;
   };
   for (int l = 0; l < c.n_layers; ++l) {
+    g_dbg_layer = l;
     const auto& Lw = m->layers[l];
     { const specedge_status ns = norm_rows(pendingY, Lw.g_attn, Hn, 0); if (ns != SPECEDGE_OK) return ns; }
     const int sq = f32_gemm(K_QKV, Lw.tm_qkv, Hn, (H + 2 * KV) * hd, c.d, false);
@@ -367,7 +414,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
       { KTimer _t(K_ATTN, st); CK(attention_launch(aa, B, st, &launches)); }
       { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
     }
-    const int so = f32_gemm(K_O, Lw.tm_o, O, c.d, H * hd, true);
+    const int so = fused ? f32_gemm_fused(K_O, Lw.tm_o, O, c.d, H * hd) : f32_gemm(K_O, Lw.tm_o, O, c.d, H * hd, true);
     if (so < 0) return SPECEDGE_E_CUDA;
     { const specedge_status ns = norm_rows(so, Lw.g_mlp, Hn, 0); if (ns != SPECEDGE_OK) return ns; }
     GemmArgs gu{};
@@ -377,7 +424,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gu.out_bf16 = Mb;
     gu.ld_out = c.ffn;
     { KTimer _t(K_GU, st); CK(gemm_launch(EPI_SWIGLU, Lw.tm_gu, Hn, gu, st, &launches)); }
-    pendingY = f32_gemm(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn, true);
+    pendingY = fused ? f32_gemm_fused(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn) : f32_gemm(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn, true);
     if (pendingY < 0) return SPECEDGE_E_CUDA;
   }
   int* y = (int*)P(w.y);
@@ -776,9 +823,21 @@ specedge_status specedge_model_tp_info(const specedge_model* m, int32_t* tp_rank
   return SPECEDGE_OK;
 }
 
+specedge_status specedge_tp_fused_enable(specedge_model* m, int32_t max_rows, void* stream) {
+  if (!m || m->tp_size < 2 || m->tp_size > kMaxFusedTp || max_rows <= 0) return SPECEDGE_E_INVALID;
+  CK(cudaSetDevice(m->device));
+  const int r = tp_fused_enable(m, max_rows, (cudaStream_t)stream);
+  if (r == 0) return SPECEDGE_OK;
+  if (r == -1 || r == -2) return SPECEDGE_E_INVALID;
+  m->tp_fused_rows = 0;
+  return SPECEDGE_E_CUDA;
+}
+
 specedge_status specedge_model_destroy(specedge_model* m) {
   if (!m) return SPECEDGE_E_INVALID;
   cudaSetDevice(m->device);
+  cudaDeviceSynchronize();
+  tp_fused_close(m);
   if (m->nccl) tp_comm_destroy(m->nccl);
   for (auto& g : m->graphs) cudaGraphExecDestroy(g.exec);
   if (m->gstream) cudaStreamDestroy(m->gstream);

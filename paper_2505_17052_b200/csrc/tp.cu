@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <vector>
 
 namespace se {
 
@@ -144,6 +145,129 @@ cudaError_t tp_argmax_gather(int* y, float* score, int R, float* gather, int tp,
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
+}
+
+
+
+// ---------------------------------------------------------------------------------------------
+// NEXT-F4: GEMM -> reduce-scatter fused over NVLink peer memory.
+// Every rank's row-parallel GEMM (O, down) stores each fp32 output row straight into the
+// receive buffer of the rank that owns the row (sequence-parallel residual: rank k owns rows
+// [k*Rl, (k+1)*Rl)), slot [src rank], through CUDA IPC mappings of the peers' buffers — the
+// transfer rides on the GEMM's own epilogue stores, tile by tile, instead of a separate NCCL
+// reduce-scatter after the GEMM.  The owner sums the tp slots in rank order inside its RMSNorm
+// (the same kernel that sums K-split partials), so the result is deterministic.
+//
+// Ordering: after the GEMM, k_tp_signal (one thread per peer) publishes an epoch with a
+// system-scope release store into every peer's flag word [src]; before the RMSNorm, k_tp_wait
+// spins with acquire loads until every peer's flag holds that epoch (bounded: traps after ~20 s
+// rather than hang).  Two receive buffers alternate per collective: a rank writes buffer b for
+// op n+2 only after it consumed op n+1, which every peer sent after consuming op n from b.
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+__global__ void k_tp_signal(unsigned long long* const* __restrict__ peer_flags, int tp, int rank,
+                            unsigned long long epoch) {
+  const int p = threadIdx.x;
+  __threadfence_system();
+  if (p < tp) {
+    unsigned long long* f = peer_flags[p] + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+  }
+}
+
+__global__ void k_tp_wait(const unsigned long long* __restrict__ my_flags, int tp, unsigned long long epoch) {
+  const int p = threadIdx.x;
+  if (p < tp) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + p) : "memory");
+      if (v >= epoch) break;
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) __trap();   // a peer never arrived: fail, do not hang the GPU
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+cudaError_t tp_fused_signal(specedge_model* m, cudaStream_t st, int* launches) {
+  ++m->tp_epoch;
+  if (launches) ++*launches;
+  k_tp_signal<<<1, 32, 0, st>>>(m->tp_peer_flags_dev, m->tp_size, m->tp_rank, m->tp_epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t tp_fused_wait(specedge_model* m, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  k_tp_wait<<<1, 32, 0, st>>>(m->tp_flags, m->tp_size, m->tp_epoch);
+  return cudaGetLastError();
+}
+
+// Collective (every rank, same arguments): receive buffers for up to max_rows rows, IPC handles
+// exchanged with an NCCL all-gather, peers' buffers and flag words mapped.
+int tp_fused_enable(specedge_model* m, int max_rows, cudaStream_t st) {
+  const int tp = m->tp_size;
+  if (tp < 2 || tp > kMaxFusedTp || max_rows <= 0 || !m->nccl) return -1;
+  if (m->tp_fused_rows >= max_rows) return 0;
+  if (m->tp_fused_rows) return -2;   // already enabled with a smaller capacity: not resizable
+  const int Rl = (max_rows + tp - 1) / tp;
+  const size_t slot = (size_t)Rl * m->cfg.d;   // floats per [src] slot
+  const size_t bytes = 2 * (size_t)tp * slot * 4 + 256;
+  char* base = nullptr;
+  if (cudaMalloc(&base, bytes) != cudaSuccess) return -3;
+  m->allocs.push_back(base);
+  cudaMemset(base, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, base) != cudaSuccess) return -4;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle");
+  char* dh = nullptr;
+  if (cudaMalloc(&dh, 64 * (size_t)tp) != cudaSuccess) return -3;
+  cudaMemcpy(dh + 64 * (size_t)m->tp_rank, &h, 64, cudaMemcpyHostToDevice);
+  if (nccl().AllGather(dh + 64 * (size_t)m->tp_rank, dh, 64, ncclUint8, reinterpret_cast<ncclComm_t>(m->nccl), st) !=
+      ncclSuccess)
+    return -5;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -5;
+  std::vector<cudaIpcMemHandle_t> hs(tp);
+  cudaMemcpy(hs.data(), dh, 64 * (size_t)tp, cudaMemcpyDeviceToHost);
+  cudaFree(dh);
+  unsigned long long* flags_host[kMaxFusedTp];
+  for (int p = 0; p < tp; ++p) {
+    char* pb = base;
+    if (p != m->tp_rank) {
+      void* q = nullptr;
+      if (cudaIpcOpenMemHandle(&q, hs[p], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return -6;
+      m->tp_ipc_opened.push_back(q);
+      pb = static_cast<char*>(q);
+    }
+    m->tp_peer_recv[p] = reinterpret_cast<float*>(pb);
+    flags_host[p] = reinterpret_cast<unsigned long long*>(pb + 2 * (size_t)tp * slot * 4);
+  }
+  m->tp_recv = reinterpret_cast<float*>(base);
+  m->tp_flags = reinterpret_cast<unsigned long long*>(base + 2 * (size_t)tp * slot * 4);
+  if (cudaMalloc(&m->tp_peer_flags_dev, sizeof(flags_host)) != cudaSuccess) return -3;
+  m->allocs.push_back(m->tp_peer_flags_dev);
+  cudaMemcpy(m->tp_peer_flags_dev, flags_host, sizeof(flags_host), cudaMemcpyHostToDevice);
+  m->tp_fused_slot = slot;
+  m->tp_fused_rows = max_rows;
+  // barrier: every rank has mapped every peer before anyone may write into a peer
+  char* one = nullptr;
+  if (cudaMalloc(&one, 8) != cudaSuccess) return -3;
+  const bool ok = nccl().AllReduce(one, one, 1, ncclUint64, ncclSum, reinterpret_cast<ncclComm_t>(m->nccl), st) ==
+                  ncclSuccess;
+  cudaStreamSynchronize(st);
+  cudaFree(one);
+  return ok ? 0 : -5;
+}
+
+void tp_fused_close(specedge_model* m) {
+  for (void* q : m->tp_ipc_opened) cudaIpcCloseMemHandle(q);
+  m->tp_ipc_opened.clear();
 }
 
 }  // namespace se

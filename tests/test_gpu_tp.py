@@ -47,12 +47,14 @@ def _setup(seed=SEED):
     return shape, W, prompts, sessions, trees
 
 
-def _worker(rank, nccl_id, mode, temperature, q):
+def _worker(rank, nccl_id, mode, temperature, q, fused=False):
     try:
         torch.cuda.set_device(rank)
         from paper_2505_17052_b200 import api
         shape, W, prompts, sessions, trees = _setup()
         model = api.Model(shape, SEED, device=rank, max_position=4096, tp_rank=rank, tp_size=TP, nccl_id=nccl_id)
+        if fused:   # NEXT-F4: O / down GEMM epilogues store straight into the owner's receive slots
+            model.tp_fused_enable(4 * 65)
         cap = max(len(p) for p in prompts) + 256
         pool = api.KVPool(model, ((cap + 63) // 64) * len(prompts) + 4, len(prompts) + 4)
         B = len(prompts)
@@ -85,13 +87,13 @@ def _worker(rank, nccl_id, mode, temperature, q):
         q.put((rank, RuntimeError(f"rank {rank}: {e}\n{traceback.format_exc()}")))
 
 
-def _run_tp(mode, temperature):
+def _run_tp(mode, temperature, fused=False):
     import torch.multiprocessing as mp
     from paper_2505_17052_b200 import api
     nccl_id = api.tp_unique_id()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, nccl_id, mode, temperature, q)) for r in range(TP)]
+    procs = [ctx.Process(target=_worker, args=(r, nccl_id, mode, temperature, q, fused)) for r in range(TP)]
     for p in procs:
         p.start()
     res = {}
@@ -105,11 +107,13 @@ def _run_tp(mode, temperature):
     return res
 
 
-@pytest.mark.parametrize("mode,temperature", [("greedy", 0.0), ("sample", 1.0)])
-def test_tp2_verify_matches_oracle(mode, temperature):
+@pytest.mark.parametrize("mode,temperature,fused", [("greedy", 0.0, False), ("sample", 1.0, False),
+                                                   ("greedy", 0.0, True), ("sample", 1.0, True)])
+def test_tp2_verify_matches_oracle(mode, temperature, fused):
+    """fused: NEXT-F4 GEMM -> reduce-scatter over NVLink peer memory instead of NCCL for C1/C2."""
     _needs_gpus(TP)
     os.environ.setdefault("NCCL_DEBUG", "WARN")
-    res = _run_tp(mode, temperature)
+    res = _run_tp(mode, temperature, fused)
     shape, W, prompts, sessions, trees = _setup()
     B = len(prompts)
     refs = OV.verify_batch(W, [OV.Request(sessions[r], trees[r].parent, trees[r].token) for r in range(B)],

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 from oracle import verify as OV  # noqa: E402
 from oracle.law import closed_form_law, slot_probs  # noqa: E402
 from oracle.model import Weights, Cache, gen_kv_fill, lm_logits, tree_forward  # noqa: E402
-from synth.configs import TINY, TINY_V16, TINY_MHA, SMALL128, LLAMA3_8B_2L  # noqa: E402
+from synth.configs import TINY, TINY_V16, TINY_MHA, SMALL128, LLAMA3_8B_2L, ModelShape  # noqa: E402
 from synth.plant import plant, draw_accept_lengths  # noqa: E402
 from synth.trees import pooled_tree, random_tree, chain_tree, Tree  # noqa: E402
 from tests.gpu_helpers import (LOGIT_TOL, MARGIN, f16_bits_to_f64, compare_outcome,  # noqa: E402
@@ -366,12 +366,16 @@ def test_full_width_two_layer_slice_matches_oracle(api):
         model.close()
 
 
-def test_long_ragged_contexts_chunked_attention_matches_oracle(api):
-    """Long contexts (>= 64 pages) switch the tcgen05 attention to per-request chunks
-    (attn_pick_chunk_tc): a 7000-token request spans 8 chunks combined by k_attn_combine, a
-    200-token one stays a single chunk written final by the attention kernel, in the same launch.
+G8 = ModelShape("g8", 2, 512, 16, 2, 128, 1024, 2048, 1e-5, 500000.0)   # G = 8 (Llama-70B's group at TP 2)
+
+
+@pytest.mark.parametrize("shape,sizes", [(SMALL128, (16, 32, 8, 63, 1)), (G8, (64, 20, 64, 5, 1))])
+def test_long_ragged_contexts_chunked_attention_matches_oracle(api, shape, sizes):
+    """Long contexts (>= 64 pages) switch the tcgen05 attention to the persistent work-balanced
+    grid: a 7000-token request is cut into up to 8 chunks combined by k_attn_combine, a 200-token
+    one stays a single chunk written final by the attention kernel, in the same launch.  G = 8 with
+    64-node trees: 5 M-tiles per request = two pair passes and a replicated single pass per item.
     Random-filled caches (gen_kv_fill on the oracle side), every slot's target compared."""
-    shape = SMALL128
     rng = np.random.default_rng(909)
     ctx = [4500, 200, 7000, 4100, 64]
     B = len(ctx)
@@ -389,7 +393,7 @@ def test_long_ragged_contexts_chunked_attention_matches_oracle(api):
                 c.k[l] = gen_kv_fill(4321, r, l, 0, ctx[r] - 1, shape.n_kv, shape.head_dim)
                 c.v[l] = gen_kv_fill(4321, r, l, 1, ctx[r] - 1, shape.n_kv, shape.head_dim)
             sessions.append(OV.Session(c, int(rng.integers(0, shape.vocab)), 2000 + r))
-        trees = [pooled_tree(rng, n, 5, 3, shape.vocab) for n in (16, 32, 8, 63, 1)]
+        trees = [pooled_tree(rng, n, 5, 3, shape.vocab) for n in sizes]
         ws = model.workspace(B, sum(t.n + 1 for t in trees), 7100)
         batch = api.Batch.from_host(hs, ctx, [s.last_token for s in sessions], [s.session_id for s in sessions],
                                     [0] * B, trees, max_context_len=7100)

@@ -64,6 +64,7 @@ def test_api_errors_without_device(libpath):
     assert create_tp(ctypes.byref(ok), 1, 0, 0, 4, ctypes.cast(nid, ctypes.c_void_p), ctypes.byref(out)) == \
         _lib.E_UNSUPPORTED   # n_kv = 2 not divisible by 4
     assert lib.specedge_model_tp_info(None, None, None, None, None) == _lib.E_INVALID
+    assert lib.specedge_tp_fused_enable(None, 64, None) == _lib.E_INVALID
 
 
 def test_product_never_imports_oracle():
