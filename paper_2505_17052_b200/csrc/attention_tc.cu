@@ -680,16 +680,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t pb = (kg - 1) & 1;
               mbar_wait(&pv_done[u * 2 + pb], ((kg - 1) >> 1) & 1);
               tc_fence_after();
-              if (rescale) {
+              // tcgen05.ld/st are warp-collective (.sync.aligned): the whole warp runs the loop,
+              // rows without a rescale multiply by 1 (a per-lane branch here deadlocked the warp)
+              const float f = rescale ? alpha : 1.f;
 #pragma unroll 1
-                for (int c = 0; c < HD / 32; ++c) {
-                  uint32_t ov[32];
-                  tmem_ld_32x32b_x32(o_own + c * 32, ov);
-                  tmem_ld_wait();
+              for (int c = 0; c < HD / 32; ++c) {
+                uint32_t ov[32];
+                tmem_ld_32x32b_x32(o_own + c * 32, ov);
+                tmem_ld_wait();
 #pragma unroll
-                  for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-                  tmem_st_32x32b_x32(o_own + c * 32, ov);
-                }
+                for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * f);
+                tmem_st_32x32b_x32(o_own + c * 32, ov);
               }
             }
           };

@@ -7,6 +7,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
+#include <cstdio>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "libspecedge is written for sm_100a only"
@@ -99,7 +100,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++n == (1u << 28)) __trap();
+#ifdef SPECEDGE_HANG_DEBUG
+    // debug builds (build.py --define=SPECEDGE_HANG_DEBUG=1): report the stuck wait and go on
+    if (++n == (1u << 24)) {
+      printf("mbar timeout: block (%d,%d) thread %d bar 0x%x parity %u\n", blockIdx.x, blockIdx.y, threadIdx.x,
+             smem_u32(bar), parity);
+      return;
+    }
+#else
+    if (++n == (1u << 28)) __trap();   // a deadlock fails the launch instead of hanging the GPU
+#endif
   }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
