@@ -350,36 +350,53 @@ __global__ void k_attn_combine(const __grid_constant__ AttnArgs a, bf16* __restr
     ns = a.nch_tab[r * a.KV + (rh % a.H) / a.G];
     if (ns == 1) return;
   }
+  // every partial this lane needs is loaded in one round (ns <= kCombineMax): the kernel is a
+  // chain of dependent loads, not bandwidth
+  constexpr int kCombineMax = 8;
+  float mv[kCombineMax], lv[kCombineMax];
+  float4 ov[kCombineMax];
+  const int d = lane * 4;
+  const bool has_d = d < hd;
+#pragma unroll
+  for (int sp = 0; sp < kCombineMax; ++sp) {
+    const bool on = sp < ns;
+    mv[sp] = on ? a.mpart[sp * stride + rh] : -INFINITY;
+    lv[sp] = on ? a.lpart[sp * stride + rh] : 0.f;
+    ov[sp] = (on && has_d) ? *reinterpret_cast<const float4*>(a.opart + (sp * stride + rh) * hd + d)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float m = -INFINITY;
-  for (int sp = 0; sp < ns; ++sp) m = fmaxf(m, a.mpart[sp * stride + rh]);
+#pragma unroll
+  for (int sp = 0; sp < kCombineMax; ++sp) m = fmaxf(m, mv[sp]);
   const float mb = m == -INFINITY ? 0.f : m;
   float l = 0.f;
-  for (int sp = 0; sp < ns; ++sp) {
-    const float ms = a.mpart[sp * stride + rh];
-    if (ms != -INFINITY) l += exp2f(ms - mb) * a.lpart[sp * stride + rh];
+  float w[kCombineMax];
+#pragma unroll
+  for (int sp = 0; sp < kCombineMax; ++sp) {
+    w[sp] = mv[sp] == -INFINITY ? 0.f : exp2f(mv[sp] - mb);
+    l += w[sp] * lv[sp];
   }
   const float inv = l > 0.f ? 1.0f / l : 0.f;
-  for (int d = lane * 4; d < hd; d += 128) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int sp = 0; sp < ns; ++sp) {
-      const float ms = a.mpart[sp * stride + rh];
-      if (ms == -INFINITY) continue;
-      const float w = exp2f(ms - mb) * inv;
-      const float4 v = *reinterpret_cast<const float4*>(a.opart + (sp * stride + rh) * hd + d);
-      acc.x += w * v.x;
-      acc.y += w * v.y;
-      acc.z += w * v.z;
-      acc.w += w * v.w;
+  if (!has_d) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int sp = 0; sp < kCombineMax; ++sp) {
+    const float ww = w[sp] * inv;
+    if (ww != 0.f) {   // skipped partials (no visible key, or sp >= ns) may hold stale values
+      acc.x += ww * ov[sp].x;
+      acc.y += ww * ov[sp].y;
+      acc.z += ww * ov[sp].z;
+      acc.w += ww * ov[sp].w;
     }
-    if (O) {
-      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y), p1 = __floats2bfloat162_rn(acc.z, acc.w);
-      uint2 u;
-      u.x = *reinterpret_cast<uint32_t*>(&p0);
-      u.y = *reinterpret_cast<uint32_t*>(&p1);
-      *reinterpret_cast<uint2*>(O + (size_t)rh * hd + d) = u;
-    }
-    if (O_f32) *reinterpret_cast<float4*>(O_f32 + (size_t)rh * hd + d) = acc;
   }
+  if (O) {
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y), p1 = __floats2bfloat162_rn(acc.z, acc.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&p0);
+    u.y = *reinterpret_cast<uint32_t*>(&p1);
+    *reinterpret_cast<uint2*>(O + (size_t)rh * hd + d) = u;
+  }
+  if (O_f32) *reinterpret_cast<float4*>(O_f32 + (size_t)rh * hd + d) = acc;
 }
 
 template <int HD>
