@@ -128,3 +128,41 @@ def test_tree_attention_matches_oracle(api, hd, G, L, N, splits):
             rel = np.linalg.norm(o[s, j] - ref) / max(np.linalg.norm(ref), 1e-30)
             worst = max(worst, rel)
     assert worst <= ATTN_TOL, worst
+
+
+@pytest.mark.parametrize("hd,G,L,N,splits", [(128, 4, 2000, 32, 1), (128, 5, 3000, 16, 4), (128, 8, 4000, 64, 2),
+                                             (64, 4, 1500, 20, 1)])
+def test_tree_attention_rescale_heavy(api, hd, G, L, N, splits):
+    """Scores whose scale grows along the context, differently per query row: the running max
+    keeps rising, so lanes of one warp disagree on the lazy O rescale (the case that once hung a
+    warp on its warp-collective TMEM loads).  Same fp64 reference as above."""
+    from synth.trees import random_tree
+    rng = np.random.default_rng(7 * hd + G + L + N)
+    S = N + 1
+    tree = random_tree(rng, N, 1000)
+    qf = rng.standard_normal((S, G, hd)) * (1.0 + 3.0 * rng.random((S, G, 1)))
+    ramp = (1.0 + 5.0 * np.arange(L) / max(L, 1))[:, None]
+    kf = rng.standard_normal((L, hd)) * ramp
+    q = torch.from_numpy(qf.astype(np.float16)).cuda()
+    kp = torch.from_numpy(kf.astype(np.float16)).cuda()
+    vp = _rand_f16(rng, (L, hd))
+    kt = torch.from_numpy((rng.standard_normal((S, hd)) * 6.0).astype(np.float16)).cuda()
+    vt = _rand_f16(rng, (S, hd))
+    anc = np.array(_anc_masks(tree.parent), dtype=np.uint64).view(np.int64)
+    anc_t = torch.from_numpy(anc).cuda()
+    o = api.debug_attention(q, kp, vp, kt, vt, anc_t, n_splits=splits).cpu().numpy().astype(np.float64)
+    qn = q.float().cpu().double().numpy()
+    kpn, vpn = kp.float().cpu().double().numpy(), vp.float().cpu().double().numpy()
+    ktn, vtn = kt.float().cpu().double().numpy(), vt.float().cpu().double().numpy()
+    vis = [[0]]
+    for i, p in enumerate(tree.parent):
+        vis.append((vis[0] if p < 0 else vis[p + 1]) + [i + 1])
+    worst = 0.0
+    for s in range(S):
+        keys = np.concatenate([kpn, ktn[vis[s]]])
+        vals = np.concatenate([vpn, vtn[vis[s]]])
+        for j in range(G):
+            ref = attention(qn[s, j][None], keys, vals)[0]
+            rel = np.linalg.norm(o[s, j] - ref) / max(np.linalg.norm(ref), 1e-30)
+            worst = max(worst, rel)
+    assert worst <= ATTN_TOL, worst
