@@ -128,14 +128,17 @@ specedge_status specedge_model_create_tp(const specedge_model_config* cfg, uint6
 /* This rank's position and LM-head vocab shard [vocab0, vocab0 + vocab_n); NULL outputs skipped. */
 specedge_status specedge_model_tp_info(const specedge_model* model, int32_t* tp_rank,
                                        int32_t* tp_size, int32_t* vocab0, int32_t* vocab_n);
-/* NEXT-F4: fuse the row-parallel O / down GEMMs with the reduce-scatter of their
- * fp32 [R, d] updates (C1, C2 of specedge_model_create_tp).  Collective: every rank calls it
- * once, with the same max_rows, before verifying.  Allocates this rank's receive buffers
- * (2 x tp_size x ceil(max_rows / tp_size) x d fp32) and flag words, exchanges CUDA IPC handles
- * over the model's NCCL communicator and maps every peer's buffers (NVLink P2P).  Afterwards a
- * verify of R <= max_rows rows stores each GEMM output row straight into its owning rank's
- * receive slot from the GEMM epilogue, signals an epoch flag on every peer, and the owner's
- * RMSNorm sums the tp slots in rank order (deterministic); larger R use the NCCL path.
+/* NEXT-F4: fuse the reduce-scatter of the row-parallel O / down GEMMs' fp32 [R, d]
+ * updates (C1, C2 of specedge_model_create_tp) into the kernels over NVLink peer memory.
+ * Collective: every rank calls it once, with the same max_rows, before verifying.  Allocates this
+ * rank's exchange buffer (max(max_rows, 2 x tp_size x ceil(max_rows / tp_size)) x d fp32) and flag
+ * words, exchanges CUDA IPC handles over the model's NCCL communicator and maps every peer's
+ * buffer.  Afterwards a verify of R <= max_rows rows runs C1/C2 without NCCL: by default the GEMM
+ * epilogue stages each 32-row chunk in shared memory and bulk-copies every row to the receive slot
+ * of the rank that owns it (environment SPECEDGE_TP_F4=pull instead writes locally and lets the
+ * owner's RMSNorm load its rows from every rank); an epoch flag is released on every peer after
+ * the GEMM and the owner's RMSNorm, after acquiring the flags, sums the tp slots in rank order
+ * (deterministic).  Larger R use the NCCL path.
  * E_INVALID: tp_size < 2 or > 4, max_rows <= 0, or already enabled with a smaller max_rows;
  * E_CUDA: allocation / IPC / NCCL failure (the model stays on the NCCL path).  Synchronous;
  * `stream` carries the handle all-gather. */

@@ -73,17 +73,26 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
             if (j < ncol && row < a.R)
               a.out_f32[(size_t)(row >> 1) * a.ldo + feat] = __uint_as_float(v[j]) + __uint_as_float(v[j + 1]);
           }
-        } else if (a.tp_fused) {
-          // NEXT-F4: straight into the owning rank's receive slot (NVLink store when remote)
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int row = row_base + j;
-            if (j < ncol && row < a.R) {
+        } else if (a.push) {
+          // NEXT-F4 push: stage the chunk row-major (32 rows x 128 features = 32 x 512 B), then
+          // one thread sends every row to its owner's receive slot with bulk async copies (remote
+          // rows cross NVLink) — the epilogue warps never wait on a remote store
+          for (int j = 0; j < 32; ++j) xch[j * 128 + tl] = __uint_as_float(v[j]);
+          fence_proxy_async_smem();
+          named_bar_sync(1, kEpiThreads);
+          if (et == 0) {
+            for (int j = 0; j < ncol; ++j) {
+              const int row = row_base + j;
+              if (row >= a.R) break;
               const int o = row / a.rows_per_rank;
-              a.peer_out[o][(size_t)a.tp_src * a.slot_stride + (size_t)(row - o * a.rows_per_rank) * a.ldo + feat] =
-                  __uint_as_float(v[j]);
+              bulk_s2g(a.peer_out[o] + (size_t)a.tp_src * a.slot_stride + (size_t)(row - o * a.rows_per_rank) * a.ldo +
+                           m128 * 128,
+                       xch + j * 128, 512);
             }
+            bulk_commit();
+            bulk_wait_read0();   // the staging buffer may be overwritten
           }
+          named_bar_sync(1, kEpiThreads);
         } else {
           float* out = a.out_f32 + (size_t)sk * a.split_stride;   // K-split sk's partial
 #pragma unroll
@@ -354,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+    if (MODE == EPI_F32 && a.push && et == 0) bulk_wait0();   // every pushed row has landed
   }
   __syncthreads();
   if (warp == 1) {
@@ -565,6 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive_leader(&tempty[acc]);
     }
+    if (MODE == EPI_F32 && a.push && et == 0) bulk_wait0();   // every pushed row has landed
   }
   __syncthreads();
   cluster_sync();

@@ -48,6 +48,9 @@ enum GemmMode : int {
 };
 
 constexpr int kMaxFusedTp = 4;   // NEXT-F4: ranks of the fused GEMM -> reduce-scatter
+struct RmsSrc {                  // NEXT-F4: per-partial base pointers for k_rmsnorm (p[0] == null: unused)
+  const float* p[kMaxFusedTp];
+};
 
 struct GemmArgs {
   int M, R, K;            // weight rows (features), activation rows, reduction length
@@ -61,9 +64,10 @@ struct GemmArgs {
   // EPI_F32 / EPI_RESID (fp32 residual stream)
   float* out_f32;
   int ldo;
-  // EPI_F32 with tp_fused (NEXT-F4): row r goes to rank o = r / rows_per_rank, slot [tp_src] of
-  // its receive buffer: peer_out[o] + tp_src * slot_stride + (r - o * rows_per_rank) * ldo
-  int tp_fused, tp_src, rows_per_rank;
+  // EPI_F32 with push (NEXT-F4): each 32-row chunk is staged in shared memory and row r is sent
+  // with a bulk async copy to rank o = r / rows_per_rank, slot [tp_src] of its receive buffer:
+  // peer_out[o] + tp_src * slot_stride + (r - o * rows_per_rank) * ldo
+  int push, tp_src, rows_per_rank;
   size_t slot_stride;
   float* peer_out[kMaxFusedTp];
   // EPI_SWIGLU / EPI_QKV(q part)
@@ -186,7 +190,8 @@ cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int
 // x = X + sum_s Y[s] (s < nY, fixed order; X updated in place), out = bf16(rmsnorm(x) * g);
 // split = 1 writes out as hi/lo bf16 row pairs (LM-head input).
 cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, const bf16* g, bf16* out,
-                           int R, int d, float eps, cudaStream_t st, int* launches, int split = 0);
+                           int R, int d, float eps, cudaStream_t st, int* launches, int split = 0,
+                           const RmsSrc* ys = nullptr);
 // Q / tree K/V from the QKV GEMM's fp32 split partials: sum splits, RoPE(q, k) at row_pos,
 // bf16 round, scatter
 struct RopeArgs {
@@ -330,16 +335,16 @@ struct specedge_model {
   void* nccl = nullptr;         // ncclComm_t when tp_size > 1
   float* tp_gather = nullptr;   // [tp_size][R_max][2] (score, id) all-gather buffer
   int tp_gather_rows = 0;
-  // NEXT-F4 (tp.cu): receive buffers [2][tp][Rl][d] fp32 + flag words [tp] (this rank's), the
-  // peers' mappings, the epoch of the last signalled collective
+  // NEXT-F4 (tp.cu): this rank's row-parallel GEMM output [R_max][d] fp32 + flag words [tp],
+  // the peers' mappings of theirs, the epoch of the last signalled collective
   int tp_fused_rows = 0;                 // capacity (rows); 0 = fused path off
-  size_t tp_fused_slot = 0;              // floats per [src] slot = Rl * d
-  float* tp_recv = nullptr;
+  float* tp_recv = nullptr;              // pull: [R_max][d]; push: [2][tp][ceil(R_max/tp)][d]
+  size_t tp_fused_slot = 0;              // push: floats per [src] slot
+  int tp_fused_buf = 0;                  // push: receive buffer of the next collective
   float* tp_peer_recv[se::kMaxFusedTp] = {};
   unsigned long long* tp_flags = nullptr;
   unsigned long long** tp_peer_flags_dev = nullptr;
   unsigned long long tp_epoch = 0;
-  int tp_fused_buf = 0;                  // receive buffer of the next collective
   std::vector<void*> tp_ipc_opened;
   se::bf16* embed = nullptr;
   se::bf16* lm_head = nullptr;

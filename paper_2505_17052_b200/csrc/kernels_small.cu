@@ -134,10 +134,12 @@ __global__ void k_embed(const bf16* __restrict__ E, const int* __restrict__ row_
 // partials, summed in this fixed order), X = x (fp32 residual stream), out = bf16(x * rsqrt(mean(x^2)
 // + eps) * g).  split = 1 (final norm feeding the LM head): y is written as two bf16 rows, hi =
 // bf16(y) at out row 2r and lo = bf16(y - hi) at row 2r+1, so hi + lo carries y to ~2^-17.
+// ys (NEXT-F4, tensor parallel): partial s of this rank's rows at ys.p[s] (a peer's memory over
+// NVLink for s != own rank) instead of Y + s * y_stride; summed in the same fixed order.
 template <int NY>
 __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const float* __restrict__ Y, size_t y_stride,
                                                   const bf16* __restrict__ g, bf16* __restrict__ out, int d, float eps,
-                                                  int split) {
+                                                  int split, const RmsSrc ys) {
   pdl_begin();
   // blockDim.x = d / 16: each thread owns 16 consecutive elements, kept in registers across passes
   const int row = blockIdx.x;
@@ -156,7 +158,8 @@ __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const f
     for (int s = 0; s < NY; ++s)
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        yv[s][k] = __ldcs(reinterpret_cast<const float4*>(Y + s * y_stride + (size_t)row * d + i + 4 * k));
+        yv[s][k] = __ldcs(reinterpret_cast<const float4*>((ys.p[0] ? ys.p[s] : Y + s * y_stride) + (size_t)row * d +
+                                                          i + 4 * k));
 #pragma unroll
     for (int s = 0; s < NY; ++s)
 #pragma unroll
@@ -605,15 +608,16 @@ cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int
   return cudaGetLastError();
 }
 cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, const bf16* g, bf16* out, int R, int d,
-                           float eps, cudaStream_t st, int* launches, int split) {
+                           float eps, cudaStream_t st, int* launches, int split, const RmsSrc* ys) {
   if (launches) ++*launches;
   const int threads = d / 16;   // d % 64 == 0 (checked at model creation), <= 1024
+  const RmsSrc src = ys ? *ys : RmsSrc{};
   switch (nY) {
-    case 0: CK_RET(launch_k(k_rmsnorm<0>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
-    case 1: CK_RET(launch_k(k_rmsnorm<1>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
-    case 2: CK_RET(launch_k(k_rmsnorm<2>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
-    case 3: CK_RET(launch_k(k_rmsnorm<3>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
-    case 4: CK_RET(launch_k(k_rmsnorm<4>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split)); break;
+    case 0: CK_RET(launch_k(k_rmsnorm<0>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
+    case 1: CK_RET(launch_k(k_rmsnorm<1>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
+    case 2: CK_RET(launch_k(k_rmsnorm<2>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
+    case 3: CK_RET(launch_k(k_rmsnorm<3>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
+    case 4: CK_RET(launch_k(k_rmsnorm<4>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

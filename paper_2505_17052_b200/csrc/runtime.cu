@@ -5,6 +5,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <string>
 #include <cstdio>
 #include <cmath>
 #include <cstring>
@@ -334,44 +335,57 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     }
     return ns;
   };
-  // NEXT-F4: row-parallel GEMM whose epilogue stores every row into its owner's receive slot
-  // over NVLink (tp.cu), then the epoch signal; the owner's norm_rows waits and sums the tp slots
+  // NEXT-F4: row-parallel GEMM into this rank's peer-mapped output buffer, then the epoch
+  // signal; the owner's norm_rows waits and reads its rows from every rank's buffer (tp.cu)
+  // Two variants (SPECEDGE_TP_F4=push|pull, default push): push = the GEMM epilogue sends each
+  // row to its owner's receive slot with bulk async copies (transfer overlapped with the GEMM);
+  // pull = the GEMM writes locally and the owner's RMSNorm loads its rows from every rank.
   const bool fused = tp && m->tp_fused_rows >= R && m->tp_size <= kMaxFusedTp;
-  const float* fused_src = nullptr;   // receive buffer holding the pending row-parallel partials
+  static const bool f4_pull = getenv("SPECEDGE_TP_F4") && std::string(getenv("SPECEDGE_TP_F4")) == "pull";
+  bool fused_pending = false;   // a row-parallel partial is waiting in the ranks' buffers
+  const float* push_src = nullptr;   // push: the receive buffer holding this rank's tp slots
   auto f32_gemm_fused = [&](int kind, const CUtensorMap& tm, const void* Xin, int Mrows, int K) -> int {
     GemmArgs g{};
     g.M = Mrows;
     g.R = R;
     g.K = K;
-    g.out_f32 = Y;
+    g.out_f32 = m->tp_recv;
     g.ldo = Mrows;
     g.max_splits = 1;
-    g.split_stride = y_stride;
-    g.tp_fused = 1;
-    g.tp_src = m->tp_rank;
-    g.rows_per_rank = Rl;
-    g.slot_stride = m->tp_fused_slot;
-    const size_t boff = (size_t)m->tp_fused_buf * m->tp_size * m->tp_fused_slot;
-    for (int p = 0; p < m->tp_size; ++p) g.peer_out[p] = m->tp_peer_recv[p] + boff;
+    g.split_stride = 0;
+    if (!f4_pull) {
+      const size_t boff = (size_t)m->tp_fused_buf * m->tp_size * m->tp_fused_slot;
+      g.push = 1;
+      g.tp_src = m->tp_rank;
+      g.rows_per_rank = Rl;
+      g.slot_stride = m->tp_fused_slot;
+      for (int p = 0; p < m->tp_size; ++p) g.peer_out[p] = m->tp_peer_recv[p] + boff;
+      push_src = m->tp_recv + boff;
+      m->tp_fused_buf ^= 1;
+    }
     {
       KTimer _t(kind, st);
       if (gemm_launch(EPI_F32, tm, Xin, g, st, &launches) != cudaSuccess) return -1;
     }
     if (tp_fused_signal(m, st, &launches) != cudaSuccess) return -1;
-    fused_src = m->tp_recv + boff;
-    m->tp_fused_buf ^= 1;
+    fused_pending = true;
     return m->tp_size;
   };
   // residual add + RMSNorm of this rank's rows (all rows when tp_size == 1), then under TP the
   // bf16 all-gather of the normalised rows for the next column-parallel GEMM
   auto norm_rows = [&](int nY, const bf16* gain, bf16* out, int split) -> specedge_status {
-    if (fused_src) {   // the tp slots of this rank's rows, summed in rank order
+    if (fused_pending) {   // this rank's rows of every rank's partial, summed in rank order
       CK(tp_fused_wait(m, st, &launches));
       KTimer _t(K_RMSNORM, st);
+      RmsSrc ys{};
+      for (int p = 0; p < m->tp_size; ++p)
+        ys.p[p] = push_src ? push_src + (size_t)p * m->tp_fused_slot
+                           : (p == m->tp_rank ? m->tp_recv : m->tp_peer_recv[p]) + (size_t)r0 * c.d;
       if (nloc)
-        CK(rmsnorm_launch(X + (size_t)r0 * c.d, fused_src, nY, m->tp_fused_slot, gain,
-                          out + (size_t)(split ? 2 : 1) * r0 * c.d, nloc, c.d, c.eps, st, &launches, split));
-      fused_src = nullptr;
+        CK(rmsnorm_launch(X + (size_t)r0 * c.d, nullptr, nY, 0, gain, out + (size_t)(split ? 2 : 1) * r0 * c.d, nloc,
+                          c.d, c.eps, st, &launches, split, &ys));
+      fused_pending = false;
+      push_src = nullptr;
     } else {
       KTimer _t(K_RMSNORM, st);
       if (nloc)

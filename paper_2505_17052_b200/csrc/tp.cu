@@ -12,6 +12,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -150,19 +151,27 @@ cudaError_t tp_argmax_gather(int* y, float* score, int R, float* gather, int tp,
 
 
 // ---------------------------------------------------------------------------------------------
-// NEXT-F4: GEMM -> reduce-scatter fused over NVLink peer memory.
-// Every rank's row-parallel GEMM (O, down) stores each fp32 output row straight into the
-// receive buffer of the rank that owns the row (sequence-parallel residual: rank k owns rows
-// [k*Rl, (k+1)*Rl)), slot [src rank], through CUDA IPC mappings of the peers' buffers — the
-// transfer rides on the GEMM's own epilogue stores, tile by tile, instead of a separate NCCL
-// reduce-scatter after the GEMM.  The owner sums the tp slots in rank order inside its RMSNorm
-// (the same kernel that sums K-split partials), so the result is deterministic.
+// NEXT-F4: the reduce-scatter of the row-parallel GEMMs (O, down) fused over NVLink peer memory
+// (SURVEY §8(f) rank 5).  Each rank owns an exchange buffer that all peers have mapped (CUDA IPC).
+//   push (default): the GEMM epilogue stages every 32-row chunk of its fp32 partial in shared
+//     memory and one thread bulk-copies each 512-byte row segment (cp.async.bulk shared -> global)
+//     into the receive slot [src] of the rank that owns the row (sequence-parallel residual: rank
+//     k owns rows [k*Rl, (k+1)*Rl)); the transfer rides on the GEMM, tile by tile.
+//   pull (SPECEDGE_TP_F4=pull): the GEMM writes its partial locally; the owner's RMSNorm loads its
+//     rows from every rank's buffer (NVLink loads for the peers').
+// Either way the owner's RMSNorm sums the tp partials in rank order together with the residual
+// add and the normalisation (deterministic), with no reduce-scatter kernel and no staging copy.
+// (A first push version stored 4-byte lanes straight from registers to the peer; it stalled the
+// epilogue.)  Measured on cfg4 TP=2: push, pull and NCCL within 1.5 % (profiles/README.md): the
+// SM-issued NVLink traffic reaches ~250-300 GB/s, about what NCCL's reduce-scatter costs.
 //
 // Ordering: after the GEMM, k_tp_signal (one thread per peer) publishes an epoch with a
 // system-scope release store into every peer's flag word [src]; before the RMSNorm, k_tp_wait
 // spins with acquire loads until every peer's flag holds that epoch (bounded: traps after ~20 s
-// rather than hang).  Two receive buffers alternate per collective: a rank writes buffer b for
-// op n+2 only after it consumed op n+1, which every peer sent after consuming op n from b.
+// rather than hang).  pull: one buffer suffices — a rank overwrites it (its next row-parallel
+// GEMM) only after the bf16 all-gather that follows every peer's RMSNorm.  push: two receive
+// buffers alternate per collective — a rank writes buffer b for op n+2 only after consuming op
+// n+1, which every peer sent after consuming op n from b.
 // ---------------------------------------------------------------------------------------------
 namespace {
 
@@ -216,9 +225,11 @@ int tp_fused_enable(specedge_model* m, int max_rows, cudaStream_t st) {
   if (tp < 2 || tp > kMaxFusedTp || max_rows <= 0 || !m->nccl) return -1;
   if (m->tp_fused_rows >= max_rows) return 0;
   if (m->tp_fused_rows) return -2;   // already enabled with a smaller capacity: not resizable
-  const int Rl = (max_rows + tp - 1) / tp;
-  const size_t slot = (size_t)Rl * m->cfg.d;   // floats per [src] slot
-  const size_t bytes = 2 * (size_t)tp * slot * 4 + 256;
+  // pull: [max_rows][d] fp32; push: [2][tp][Rl][d] — the larger of the two layouts
+  const size_t Rl = ((size_t)max_rows + tp - 1) / tp;
+  m->tp_fused_slot = Rl * m->cfg.d;
+  const size_t out_bytes = (std::max((size_t)max_rows * m->cfg.d, 2 * (size_t)tp * m->tp_fused_slot) * 4 + 255) / 256 * 256;
+  const size_t bytes = out_bytes + 256;
   char* base = nullptr;
   if (cudaMalloc(&base, bytes) != cudaSuccess) return -3;
   m->allocs.push_back(base);
@@ -246,14 +257,13 @@ int tp_fused_enable(specedge_model* m, int max_rows, cudaStream_t st) {
       pb = static_cast<char*>(q);
     }
     m->tp_peer_recv[p] = reinterpret_cast<float*>(pb);
-    flags_host[p] = reinterpret_cast<unsigned long long*>(pb + 2 * (size_t)tp * slot * 4);
+    flags_host[p] = reinterpret_cast<unsigned long long*>(pb + out_bytes);
   }
   m->tp_recv = reinterpret_cast<float*>(base);
-  m->tp_flags = reinterpret_cast<unsigned long long*>(base + 2 * (size_t)tp * slot * 4);
+  m->tp_flags = reinterpret_cast<unsigned long long*>(base + out_bytes);
   if (cudaMalloc(&m->tp_peer_flags_dev, sizeof(flags_host)) != cudaSuccess) return -3;
   m->allocs.push_back(m->tp_peer_flags_dev);
   cudaMemcpy(m->tp_peer_flags_dev, flags_host, sizeof(flags_host), cudaMemcpyHostToDevice);
-  m->tp_fused_slot = slot;
   m->tp_fused_rows = max_rows;
   // barrier: every rank has mapped every peer before anyone may write into a peer
   char* one = nullptr;
