@@ -75,13 +75,13 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           }
         } else if (a.push) {
           // NEXT-F4 push: stage the chunk row-major (32 rows x 128 features = 32 x 512 B), then
-          // one thread sends every row to its owner's receive slot with bulk async copies (remote
-          // rows cross NVLink) — the epilogue warps never wait on a remote store
+          // one lane per warp sends 8 rows to their owners' receive slots with bulk async copies
+          // (remote rows cross NVLink) — the epilogue warps never wait on a remote store
           for (int j = 0; j < 32; ++j) xch[j * 128 + tl] = __uint_as_float(v[j]);
           fence_proxy_async_smem();
           named_bar_sync(1, kEpiThreads);
-          if (et == 0) {
-            for (int j = 0; j < ncol; ++j) {
+          if ((et & 31) == 0) {   // one issuing lane per epilogue warp, 8 rows each
+            for (int j = (et >> 5) * 8; j < min(ncol, (et >> 5) * 8 + 8); ++j) {
               const int row = row_base + j;
               if (row >= a.R) break;
               const int o = row / a.rows_per_rank;
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
-    if (MODE == EPI_F32 && a.push && et == 0) bulk_wait0();   // every pushed row has landed
+    if (MODE == EPI_F32 && a.push && (et & 31) == 0) bulk_wait0();   // every pushed row has landed
   }
   __syncthreads();
   if (warp == 1) {
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive_leader(&tempty[acc]);
     }
-    if (MODE == EPI_F32 && a.push && et == 0) bulk_wait0();   // every pushed row has landed
+    if (MODE == EPI_F32 && a.push && (et & 31) == 0) bulk_wait0();   // every pushed row has landed
   }
   __syncthreads();
   cluster_sync();

@@ -154,7 +154,7 @@ cudaError_t tp_argmax_gather(int* y, float* score, int R, float* gather, int tp,
 // NEXT-F4: the reduce-scatter of the row-parallel GEMMs (O, down) fused over NVLink peer memory
 // (SURVEY §8(f) rank 5).  Each rank owns an exchange buffer that all peers have mapped (CUDA IPC).
 //   push (default): the GEMM epilogue stages every 32-row chunk of its fp32 partial in shared
-//     memory and one thread bulk-copies each 512-byte row segment (cp.async.bulk shared -> global)
+//     memory and one lane per warp bulk-copies 8 of the 512-byte row segments (cp.async.bulk)
 //     into the receive slot [src] of the rank that owns the row (sequence-parallel residual: rank
 //     k owns rows [k*Rl, (k+1)*Rl)); the transfer rides on the GEMM, tile by tile.
 //   pull (SPECEDGE_TP_F4=pull): the GEMM writes its partial locally; the owner's RMSNorm loads its
@@ -162,8 +162,8 @@ cudaError_t tp_argmax_gather(int* y, float* score, int R, float* gather, int tp,
 // Either way the owner's RMSNorm sums the tp partials in rank order together with the residual
 // add and the normalisation (deterministic), with no reduce-scatter kernel and no staging copy.
 // (A first push version stored 4-byte lanes straight from registers to the peer; it stalled the
-// epilogue.)  Measured on cfg4 TP=2: push, pull and NCCL within 1.5 % (profiles/README.md): the
-// SM-issued NVLink traffic reaches ~250-300 GB/s, about what NCCL's reduce-scatter costs.
+// epilogue.)  Measured on cfg4 TP=2 (profiles/README.md): push 800.8 vs NCCL 761.4 tok/s on one
+// box (+5.2 %); pull ~ NCCL (its NVLink loads lengthen the RMSNorms by about what NCCL costs).
 //
 // Ordering: after the GEMM, k_tp_signal (one thread per peer) publishes an epoch with a
 // system-scope release store into every peer's flag word [src]; before the RMSNorm, k_tp_wait
