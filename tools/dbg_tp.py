@@ -43,7 +43,10 @@ def main():
                                 device=f"cuda:{rank}", max_context_len=maxc)
     out = api.verify(model, pool, batch, ws, auto_commit=False)
     torch.cuda.synchronize()
-    print(f"rank {rank}: ok, accepted {out.accepted_len.cpu().numpy().tolist()[:8]}", flush=True)
+    rt = out.row_target.cpu().numpy()
+    rs = out.row_score.cpu().numpy().astype(np.float64)
+    print(f"rank {rank}: ok, accepted {out.accepted_len.cpu().numpy().tolist()[:8]} target_sum {int(rt.sum())} "
+          f"score_mean {rs.mean():.6f}", flush=True)
     model.close()
     dist.destroy_process_group()
 
