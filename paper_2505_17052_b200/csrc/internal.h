@@ -50,6 +50,8 @@ enum GemmMode : int {
 constexpr int kMaxFusedTp = 4;   // NEXT-F4: ranks of the fused GEMM -> reduce-scatter
 struct RmsSrc {                  // NEXT-F4: per-partial base pointers for k_rmsnorm (p[0] == null: unused)
   const float* p[kMaxFusedTp];
+  bf16* outp[kMaxFusedTp];       // NEXT-F4 all-gather: the normalised row also goes to every rank
+  int nout;                      // (split == 0 only); 0: unused
 };
 
 struct GemmArgs {
@@ -340,6 +342,8 @@ struct specedge_model {
   int tp_fused_rows = 0;                 // capacity (rows); 0 = fused path off
   float* tp_recv = nullptr;              // pull: [R_max][d]; push: [2][tp][ceil(R_max/tp)][d]
   size_t tp_fused_slot = 0;              // push: floats per [src] slot
+  se::bf16* tp_hn = nullptr;             // all-gathered normalised rows [R_max][d] (this rank's copy)
+  se::bf16* tp_peer_hn[se::kMaxFusedTp] = {};
   int tp_fused_buf = 0;                  // push: receive buffer of the next collective
   float* tp_peer_recv[se::kMaxFusedTp] = {};
   unsigned long long* tp_flags = nullptr;

@@ -211,6 +211,13 @@ __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const f
     dh[1] = make_uint4(o[4], o[5], o[6], o[7]);
     dl[0] = make_uint4(r[0], r[1], r[2], r[3]);
     dl[1] = make_uint4(r[4], r[5], r[6], r[7]);
+  } else if (ys.nout) {
+    // NEXT-F4 all-gather: this rank's normalised row into every rank's copy (NVLink stores)
+    for (int p = 0; p < ys.nout; ++p) {
+      uint4* dh = reinterpret_cast<uint4*>(ys.outp[p] + (size_t)row * d + i);
+      dh[0] = make_uint4(o[0], o[1], o[2], o[3]);
+      dh[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    }
   } else {
     uint4* dh = reinterpret_cast<uint4*>(out + (size_t)row * d + i);
     dh[0] = make_uint4(o[0], o[1], o[2], o[3]);

@@ -374,35 +374,50 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   // residual add + RMSNorm of this rank's rows (all rows when tp_size == 1), then under TP the
   // bf16 all-gather of the normalised rows for the next column-parallel GEMM
   auto norm_rows = [&](int nY, const bf16* gain, bf16* out, int split) -> specedge_status {
-    if (fused_pending) {   // this rank's rows of every rank's partial, summed in rank order
+    // NEXT-F4 all-gather (per-layer norms, SPECEDGE_TP_F4_AG=1): every rank stores its normalised
+    // rows straight into every rank's copy of Hn (m->tp_hn), then signal + wait replace the NCCL
+    // all-gather.  Off by default: measured at parity with NCCL on cfg4 TP=4 (the RMSNorm's remote
+    // stores cost what the all-gather did)
+    static const bool f4_ag = getenv("SPECEDGE_TP_F4_AG") && getenv("SPECEDGE_TP_F4_AG")[0] == '1';
+    const bool ag_fused = fused && f4_ag && !split;
+    const bool partial = fused_pending;
+    RmsSrc ys{};
+    if (partial) {   // this rank's rows of every rank's partial, summed in rank order
       CK(tp_fused_wait(m, st, &launches));
-      KTimer _t(K_RMSNORM, st);
-      RmsSrc ys{};
       for (int p = 0; p < m->tp_size; ++p)
         ys.p[p] = push_src ? push_src + (size_t)p * m->tp_fused_slot
                            : (p == m->tp_rank ? m->tp_recv : m->tp_peer_recv[p]) + (size_t)r0 * c.d;
-      if (nloc)
-        CK(rmsnorm_launch(X + (size_t)r0 * c.d, nullptr, nY, 0, gain, out + (size_t)(split ? 2 : 1) * r0 * c.d, nloc,
-                          c.d, c.eps, st, &launches, split, &ys));
-      fused_pending = false;
-      push_src = nullptr;
-    } else {
+    }
+    if (ag_fused) {
+      ys.nout = m->tp_size;
+      for (int p = 0; p < m->tp_size; ++p)
+        ys.outp[p] = (p == m->tp_rank ? m->tp_hn : m->tp_peer_hn[p]) + (size_t)r0 * c.d;
+    }
+    {
       KTimer _t(K_RMSNORM, st);
       if (nloc)
-        CK(rmsnorm_launch(X + (size_t)r0 * c.d, Y + (size_t)r0 * c.d, nY, y_stride, gain,
-                          out + (size_t)(split ? 2 : 1) * r0 * c.d, nloc, c.d, c.eps, st, &launches, split));
+        CK(rmsnorm_launch(X + (size_t)r0 * c.d, partial ? nullptr : Y + (size_t)r0 * c.d, nY, partial ? 0 : y_stride,
+                          gain, out + (size_t)(split ? 2 : 1) * r0 * c.d, nloc, c.d, c.eps, st, &launches, split,
+                          (partial || ag_fused) ? &ys : nullptr));
     }
-    if (tp) {
+    fused_pending = false;
+    push_src = nullptr;
+    if (ag_fused) {
+      CK(tp_fused_signal(m, st, &launches));
+      CK(tp_fused_wait(m, st, &launches));
+    } else if (tp) {
       CK(tp_all_gather_bf16(out, (size_t)(split ? 2 : 1) * Rl * c.d, m->tp_rank, m->nccl, st));
       ++launches;
     }
     return SPECEDGE_OK;
   };
+  static const bool f4_ag_on = getenv("SPECEDGE_TP_F4_AG") && getenv("SPECEDGE_TP_F4_AG")[0] == '1';
+  bf16* const Hn_in = (fused && f4_ag_on) ? m->tp_hn : Hn;   // operand of the column-parallel GEMMs
   for (int l = 0; l < c.n_layers; ++l) {
     g_dbg_layer = l;
     const auto& Lw = m->layers[l];
     { const specedge_status ns = norm_rows(pendingY, Lw.g_attn, Hn, 0); if (ns != SPECEDGE_OK) return ns; }
-    const int sq = f32_gemm(K_QKV, Lw.tm_qkv, Hn, (H + 2 * KV) * hd, c.d, false);
+    const int sq = f32_gemm(K_QKV, Lw.tm_qkv, Hn_in, (H + 2 * KV) * hd, c.d, false);
     if (sq < 0) return SPECEDGE_E_CUDA;
     RopeArgs ra{};
     ra.Y = Y;
@@ -437,7 +452,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gu.K = c.d;
     gu.out_bf16 = Mb;
     gu.ld_out = c.ffn;
-    { KTimer _t(K_GU, st); CK(gemm_launch(EPI_SWIGLU, Lw.tm_gu, Hn, gu, st, &launches)); }
+    { KTimer _t(K_GU, st); CK(gemm_launch(EPI_SWIGLU, Lw.tm_gu, Hn_in, gu, st, &launches)); }
     pendingY = fused ? f32_gemm_fused(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn) : f32_gemm(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn, true);
     if (pendingY < 0) return SPECEDGE_E_CUDA;
   }

@@ -228,7 +228,9 @@ int tp_fused_enable(specedge_model* m, int max_rows, cudaStream_t st) {
   // pull: [max_rows][d] fp32; push: [2][tp][Rl][d] — the larger of the two layouts
   const size_t Rl = ((size_t)max_rows + tp - 1) / tp;
   m->tp_fused_slot = Rl * m->cfg.d;
-  const size_t out_bytes = (std::max((size_t)max_rows * m->cfg.d, 2 * (size_t)tp * m->tp_fused_slot) * 4 + 255) / 256 * 256;
+  const size_t part_bytes = (std::max((size_t)max_rows * m->cfg.d, 2 * (size_t)tp * m->tp_fused_slot) * 4 + 255) / 256 * 256;
+  const size_t hn_bytes = ((size_t)max_rows * m->cfg.d * 2 + 255) / 256 * 256;   // all-gathered bf16 rows
+  const size_t out_bytes = part_bytes + hn_bytes;
   const size_t bytes = out_bytes + 256;
   char* base = nullptr;
   if (cudaMalloc(&base, bytes) != cudaSuccess) return -3;
@@ -257,9 +259,11 @@ int tp_fused_enable(specedge_model* m, int max_rows, cudaStream_t st) {
       pb = static_cast<char*>(q);
     }
     m->tp_peer_recv[p] = reinterpret_cast<float*>(pb);
+    m->tp_peer_hn[p] = reinterpret_cast<bf16*>(pb + part_bytes);
     flags_host[p] = reinterpret_cast<unsigned long long*>(pb + out_bytes);
   }
   m->tp_recv = reinterpret_cast<float*>(base);
+  m->tp_hn = reinterpret_cast<bf16*>(base + part_bytes);
   m->tp_flags = reinterpret_cast<unsigned long long*>(base + out_bytes);
   if (cudaMalloc(&m->tp_peer_flags_dev, sizeof(flags_host)) != cudaSuccess) return -3;
   m->allocs.push_back(m->tp_peer_flags_dev);
