@@ -756,7 +756,8 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
   a.splits = 1;
   static const int env_max = getenv("SPECEDGE_MAX_SPLITS") ? atoi(getenv("SPECEDGE_MAX_SPLITS")) : 0;
   if (env_max > 0) a.max_splits = std::min(a.max_splits, env_max);
-  if (mode == EPI_F32 && !a.pair && a.max_splits > 1 && ntiles < nclusters * 3 / 2) {
+  const bool full_wave = a.unsplit_if_full && ntiles * 10 >= nclusters * 9 && ntiles <= nclusters;
+  if (mode == EPI_F32 && !a.pair && a.max_splits > 1 && ntiles < nclusters * 3 / 2 && !full_wave) {
     int sp = (2 * nclusters + ntiles / 2) / ntiles;
     sp = std::min(sp, a.max_splits);
     while (sp > 1 && a.num_kb / sp < 8) --sp;

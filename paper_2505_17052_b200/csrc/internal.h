@@ -62,6 +62,7 @@ struct GemmArgs {
   int nc;                 // CTA-pair kernel: pairs per cluster sharing one weight tile (TMA multicast)
   int n_groups;           // CTA-pair kernel: ceil(n_tiles_n / nc)
   int splits, kb_per_split, max_splits;   // K-split (EPI_F32): slice sk at out_f32 + sk*split_stride
+  int unsplit_if_full;    // EPI_F32: no K-split when the tiles already fill >= 90 % of one wave
   size_t split_stride;
   // EPI_F32 / EPI_RESID (fp32 residual stream)
   float* out_f32;

@@ -48,9 +48,18 @@ int num_sms() {
 
 thread_local int g_last_launches = 0;
 
+// K-split cap per fp32 GEMM kind (consumers sum the partials: RoPE after QKV, RMSNorm after O /
+// down).  Env SPECEDGE_SPLITS_QKV / _O / _DOWN override (A/B); defaults from cfg2 measurements.
+int kind_splits(int kind);
+
 // ---- optional per-kernel event timing (bench instrumentation) ----
 enum Kind { K_PREP, K_EMBED, K_RMSNORM, K_QKV, K_ATTN, K_COMBINE, K_O, K_GU, K_DOWN, K_LM, K_LMRED, K_WALK, K_COMMIT,
             K_ROPE, K_NKINDS };
+int kind_splits(int kind) {
+  auto env = [](const char* n, int d) { return getenv(n) ? std::max(1, atoi(getenv(n))) : d; };
+  static const int qkv = env("SPECEDGE_SPLITS_QKV", 4), o = env("SPECEDGE_SPLITS_O", 4), down = env("SPECEDGE_SPLITS_DOWN", 4);
+  return kind == K_QKV ? qkv : (kind == K_O ? o : (kind == K_DOWN ? down : 4));
+}
 struct Timing {
   bool on = false;
   uint32_t mask = 0;
@@ -322,7 +331,10 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     g.K = K;
     g.out_f32 = Y;
     g.ldo = Mrows;
-    g.max_splits = (tp && row_parallel) ? 1 : kGemmSplits;
+    g.max_splits = (tp && row_parallel) ? 1 : kind_splits(kind);
+    // QKV: its partials are summed by the RoPE kernel; a full wave needs no split (cfg2: 72 pair
+    // tiles on 74 pairs -> QKV + RoPE 1.42 -> 1.31 ms per step)
+    g.unsplit_if_full = kind == K_QKV ? 1 : 0;
     g.split_stride = y_stride;
     {
       KTimer _t(kind, st);
