@@ -333,70 +333,75 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 __global__ void k_attn_combine(const __grid_constant__ AttnArgs a, bf16* __restrict__ O,
                                float* __restrict__ O_f32) {
   pdl_begin();
-  const int rh = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // row * H + head
+  // one warp per (row, kv head g): the chunk count is looked up once for the G query heads of
+  // the group; every partial a head needs is loaded in one round, two heads in flight
+  const int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // row * KV + g
   const int lane = threadIdx.x & 31;
-  if (rh >= a.R * a.H) return;
+  if (item >= a.R * a.KV) return;
+  const int row = item / a.KV, g = item % a.KV;
   const int hd = a.hd;
   const size_t stride = (size_t)a.R * a.H;
   int ns = a.n_splits;
   if (a.per_req == 1) {
-    const int r = a.row_req ? a.row_req[rh / a.H] : 0;
+    const int r = a.row_req ? a.row_req[row] : 0;
     const int npages = (a.req_L[r] + 63) / 64;
     ns = max(1, (npages + a.pages_per_split - 1) / a.pages_per_split);
     if (ns == 1) return;   // written final by the attention kernel
   } else if (a.per_req == 2) {
     // balanced tcgen05 attention: the kernel recorded the chunk count of every (r, g)
-    const int r = a.row_req ? a.row_req[rh / a.H] : 0;
-    ns = a.nch_tab[r * a.KV + (rh % a.H) / a.G];
+    const int r = a.row_req ? a.row_req[row] : 0;
+    ns = a.nch_tab[r * a.KV + g];
     if (ns == 1) return;
   }
-  // every partial this lane needs is loaded in one round (ns <= kCombineMax): the kernel is a
-  // chain of dependent loads, not bandwidth
   constexpr int kCombineMax = 8;
-  float mv[kCombineMax], lv[kCombineMax];
-  float4 ov[kCombineMax];
   const int d = lane * 4;
   const bool has_d = d < hd;
+#pragma unroll 2
+  for (int j = 0; j < a.G; ++j) {
+    const size_t rh = (size_t)row * a.H + (size_t)g * a.G + j;
+    float mv[kCombineMax], lv[kCombineMax];
+    float4 ov[kCombineMax];
 #pragma unroll
-  for (int sp = 0; sp < kCombineMax; ++sp) {
-    const bool on = sp < ns;
-    mv[sp] = on ? a.mpart[sp * stride + rh] : -INFINITY;
-    lv[sp] = on ? a.lpart[sp * stride + rh] : 0.f;
-    ov[sp] = (on && has_d) ? *reinterpret_cast<const float4*>(a.opart + (sp * stride + rh) * hd + d)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  float m = -INFINITY;
-#pragma unroll
-  for (int sp = 0; sp < kCombineMax; ++sp) m = fmaxf(m, mv[sp]);
-  const float mb = m == -INFINITY ? 0.f : m;
-  float l = 0.f;
-  float w[kCombineMax];
-#pragma unroll
-  for (int sp = 0; sp < kCombineMax; ++sp) {
-    w[sp] = mv[sp] == -INFINITY ? 0.f : exp2f(mv[sp] - mb);
-    l += w[sp] * lv[sp];
-  }
-  const float inv = l > 0.f ? 1.0f / l : 0.f;
-  if (!has_d) return;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int sp = 0; sp < kCombineMax; ++sp) {
-    const float ww = w[sp] * inv;
-    if (ww != 0.f) {   // skipped partials (no visible key, or sp >= ns) may hold stale values
-      acc.x += ww * ov[sp].x;
-      acc.y += ww * ov[sp].y;
-      acc.z += ww * ov[sp].z;
-      acc.w += ww * ov[sp].w;
+    for (int sp = 0; sp < kCombineMax; ++sp) {
+      const bool on = sp < ns;
+      mv[sp] = on ? a.mpart[sp * stride + rh] : -INFINITY;
+      lv[sp] = on ? a.lpart[sp * stride + rh] : 0.f;
+      ov[sp] = (on && has_d) ? *reinterpret_cast<const float4*>(a.opart + (sp * stride + rh) * hd + d)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    float m = -INFINITY;
+#pragma unroll
+    for (int sp = 0; sp < kCombineMax; ++sp) m = fmaxf(m, mv[sp]);
+    const float mb = m == -INFINITY ? 0.f : m;
+    float l = 0.f;
+    float w[kCombineMax];
+#pragma unroll
+    for (int sp = 0; sp < kCombineMax; ++sp) {
+      w[sp] = mv[sp] == -INFINITY ? 0.f : exp2f(mv[sp] - mb);
+      l += w[sp] * lv[sp];
+    }
+    const float inv = l > 0.f ? 1.0f / l : 0.f;
+    if (!has_d) continue;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int sp = 0; sp < kCombineMax; ++sp) {
+      const float ww = w[sp] * inv;
+      if (ww != 0.f) {   // skipped partials (no visible key, or sp >= ns) may hold stale values
+        acc.x += ww * ov[sp].x;
+        acc.y += ww * ov[sp].y;
+        acc.z += ww * ov[sp].z;
+        acc.w += ww * ov[sp].w;
+      }
+    }
+    if (O) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y), p1 = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&p0);
+      u.y = *reinterpret_cast<uint32_t*>(&p1);
+      *reinterpret_cast<uint2*>(O + rh * hd + d) = u;
+    }
+    if (O_f32) *reinterpret_cast<float4*>(O_f32 + rh * hd + d) = acc;
   }
-  if (O) {
-    __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y), p1 = __floats2bfloat162_rn(acc.z, acc.w);
-    uint2 u;
-    u.x = *reinterpret_cast<uint32_t*>(&p0);
-    u.y = *reinterpret_cast<uint32_t*>(&p1);
-    *reinterpret_cast<uint2*>(O + (size_t)rh * hd + d) = u;
-  }
-  if (O_f32) *reinterpret_cast<float4*>(O_f32 + (size_t)rh * hd + d) = acc;
 }
 
 template <int HD>
@@ -466,7 +471,7 @@ cudaError_t attention_launch(const AttnArgs& a, int B, cudaStream_t st, int* lau
 cudaError_t attn_combine_launch(const AttnArgs& a, bf16* O, float* O_f32, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
   {
-    cudaError_t le = launch_k(k_attn_combine, dim3((a.R * a.H + 7) / 8), dim3(256), 0, st, a, O, O_f32);
+    cudaError_t le = launch_k(k_attn_combine, dim3((a.R * a.KV + 7) / 8), dim3(256), 0, st, a, O, O_f32);
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
