@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.G;
   const int spm = ta.slots_per_mt;
-  int* s_sched = reinterpret_cast<int*>(s_ml + 512);             // [4] balanced-mode cursor
+  int* s_sched = reinterpret_cast<int*>(s_ml + 512);             // [4] balanced-mode cursor, [4] merge flag
   // ---- work items.  An item = (request r, kv head g, a range of the request's 64-key
   // sub-tiles: pages [p_begin, p_begin + npg) then tree halves [th0, th0 + ntree)), chunk c of
   // the nch chunks of (r, g).  Static mode: the item of blockIdx (x = r*KV + g, y = chunk of
@@ -844,6 +844,58 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(o_empty);
       if (rep_of(p, 0) > 1 || (pr && rep_of(p, 1) > 1)) mbar_arrive(scr_done);
       named_bar_sync(2, 256);   // s_ml / ring reuse by the next pass
+      if (balanced && a.merge_cnt && !single && p == n_pass - 1) {
+        // the last CTA to finish a chunk of (r, g) merges all its chunks (split-KV combine, from
+        // L2): the classic fence / counter / last-arriver pattern, no CTA ever waits on another
+        const int et = (warp - 2) * 32 + lane;   // 0..255
+        __threadfence();
+        named_bar_sync(2, 256);
+        if (et == 0) {
+          int* cnt = a.merge_cnt + r * a.KV + g;
+          const int prev = atomicAdd(cnt, 1);
+          s_sched[4] = prev == nch - 1;
+          if (prev == nch - 1) *cnt = 0;   // ready for the next launch
+        }
+        named_bar_sync(2, 256);
+        if (s_sched[4]) {
+          __threadfence();
+          const size_t RH = (size_t)a.R * a.H;
+          const int nrow = S * G;
+          for (int idx = et; idx < nrow * (HD / 4); idx += 256) {
+            const int rl = idx / (HD / 4), d = (idx % (HD / 4)) * 4;
+            const size_t rh = (size_t)(row0 + rl / G) * a.H + (size_t)g * G + rl % G;
+            float mv[8], lv[8];
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              mv[c] = c < nch ? __ldcg(a.mpart + c * RH + rh) : -INFINITY;
+              lv[c] = c < nch ? __ldcg(a.lpart + c * RH + rh) : 0.f;
+              mx = fmaxf(mx, mv[c]);
+            }
+            float lt = 0.f;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              if (mv[c] == -INFINITY) continue;
+              const float w = ex2f(mv[c] - mx);
+              lt += w * lv[c];
+              const float4 v = __ldcg(reinterpret_cast<const float4*>(a.opart + (c * RH + rh) * HD + d));
+              acc.x = fmaf(w, v.x, acc.x);
+              acc.y = fmaf(w, v.y, acc.y);
+              acc.z = fmaf(w, v.z, acc.z);
+              acc.w = fmaf(w, v.w, acc.w);
+            }
+            const float inv = lt > 0.f ? 1.f / lt : 0.f;
+            if (ta.O)
+              *reinterpret_cast<uint2*>(ta.O + rh * HD + d) =
+                  make_uint2(pack2_bf16(acc.x * inv, acc.y * inv), pack2_bf16(acc.z * inv, acc.w * inv));
+            if (ta.O_f32)
+              *reinterpret_cast<float4*>(ta.O_f32 + rh * HD + d) =
+                  make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+          }
+        }
+        named_bar_sync(2, 256);   // s_sched[4] reuse
+      }
     }
     }
   }
@@ -911,8 +963,8 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
   TcArgs ta{a, O, O_f32, spm, pf, trace};
   if (trace) cudaMemsetAsync(trace, 0, 1024 * 8, st);
   constexpr int NST = ring_stages(HD, NQ);
-  const size_t smem = (size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 16;
-  static_assert((size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 16 <=
+  const size_t smem = (size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 32;
+  static_assert((size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 32 <=
                     (size_t)kSmemMax, "attention smem");
   static bool attr = false;
   if (!attr) {

@@ -151,6 +151,8 @@ struct AttnArgs {
   const int* row_req;
   int B, grid_ctas;
   int* nch_tab;               // per_req = 2: [B][KV] chunk counts, written by the attention kernel
+  int* merge_cnt;             // per_req = 2 with merge_cnt: [B][KV] finished-chunk counters (zero
+                              // between launches); the last CTA per (r, g) merges (null: combine kernel)
 };
 cudaError_t attention_launch(const AttnArgs& a, int B, cudaStream_t st, int* launches);
 cudaError_t attn_combine_launch(const AttnArgs& a, bf16* O, float* O_f32, cudaStream_t st,

@@ -125,7 +125,7 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
   size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
-  size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, attn_nch, part_val, part_idx, y, score, tp_gather;
+  size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, attn_nch, attn_cnt, part_val, part_idx, y, score, tp_gather;
   size_t part_m, part_s, lse, row_qnode, pchild, resid_y, resid_s;   // SAMPLE_PQ_DENSE
   size_t noise;                                                       // [R][V] Gumbel noise (sampled modes)
   size_t stage_in, stage_out, total;
@@ -169,6 +169,7 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.mpart = take(4 * (size_t)kMaxSplits * R * H);
   w.lpart = take(4 * (size_t)kMaxSplits * R * H);
   w.attn_nch = take(4 * (size_t)B * KV);   // balanced attention: chunks per (request, kv head)
+  w.attn_cnt = take(4 * (size_t)B * KV);   // balanced attention: finished-chunk counters
   const size_t vt = (c.vocab + 127) / 128;
   w.part_val = take(4 * (size_t)R * vt);
   w.part_idx = take(4 * (size_t)R * vt);
@@ -301,6 +302,12 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     aa.per_req = 2;
     aa.row_req = pa.row_req;
     aa.nch_tab = (int*)P(w.attn_nch);
+    // in-kernel merge when a (request, kv head) has at most one 128-row M-tile (cfg5: 85 rows);
+    // bigger groups (cfg4: 520 rows) would stall the merging CTA's pipeline -> combine kernel
+    if ((in->max_nodes + 1) * G <= 128) {
+      aa.merge_cnt = (int*)P(w.attn_cnt);
+      CK(cudaMemsetAsync(aa.merge_cnt, 0, sizeof(int) * (size_t)B * KV, st));   // self-resetting after
+    }
     aa.grid_ctas = num_sms();
     aa.pages_per_split = std::max(1, (max_pages + kMaxSplits - 1) / kMaxSplits);   // unused by the kernel
   } else if (use_tc) {   // per-request chunks (attn_pick_chunk_tc caps them at 8 = kMaxSplits)
@@ -450,7 +457,8 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     aa.layer = l;
     if (use_tc) {
       { KTimer _t(K_ATTN, st); CK(attention_tc_launch(aa, B, O, nullptr, st, &launches)); }
-      if (aa.n_splits > 1) { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
+      // balanced mode merges its chunks inside the attention kernel (last CTA per (r, g))
+      if (aa.n_splits > 1 && !(aa.per_req == 2 && aa.merge_cnt)) { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }
     } else {
       { KTimer _t(K_ATTN, st); CK(attention_launch(aa, B, st, &launches)); }
       { KTimer _t(K_COMBINE, st); CK(attn_combine_launch(aa, O, nullptr, st, &launches)); }

@@ -369,12 +369,15 @@ def test_full_width_two_layer_slice_matches_oracle(api):
 G8 = ModelShape("g8", 2, 512, 16, 2, 128, 1024, 2048, 1e-5, 500000.0)   # G = 8 (Llama-70B's group at TP 2)
 
 
-@pytest.mark.parametrize("shape,sizes", [(SMALL128, (16, 32, 8, 63, 1)), (G8, (64, 20, 64, 5, 1))])
+@pytest.mark.parametrize("shape,sizes", [(SMALL128, (16, 32, 8, 63, 1)), (G8, (64, 20, 64, 5, 1)),
+                                         (SMALL128, (16, 8, 12, 20, 1))])
 def test_long_ragged_contexts_chunked_attention_matches_oracle(api, shape, sizes):
     """Long contexts (>= 64 pages) switch the tcgen05 attention to the persistent work-balanced
     grid: a 7000-token request is cut into up to 8 chunks combined by k_attn_combine, a 200-token
     one stays a single chunk written final by the attention kernel, in the same launch.  G = 8 with
     64-node trees: 5 M-tiles per request = two pair passes and a replicated single pass per item.
+    Trees of <= 31 nodes (<= 128 rows per kv head): the chunks are merged inside the attention
+    kernel by the last CTA of each (request, kv head) instead of the combine kernel.
     Random-filled caches (gen_kv_fill on the oracle side), every slot's target compared."""
     rng = np.random.default_rng(909)
     ctx = [4500, 200, 7000, 4100, 64]
