@@ -721,15 +721,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_ml[u * 256 + 128 + q * 32 + lane] = l;
       }
       if (rf > 1) {
-        // partial (m, l, O) of every replica (of both units in a single pass) -> the K/V ring,
-        // idle now: a replicated tile is always the last M-tile, so this is the last pass and
-        // o_full says every MMA reading the ring has completed
-        const int np_ = pr ? rf : 2 * rf;
-        const int pidx = (pr ? 0 : u) * rf + rq;
+        // partial (m, l, O) of every replica -> the K/V ring, idle now: o_full says every MMA
+        // reading the ring has completed, and the producer loads nothing into it before this
+        // pass's scr_done
+        // replica partial pidx = u*rf + rq occupies rows [pidx*rrows, (pidx+1)*rrows) of a
+        // 256-row scratch (rf * rrows = 128 per unit): in a pair pass each unit merges its own
+        // replicas, in a single pass both units' replicas of the one tile are merged together
+        const int pidx = u * rf + rq;
         constexpr int PS = HD + 4;                        // padded row stride (floats)
-        float* part = reinterpret_cast<float*>(sK);       // [np_][rrows][PS]
-        float* pm = part + (size_t)np_ * rrows * PS;      // [np_][rrows]
-        float* pl = pm + np_ * rrows;
+        float* part = reinterpret_cast<float*>(sK);       // [256 rows][PS]
+        float* pm = part + (size_t)256 * PS;              // [256 rows]
+        float* pl = pm + 256;
         pm[pidx * rrows + ri] = m_used;
         pl[pidx * rrows + ri] = l;
         float* dst = part + ((size_t)pidx * rrows + ri) * PS;
@@ -797,11 +799,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         // merge the replicas: the unit's (pair pass) or both units' (single pass) threads
         // cooperate over (row, 32-column chunk) items of the tile
-        const int np_ = pr ? rf : 2 * rf;
+        const int np_ = pr ? rf : 2 * rf;          // partials to merge, from pidx p0
+        const int p0 = pr ? u * rf : 0;
         constexpr int PS = HD + 4;
-        const float* part = reinterpret_cast<const float*>(sK);
-        const float* pm = part + (size_t)np_ * rrows * PS;
-        const float* pl = pm + np_ * rrows;
+        const float* part = reinterpret_cast<const float*>(sK) + (size_t)p0 * rrows * PS;
+        const float* pm = reinterpret_cast<const float*>(sK) + (size_t)256 * PS + p0 * rrows;
+        const float* pl = pm + 256;
         const int nthr = pr ? 128 : 256;
         const int tid = pr ? q * 32 + lane : (u * 128 + q * 32 + lane);
         const int items = rows_mt * (HD / 32);
@@ -942,10 +945,18 @@ bool tmap_q(CUtensorMap* m, const void* base, uint64_t R, int H, int hd, int G, 
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Slots per 128-row M-tile: floor(128/G), or floor(64/G) with SPECEDGE_ATTN_HALF_TILES=1 (every
+// full tile then runs with 2-way row replication, i.e. half the keys per softmax thread, at the
+// price of more passes over the KV stream)
+int attn_slots_per_tile(int G) {
+  static const bool half = getenv("SPECEDGE_ATTN_HALF_TILES") && getenv("SPECEDGE_ATTN_HALF_TILES")[0] == '1';
+  return (half && G <= 64) ? 64 / G : 128 / G;
+}
+
 template <int HD, int NQ>
 cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStream_t st) {
   CUtensorMap tq, tp, tt;
-  const int spm = 128 / a.G;
+  const int spm = attn_slots_per_tile(a.G);
   const uint64_t pool_rows = (uint64_t)(a.layer + 1) * a.num_pages * 2 * a.KV * 64;
   const uint64_t tree_rows = (uint64_t)(a.layer + 1) * 2 * a.KV * a.R_cap;
   // replicated loads of small tail tiles: boxes of floor(64/G) / floor(32/G) slots (a tile is
@@ -1006,7 +1017,7 @@ cudaError_t attention_tc_launch(const AttnArgs& a, int B, bf16* O, float* O_f32,
   if (launches) ++*launches;
   // one Q tile (and a deeper K/V ring) when every request's rows fit one M-tile
   static const int force_nq = getenv("SPECEDGE_ATTN_NQ") ? atoi(getenv("SPECEDGE_ATTN_NQ")) : 0;
-  const bool one = force_nq ? force_nq == 1 : a.max_rows / a.G <= 128 / a.G;
+  const bool one = force_nq ? force_nq == 1 : a.max_rows / a.G <= attn_slots_per_tile(a.G);
   if (a.hd == 128) return one ? launch_tc<128, 1>(a, B, O, O_f32, st) : launch_tc<128, 2>(a, B, O, O_f32, st);
   if (a.hd == 64) return one ? launch_tc<64, 1>(a, B, O, O_f32, st) : launch_tc<64, 2>(a, B, O, O_f32, st);
   return cudaErrorInvalidValue;
