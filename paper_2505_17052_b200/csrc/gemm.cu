@@ -119,6 +119,56 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         }
       }
       named_bar_sync(1, kEpiThreads);
+    } else if constexpr (MODE == EPI_QKV) {
+      // 128-feature tile m128 = one head (head_dim 128): q heads [0, H), k heads [H, H+KV), v
+      // heads after.  q / k: rotate-half RoPE at row_pos (pairs (i, i+64) sit in lanes i and
+      // i+64, exchanged through shared memory as in the SwiGLU epilogue); v: plain fp16 copy.
+      // Same arithmetic and rounding as k_qkv_rope (fp32 in, one fp16 rounding out).
+      const int head = m128;
+      const int H = a.n_heads, KV = a.n_kv;
+      f16* const Qo = reinterpret_cast<f16*>(a.out_bf16);
+      f16* const kv = reinterpret_cast<f16*>(a.tree_kv);
+      if (head >= H + KV) {   // v head: lane tl = element tl of the row
+        const int kvh = head - H - KV;
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+          const int row = row_base + j;
+          if (j < ncol && row < a.R)
+            kv[((((size_t)a.layer * 2 + 1) * KV + kvh) * a.R_cap + row) * 128 + tl] = __float2half_rn(__uint_as_float(v[j]));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
+        named_bar_sync(1, kEpiThreads);
+        const int f = et & 63, hsel = et >> 6;   // pair (f, f + 64), rows [16 hsel, 16 hsel + 16)
+        f16* const base = head < H ? Qo + (size_t)head * 128
+                                   : kv + (((size_t)a.layer * 2 + 0) * KV + (head - H)) * a.R_cap * 128;
+        const size_t rstride = head < H ? (size_t)H * 128 : 128;
+        // all 16 rows' positions, then all cos / sin, in flight together (the epilogue must not
+        // serialise on dependent global loads)
+        int pos[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int row = row_base + hsel * 16 + jj;
+          pos[jj] = (hsel * 16 + jj < ncol && row < a.R) ? __ldg(a.row_pos + row) : -1;
+        }
+        float cs[16], sn[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          cs[jj] = pos[jj] >= 0 ? __ldg(a.rope_cos + (size_t)pos[jj] * 64 + f) : 0.f;
+          sn[jj] = pos[jj] >= 0 ? __ldg(a.rope_sin + (size_t)pos[jj] * 64 + f) : 0.f;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          if (pos[jj] < 0) continue;
+          const int j = hsel * 16 + jj;
+          const float x1 = xch[f * kXchStride + j], x2 = xch[(f + 64) * kXchStride + j];
+          f16* dst = base + (size_t)(row_base + j) * rstride;
+          dst[f] = __float2half_rn(x1 * cs[jj] - x2 * sn[jj]);
+          dst[f + 64] = __float2half_rn(x2 * cs[jj] + x1 * sn[jj]);
+        }
+        named_bar_sync(1, kEpiThreads);
+      }
     } else if constexpr (MODE == EPI_ARGMAX || MODE == EPI_PQ1 || MODE == EPI_PQ2) {
       // a.pair: physical rows (2r, 2r+1) = hi/lo parts of logical row r -> 16 logical columns
       const int np = a.pair ? 16 : 32;
@@ -702,6 +752,21 @@ int gemm_splits_last() { return g_last_splits; }
 
 // Activation-row tile: the fewest <= 256-row tiles, rows rounded up to a multiple of 16
 // (measured: 5 x 224 beats 6 x 176 for the 1056-row LM head; larger N per MMA instruction)
+// The QKV projection runs with the fused RoPE epilogue (EPI_QKV, never K-split) when the fp32
+// path would not split it either: its pair tiles fill 90-100 % of one wave of CTA pairs, or at
+// least 1.5 waves (host-side estimate with one pair per two SMs).
+bool gemm_qkv_fused_ok(int M, int R) {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int bn = gemm_pick_bn(R);
+  const int ntiles = ((M + 255) / 256) * ((R + bn - 1) / bn);
+  const int nc = g_num_sms / 2;
+  return (ntiles * 10 >= nc * 9 && ntiles <= nc) || ntiles * 2 >= nc * 3;
+}
+
 int gemm_pick_bn(int R) {
   const int nt = (R + 255) / 256;
   int bn = (R + nt - 1) / nt;
@@ -750,6 +815,7 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
     case EPI_ARGMAX: pe = prep_mode2<EPI_ARGMAX>(); nclusters = max_clusters2<EPI_ARGMAX>(2 * nc, smem); break;
     case EPI_PQ1: pe = prep_mode2<EPI_PQ1>(); nclusters = max_clusters2<EPI_PQ1>(2 * nc, smem); break;
     case EPI_PQ2: pe = prep_mode2<EPI_PQ2>(); nclusters = max_clusters2<EPI_PQ2>(2 * nc, smem); break;
+    case EPI_QKV: pe = prep_mode2<EPI_QKV>(); nclusters = max_clusters2<EPI_QKV>(2 * nc, smem); break;
     default: return cudaErrorInvalidValue;
   }
   if (pe != cudaSuccess) return pe;
@@ -775,6 +841,7 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
     case EPI_ARGMAX: return launch_mode2<EPI_ARGMAX>(tmW, tmX, b, smem, grid, st);
     case EPI_PQ1: return launch_mode2<EPI_PQ1>(tmW, tmX, b, smem, grid, st);
     case EPI_PQ2: return launch_mode2<EPI_PQ2>(tmW, tmX, b, smem, grid, st);
+    case EPI_QKV: return launch_mode2<EPI_QKV>(tmW, tmX, b, smem, grid, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -830,6 +897,7 @@ cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArg
     case EPI_ARGMAX: return launch_mode<EPI_ARGMAX>(tmW, tmX, a, smem, grid, st);
     case EPI_PQ1: return launch_mode<EPI_PQ1>(tmW, tmX, a, smem, grid, st);
     case EPI_PQ2: return launch_mode<EPI_PQ2>(tmW, tmX, a, smem, grid, st);
+    case EPI_QKV: return launch_mode<EPI_QKV>(tmW, tmX, a, smem, grid, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -45,6 +45,7 @@ enum GemmMode : int {
   EPI_ARGMAX = 4,  // per (row, 128-vocab tile) max / Gumbel-max   (a9)
   EPI_PQ1 = 5,     // NEXT-F2 pass 1: EPI_ARGMAX (Gumbel-max) + per-tile (max, sum exp) of l/T
   EPI_PQ2 = 6,     // NEXT-F2 pass 2: per-tile Gumbel-max of log max(0, p - q) + p(child token)
+  EPI_QKV = 7,     // a4 with RoPE fused (head_dim 128, unsplit): q -> Q fp16, k/v -> tree K/V fp16
 };
 
 constexpr int kMaxFusedTp = 4;   // NEXT-F4: ranks of the fused GEMM -> reduce-scatter
@@ -114,6 +115,7 @@ cudaError_t gumbel_fill_launch(float* noise, int R, int vocab, int vocab_off, co
 // Build a 2D bf16 tensor map [rows][cols] (cols contiguous), box {64, box_rows}, 128B swizzle.
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 int gemm_pick_bn(int R);
+bool gemm_qkv_fused_ok(int M, int R);
 int gemm_splits_last();   // K-splits chosen by the last gemm_launch on this thread
 void gemm_force_single(bool on);   // tests/probes: disable the CTA-pair kernel
 cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArgs a,

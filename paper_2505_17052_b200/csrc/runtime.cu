@@ -432,28 +432,53 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   };
   static const bool f4_ag_on = getenv("SPECEDGE_TP_F4_AG") && getenv("SPECEDGE_TP_F4_AG")[0] == '1';
   bf16* const Hn_in = (fused && f4_ag_on) ? m->tp_hn : Hn;   // operand of the column-parallel GEMMs
+  // QKV GEMM with the RoPE epilogue (SPECEDGE_QKV_FUSED=1; head_dim 128, when it would run
+  // unsplit anyway).  Off by default: measured on cfg2 the fused epilogue outlasts the short
+  // QKV mainloop (1.57 vs 0.97 + 0.35 ms per step with the separate RoPE kernel)
+  static const bool qkv_fuse_env = getenv("SPECEDGE_QKV_FUSED") && getenv("SPECEDGE_QKV_FUSED")[0] == '1';
+  const bool qkv_fused = qkv_fuse_env && hd == 128 && gemm_qkv_fused_ok((H + 2 * KV) * hd, R);
   for (int l = 0; l < c.n_layers; ++l) {
     g_dbg_layer = l;
     const auto& Lw = m->layers[l];
     { const specedge_status ns = norm_rows(pendingY, Lw.g_attn, Hn, 0); if (ns != SPECEDGE_OK) return ns; }
-    const int sq = f32_gemm(K_QKV, Lw.tm_qkv, Hn_in, (H + 2 * KV) * hd, c.d, false);
-    if (sq < 0) return SPECEDGE_E_CUDA;
-    RopeArgs ra{};
-    ra.Y = Y;
-    ra.nY = sq;
-    ra.y_stride = y_stride;
-    ra.R = R;
-    ra.H = H;
-    ra.KV = KV;
-    ra.hd = hd;
-    ra.layer = l;
-    ra.R_cap = R_cap;
-    ra.row_pos = pa.row_pos;
-    ra.rope_cos = m->rope_cos;
-    ra.rope_sin = m->rope_sin;
-    ra.Q = Q;
-    ra.tree_kv = tree_kv;
-    { KTimer _t(K_ROPE, st); CK(qkv_rope_launch(ra, st, &launches)); }
+    if (qkv_fused) {
+      // a4 with RoPE in the GEMM epilogue: q -> Q, k / v -> tree K/V, no fp32 round trip
+      GemmArgs gq{};
+      gq.M = (H + 2 * KV) * hd;
+      gq.R = R;
+      gq.K = c.d;
+      gq.out_bf16 = reinterpret_cast<bf16*>(Q);
+      gq.tree_kv = reinterpret_cast<bf16*>(tree_kv);
+      gq.R_cap = R_cap;
+      gq.layer = l;
+      gq.n_heads = H;
+      gq.n_kv = KV;
+      gq.head_dim = hd;
+      gq.row_pos = pa.row_pos;
+      gq.rope_cos = m->rope_cos;
+      gq.rope_sin = m->rope_sin;
+      KTimer _t(K_QKV, st);
+      CK(gemm_launch(EPI_QKV, Lw.tm_qkv, Hn_in, gq, st, &launches));
+    } else {
+      const int sq = f32_gemm(K_QKV, Lw.tm_qkv, Hn_in, (H + 2 * KV) * hd, c.d, false);
+      if (sq < 0) return SPECEDGE_E_CUDA;
+      RopeArgs ra{};
+      ra.Y = Y;
+      ra.nY = sq;
+      ra.y_stride = y_stride;
+      ra.R = R;
+      ra.H = H;
+      ra.KV = KV;
+      ra.hd = hd;
+      ra.layer = l;
+      ra.R_cap = R_cap;
+      ra.row_pos = pa.row_pos;
+      ra.rope_cos = m->rope_cos;
+      ra.rope_sin = m->rope_sin;
+      ra.Q = Q;
+      ra.tree_kv = tree_kv;
+      { KTimer _t(K_ROPE, st); CK(qkv_rope_launch(ra, st, &launches)); }
+    }
     aa.layer = l;
     if (use_tc) {
       { KTimer _t(K_ATTN, st); CK(attention_tc_launch(aa, B, O, nullptr, st, &launches)); }
