@@ -1,11 +1,16 @@
 // Tree-masked paged split-KV attention on tcgen05 ("custom attention
 // masking for each token sequence in the batch ... without cross-sequence interference").
 //
-// One CTA per (request r, kv head g, split sp).  Query rows of the item are the request's S slots
-// x the G query heads sharing kv head g (row = s*G + j), cut into 128-row M-tiles of
-// G*floor(128/G) rows.  Keys stream in 64-key sub-tiles (one page of the paged cache each, then —
-// in the last split — the S tree slots from the tree K/V scratch, masked by the uint64
-// ancestor-or-self bitmask) through a 5-stage TMA ring.
+// Work item = (request r, kv head g, a range of the request's 64-key sub-tiles: pages of the paged
+// cache, then the tree slots from the tree K/V scratch, masked by the uint64 ancestor-or-self
+// bitmask).  Query rows of an item are the request's S slots x the G query heads sharing kv head g
+// (row = s*G + j), cut into 128-row M-tiles of G*floor(128/G) rows.  Sub-tiles stream through a
+// TMA ring (hd 128: 5 stages with two Q tiles, 6 with one).
+//   static mode:   one CTA per (r, g, chunk of pages_per_split pages; the tree in the last chunk)
+//   balanced mode: a persistent grid; the concatenated (r, g) sub-tile sequences are split
+//                  evenly over the CTAs, the pipeline runs on across a CTA's items, and for groups
+//                  of <= 128 rows the last CTA to finish a chunk of (r, g) merges all its chunks
+//                  (long contexts: cfg5), otherwise k_attn_combine does.
 //
 // Two "units" share the CTA; a unit = one softmax warpgroup + its TMEM (two 64-column S buffers
 // + a 128-column O accumulator).  A pass streams the KV once:
