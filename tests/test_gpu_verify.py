@@ -420,3 +420,37 @@ def test_long_ragged_contexts_chunked_attention_matches_oracle(api, shape, sizes
     finally:
         pool.close()
         model.close()
+
+
+def test_verify_is_bitwise_deterministic(api):
+    """Two verifies of the same batch give bit-identical logits, targets and scores: every
+    reduction has a fixed order (K-split partials summed in split order by the consumer, split-KV
+    chunks merged in chunk order — also by whichever CTA of the balanced attention finishes last)."""
+    shape = SMALL128
+    rng = np.random.default_rng(4242)
+    ctx = [5000, 300, 6100, 64]
+    B = len(ctx)
+    model = api.Model(shape, 5, max_position=8192)
+    pool = api.KVPool(model, sum((c + 127) // 64 for c in ctx) + 8, B)
+    try:
+        hs = []
+        for r in range(B):
+            h = pool.alloc(ctx[r] + 64)
+            pool.fill_random(h, ctx[r] - 1, 99, r)
+            hs.append(h)
+        trees = [pooled_tree(rng, n, 5, 3, shape.vocab) for n in (20, 8, 31, 1)]   # <= 128 rows/kv head
+        ws = model.workspace(B, sum(t.n + 1 for t in trees), 6200)
+        batch = api.Batch.from_host(hs, ctx, [3] * B, [500 + r for r in range(B)], [0] * B, trees,
+                                    max_context_len=6200)
+        runs = []
+        for _ in range(2):
+            out = api.verify(model, pool, batch, ws, mode=api.L.SAMPLE_TREE, temperature=1.0, seed=3,
+                             auto_commit=False)
+            lg = api.debug_last_logits(model, ws, batch).cpu().numpy()
+            runs.append((lg.view(np.uint32).copy(), out.row_target.cpu().numpy().copy(),
+                         out.row_score.cpu().numpy().view(np.uint32).copy()))
+        for a, b in zip(runs[0], runs[1]):
+            assert np.array_equal(a, b)
+    finally:
+        pool.close()
+        model.close()
