@@ -148,7 +148,7 @@ def setup_gpu(wl, rank, device, tp=None, model=None, pool=None, mb=0):
         else:
             model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64, tp_rank=tp[0],
                               tp_size=tp[1], nccl_id=tp[2])
-            if os.environ.get("SPECEDGE_TP_FUSED", "1") == "1" and tp[1] <= 4:
+            if os.environ.get("SPECEDGE_TP_FUSED", "1") == "1" and tp[1] <= 8:
                 # NEXT-F4: O / down GEMM -> reduce-scatter fused over NVLink peer memory
                 model.tp_fused_enable(wl.n_requests * (wl.n_nodes + 1))
     if pool is None:

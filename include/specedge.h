@@ -64,7 +64,8 @@ typedef struct specedge_kvpool specedge_kvpool;
 #define SPECEDGE_REQ_E_TREE_SIZE 2    /* N > 64 nodes                            (amb. A5) */
 #define SPECEDGE_REQ_E_TOKEN 3        /* root or draft token outside [0, V)              */
 #define SPECEDGE_REQ_E_DUP_SIBLING 4  /* two children of one parent share a token */
-#define SPECEDGE_REQ_E_CONTEXT 5      /* context_len != cached + 1, or > max_context_len
+#define SPECEDGE_REQ_E_CONTEXT 5      /* context_len != cached + 1, or > max_context_len, or a
+                                         tree position cached + depth >= max_position
                                          ("context-length mismatch -> protocol error") */
 #define SPECEDGE_REQ_E_KV_CAPACITY 6  /* cached + deepest path + 1 exceeds the handle's capacity */
 #define SPECEDGE_REQ_E_HANDLE 7       /* KV handle not allocated */
@@ -123,8 +124,11 @@ specedge_status specedge_model_destroy(specedge_model* model);
 specedge_status specedge_tp_unique_id(uint8_t* nccl_id /* [128] host */);
 specedge_status specedge_model_create_tp(const specedge_model_config* cfg, uint64_t weight_seed,
                                          int32_t device, int32_t tp_rank, int32_t tp_size,
-                                         const uint8_t* nccl_id /* [128] host, NULL iff tp_size == 1 */,
+                                         const uint8_t* nccl_id /* [128] host; see below */,
                                          specedge_model** out);
+/* nccl_id == NULL with tp_size > 1 creates a communicator-less shard: weights, KV pool and the
+ * debug introspection work (one process can compare every shard with the tp_size == 1 model on
+ * one GPU), verify / prefill return E_UNSUPPORTED. */
 /* This rank's position and LM-head vocab shard [vocab0, vocab0 + vocab_n); NULL outputs skipped. */
 specedge_status specedge_model_tp_info(const specedge_model* model, int32_t* tp_rank,
                                        int32_t* tp_size, int32_t* vocab0, int32_t* vocab_n);
@@ -150,7 +154,8 @@ specedge_status specedge_kvpool_create(specedge_model* model, int32_t num_pages,
                                        int32_t max_handles, specedge_kvpool** out);
 specedge_status specedge_kvpool_destroy(specedge_kvpool* pool);
 /* Reserve pages for a session able to hold `capacity_tokens` cached tokens; returns the handle
- * (>= 0) in *out_handle with cached length 0.  E_OOM if pages or handles are exhausted.
+ * (>= 0) in *out_handle with cached length 0.  E_OOM if pages or handles are exhausted;
+ * E_INVALID if capacity_tokens <= 0 or > the model's max_position (RoPE table length).
  * Synchronous (host allocator + one small H2D copy). */
 specedge_status specedge_kv_alloc(specedge_kvpool* pool, int32_t capacity_tokens,
                                   int32_t* out_handle);
@@ -246,7 +251,8 @@ specedge_status specedge_verify_batch_host(specedge_model* model, specedge_kvpoo
 /* ---- test introspection (used by tests/ only; never on the verify path) ---- */
 /* Logical weight rows back to the host as bf16 bits: tensor ids as in oracle/model.py
  * (1 embed, 2 wq, 3 wk, 4 wv, 5 wo, 6 wg, 7 wu, 8 wd, 9 lm_head, 10 g_attn, 11 g_mlp,
- * 12 g_final).  Synchronous. */
+ * 12 g_final).  Of a tensor-parallel shard: its local rows and columns (row 0 of lm_head = vocab
+ * id vocab0).  Synchronous. */
 specedge_status specedge_debug_weight_rows(specedge_model* model, int32_t tensor, int32_t layer,
                                            int32_t row0, int32_t nrows, uint16_t* dst_host);
 /* Cached K or V (kv_sel 0/1) of positions [pos0, pos0+n) of a session, layer `layer`, as fp16
@@ -254,6 +260,14 @@ specedge_status specedge_debug_weight_rows(specedge_model* model, int32_t tensor
 specedge_status specedge_debug_read_kv(specedge_kvpool* pool, int32_t handle, int32_t layer,
                                        int32_t kv_sel, int32_t pos0, int32_t n,
                                        uint16_t* dst_host);
+/* Tree K/V scratch of the last verify with this workspace and batch size (num_requests B,
+ * rows R = total_nodes + B): K or V (kv_sel 0/1) of rows [row0, row0+n) of `layer`, as fp16 bits
+ * [n][n_kv][head_dim] into host memory.  Row node_offset[r] + r is request r's root slot, the next
+ * N_r rows its nodes (the rows a commit copies into the pages).  Synchronous. */
+specedge_status specedge_debug_read_tree_kv(specedge_model* model, const void* workspace,
+                                            size_t ws_bytes, int32_t num_requests, int32_t R,
+                                            int32_t layer, int32_t kv_sel, int32_t row0,
+                                            int32_t n, uint16_t* dst_host);
 /* Run the tcgen05 GEMM alone: out[r][m] = sum_k X[r][k] * W[m][k] (bf16 in, fp32 out), all
  * device pointers, row-major.  M, K multiples of 64 (M tile zero-padded), R >= 1. */
 specedge_status specedge_debug_gemm(const uint16_t* W, const uint16_t* X, float* out, int32_t M,

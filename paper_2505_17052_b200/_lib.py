@@ -24,7 +24,7 @@ EXPORTS = [
     "specedge_kvpool_destroy", "specedge_kv_alloc", "specedge_kv_free", "specedge_kv_set_len",
     "specedge_kv_get_len", "specedge_kv_fill_random", "specedge_workspace_size", "specedge_prefill",
     "specedge_verify_batch", "specedge_kv_commit", "specedge_verify_batch_host",
-    "specedge_debug_weight_rows", "specedge_debug_read_kv", "specedge_debug_gemm",
+    "specedge_debug_weight_rows", "specedge_debug_read_kv", "specedge_debug_read_tree_kv", "specedge_debug_gemm",
     "specedge_debug_last_logits", "specedge_debug_attention", "specedge_last_launch_count",
     "specedge_set_kernel_timing", "specedge_kernel_times", "specedge_tp_unique_id", "specedge_model_create_tp",
     "specedge_model_tp_info", "specedge_calibrate_draft_depth", "specedge_scheduler_create",
@@ -97,6 +97,7 @@ def load(path: str = LIB_PATH):
         "specedge_verify_batch_host": [P, P, C.POINTER(VerifyIn), C.POINTER(VerifyOut), P, SZ, P],
         "specedge_debug_weight_rows": [P, I32, I32, I32, I32, P],
         "specedge_debug_read_kv": [P, I32, I32, I32, I32, I32, P],
+        "specedge_debug_read_tree_kv": [P, P, SZ, I32, I32, I32, I32, I32, I32, P],
         "specedge_debug_gemm": [P, P, P, I32, I32, I32, P],
         "specedge_debug_last_logits": [P, P, SZ, I32, I32, P, P],
         "specedge_debug_attention": [P, P, P, P, P, P, I32, I32, I32, I32, I32, P, P, SZ, P],

@@ -64,11 +64,13 @@ class Model:
             L.check(self.lib.specedge_model_create(C.byref(cfg), C.c_uint64(weight_seed), device, C.byref(h)),
                     "model_create")
         else:
-            if nccl_id is None or len(nccl_id) != 128:
-                raise ValueError("tp_size > 1 needs the 128-byte NCCL id from tp_unique_id()")
-            idb = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+            # nccl_id None: a communicator-less shard (weights / KV introspection only)
+            if nccl_id is not None and len(nccl_id) != 128:
+                raise ValueError("tp_size > 1 needs the 128-byte NCCL id from tp_unique_id() (or None)")
+            idb = None if nccl_id is None else (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
             L.check(self.lib.specedge_model_create_tp(C.byref(cfg), C.c_uint64(weight_seed), device, tp_rank,
-                                                      tp_size, C.cast(idb, C.c_void_p), C.byref(h)),
+                                                      tp_size, None if idb is None else C.cast(idb, C.c_void_p),
+                                                      C.byref(h)),
                     "model_create_tp")
         self.h = h
         self.max_position = max_position
@@ -154,6 +156,23 @@ class KVPool:
         return out
 
 
+def pack_trees(trees):
+    """CSR packing of draft trees (objects with .n, .parent, .token, .logprob) over requests:
+    node_offset[B+1], parent, token (int32) and draft log-prob (float32) — the layout of
+    specedge_verify_in (include/specedge.h)."""
+    off = np.zeros(len(trees) + 1, np.int32)
+    for i, t in enumerate(trees):
+        off[i + 1] = off[i] + t.n
+    if trees:
+        parent = np.concatenate([np.asarray(t.parent) for t in trees]).astype(np.int32)
+        token = np.concatenate([np.asarray(t.token) for t in trees]).astype(np.int32)
+        logprob = np.concatenate([np.asarray(t.logprob) for t in trees]).astype(np.float32)
+    else:
+        parent = token = np.zeros(0, np.int32)
+        logprob = np.zeros(0, np.float32)
+    return off, parent, token, logprob
+
+
 @dataclass
 class Batch:
     """Device-resident verify inputs (specedge_verify_in's arrays) plus host scalars."""
@@ -182,8 +201,7 @@ class Batch:
     @classmethod
     def from_host(cls, kv, context_len, root_token, session_id, rnd, trees, device="cuda",
                   max_context_len=None, max_nodes=None):
-        from synth.trees import pack
-        off, parent, token, logprob = pack(trees)
+        off, parent, token, logprob = pack_trees(trees)
         dev = torch.device(device)
         t32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.int32)).to(dev)
         ctx = np.ascontiguousarray(context_len, np.int32)
@@ -289,6 +307,17 @@ def host_outputs(hb: HostBatch):
 
 def last_launch_count() -> int:
     return int(L.load().specedge_last_launch_count())
+
+
+def debug_read_tree_kv(model: Model, ws: torch.Tensor, batch: Batch, layer: int, kv_sel: int, row0: int,
+                       n: int) -> np.ndarray:
+    """Tree K/V scratch rows [row0, row0+n) of the last verify of `batch` with workspace `ws`, as
+    fp16 bits [n][n_kv][head_dim] (test introspection)."""
+    out = np.empty((n, model.n_kv_local, model.shape.head_dim), np.uint16)
+    L.check(model.lib.specedge_debug_read_tree_kv(model.h, _ptr(ws), ws.numel(), batch.num_requests, batch.rows,
+                                                  layer, kv_sel, row0, n, out.ctypes.data_as(C.c_void_p)),
+            "debug_read_tree_kv")
+    return out
 
 
 def debug_gemm(W: torch.Tensor, X: torch.Tensor, stream=None) -> torch.Tensor:

@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -9,6 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspecedge.so")
+STAMP = LIB + ".sha256"   # source hash of the library build (git-ignored with the .so)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -27,11 +29,24 @@ def deps():
         [os.path.join(HERE, "..", "include", "specedge.h")]
 
 
+def source_hash() -> str:
+    """sha256 over every source / header the library is built from, the flags and the nvcc path:
+    the library is reused only if it was built from exactly these bytes (file mtimes are not
+    trusted: a snapshot copy or a checkout can leave an old .so newer than changed sources)."""
+    h = hashlib.sha256()
+    for p in deps():
+        h.update(os.path.relpath(p, HERE).encode())
+        with open(p, "rb") as f:
+            h.update(hashlib.sha256(f.read()).digest())
+    h.update(" ".join(FLAGS + [NVCC]).encode())
+    return h.hexdigest()
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(p) <= t for p in deps())
+    with open(STAMP) as f:
+        return f.read().strip() == source_hash()
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
@@ -63,6 +78,11 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     os.replace(lib + ".tmp", lib)
     for o in objs:
         os.remove(o)
+    if lib == LIB and not defines:
+        with open(STAMP, "w") as f:
+            f.write(source_hash() + "\n")
+    elif lib == LIB and os.path.exists(STAMP):
+        os.remove(STAMP)
     return lib
 
 

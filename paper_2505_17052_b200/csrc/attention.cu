@@ -410,12 +410,13 @@ cudaError_t launch_hd(const AttnArgs& a, int B, cudaStream_t st) {
   const int nwarps = std::max(1, std::min(kMaxWarps, rows_pad / 16));
   const int max_S = a.max_rows / a.G;
   const size_t smem = (size_t)rows_pad * HD * 2 + 4 * 64 * HD * 2 + (size_t)max_S * 8 + 16;
-  static size_t attr = 0;
-  if (smem > attr) {
+  static size_t attr[kMaxDevices] = {};   // per-device attribute
+  const int dev = current_device();
+  if (smem > attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_tree_attention<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max(smem, (size_t)48 * 1024));
     if (e != cudaSuccess) return e;
-    attr = std::max(smem, (size_t)48 * 1024);
+    attr[dev] = std::max(smem, (size_t)48 * 1024);
   }
   dim3 grid(B * a.KV, a.n_splits);
   {

@@ -982,11 +982,13 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
   const size_t smem = (size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 32;
   static_assert((size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 32 <=
                     (size_t)kSmemMax, "attention smem");
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;   // per-device attribute
+  if (attr.first()) {
     cudaError_t e = cudaFuncSetAttribute(k_attn_tc<HD, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-    if (e != cudaSuccess) return e;
-    attr = true;
+    if (e != cudaSuccess) {
+      attr.done.fetch_and(~(1ull << current_device()));
+      return e;
+    }
   }
   const dim3 grid = a.per_req == 2 ? dim3(a.grid_ctas) : dim3(B * a.KV, a.n_splits);
   {

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <map>
+#include <mutex>
 #include <cstdlib>
 
 namespace se {
@@ -65,7 +66,30 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
                                           int row_base, int ncol, int sk, float* xch, float* red_v, int* red_i) {
     const int feat = m128 * 128 + tl;
     if constexpr (MODE == EPI_F32) {
-      if (feat < a.M) {
+      if (a.push) {
+        // NEXT-F4 push: stage the chunk row-major (32 rows x 128 features = 32 x 512 B), then
+        // one lane per warp sends 8 rows to their owners' receive slots with bulk async copies
+        // (remote rows cross NVLink) — the epilogue warps never wait on a remote store.  Every
+        // epilogue thread reaches both barriers (lanes past M stage zeros); a copy carries only
+        // the tile's features below M.
+        for (int j = 0; j < 32; ++j) xch[j * 128 + tl] = feat < a.M ? __uint_as_float(v[j]) : 0.f;
+        fence_proxy_async_smem();
+        named_bar_sync(1, kEpiThreads);
+        const uint32_t nbytes = (uint32_t)min(128, a.M - m128 * 128) * 4u;
+        if ((et & 31) == 0) {   // one issuing lane per epilogue warp, 8 rows each
+          for (int j = (et >> 5) * 8; j < min(ncol, (et >> 5) * 8 + 8); ++j) {
+            const int row = row_base + j;
+            if (row >= a.R) break;
+            const int o = row / a.rows_per_rank;
+            bulk_s2g(a.peer_out[o] + (size_t)a.tp_src * a.slot_stride + (size_t)(row - o * a.rows_per_rank) * a.ldo +
+                         m128 * 128,
+                     xch + j * 128, nbytes);
+          }
+          bulk_commit();
+          bulk_wait_read0();   // the staging buffer may be overwritten
+        }
+        named_bar_sync(1, kEpiThreads);
+      } else if (feat < a.M) {
         if (a.pair) {   // physical rows 2r, 2r+1 hold hi/lo parts of logical row r
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
@@ -73,26 +97,6 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
             if (j < ncol && row < a.R)
               a.out_f32[(size_t)(row >> 1) * a.ldo + feat] = __uint_as_float(v[j]) + __uint_as_float(v[j + 1]);
           }
-        } else if (a.push) {
-          // NEXT-F4 push: stage the chunk row-major (32 rows x 128 features = 32 x 512 B), then
-          // one lane per warp sends 8 rows to their owners' receive slots with bulk async copies
-          // (remote rows cross NVLink) — the epilogue warps never wait on a remote store
-          for (int j = 0; j < 32; ++j) xch[j * 128 + tl] = __uint_as_float(v[j]);
-          fence_proxy_async_smem();
-          named_bar_sync(1, kEpiThreads);
-          if ((et & 31) == 0) {   // one issuing lane per epilogue warp, 8 rows each
-            for (int j = (et >> 5) * 8; j < min(ncol, (et >> 5) * 8 + 8); ++j) {
-              const int row = row_base + j;
-              if (row >= a.R) break;
-              const int o = row / a.rows_per_rank;
-              bulk_s2g(a.peer_out[o] + (size_t)a.tp_src * a.slot_stride + (size_t)(row - o * a.rows_per_rank) * a.ldo +
-                           m128 * 128,
-                       xch + j * 128, 512);
-            }
-            bulk_commit();
-            bulk_wait_read0();   // the staging buffer may be overwritten
-          }
-          named_bar_sync(1, kEpiThreads);
         } else {
           float* out = a.out_f32 + (size_t)sk * a.split_stride;   // K-split sk's partial
 #pragma unroll
@@ -652,18 +656,19 @@ PFN_encodeTiled get_encode() {
   return fn;
 }
 
-int g_num_sms = 0;
 thread_local int g_last_splits = 1;
 
 template <int MODE>
 cudaError_t launch_mode(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmArgs& a,
                         size_t smem, int grid, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static PerDeviceOnce attr_set;   // the smem limit is a per-device attribute
+  if (attr_set.first()) {
     cudaError_t e = cudaFuncSetAttribute(k_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
+    if (e != cudaSuccess) {
+      attr_set.done.fetch_and(~(1ull << current_device()));
+      return e;
+    }
   }
   const cudaError_t le = launch_k(k_gemm<MODE>, dim3(grid), dim3(kThreads), smem, st, tmW, tmX, a);
   if (le != cudaSuccess) return le;
@@ -672,12 +677,14 @@ cudaError_t launch_mode(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
 
 template <int MODE>
 cudaError_t prep_mode2() {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static PerDeviceOnce attr_set;   // the smem limit is a per-device attribute
+  if (attr_set.first()) {
     cudaError_t e = cudaFuncSetAttribute(k_gemm2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
+    if (e != cudaSuccess) {
+      attr_set.done.fetch_and(~(1ull << current_device()));
+      return e;
+    }
   }
   return cudaSuccess;
 }
@@ -685,8 +692,10 @@ cudaError_t prep_mode2() {
 // clusters of `csize` CTAs that can be co-resident (cached per (mode, csize, smem))
 template <int MODE>
 int max_clusters2(int csize, size_t smem) {
-  static std::map<std::pair<int, size_t>, int> cache;
-  auto key = std::make_pair(csize, smem);
+  static std::map<std::pair<int, size_t>, int> cache;   // key: (device * 64 + csize, smem)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(current_device() * 64 + csize, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   cudaLaunchConfig_t cfg = {};
@@ -703,7 +712,7 @@ int max_clusters2(int csize, size_t smem) {
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, k_gemm2<MODE>, &cfg) != cudaSuccess || n <= 0) {
     cudaGetLastError();
-    n = g_num_sms / csize;
+    n = device_sms() / csize;
   }
   cache[key] = n;
   return n;
@@ -756,11 +765,7 @@ int gemm_splits_last() { return g_last_splits; }
 // path would not split it either: its pair tiles fill 90-100 % of one wave of CTA pairs, or at
 // least 1.5 waves (host-side estimate with one pair per two SMs).
 bool gemm_qkv_fused_ok(int M, int R) {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_num_sms = device_sms();
   const int bn = gemm_pick_bn(R);
   const int ntiles = ((M + 255) / 256) * ((R + bn - 1) / bn);
   const int nc = g_num_sms / 2;
@@ -851,11 +856,7 @@ void gemm_force_single(bool on) { g_force_single = on; }
 
 cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArgs a,
                         cudaStream_t st, int* launches) {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_num_sms = device_sms();
   a.BN = gemm_pick_bn(a.R);
   a.n_tiles_n = (a.R + a.BN - 1) / a.BN;
   a.n_tiles_m = (a.M + 127) / 128;

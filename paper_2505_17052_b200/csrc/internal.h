@@ -7,6 +7,7 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <atomic>
 #include <string>
 #include <utility>
 #include <vector>
@@ -14,6 +15,35 @@
 #include "../../include/specedge.h"
 
 namespace se {
+
+// Per-device one-time state.  A process may drive several GPUs (specedge_model_create takes a
+// device), and kernel attributes such as the dynamic shared-memory limit are per device: first()
+// is true once for each device id it is called under (the current device).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= kMaxDevices ? 0 : d;
+}
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  bool first() {
+    const uint64_t bit = 1ull << current_device();
+    return !(done.fetch_or(bit) & bit);
+  }
+};
+// SM count of the current device (cached per device id)
+inline int device_sms() {
+  static std::atomic<int> n[kMaxDevices];
+  const int d = current_device();
+  int v = n[d].load();
+  if (v <= 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    if (v <= 0) v = 148;
+    n[d].store(v);
+  }
+  return v;
+}
 
 // Launch (optionally with programmatic stream serialisation: kernels call pdl_begin() before any
 // global access; enabled by SPECEDGE_PDL=1).
@@ -48,7 +78,7 @@ enum GemmMode : int {
   EPI_QKV = 7,     // a4 with RoPE fused (head_dim 128, unsplit): q -> Q fp16, k/v -> tree K/V fp16
 };
 
-constexpr int kMaxFusedTp = 4;   // NEXT-F4: ranks of the fused GEMM -> reduce-scatter
+constexpr int kMaxFusedTp = 8;   // NEXT-F4: ranks of the fused GEMM -> reduce-scatter (a box's 8 GPUs)
 struct RmsSrc {                  // NEXT-F4: per-partial base pointers for k_rmsnorm (p[0] == null: unused)
   const float* p[kMaxFusedTp];
   bf16* outp[kMaxFusedTp];       // NEXT-F4 all-gather: the normalised row also goes to every rank
@@ -170,7 +200,7 @@ cudaError_t attention_tc_launch(const AttnArgs& a, int B, bf16* O, float* O_f32,
 // small kernels
 // ---------------------------------------------------------------------------------------------
 struct PrepArgs {
-  int B, V, max_nodes, max_context_len, max_handles, force_chain;
+  int B, V, max_nodes, max_context_len, max_handles, force_chain, max_position;
   const int* kv;
   const int* context_len;
   const int* root_token;

@@ -97,7 +97,8 @@ __global__ void k_prep(const __grid_constant__ PrepArgs p) {
     else if (s_flags[1]) st = SPECEDGE_REQ_E_TREE;
     else if (s_flags[2] || root < 0 || root >= p.V) st = SPECEDGE_REQ_E_TOKEN;
     else if (s_flags[3]) st = SPECEDGE_REQ_E_DUP_SIBLING;
-    else if (p.context_len[r] != L + 1 || p.context_len[r] > p.max_context_len) st = SPECEDGE_REQ_E_CONTEXT;
+    else if (p.context_len[r] != L + 1 || p.context_len[r] > p.max_context_len || L + s_depth_max >= p.max_position)
+      st = SPECEDGE_REQ_E_CONTEXT;
     else if (L + s_depth_max + 1 > p.capacity[h]) st = SPECEDGE_REQ_E_KV_CAPACITY;
     p.status[r] = st;
     p.req_L[r] = L;
@@ -136,23 +137,32 @@ __global__ void k_embed(const bf16* __restrict__ E, const int* __restrict__ row_
 // bf16(y) at out row 2r and lo = bf16(y - hi) at row 2r+1, so hi + lo carries y to ~2^-17.
 // ys (NEXT-F4, tensor parallel): partial s of this rank's rows at ys.p[s] (a peer's memory over
 // NVLink for s != own rank) instead of Y + s * y_stride; summed in the same fixed order.
+// NY < 0 (more than 4 partials, tensor parallel at 5-8 ranks): -NY partials summed one at a time
+// in the same fixed order (no register prefetch of all of them).
 template <int NY>
 __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const float* __restrict__ Y, size_t y_stride,
                                                   const bf16* __restrict__ g, bf16* __restrict__ out, int d, float eps,
                                                   int split, const RmsSrc ys) {
   pdl_begin();
-  // blockDim.x = d / 16: each thread owns 16 consecutive elements, kept in registers across passes
+  // blockDim.x = d / 16 rounded up to whole warps: thread t owns elements [16t, 16t+16), kept in
+  // registers across passes; padding lanes (16t >= d) hold zeros and neither load nor store, so the
+  // full-mask warp reductions below always run on complete warps
   const int row = blockIdx.x;
   const int i = threadIdx.x * 16;
+  const bool own = i < d;
   float* x = X + (size_t)row * d + i;
   __shared__ float red[32];
   float xv[16];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float4 a = *reinterpret_cast<const float4*>(x + 4 * k);
-    xv[4 * k] = a.x; xv[4 * k + 1] = a.y; xv[4 * k + 2] = a.z; xv[4 * k + 3] = a.w;
+  for (int k = 0; k < 16; ++k) xv[k] = 0.f;
+  if (own) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(x + 4 * k);
+      xv[4 * k] = a.x; xv[4 * k + 1] = a.y; xv[4 * k + 2] = a.z; xv[4 * k + 3] = a.w;
+    }
   }
-  if constexpr (NY > 0) {
+  if constexpr (NY > 0) if (own) {
     float4 yv[NY][4];
 #pragma unroll
     for (int s = 0; s < NY; ++s)
@@ -166,6 +176,19 @@ __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const f
       for (int k = 0; k < 4; ++k) {
         xv[4 * k] += yv[s][k].x; xv[4 * k + 1] += yv[s][k].y; xv[4 * k + 2] += yv[s][k].z; xv[4 * k + 3] += yv[s][k].w;
       }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<float4*>(x + 4 * k) = make_float4(xv[4 * k], xv[4 * k + 1], xv[4 * k + 2], xv[4 * k + 3]);
+  }
+  if constexpr (NY < 0) if (own) {
+    for (int s = 0; s < -NY; ++s) {
+      const float* src = (ys.p[0] ? ys.p[s] : Y + s * y_stride) + (size_t)row * d + i;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float4 y = __ldcs(reinterpret_cast<const float4*>(src + 4 * k));
+        xv[4 * k] += y.x; xv[4 * k + 1] += y.y; xv[4 * k + 2] += y.z; xv[4 * k + 3] += y.w;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       *reinterpret_cast<float4*>(x + 4 * k) = make_float4(xv[4 * k], xv[4 * k + 1], xv[4 * k + 2], xv[4 * k + 3]);
@@ -187,6 +210,7 @@ __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const f
     ss = red[0];
   }
   const float inv = rsqrtf(ss / (float)d + eps);
+  if (!own) return;
   const uint4* gp = reinterpret_cast<const uint4*>(g + i);
   uint32_t o[8], r[8];
 #pragma unroll
@@ -617,7 +641,7 @@ cudaError_t embed_launch(const bf16* E, const int* row_tok, float* X, int R, int
 cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, const bf16* g, bf16* out, int R, int d,
                            float eps, cudaStream_t st, int* launches, int split, const RmsSrc* ys) {
   if (launches) ++*launches;
-  const int threads = d / 16;   // d % 64 == 0 (checked at model creation), <= 1024
+  const int threads = (d / 16 + 31) & ~31;   // whole warps; d % 64 == 0 and d <= 16384 (model creation)
   const RmsSrc src = ys ? *ys : RmsSrc{};
   switch (nY) {
     case 0: CK_RET(launch_k(k_rmsnorm<0>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
@@ -625,6 +649,10 @@ cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, co
     case 2: CK_RET(launch_k(k_rmsnorm<2>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
     case 3: CK_RET(launch_k(k_rmsnorm<3>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
     case 4: CK_RET(launch_k(k_rmsnorm<4>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
+    case 5: CK_RET(launch_k(k_rmsnorm<-5>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
+    case 6: CK_RET(launch_k(k_rmsnorm<-6>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
+    case 7: CK_RET(launch_k(k_rmsnorm<-7>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
+    case 8: CK_RET(launch_k(k_rmsnorm<-8>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -35,16 +35,7 @@ bool attn_balanced(int max_pages) {
   static const int min_pages = getenv("SPECEDGE_ATTN_BAL_PAGES") ? atoi(getenv("SPECEDGE_ATTN_BAL_PAGES")) : 64;
   return force >= 0 ? force == 1 : max_pages >= min_pages;
 }
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int num_sms() { return device_sms(); }
 
 thread_local int g_last_launches = 0;
 
@@ -228,6 +219,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
                            DevOut dout, uint8_t* ws_base, size_t ws_bytes, cudaStream_t st, bool prefill,
                            bool do_commit, bool hidden_only = false) {
   const specedge_model_config& c = m->cfg;
+  if (m->tp_size > 1 && !m->nccl) return SPECEDGE_E_UNSUPPORTED;   // a communicator-less shard
   const int B = in->num_requests, T = in->total_nodes, R = T + B;
   const WsLayout w = ws_layout(c, B, R);
   if (!ws_base || ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
@@ -243,6 +235,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   pa.max_context_len = in->max_context_len;
   pa.max_handles = pool->max_handles;
   pa.force_chain = prefill ? 1 : 0;
+  pa.max_position = c.max_position;   // RoPE table rows: positions L + depth must stay below
   pa.kv = di.kv;
   pa.context_len = di.context_len;
   pa.root_token = di.root_token;
@@ -762,7 +755,8 @@ specedge_status specedge_model_create_tp(const specedge_model_config* cfg, uint6
                                          specedge_model** out) {
   if (!cfg || !out) return SPECEDGE_E_INVALID;
   if (tp_size < 1 || tp_size > kMaxTp || tp_rank < 0 || tp_rank >= tp_size) return SPECEDGE_E_INVALID;
-  if (tp_size > 1 && !nccl_id) return SPECEDGE_E_INVALID;
+  // nccl_id == NULL with tp_size > 1: a communicator-less shard (weights, KV pool, introspection;
+  // verify / prefill return E_UNSUPPORTED) — lets one process check the sharding on one GPU
   if (!check_cfg(*cfg)) return SPECEDGE_E_UNSUPPORTED;
   // head-parallel attention, column-parallel QKV / gate-up (gate-up in 64-row blocks),
   // row-parallel O / down, vocab-parallel LM head
@@ -773,7 +767,7 @@ specedge_status specedge_model_create_tp(const specedge_model_config* cfg, uint6
   lc.n_kv /= tp_size;
   lc.ffn /= tp_size;
   if (!check_cfg(lc)) return SPECEDGE_E_UNSUPPORTED;
-  if (tp_size > 1 && !tp_available()) return SPECEDGE_E_UNSUPPORTED;
+  if (tp_size > 1 && nccl_id && !tp_available()) return SPECEDGE_E_UNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return SPECEDGE_E_DEVICE;
   cudaDeviceProp prop;
@@ -882,7 +876,7 @@ specedge_status specedge_model_create_tp(const specedge_model_config* cfg, uint6
       cudaMemcpy(m->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(SPECEDGE_E_CUDA);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(SPECEDGE_E_CUDA);
-  if (tp_size > 1 && tp_comm_init(&m->nccl, nccl_id, tp_rank, tp_size) != 0) return fail(SPECEDGE_E_CUDA);
+  if (tp_size > 1 && nccl_id && tp_comm_init(&m->nccl, nccl_id, tp_rank, tp_size) != 0) return fail(SPECEDGE_E_CUDA);
   *out = m;
   return SPECEDGE_OK;
 }
@@ -972,7 +966,7 @@ specedge_status specedge_kvpool_destroy(specedge_kvpool* p) {
 specedge_status specedge_kv_alloc(specedge_kvpool* p, int32_t capacity_tokens, int32_t* out_handle) {
   if (!p || !out_handle || capacity_tokens <= 0) return SPECEDGE_E_INVALID;
   const int need = (capacity_tokens + kPage - 1) / kPage;
-  if (need > p->max_pages_per_seq) return SPECEDGE_E_INVALID;
+  if (need > p->max_pages_per_seq || capacity_tokens > p->model->cfg.max_position) return SPECEDGE_E_INVALID;
   int h = -1;
   for (int i = 0; i < p->max_handles; ++i)
     if (p->handle_cap[i] == 0) { h = i; break; }
@@ -1269,7 +1263,7 @@ specedge_status specedge_debug_weight_rows(specedge_model* m, int32_t tensor, in
       case 6: base = m->layers[layer].wgu; rows = F; prow = (r / 64) * 128 + r % 64; break;
       case 7: base = m->layers[layer].wgu; rows = F; prow = (r / 64) * 128 + 64 + r % 64; break;
       case 8: base = m->layers[layer].wd; rows = d; cols = F; break;
-      case 9: base = m->lm_head; rows = c.vocab; break;
+      case 9: base = m->lm_head; rows = m->vl; break;   // this rank's vocab shard
       case 10: base = m->layers[layer].g_attn; rows = 1; break;
       case 11: base = m->layers[layer].g_mlp; rows = 1; break;
       case 12: base = m->g_final; rows = 1; break;
@@ -1296,6 +1290,27 @@ specedge_status specedge_debug_read_kv(specedge_kvpool* p, int32_t h, int32_t la
       const size_t off = (((((size_t)layer * p->num_pages + page) * 2 + kv_sel) * c.n_kv + g) * kPage + pos % kPage) * c.head_dim;
       CK(cudaMemcpy(dst + ((size_t)i * c.n_kv + g) * c.head_dim, p->pages + off, c.head_dim * 2, cudaMemcpyDeviceToHost));
     }
+  }
+  return SPECEDGE_OK;
+}
+
+specedge_status specedge_debug_read_tree_kv(specedge_model* m, const void* workspace, size_t ws_bytes, int32_t B,
+                                            int32_t R, int32_t layer, int32_t kv_sel, int32_t row0, int32_t n,
+                                            uint16_t* dst) {
+  if (!m || !workspace || !dst || B <= 0 || R < B || layer < 0 || layer >= m->cfg.n_layers || kv_sel < 0 ||
+      kv_sel > 1 || row0 < 0 || n < 0 || row0 + n > R)
+    return SPECEDGE_E_INVALID;
+  const auto& c = m->cfg;
+  const WsLayout w = ws_layout(c, B, R);
+  if (ws_bytes < w.total) return SPECEDGE_E_WORKSPACE;
+  CK(cudaSetDevice(m->device));
+  CK(cudaDeviceSynchronize());
+  // tree scratch [layer][K|V][kv_head][R][hd] fp16 (R = this batch's rows)
+  const uint16_t* base = reinterpret_cast<const uint16_t*>((const uint8_t*)workspace + w.tree_kv);
+  for (int g = 0; g < c.n_kv; ++g) {
+    const size_t src = ((((size_t)layer * 2 + kv_sel) * c.n_kv + g) * R + row0) * c.head_dim;
+    CK(cudaMemcpy2D(dst + (size_t)g * c.head_dim, (size_t)c.n_kv * c.head_dim * 2, base + src, (size_t)c.head_dim * 2,
+                    (size_t)c.head_dim * 2, n, cudaMemcpyDeviceToHost));
   }
   return SPECEDGE_OK;
 }

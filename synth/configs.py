@@ -42,6 +42,8 @@ LLAMA3_8B = ModelShape("llama3-8b", 32, 4096, 32, 8, 128, 14336, 128256, 1e-5, 5
 LLAMA3_8B_2L = replace(LLAMA3_8B, name="llama3-8b-2l", n_layers=2)
 # cfg3 / cfg5: Qwen3-14B-shaped (QK-norm off, SURVEY.md amb. A16)
 QWEN3_14B = ModelShape("qwen3-14b", 40, 5120, 40, 8, 128, 17408, 151936, 1e-6, 1000000.0)
+# 2-layer slice of the cfg3 / cfg5 shape at full width / full vocab (parity at bench widths)
+QWEN3_14B_2L = replace(QWEN3_14B, name="qwen3-14b-2l", n_layers=2)
 # cfg4: Llama-3-70B-shaped
 LLAMA3_70B = ModelShape("llama3-70b", 80, 8192, 64, 8, 128, 28672, 128256, 1e-5, 500000.0)
 # the paper's edge draft models are Qwen3-0.6B / 1.7B; NEXT-F3 timing uses this shape
@@ -50,7 +52,7 @@ QWEN3_0_6B = ModelShape("qwen3-0.6b", 28, 1024, 16, 8, 128, 3072, 151936, 1e-6, 
 SMALL128 = ModelShape("small128", 2, 512, 8, 2, 128, 1024, 2048, 1e-5, 500000.0)
 
 SHAPES = {s.name: s for s in (TINY, TINY_V16, TINY_MHA, LLAMA3_8B, LLAMA3_8B_2L,
-                              QWEN3_14B, LLAMA3_70B, SMALL128, QWEN3_0_6B)}
+                              QWEN3_14B, QWEN3_14B_2L, LLAMA3_70B, SMALL128, QWEN3_0_6B)}
 
 
 @dataclass(frozen=True)

@@ -1,27 +1,53 @@
 """Helpers for the GPU parity tests: build the same seeded state on the oracle side and on the
-library side, and compare results under SURVEY amb. A21 (exactness of acceptance outputs is
-required wherever every visited node's top-1 margin, computed from ORACLE scores, exceeds 1e-2).
+library side, and compare results under SURVEY amb. A21 with north_star's numbers.
 
-Inputs come only from synth/ and oracle/; nothing the CUDA path computes is fed to the oracle."""
+The parity contract (DESIGN.md §4 R-tolerances).  No threshold depends on the library's own
+measured error:
+  * target token per slot: bit-exact wherever the ORACLE top-1 margin exceeds MARGIN = 1e-2
+    (north_star "bit-exact whenever top-1 logit margins exceed 1e-2");
+  * accept walk + bonus: always bit-exact given the library's own per-slot targets (the oracle
+    walk O4 run on the GPU's row_target must reproduce the GPU's accepted nodes, tokens, bonus);
+  * acceptance outcome: equal to the oracle's, unless the first visited slot where the GPU's
+    target differs has oracle margin <= MARGIN (then "exempt": counted, never larger than the
+    number of requests whose oracle path visits such a slot);
+  * logits: max-abs <= 2e-2 (north_star), or, where the oracle's own float32-matmul variant
+    already deviates from its float64 result by more on the same inputs, <= NOISE_FACTOR x that
+    self-deviation (a bound computed from the oracle alone, oracle_noise_floor), and 99.9 % of
+    logits within 2e-2 in every case;
+  * committed KV: the pages at L..L+a hold, bit for bit, the tree-scratch rows of the root and
+    the accepted slots (exact indices).
+
+Inputs come only from synth/ and oracle/; nothing the CUDA path computes is fed to the oracle.
+Set SPECEDGE_PARITY_LOG=path to append one JSON line of statistics per check (error
+quantiles, oracle self-noise, exempt counts) for the record in profiles/."""
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
+
+from oracle import verify as OV
 
 MARGIN = 1e-2          # north_star: "bit-exact whenever top-1 logit margins exceed 1e-2"
 LOGIT_TOL = 2e-2       # north_star: "logits must agree within max-abs 2e-2 (bf16)"
 ATTN_TOL = 1e-3        # north_star: "attention outputs within 1e-3 relative (fp32 accumulate)"
-# north_star's logit bound (2e-2 max-abs) sits at the noise floor of the
-# storage contract: rounding K/V, q, O, M and h to 16 bits turns arithmetic-order differences into
-# ~1e-2 logit noise (the oracle's own float32-matmul variant deviates from float64 by up to 2.8e-2,
-# tools/diag_drift.py).  The library must keep 99.9% of logits within 2e-2 (north_star) and every
-# logit within LOGIT_MAX = 3.5e-2 (derived: 1.25 x the largest oracle self-deviation observed).
 LOGIT_Q = 0.999
-LOGIT_MAX = 3.5e-2
+NOISE_FACTOR = 1.25    # x the oracle's own float32-vs-float64 max deviation on the same inputs
+
+
+def _log(kind, **info):
+    path = os.environ.get("SPECEDGE_PARITY_LOG")
+    if not path:
+        return
+    test = os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0]
+    with open(path, "a") as f:
+        f.write(json.dumps(dict(test=test, kind=kind, **info)) + "\n")
 
 
 def oracle_noise_floor(run):
-    """|logits(float32 matmuls) - logits(float64)| of the oracle on the same inputs (reported
-    next to the library's error).  `run()` rebuilds sessions and returns the logits."""
+    """|logits(float32 matmuls) - logits(float64)| of the oracle on the same inputs.  `run()`
+    rebuilds the oracle state and returns the logits; the library is not involved."""
     import oracle.model as OM
     ref = run()
     old = OM.MATMUL_DTYPE
@@ -33,13 +59,23 @@ def oracle_noise_floor(run):
     return ref, np.abs(alt - ref)
 
 
+def logit_bound(noise=None):
+    if noise is None:
+        return LOGIT_TOL
+    return max(LOGIT_TOL, NOISE_FACTOR * float(np.max(noise)))
+
+
 def check_logits(gpu, ref, noise=None):
+    """Max-abs and 99.9 % bounds on |gpu - oracle| logits (module docstring)."""
     d = np.abs(np.asarray(gpu, np.float64) - ref)
-    info = dict(gpu_q999=float(np.quantile(d, LOGIT_Q)), gpu_q99=float(np.quantile(d, 0.99)), gpu_max=float(d.max()))
+    bound = logit_bound(noise)
+    info = dict(n=int(d.size), gpu_max=float(d.max()), gpu_q999=float(np.quantile(d, LOGIT_Q)),
+                gpu_q99=float(np.quantile(d, 0.99)), bound=bound)
     if noise is not None:
-        info.update(noise_q99=float(np.quantile(noise, 0.99)), noise_max=float(noise.max()))
+        info.update(noise_max=float(np.max(noise)), noise_q99=float(np.quantile(noise, 0.99)))
+    _log("logits", **info)
     assert info["gpu_q999"] <= LOGIT_TOL, info
-    assert info["gpu_max"] <= LOGIT_MAX, info
+    assert info["gpu_max"] <= bound, info
     return d
 
 
@@ -48,27 +84,75 @@ def top2_margin(scores):
     return s[..., -1] - s[..., -2]
 
 
-def visited_slots(parent, acc_nodes):
-    return [0] + [n + 1 for n in acc_nodes]
-
-
-def compare_outcome(o_ref, slot_scores, gpu, r, eps=0.0):
-    """Returns 'exact' if equal, 'exempt' if a visited node's oracle margin is <= max(1e-2, 2*eps)
-    (eps = the measured max |score error| of the library on this request: below 2*eps the
-    argmax may legitimately differ), else raises."""
-    margins = top2_margin(slot_scores)
-    vis = visited_slots(None, o_ref.accepted_node)
-    a = int(gpu["accepted_len"][r])
-    same = (a == o_ref.accepted_len and int(gpu["bonus"][r]) == o_ref.bonus and
-            list(gpu["accepted_token"][r][:a]) == o_ref.accepted_token and
-            list(gpu["accepted_node"][r][:a]) == o_ref.accepted_node)
-    if same:
+def check_request(tree, o_ref, ref_scores, g, r, score_tol=None):
+    """All acceptance checks of request r (module docstring).  tree: .parent/.token of the
+    request's draft tree; o_ref: oracle Outcome; ref_scores: the oracle's [S, V] score rows whose
+    argmax is y (logits, or l/T + g in sampled mode); g: split_outputs of the library run;
+    score_tol: bound on |row_score - oracle top-1 score| (default: the logit bound).
+    Returns 'exact' or 'exempt'."""
+    margins = top2_margin(ref_scores)
+    gt = np.asarray(g["row_target"][r])
+    assert gt.shape[0] == margins.shape[0], (gt.shape, margins.shape)
+    sure = margins > MARGIN
+    bad = np.nonzero(sure & (gt != o_ref.row_target))[0]
+    assert bad.size == 0, dict(request=r, slots=bad.tolist(), margins=margins[bad].tolist())
+    tol = LOGIT_TOL if score_tol is None else score_tol
+    ds = np.abs(np.asarray(g["row_score"][r], np.float64) - np.asarray(ref_scores, np.float64).max(-1))
+    assert ds.max() <= tol, (r, float(ds.max()), tol)
+    # the walk + bonus on the library's own targets: exact, always
+    acc_t, acc_n, bonus = OV.walk(tree.parent, tree.token, gt)
+    a = int(g["accepted_len"][r])
+    got = (a, list(map(int, g["accepted_token"][r][:a])), list(map(int, g["accepted_node"][r][:a])),
+           int(g["bonus"][r]))
+    assert got == (len(acc_t), acc_t, acc_n, bonus), (r, got, (len(acc_t), acc_t, acc_n, bonus))
+    if got == (o_ref.accepted_len, o_ref.accepted_token, o_ref.accepted_node, o_ref.bonus):
         return "exact"
-    if min(margins[v] for v in vis) <= max(MARGIN, 2.0 * eps):
-        return "exempt"
-    raise AssertionError(f"request {r}: gpu (a={a}, bonus={int(gpu['bonus'][r])}) != oracle "
-                         f"(a={o_ref.accepted_len}, bonus={o_ref.bonus}) with margins "
-                         f"{[float(margins[v]) for v in vis]}")
+    vis = [0] + [n + 1 for n in o_ref.accepted_node]
+    first = next(v for v in vis if gt[v] != o_ref.row_target[v])
+    assert margins[first] <= MARGIN, (r, first, float(margins[first]))
+    return "exempt"
+
+
+def low_margin_path(o_ref, ref_scores):
+    """True if the oracle's accepted path visits a slot with margin <= MARGIN (the only requests
+    that may be exempt)."""
+    m = top2_margin(ref_scores)
+    return any(m[v] <= MARGIN for v in [0] + [n + 1 for n in o_ref.accepted_node])
+
+
+def check_batch(trees, refs, ref_scores, g, score_tol=None):
+    """check_request over a batch; the exempt count is bounded by the oracle's low-margin paths.
+    Returns the list of kinds."""
+    kinds = [check_request(trees[r], refs[r], ref_scores[r], g, r, score_tol) for r in range(len(trees))]
+    low = sum(low_margin_path(refs[r], ref_scores[r]) for r in range(len(trees)))
+    n_slots = sum(int(np.asarray(s).shape[0]) for s in ref_scores)
+    n_low_slots = sum(int((top2_margin(s) <= MARGIN).sum()) for s in ref_scores)
+    _log("acceptance", requests=len(trees), exempt=kinds.count("exempt"), low_margin_paths=int(low),
+         slots=n_slots, low_margin_slots=n_low_slots)
+    assert kinds.count("exempt") <= low
+    return kinds
+
+
+def check_commit(api, model, pool, ws, batch, g, handles, L0):
+    """Committed KV indices, bit-exact: for every request with status OK, positions L0 .. L0+a of
+    every layer hold exactly the tree-scratch rows of the root slot and of the accepted nodes' slots
+    (in path order), and the cached length advanced by a+1.  Call after a verify with auto_commit
+    (or verify + kv_commit) of `batch` with workspace `ws`, before the workspace is reused."""
+    off = batch.node_offset.cpu().numpy()
+    lens = pool.get_len(handles)
+    for r, h in enumerate(handles):
+        if int(g["status"][r]) != 0:
+            assert lens[r] == L0[r], (r, lens[r], L0[r])
+            continue
+        a = int(g["accepted_len"][r])
+        assert lens[r] == L0[r] + a + 1, (r, lens[r], L0[r], a)
+        row0 = int(off[r]) + r
+        slots = [0] + [int(n) + 1 for n in g["accepted_node"][r][:a]]
+        for layer in range(model.shape.n_layers):
+            for kv_sel in (0, 1):
+                tree = api.debug_read_tree_kv(model, ws, batch, layer, kv_sel, row0, int(off[r + 1] - off[r]) + 1)
+                got = pool.read_kv(h, layer, kv_sel, L0[r], a + 1)
+                assert np.array_equal(got, tree[slots]), (r, layer, kv_sel)
 
 
 def split_outputs(out, batch):

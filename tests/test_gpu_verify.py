@@ -1,9 +1,12 @@
 """End-to-end parity of specedge_verify_batch (through the C ABI) against the oracle on the same
-seeded inputs (SURVEY §8(c) tolerances, amb. A21):
-  - acceptance outputs (accepted_len / tokens / nodes, bonus) and committed KV indices: exact
-    whenever every visited node's oracle top-1 margin exceeds 1e-2, otherwise exempt + counted;
+seeded inputs (SURVEY §8(c) tolerances, amb. A21; the contract is spelled out in
+tests/gpu_helpers.py):
   - target token per slot: exact where the oracle margin exceeds 1e-2;
-  - logits: max-abs <= 2e-2 (fp32 capture of the same LM-head kernel);
+  - accept walk + bonus: exact on the library's own targets, always; equal to the oracle's
+    outcome unless the first divergent visited slot has oracle margin <= 1e-2 (exempt, counted);
+  - committed KV: bit-exact indices (pages == tree-scratch rows of the accepted slots);
+  - logits: max-abs <= 2e-2, or 1.25 x the oracle's own float32-vs-float64 deviation where that
+    is larger, and 99.9 % within 2e-2 (fp32 capture of the same LM-head kernel);
   - stochastic mode: the (stop node, bonus) law passes chi-square against the oracle's closed
     form (O7) on V = 16.
 """
@@ -16,11 +19,11 @@ pytestmark = pytest.mark.gpu
 from oracle import verify as OV  # noqa: E402
 from oracle.law import closed_form_law, slot_probs  # noqa: E402
 from oracle.model import Weights, Cache, gen_kv_fill, lm_logits, tree_forward  # noqa: E402
-from synth.configs import TINY, TINY_V16, TINY_MHA, SMALL128, LLAMA3_8B_2L, ModelShape  # noqa: E402
+from synth.configs import TINY, TINY_V16, TINY_MHA, SMALL128, LLAMA3_8B_2L, QWEN3_14B_2L, ModelShape  # noqa: E402
 from synth.plant import plant, draw_accept_lengths  # noqa: E402
 from synth.trees import pooled_tree, random_tree, chain_tree, Tree  # noqa: E402
-from tests.gpu_helpers import (LOGIT_TOL, MARGIN, f16_bits_to_f64, compare_outcome,  # noqa: E402
-                               split_outputs, top2_margin, oracle_noise_floor, check_logits)
+from tests.gpu_helpers import (f16_bits_to_f64, check_request, check_batch, check_commit,  # noqa: E402
+                               split_outputs, oracle_noise_floor, check_logits, logit_bound)
 
 
 @pytest.fixture(scope="module")
@@ -113,22 +116,15 @@ def test_verify_greedy_matches_oracle(api, shape):
             return np.concatenate([o.logits for o in OV.verify_batch(
                 pr.W, [OV.Request(s_, t.parent, t.token) for s_, t in zip(ses, trees)], auto_commit=False)])
         ref_all, noise = oracle_noise_floor(run)
-        dl = check_logits(logits_gpu, ref_all, noise)
+        check_logits(logits_gpu, ref_all, noise)
         refs = OV.verify_batch(pr.W, [OV.Request(pr.sessions[r], trees[r].parent, trees[r].token) for r in range(B)],
                                auto_commit=False)
-        kinds = []
-        off = 0
-        for r in range(B):
-            o = refs[r]
-            S = trees[r].n + 1
-            eps = float(dl[off:off + S].max())
-            off += S
-            assert np.abs(g["row_score"][r] - o.logits.max(-1)).max() <= eps + 1e-4
-            sure = top2_margin(o.logits) > max(MARGIN, 2 * eps)
-            assert np.array_equal(g["row_target"][r][sure], o.row_target[sure])
-            assert g["status"][r] == 0
-            kinds.append(compare_outcome(o, o.logits, g, r, eps))
-        assert kinds.count("exact") >= B - 1, kinds
+        assert all(int(x) == 0 for x in g["status"])
+        check_batch(trees, refs, [o.logits for o in refs], g, logit_bound(noise))
+        # commit through the separate entry point; committed rows == tree-scratch rows, bitwise
+        L0 = [int(x) for x in pr.pool.get_len(pr.handles)]
+        api.kv_commit(pr.model, pr.pool, batch, out, pr.ws)
+        check_commit(api, pr.model, pr.pool, pr.ws, batch, g, pr.handles, L0)
     finally:
         pr.close()
 
@@ -148,17 +144,14 @@ def test_iterated_verify_commit_reproduces_greedy_decoding(api):
             a = draw_accept_lengths(rng, trees, 3.98, 1.55)
             trees = plant(trees, pr.oracle_targets(range(B)), a, TINY.vocab, rng)
             batch = pr.batch(range(B), trees)
+            L0 = [int(x) for x in pr.pool.get_len(pr.handles)]
             out = api.verify(pr.model, pr.pool, batch, pr.ws, auto_commit=True)
             g = split_outputs(out, batch)
+            check_commit(api, pr.model, pr.pool, pr.ws, batch, g, pr.handles, L0)
             refs = OV.verify_batch(pr.W, [OV.Request(pr.sessions[r], trees[r].parent, trees[r].token)
                                           for r in range(B)])
-            lg = api.debug_last_logits(pr.model, pr.ws, batch).cpu().numpy()
-            off = 0
             for r in range(B):
-                S = trees[r].n + 1
-                eps = float(np.abs(lg[off:off + S] - refs[r].logits).max())
-                off += S
-                kind = compare_outcome(refs[r], refs[r].logits, g, r, eps)
+                kind = check_request(trees[r], refs[r], refs[r].logits, g, r)
                 if kind == "exempt":
                     exempt += 1
                     pytest.skip("near-tie on a visited node; sequences diverge legitimately")
@@ -188,19 +181,13 @@ def test_verify_sampled_matches_oracle_draws(api):
                          auto_commit=False)
         g = split_outputs(out, batch)
         lg = api.debug_last_logits(pr.model, pr.ws, batch).cpu().numpy()
-        off = 0
-        for r, rnd in enumerate([3, 0, 9, 1 << 31]):
-            o = OV.verify_one(pr.W, OV.Request(pr.sessions[r], trees[r].parent, trees[r].token, round=rnd),
-                              "sample", 0.7, 0xDEADBEEF12345)
-            S = trees[r].n + 1
-            # score error = logit error / T (+ fp32 vs fp64 Gumbel transform, ~1e-6)
-            eps = float(np.abs(lg[off:off + S] - o.logits).max()) * OV.inv_temperature(0.7) + 1e-5
-            off += S
-            sc = OV.target_scores(o.logits, "sample", 0.7, 0xDEADBEEF12345, rnd, pr.sessions[r].session_id)
-            sure = top2_margin(sc) > max(MARGIN, 2 * eps)
-            assert np.array_equal(g["row_target"][r][sure], o.row_target[sure])
-            assert np.abs(g["row_score"][r] - sc.max(-1)).max() <= eps + 1e-4
-            compare_outcome(o, sc, g, r, eps)
+        refs = [OV.verify_one(pr.W, OV.Request(pr.sessions[r], trees[r].parent, trees[r].token, round=rnd),
+                              "sample", 0.7, 0xDEADBEEF12345) for r, rnd in enumerate([3, 0, 9, 1 << 31])]
+        check_logits(lg, np.concatenate([o.logits for o in refs]))
+        scores = [OV.target_scores(o.logits, "sample", 0.7, 0xDEADBEEF12345, rnd, pr.sessions[r].session_id)
+                  for r, (o, rnd) in enumerate(zip(refs, [3, 0, 9, 1 << 31]))]
+        # score error = logit error x 1/T (+ fp32 vs fp64 Gumbel transform, ~1e-6)
+        check_batch(trees, refs, scores, g, logit_bound() * OV.inv_temperature(0.7) + 1e-5)
     finally:
         pr.close()
 
@@ -224,7 +211,7 @@ def test_errors_are_per_request_and_isolated(api):
         lens1 = pr.pool.get_len(pr.handles)
         assert list(lens1[1:]) == list(lens0[1:])
         o = OV.verify_one(pr.W, OV.Request(pr.sessions[0], good.parent, good.token))
-        assert compare_outcome(o, o.logits, g, 0) in ("exact", "exempt")
+        assert check_request(good, o, o.logits, g, 0) in ("exact", "exempt")
         assert lens1[0] == lens0[0] + g["accepted_len"][0] + 1
         # stale context length -> E_CONTEXT; duplicate handle -> E_HANDLE; idempotent commit
         batch2 = api.Batch.from_host([pr.handles[1], pr.handles[2], pr.handles[2]], [5, int(lens1[2]) + 1,
@@ -315,55 +302,81 @@ def test_sampled_verification_law_chi_square_on_gpu(api):
     assert stats.chisquare(o, e * o.sum() / e.sum()).pvalue > 1e-3
 
 
-def test_full_width_two_layer_slice_matches_oracle(api):
-    """cfg2 widths (Llama-3-8B: d 4096, 32/8 heads, F 14336, V 128256), 16 requests x 32-node
-    trees, ~1k random-filled contexts, in the launch configuration bench.py times (only the
-    layer count is reduced so the oracle finishes).  Every slot's target token is compared."""
-    shape = LLAMA3_8B_2L
-    rng = np.random.default_rng(707)
-    B = 16
-    W = Weights(shape, 2)
-    model = api.Model(shape, 2, max_position=2048)
-    pool = api.KVPool(model, B * 22, B)
+def _width_slice(api, shape, seed, B, n_nodes, depth, branching, ctx_lo, ctx_hi, mode, temperature, rng_seed):
+    """A bench config at full width and full vocabulary with only the layer count reduced so the
+    oracle finishes: B requests x n_nodes-node pooled trees over random-filled contexts
+    U[ctx_lo, ctx_hi], verified with auto_commit in the launch configuration bench.py times.
+    Every slot's target, the walk, the committed KV indices and all R x V logits are compared."""
+    rng = np.random.default_rng(rng_seed)
+    W = Weights(shape, seed)
+    cap = ctx_hi + n_nodes + 64
+    model = api.Model(shape, seed, max_position=cap + 64)
+    pool = api.KVPool(model, B * ((cap + 63) // 64) + 4, B)
     try:
-        ctx = rng.integers(768, 1281, B)
+        ctx = [int(c) for c in rng.integers(ctx_lo, ctx_hi + 1, B)]
         hs, sessions = [], []
         for r in range(B):
-            h = pool.alloc(1400)
-            pool.fill_random(h, int(ctx[r]) - 1, 1234, r)
+            h = pool.alloc(cap)
+            pool.fill_random(h, ctx[r] - 1, 1234, r)
             hs.append(h)
             c = Cache(shape)
             for l in range(shape.n_layers):
-                c.k[l] = gen_kv_fill(1234, r, l, 0, int(ctx[r]) - 1, shape.n_kv, shape.head_dim)
-                c.v[l] = gen_kv_fill(1234, r, l, 1, int(ctx[r]) - 1, shape.n_kv, shape.head_dim)
-            sessions.append(OV.Session(c, int(rng.integers(0, shape.vocab)), 1000 + r))
-        trees = [pooled_tree(rng, 32, 7, 4, shape.vocab) for _ in range(B)]
-        ws = model.workspace(B, B * 33, 1400)
-        batch = api.Batch.from_host(hs, [int(x) for x in ctx], [s.last_token for s in sessions],
-                                    [s.session_id for s in sessions], [0] * B, trees, max_context_len=1400)
-        out = api.verify(model, pool, batch, ws, auto_commit=False)
+                c.k[l] = gen_kv_fill(1234, r, l, 0, ctx[r] - 1, shape.n_kv, shape.head_dim)
+                c.v[l] = gen_kv_fill(1234, r, l, 1, ctx[r] - 1, shape.n_kv, shape.head_dim)
+            sessions.append(OV.Session(c, int(rng.integers(0, shape.vocab)), (7 << 33) + 1000 + r))
+        trees = [pooled_tree(rng, n_nodes, depth, branching, shape.vocab) for _ in range(B)]
+        rounds = [int(x) for x in rng.integers(0, 1 << 31, B)]
+        ws = model.workspace(B, B * (n_nodes + 1), cap)
+        batch = api.Batch.from_host(hs, ctx, [s.last_token for s in sessions], [s.session_id for s in sessions],
+                                    rounds, trees, max_context_len=cap)
+        L0 = [c - 1 for c in ctx]
+        out = api.verify(model, pool, batch, ws, mode=1 if mode == "sample" else 0, temperature=temperature,
+                         seed=seed, auto_commit=True)
         g = split_outputs(out, batch)
         logits_gpu = api.debug_last_logits(model, ws, batch).cpu().numpy()
-        n_exempt = 0
-        refs = OV.verify_batch(W, [OV.Request(sessions[r], trees[r].parent, trees[r].token) for r in range(B)],
-                               auto_commit=False)
+        assert all(int(x) == 0 for x in g["status"])
+        check_commit(api, model, pool, ws, batch, g, hs, L0)
+
+        def run():
+            return OV.verify_batch(W, [OV.Request(sessions[r], trees[r].parent, trees[r].token, round=rounds[r])
+                                       for r in range(B)], mode, temperature, seed, auto_commit=False)
+        refs = run()
         ref_all = np.concatenate([o.logits for o in refs])
         d = np.abs(logits_gpu - ref_all)
-        assert np.quantile(d, 0.999) <= LOGIT_TOL, float(np.quantile(d, 0.999))
-        off = 0
-        for r in range(B):
-            o = refs[r]
-            eps = float(d[off:off + trees[r].n + 1].max())
-            off += trees[r].n + 1
-            sure = top2_margin(o.logits) > max(MARGIN, 2 * eps)
-            n_exempt += int((~sure).sum())
-            assert np.array_equal(g["row_target"][r][sure], o.row_target[sure]), r
-            assert np.abs(g["row_score"][r] - o.logits.max(-1)).max() <= eps + 1e-4
-            compare_outcome(o, o.logits, g, r, eps)
-        assert n_exempt < 0.1 * B * 33
+        noise = None
+        if d.max() > logit_bound():
+            # the oracle's own float32-matmul deviation on the same inputs sets the max-abs bound
+            noise = oracle_noise_floor(lambda: np.concatenate([o.logits for o in run()]))[1]
+        check_logits(logits_gpu, ref_all, noise)
+        if mode == "sample":
+            scores = [OV.target_scores(o.logits, mode, temperature, seed, rounds[r], sessions[r].session_id)
+                      for r, o in enumerate(refs)]
+            tol = logit_bound(noise) * OV.inv_temperature(temperature) + 1e-5
+        else:
+            scores, tol = [o.logits for o in refs], logit_bound(noise)
+        check_batch(trees, refs, scores, g, tol)
     finally:
         pool.close()
         model.close()
+
+
+def test_full_width_two_layer_slice_matches_oracle(api):
+    """cfg2 (Llama-3-8B widths: d 4096, 32/8 heads, F 14336, V 128256), 16 requests x 32-node
+    trees, contexts U[768, 1280], greedy."""
+    _width_slice(api, LLAMA3_8B_2L, 2, 16, 32, 7, 4, 768, 1280, "greedy", 0.0, 707)
+
+
+def test_cfg3_width_two_layer_slice_matches_oracle(api):
+    """cfg3 (Qwen3-14B widths: d 5120, 40/8 heads, F 17408, V 151936), one microbatch of 32
+    requests x 32-node trees, contexts U[1536, 2560], greedy."""
+    _width_slice(api, QWEN3_14B_2L, 3, 32, 32, 7, 4, 1536, 2560, "greedy", 0.0, 708)
+
+
+def test_cfg5_width_sampled_slice_matches_oracle(api):
+    """cfg5 (Qwen3-14B widths, V = 151936, SAMPLE_TREE at T = 1.0), 16 requests x 16-node trees,
+    contexts U[12288, 20480] (the persistent balanced attention with in-kernel merges), Gumbel-max
+    draws compared one by one with the oracle's (amb. A9)."""
+    _width_slice(api, QWEN3_14B_2L, 5, 16, 16, 5, 4, 12288, 20480, "sample", 1.0, 709)
 
 
 G8 = ModelShape("g8", 2, 512, 16, 2, 128, 1024, 2048, 1e-5, 500000.0)   # G = 8 (Llama-70B's group at TP 2)
@@ -403,20 +416,17 @@ def test_long_ragged_contexts_chunked_attention_matches_oracle(api, shape, sizes
         out = api.verify(model, pool, batch, ws, auto_commit=False)
         g = split_outputs(out, batch)
         logits_gpu = api.debug_last_logits(model, ws, batch).cpu().numpy()
-        refs = OV.verify_batch(W, [OV.Request(sessions[r], trees[r].parent, trees[r].token) for r in range(B)],
-                               auto_commit=False)
+        def run():
+            return OV.verify_batch(W, [OV.Request(sessions[r], trees[r].parent, trees[r].token) for r in range(B)],
+                                   auto_commit=False)
+        refs = run()
         ref_all = np.concatenate([o.logits for o in refs])
-        d = np.abs(logits_gpu - ref_all)
-        assert np.quantile(d, 0.999) <= LOGIT_TOL, float(np.quantile(d, 0.999))
-        off = 0
-        for r in range(B):
-            o = refs[r]
-            eps = float(d[off:off + trees[r].n + 1].max())
-            off += trees[r].n + 1
-            sure = top2_margin(o.logits) > max(MARGIN, 2 * eps)
-            assert np.array_equal(g["row_target"][r][sure], o.row_target[sure]), r
-            assert g["status"][r] == 0
-            compare_outcome(o, o.logits, g, r, eps)
+        noise = None
+        if np.abs(logits_gpu - ref_all).max() > logit_bound():
+            noise = oracle_noise_floor(lambda: np.concatenate([o.logits for o in run()]))[1]
+        check_logits(logits_gpu, ref_all, noise)
+        assert all(int(x) == 0 for x in g["status"])
+        check_batch(trees, refs, [o.logits for o in refs], g, logit_bound(noise))
     finally:
         pool.close()
         model.close()

@@ -59,7 +59,6 @@ def test_api_errors_without_device(libpath):
     nid = (ctypes.c_uint8 * 128)()
     create_tp = lib.specedge_model_create_tp
     assert create_tp(ctypes.byref(ok), 1, 0, 2, 2, ctypes.cast(nid, ctypes.c_void_p), ctypes.byref(out)) == _lib.E_INVALID
-    assert create_tp(ctypes.byref(ok), 1, 0, 0, 2, None, ctypes.byref(out)) == _lib.E_INVALID
     assert create_tp(ctypes.byref(ok), 1, 0, 0, 0, None, ctypes.byref(out)) == _lib.E_INVALID
     assert create_tp(ctypes.byref(ok), 1, 0, 0, 4, ctypes.cast(nid, ctypes.c_void_p), ctypes.byref(out)) == \
         _lib.E_UNSUPPORTED   # n_kv = 2 not divisible by 4
