@@ -144,7 +144,7 @@ def setup_gpu(wl, rank, device, tp=None, model=None, pool=None, mb=0):
     max_ctx = max(max(contexts(wl, rank + 64 * m)) for m in range(wl.microbatches)) + wl.n_nodes + 64
     if model is None:
         if tp is None:
-            model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64)
+            model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 1024)
         else:
             model = api.Model(shape, wl.weight_seed, device=device, max_position=max_ctx + 64, tp_rank=tp[0],
                               tp_size=tp[1], nccl_id=tp[2])
@@ -388,6 +388,9 @@ def run_gpu(args, world, rank, local):
             per = kernel_table[k]["ms_per_step"] / kernel_table[k]["launches"] / 1e3
             kernel_table[k]["tflops"] = round(w["flops"] / per / 1e12, 1)
             kernel_table[k]["gbs"] = round(w["bytes"] / per / 1e9, 1)
+    serving = None
+    if not tp and len(mbs) == 1 and not args.no_serving:
+        serving = serving_leg(wl, model, local)
     if rank != 0:
         if dist:
             dist.barrier()
@@ -422,10 +425,146 @@ def run_gpu(args, world, rank, local):
     }
     if not args.no_cpu_baseline and world == 1:
         result["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
+    if serving is not None:
+        result["serving"] = serving
     print(json.dumps(result), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------ serving-realistic leg
+def serving_leg(wl, model, device, steps=60, sessions_per_slot=2, seed=77):
+    """A serving loop with nothing rewound (SURVEY §8(d) metric under P:303-306): 2x the
+    batch capacity of sessions are resident (edges = 2 x batch), the NEXT-F1 scheduler plans
+    every batch (FIFO, work conserving, at most capacity members) and is fed the measured verify
+    times; every request carries a freshly drawn tree; verify commits, so contexts grow step by step;
+    batch size and node count vary from step to step.  Inputs are staged from pinned host memory
+    into fixed device buffers inside each step's events (one constant max_context_len bound), so the
+    library's graph cache reuses one captured graph per (batch size, node count).  Acceptance is the
+    random-init model's own (unplanted); tok/s is also reported normalised to the paper's 3.98
+    tokens/verify (Table 1) via rows of work per step."""
+    import torch
+    from paper_2505_17052_b200 import api
+    from synth.trees import pooled_tree
+    shape, cap_b = wl.shape, wl.n_requests
+    n_ses = sessions_per_slot * cap_b
+    rng = np.random.default_rng([seed, 1])
+    ctx = [int(x) for x in rng.integers(wl.ctx_lo, wl.ctx_hi + 1, n_ses)]
+    grow = steps * (wl.depth + 2)
+    cap = max(ctx) + grow + wl.n_nodes + 64
+    if cap > model.max_position:
+        return {"skipped": f"max_position {model.max_position} < {cap}"}
+    pool = api.KVPool(model, sum((c + grow + wl.n_nodes + 64 + 63) // 64 for c in ctx) + 4, n_ses + 2)
+    handles = []
+    for i, c in enumerate(ctx):
+        h = pool.alloc(c + grow + wl.n_nodes + 64)
+        pool.fill_random(h, c - 1, wl.ctx_seed, 7000 + i)
+        handles.append(h)
+    roots = [int(t) for t in rng.integers(0, shape.vocab, n_ses)]
+    rounds = [0] * n_ses
+    Tmax = cap_b * wl.n_nodes
+    dev = f"cuda:{device}"
+    ws = model.workspace(cap_b, Tmax + cap_b, cap)
+    # fixed device input / output buffers and their pinned host staging
+    names = dict(kv=(cap_b, torch.int32), context_len=(cap_b, torch.int32), root_token=(cap_b, torch.int32),
+                 session_id=(cap_b, torch.int64), round=(cap_b, torch.int32), node_offset=(cap_b + 1, torch.int32),
+                 parent=(Tmax, torch.int32), token=(Tmax, torch.int32), draft_logprob=(Tmax, torch.float32))
+    dbuf = {k: torch.zeros(n, dtype=dt, device=dev) for k, (n, dt) in names.items()}
+    hbuf = {k: torch.zeros(n, dtype=dt).pin_memory() for k, (n, dt) in names.items()}
+    out_full = api.Outputs(*(torch.zeros(n, dtype=torch.int32, device=dev) for n in
+                             (cap_b, cap_b, Tmax, Tmax, cap_b, Tmax + cap_b)),
+                           torch.zeros(Tmax + cap_b, dtype=torch.float32, device=dev))
+    h_acc = torch.zeros(cap_b, dtype=torch.int32).pin_memory()
+    sched = api.Scheduler(cap_b, init_verify_ms=10.0, init_draft_pass_ms=11.0, init_rtt_ms=40.0)
+    stream = torch.cuda.current_stream()
+    sid = [(1 << 40) + i for i in range(n_ses)]
+    by_sid = {s_: i for i, s_ in enumerate(sid)}
+    # simulated edges: a session's next request arrives rtt + depth x draft_pass ms after its verify
+    # completes (P:303-306; depth = the scheduler's calibrated depth, draft pass 11 ms as P:516)
+    rtt = [float(x) for x in rng.uniform(15.0, 50.0, n_ses)]
+    pending = sorted((float(x), i) for i, x in enumerate(rng.uniform(0.0, 20.0, n_ses)))
+    sim_ms, idle_ms = 0.0, 0.0
+    api.graph_stats(model, reset=True)
+    rec, t_host = [], 0.0
+    t_wall0 = time.perf_counter()
+    step = 0
+    while step < steps + 5:
+        th = time.perf_counter()
+        while pending and pending[0][0] <= sim_ms:
+            t_r, i = pending.pop(0)
+            sched.admit(sid[i], handles[i], ctx[i], t_r)
+        members, _ = sched.plan()
+        if not members:   # server idle until the next arrival
+            idle_ms += pending[0][0] - sim_ms
+            sim_ms = pending[0][0]
+            continue
+        idx = [by_sid[m_[0]] for m_ in members]
+        B = len(idx)
+        trees = [pooled_tree(rng, wl.n_nodes, wl.depth, wl.branching, shape.vocab) for _ in idx]
+        off, parent, token, logprob = api.pack_trees(trees)
+        T = int(off[-1])
+        hbuf["kv"][:B] = torch.as_tensor([handles[i] for i in idx], dtype=torch.int32)
+        hbuf["context_len"][:B] = torch.as_tensor([ctx[i] for i in idx], dtype=torch.int32)
+        hbuf["root_token"][:B] = torch.as_tensor([roots[i] for i in idx], dtype=torch.int32)
+        hbuf["session_id"][:B] = torch.as_tensor([sid[i] for i in idx], dtype=torch.int64)
+        hbuf["round"][:B] = torch.as_tensor([rounds[i] for i in idx], dtype=torch.int32)
+        hbuf["node_offset"][:B + 1] = torch.from_numpy(off)
+        hbuf["parent"][:T] = torch.from_numpy(parent)
+        hbuf["token"][:T] = torch.from_numpy(token)
+        hbuf["draft_logprob"][:T] = torch.from_numpy(logprob)
+        t_host += time.perf_counter() - th if step >= 5 else 0.0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n_in = dict(kv=B, context_len=B, root_token=B, session_id=B, round=B, node_offset=B + 1, parent=T, token=T,
+                    draft_logprob=T)
+        for k, n in n_in.items():
+            dbuf[k][:n].copy_(hbuf[k][:n], non_blocking=True)
+        batch = api.Batch(dbuf["kv"][:B], dbuf["context_len"][:B], dbuf["root_token"][:B], dbuf["session_id"][:B],
+                          dbuf["round"][:B], dbuf["node_offset"][:B + 1], dbuf["parent"], dbuf["token"],
+                          dbuf["draft_logprob"], T, wl.n_nodes, cap)
+        api.verify(model, pool, batch, ws, auto_commit=True, out=out_full)
+        h_acc[:B].copy_(out_full.accepted_len[:B], non_blocking=True)
+        hb = out_full.bonus[:B].cpu()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        acc = h_acc[:B].tolist()
+        th = time.perf_counter()
+        for k_, i in enumerate(idx):
+            ctx[i] += acc[k_] + 1
+            roots[i] = int(hb[k_])
+            rounds[i] += 1
+        sim_ms += ms
+        sched.complete([sid[i] for i in idx], ms)
+        depth = max(1, sched.state()["depth"])
+        for i in idx:
+            pending.append((sim_ms + rtt[i] + depth * 11.0, i))
+        pending.sort()
+        if step >= 5:
+            t_host += time.perf_counter() - th
+            rec.append((B, T, ms, sum(a + 1 for a in acc)))
+        step += 1
+    wall = time.perf_counter() - t_wall0
+    gs = api.graph_stats(model)
+    sched_depth = sched.state()["depth"]
+    pool.close()
+    sched.close()
+    ms_all = [r_[2] for r_ in rec]
+    tot_ms = sum(ms_all)
+    return {"steps": len(rec), "sessions": n_ses, "batch_capacity": cap_b,
+            "batch_sizes": sorted(set(r_[0] for r_ in rec)), "mean_batch": round(float(np.mean([r_[0] for r_ in rec])), 2),
+            "p50_ms": round(float(np.median(ms_all)), 4), "p90_ms": round(float(np.quantile(ms_all, 0.9)), 4),
+            "tokens_per_s_measured": round(sum(r_[3] for r_ in rec) / (tot_ms / 1e3), 1),
+            "tokens_per_verify_measured": round(sum(r_[3] for r_ in rec) / sum(r_[0] for r_ in rec), 3),
+            "tokens_per_s_at_3.98": round(3.98 * sum(r_[0] for r_ in rec) / (tot_ms / 1e3), 1),
+            "rows_per_s": round(sum(r_[1] + r_[0] for r_ in rec) / (tot_ms / 1e3), 1),
+            "graph_cache": gs, "host_ms_per_step": round(1e3 * t_host / max(1, len(rec)), 3),
+            "server_busy_frac": round((sim_ms - idle_ms) / max(1e-9, sim_ms), 3),
+            "depth_calibrated": sched_depth,
+            "wall_s": round(wall, 2),
+            "note": "device time per step includes the H2D of the step's inputs and the D2H of its outputs; "
+                    "scheduler and tree drawing are host time (host_ms_per_step)"}
 
 
 # ------------------------------------------------------------------------------- CPU oracle arm
@@ -528,6 +667,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host each step")
+    ap.add_argument("--no-serving", action="store_true", help="skip the serving-realistic leg")
     args = ap.parse_args()
     world, rank, local = _dist()
     if args.impl == "reference":

@@ -288,6 +288,13 @@ specedge_status specedge_debug_attention(const uint16_t* q, const uint16_t* k_pr
                                          int32_t n_splits, float* o, void* workspace,
                                          size_t ws_bytes, void* stream);
 
+/* CUDA-graph cache of whole verify steps: out3 = {replays of a cached graph, captures (a
+ * signature's second use), plain launches (a signature's first use)} since the last reset.  A
+ * signature is (num_requests, total_nodes, max_nodes, max_context_len, mode, temperature, seed,
+ * auto_commit, buffer addresses): a serving loop that keeps its buffers and passes a constant
+ * max_context_len bound reuses one graph per (batch size, node count).  Host only. */
+specedge_status specedge_graph_stats(const specedge_model* model, int64_t* out3, int32_t reset);
+
 /* Number of kernels the last verify_batch call launched (host counter, for the benchmark's
  * gpu_launches field). */
 int32_t specedge_last_launch_count(void);

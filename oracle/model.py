@@ -9,8 +9,9 @@ LM head, no biases, QK-norm off.
 
 Storage points (reading R-precision, revising SURVEY amb. A12): bf16 for weights,
 embeddings and the GEMM input operands (normed h, attention output O, MLP hidden M); fp16 for the
-attention operands q, k (post-RoPE) and v, hence the KV cache (so that softmax P can enter the PV
-product as fp16: P in bf16 breaks the 1e-3 attention tolerance).  Unrounded: the residual stream
+attention operands q, k (post-RoPE) and v, hence the KV cache, and for the softmax numerator P
+as the PV product consumes it (numerics.attention_weights; P in bf16 would break the 1e-3
+attention tolerance).  Unrounded: the residual stream
 x (the GPU keeps it in fp32) and the final-norm output (the GPU passes it to the LM head as a
 hi/lo pair of bf16 operands); rounding those two amplifies arithmetic-order noise past the
 north_star logit tolerance (measured).
@@ -38,7 +39,7 @@ import math
 import numpy as np
 
 from . import philox
-from .numerics import bf16, f16, rmsnorm, rope, silu, attention
+from .numerics import bf16, f16, rmsnorm, rope, silu, attention, attention_weights
 
 # Matmul arithmetic of the oracle.  float64 is the reference; tests switch it to float32 (same
 # storage contract) to measure the oracle's own arithmetic-noise floor, against which the
@@ -294,8 +295,6 @@ def prefill_dense(W: Weights, tokens):
         for h in range(s.n_heads):
             sc = (q[:, h] @ k[:, h // G].T) / np.sqrt(s.head_dim)
             sc = np.where(mask, sc, -np.inf)
-            p = np.exp(sc - sc.max(axis=1, keepdims=True))
-            p /= p.sum(axis=1, keepdims=True)
-            o[:, h] = p @ v[:, h // G]
+            o[:, h] = attention_weights(sc) @ v[:, h // G]
         x = _post_attn(W, l, x, o)
     return final_hidden(W, x), cache

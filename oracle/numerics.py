@@ -84,11 +84,29 @@ def softmax(s, axis=-1):
     return e / np.sum(e, axis=axis, keepdims=True)
 
 
+# Storage point of the softmax numerator (DESIGN.md R-precision; SURVEY amb. A12: "optionally
+# P -> fp16/bf16 to mirror the kernel").  The library's PV product takes P as an fp16 operand
+# while the normaliser sums the unrounded exponentials, so the oracle rounds the same point:
+# softmax weight = f16(exp(s - max)) / sum exp(s - max).  False = the plain softmax (pins).
+ATTN_P_F16 = True
+
+
+def attention_weights(s):
+    """Softmax over the last axis as the PV product consumes it (see ATTN_P_F16); -inf scores
+    (masked keys) get weight 0."""
+    s = np.asarray(s, np.float64)
+    m = np.max(s, axis=-1, keepdims=True)
+    e = np.exp(s - m)
+    num = f16(e) if ATTN_P_F16 else e
+    return num / np.sum(e, axis=-1, keepdims=True)
+
+
 def attention(q, k, v):
     """Scaled-dot-product attention of one query set over one key set (SURVEY amb. A15).
 
-    q [nq, hd], k [nk, hd], v [nk, hd] -> [nq, hd]; scores q.k/sqrt(hd), softmax over keys.
+    q [nq, hd], k [nk, hd], v [nk, hd] -> [nq, hd]; scores q.k/sqrt(hd), softmax over keys with
+    the numerator stored in fp16 (ATTN_P_F16).
     """
     hd = q.shape[-1]
     s = (q @ k.T) / np.sqrt(hd)
-    return softmax(s, axis=-1) @ v
+    return attention_weights(s) @ v

@@ -305,6 +305,13 @@ def host_outputs(hb: HostBatch):
                 row_target=z(R), row_score=z(R, torch.float32))
 
 
+def graph_stats(model: Model, reset: bool = False) -> dict:
+    """Verify-step CUDA-graph cache counters (include/specedge.h specedge_graph_stats)."""
+    out = (C.c_int64 * 3)()
+    L.check(model.lib.specedge_graph_stats(model.h, C.cast(out, C.c_void_p), 1 if reset else 0), "graph_stats")
+    return dict(replays=out[0], captures=out[1], plain=out[2])
+
+
 def last_launch_count() -> int:
     return int(L.load().specedge_last_launch_count())
 

@@ -39,25 +39,12 @@ __host__ __device__ inline SmemLayout smem_layout(int stages, int BN) {
   L.b_off = L.a_off + stages * kABytes;
   L.xch_off = L.b_off + stages * (uint32_t)BN * 128u;
   L.red_off = L.xch_off + 128 * kXchStride * 4;
-  L.bar_off = L.red_off + 4 * 32 * 8;
+  L.bar_off = L.red_off + 4 * 32 * 12;   // red_v, red_i, red_s2 [128] each
   L.total = L.bar_off + (2 * stages + 4) * 8 + 16;
   return L;
 }
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
-
-// Gumbel noise for (row, vocab v) — SURVEY amb. A9: key (lo32(seed) ^ round, hi32(seed)),
-// counter (v>>2, slot, lo32(session), hi32(session)), word v&3, u = ((x>>8)|1) 2^-24.
-__device__ __forceinline__ float gumbel_noise(const GemmArgs& a, int row, int v) {
-  const int req = a.row_req[row];
-  const uint32_t rnd = a.req_round[req];
-  const uint64_t ses = a.req_session[req];
-  U4 c{(uint32_t)v >> 2, (uint32_t)a.row_slot[row], (uint32_t)ses, (uint32_t)(ses >> 32)};
-  U4 r = philox4x32_10(c, a.seed_lo ^ rnd, a.seed_hi);
-  const uint32_t w = u4_word(r, v & 3);
-  const float u = (float)((w >> 8) | 1u) * 5.9604644775390625e-08f;  // exact
-  return -logf(-logf(u));
-}
 
 // Epilogue of one 32-column chunk of a 128-feature accumulator tile.  v[j] = D[feature][row]
 // for feature = m128*128 + tl (tl = TMEM lane) and row = row_base + j, j < ncol.
@@ -186,19 +173,50 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         if (!fv || j >= ncol || row >= a.R) return __int_as_float(0x7fc00000);
         return a.pair ? __uint_as_float(v[2 * jj]) + __uint_as_float(v[2 * jj + 1]) : __uint_as_float(v[jj]);
       };
-      // ---- Gumbel noise of (row, vg), precomputed for the whole [R][vocab] block by k_gumbel_fill
-      // (a full-occupancy kernel: in this 4-warp epilogue the Philox rounds would cost more than the
-      // MMA main loop hides); coalesced across the lanes' consecutive vocab ids
-      float gn[32];
-      if (MODE == EPI_PQ2 || a.sample) {
-#pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          if (jj >= np) break;
+      // ---- Gumbel noise g(seed, round, session, slot, vg) (SURVEY amb. A9), generated here: no
+      // [R][vocab] noise tensor ever reaches HBM.  One Philox4x32-10 block covers 4 consecutive
+      // vocab ids = the 4 lanes of a quad (vocab_off % 4 == 0), so lane q of a quad computes the
+      // block of logical row j4 + q and stores its 4 words into the quad's 4 cells of that row of
+      // the exchange buffer (conflict-free: bank = 4k + q); every lane then reads its own cell.
+      // The raw words are turned into noise in the score loop below, which overwrites the cells.
+      const bool noisy = MODE == EPI_PQ2 || a.sample;
+      const bool quad_ok = (a.vocab_off & 3) == 0;
+      if (noisy && quad_ok) {
+        const int qd = tl & 3;
+        for (int j4 = 0; j4 < np; j4 += 4) {
+          const int jj = j4 + qd;
           const int j = a.pair ? 2 * jj : jj;
           const int row = min(row_base + j, a.R - 1);
-          gn[jj] = fv ? a.noise[(size_t)(a.pair ? row >> 1 : row) * a.vocab + feat] : 0.f;
+          const int lr = a.pair ? row >> 1 : row;
+          const int req = a.row_req[lr];
+          const uint64_t ses = a.req_session[req];
+          const U4 w = philox4x32_10(U4{(uint32_t)vg >> 2, (uint32_t)a.row_slot[lr], (uint32_t)ses, (uint32_t)(ses >> 32)},
+                                     a.seed_lo ^ a.req_round[req], a.seed_hi);
+          uint32_t* cell = reinterpret_cast<uint32_t*>(xch) + (tl & ~3) * kXchStride + jj;
+          cell[0] = w.x;
+          cell[kXchStride] = w.y;
+          cell[2 * kXchStride] = w.z;
+          cell[3 * kXchStride] = w.w;
         }
+        __syncwarp();
       }
+      auto gumbel_at = [&](int jj) -> float {
+        uint32_t wd;
+        if (quad_ok) {
+          wd = reinterpret_cast<const uint32_t*>(xch)[tl * kXchStride + jj];
+        } else {   // a vocab shard not aligned to 4 ids: this lane's own block
+          const int j = a.pair ? 2 * jj : jj;
+          const int row = min(row_base + j, a.R - 1);
+          const int lr = a.pair ? row >> 1 : row;
+          const int req = a.row_req[lr];
+          const uint64_t ses = a.req_session[req];
+          const U4 w = philox4x32_10(U4{(uint32_t)vg >> 2, (uint32_t)a.row_slot[lr], (uint32_t)ses, (uint32_t)(ses >> 32)},
+                                     a.seed_lo ^ a.req_round[req], a.seed_hi);
+          wd = u4_word(w, vg & 3);
+        }
+        const float u = (float)((wd >> 8) | 1u) * 5.9604644775390625e-08f;   // exact, in (0, 1)
+        return -logf(-logf(u));
+      };
       // ---- scores for the tile argmax
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj) {
@@ -214,35 +232,41 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
               const float pv = __expf(fmaf(l, a.inv_t, -a.lse[lr]));
               if (vg == a.node_token[qn]) a.pchild[lr] = pv;
               const float r = pv - a.draft_q[(size_t)qn * a.vocab_q + vg];
-              if (r > 0.f) sc = __logf(r) + gn[jj];
+              if (r > 0.f) sc = __logf(r) + gumbel_at(jj);
             }
           } else {
-            sc = a.sample ? l * a.inv_t + gn[jj] : l;
+            sc = a.sample ? l * a.inv_t + gumbel_at(jj) : l;
           }
         }
         xch[tl * kXchStride + jj] = sc;
       }
       named_bar_sync(1, kEpiThreads);
       const int ngrp = 128 / np, per = 128 / ngrp;
+      // tile argmax per row (ties -> lowest id: features scanned in increasing order); a.top2
+      // also keeps the tile's second-best score (k_lm_refine's candidate window, hi-only pass)
+      float* red_s2 = red_v + 256;
       {
         const int jj = et % np, g = et / np;
-        float best = -INFINITY;
+        float best = -INFINITY, sec = -INFINITY;
         int bi = 0x7fffffff;
         for (int l = 0; l < per; ++l) {
           const float sc = xch[(g * per + l) * kXchStride + jj];
-          if (sc > best) { best = sc; bi = a.vocab_off + m128 * 128 + g * per + l; }
+          if (sc > best) { sec = best; best = sc; bi = a.vocab_off + m128 * 128 + g * per + l; }
+          else if (sc > sec) sec = sc;
         }
         red_v[g * np + jj] = best;
         red_i[g * np + jj] = bi;
+        red_s2[g * np + jj] = sec;
       }
       named_bar_sync(1, kEpiThreads);
       if (et < np) {
         const int jj = et;
-        float best = red_v[jj];
+        float best = red_v[jj], sec = red_s2[jj];
         int bi = red_i[jj];
         for (int g = 1; g < ngrp; ++g) {
           const float sc = red_v[g * np + jj];
-          if (sc > best) { best = sc; bi = red_i[g * np + jj]; }
+          if (sc > best) { sec = fmaxf(best, red_s2[g * np + jj]); best = sc; bi = red_i[g * np + jj]; }
+          else sec = fmaxf(sec, fmaxf(sc, red_s2[g * np + jj]));
         }
         const int j = a.pair ? 2 * jj : jj;
         const int row = row_base + j;
@@ -250,6 +274,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           const int lr = a.pair ? row >> 1 : row;
           a.part_val[(size_t)lr * a.ntm128 + m128] = best;
           a.part_idx[(size_t)lr * a.ntm128 + m128] = bi;
+          if (a.top2) a.part_val2[(size_t)lr * a.ntm128 + m128] = sec;
         }
       }
       named_bar_sync(1, kEpiThreads);
@@ -744,11 +769,12 @@ cudaError_t launch_mode2(const CUtensorMap& tmW, const CUtensorMap& tmX, const G
 
 }  // namespace
 
-bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                  uint64_t row_stride) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
+  cuuint64_t strides[1] = {(row_stride ? row_stride : cols) * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
@@ -795,7 +821,8 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
   a.stages = stages;
   const size_t smem = smem_layout(stages, HB).total + 1024;
   CUtensorMap tmX;
-  if (!make_tmap_2d(&tmX, X, (uint64_t)a.R, (uint64_t)a.K, (uint32_t)HB)) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tmX, X, (uint64_t)a.R, (uint64_t)a.K, (uint32_t)HB, (uint64_t)a.x_stride))
+    return cudaErrorInvalidValue;
   const int n_pairs = (a.M + 255) / 256;
   // pairs per cluster sharing each weight tile through TMA multicast (SPECEDGE_GEMM_NC = 0: the
   // N-tiles of one 256-feature tile, up to 4 pairs).  Off by default: measured on cfg2 it cuts
@@ -877,7 +904,8 @@ cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArg
   a.stages = stages;
   const size_t smem = smem_layout(stages, a.BN).total + 1024;
   CUtensorMap tmX;
-  if (!make_tmap_2d(&tmX, X, (uint64_t)a.R, (uint64_t)a.K, (uint32_t)a.BN)) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tmX, X, (uint64_t)a.R, (uint64_t)a.K, (uint32_t)a.BN, (uint64_t)a.x_stride))
+    return cudaErrorInvalidValue;
   const int ntiles = a.n_tiles_m * a.n_tiles_n;
   // K-split (EPI_F32 only, caller provides max_splits slices of split_stride floats): give every
   // CTA >= 2 units so the epilogue of one overlaps the MMAs of the next, and fill the SMs.

@@ -87,6 +87,8 @@ struct RmsSrc {                  // NEXT-F4: per-partial base pointers for k_rms
 
 struct GemmArgs {
   int M, R, K;            // weight rows (features), activation rows, reduction length
+  int x_stride;           // activation row stride in elements (0: K); the hi-only LM head reads
+                          // the even (hi) rows of the interleaved hi/lo final hidden
   int BN, n_tiles_n, n_tiles_m, num_kb, stages, tmem_cols;
   int ntm128;             // 128-feature tiles (stride of the ARGMAX partials)
   int pair;               // EPI_F32/EPI_ARGMAX: rows (2r, 2r+1) are hi/lo bf16 parts of row r
@@ -116,6 +118,8 @@ struct GemmArgs {
   // EPI_ARGMAX
   float* part_val;        // [R][n_tiles_m]
   int* part_idx;
+  int top2;               // also store the tile's second-best score (part_val2): hi-only LM head
+  float* part_val2;
   int vocab, sample;      // vocab: rows of this (vocab-shard) LM head
   int vocab_off;          // global id of local row 0 (tensor parallel vocab shard)
   float inv_t;
@@ -133,17 +137,12 @@ struct GemmArgs {
   const float* draft_q;   // [total_nodes][vocab_q] fp32
   int vocab_q;            // row stride of draft_q (= V)
   float* pchild;          // [R] p(child token) at this slot          (PQ2)
-  const float* noise;     // [R][vocab] Gumbel noise (sampled modes), from gumbel_fill_launch
 };
-// Gumbel noise g(seed, round, session, slot, v) for rows [0, R) x local vocab [0, vocab) (global
-// id vocab_off + v), amb. A9: Philox4x32-10 counter (v >> 2, slot, lo32(session), hi32(session)),
-// key (lo32(seed) ^ round, hi32(seed)), word v & 3, u = ((w >> 8) | 1) 2^-24, g = -log(-log u)
-cudaError_t gumbel_fill_launch(float* noise, int R, int vocab, int vocab_off, const int* row_req, const int* row_slot,
-                               const uint32_t* req_round, const uint64_t* req_session, uint32_t seed_lo,
-                               uint32_t seed_hi, cudaStream_t st, int* launches);
 
 // Build a 2D bf16 tensor map [rows][cols] (cols contiguous), box {64, box_rows}, 128B swizzle.
-bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// row_stride: elements between rows (0: cols, i.e. contiguous rows)
+bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                  uint64_t row_stride = 0);
 int gemm_pick_bn(int R);
 bool gemm_qkv_fused_ok(int M, int R);
 int gemm_splits_last();   // K-splits chosen by the last gemm_launch on this thread
@@ -245,6 +244,35 @@ struct RopeArgs {
 cudaError_t qkv_rope_launch(const RopeArgs& r, cudaStream_t st, int* launches);
 cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, int* y, float* score,
                              int* row_target, float* row_score, cudaStream_t st, int* launches);
+// a9 second stage of the hi-only LM head (k_lm_refine): the GEMM scores every vocab id with the
+// hi part of the final hidden only; per (row, tile) it keeps the best (value, id) and the second
+// best value.  |lo . W_v| <= ||lo||_2 max_v ||W_v||_2 (Cauchy-Schwarz), so the true argmax of
+// (hi + lo) . W lies among the ids whose hi score is within W_r = 2 (||lo|| + rho) wmax scale of the
+// best hi score (rho: worst-case fp32 accumulation error); every such candidate (its tile's best,
+// or all 128 ids of a tile whose second best also falls in the window) is rescored exactly with
+// (hi + lo) . W_v on the CUDA cores, and the argmax of the rescored set (ties -> lowest id) is the
+// row's target.
+struct RefineArgs {
+  int R, ntiles, d, vocab, vocab_off, sample;
+  float inv_t, wmax;
+  const float* part_val;    // [R][ntiles]
+  const int* part_idx;      // [R][ntiles] global ids
+  const float* part_val2;   // [R][ntiles]
+  const bf16* hf;           // [2R][d]: hi row 2r, lo row 2r+1
+  const bf16* w;            // LM head shard [vocab][d]
+  uint32_t seed_lo, seed_hi;
+  const int* row_req;
+  const int* row_slot;
+  const uint32_t* req_round;
+  const uint64_t* req_session;
+  int* y;
+  float* score;
+  int* row_target;          // nullable
+  float* row_score;         // nullable
+};
+cudaError_t lm_refine_launch(const RefineArgs& a, cudaStream_t st, int* launches);
+// max over rows of ||W_v||_2 (fp32) of a [rows][d] bf16 matrix into *out (device float, >= 0)
+cudaError_t row_norm_max_launch(const bf16* w, int rows, int d, float* out, cudaStream_t st);
 struct WalkArgs {
   int B, force_chain;
   const int* status;
@@ -387,6 +415,7 @@ struct specedge_model {
   std::vector<void*> tp_ipc_opened;
   se::bf16* embed = nullptr;
   se::bf16* lm_head = nullptr;
+  float lm_wmax = 0.f;          // max_v ||W_v||_2 of this rank's LM-head rows (k_lm_refine window)
   se::bf16* g_final = nullptr;
   struct Layer {
     se::bf16 *wqkv, *wo, *wgu, *wd, *g_attn, *g_mlp;
@@ -405,7 +434,9 @@ struct specedge_model {
     std::string key;
     cudaGraphExec_t exec;
   };
-  std::vector<Graph> graphs;
+  std::vector<Graph> graphs;        // up to 32 instantiated signatures, most recent first
+  std::vector<std::string> graph_seen;   // signatures used once (captured on their second use)
+  int64_t graph_stats[3] = {0, 0, 0};    // replays, captures, plain (uncaptured) runs
   cudaStream_t gstream = nullptr;
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
 };

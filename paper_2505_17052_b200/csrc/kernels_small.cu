@@ -331,6 +331,122 @@ __global__ void k_lm_reduce(const float* __restrict__ pv, const int* __restrict_
   }
 }
 
+// ------------------------------------------------------------- K9c hi-only LM head refinement
+// One warp per row (RefineArgs in internal.h).  Lanes hold 8-element slices of the row; the window
+// uses the row's own ||hi||_2, ||lo||_2 (read once here, so tensor-parallel ranks need no extra
+// collective) and the shard's max_v ||W_v||_2.
+__global__ void k_lm_refine(const __grid_constant__ RefineArgs a) {
+  pdl_begin();
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= a.R) return;
+  const float* pv = a.part_val + (size_t)row * a.ntiles;
+  const float* pv2 = a.part_val2 + (size_t)row * a.ntiles;
+  const int* pi = a.part_idx + (size_t)row * a.ntiles;
+  const uint4* hi = reinterpret_cast<const uint4*>(a.hf + (size_t)(2 * row) * a.d);
+  const uint4* lo = reinterpret_cast<const uint4*>(a.hf + (size_t)(2 * row + 1) * a.d);
+  const int nv = a.d / 8;
+  float M = -INFINITY;
+  for (int t = lane; t < a.ntiles; t += 32) M = fmaxf(M, pv[t]);
+  float sh = 0.f, sl = 0.f;
+  for (int e = lane; e < nv; e += 32) {
+    const uint4 h = hi[e], l = lo[e];
+    const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float h0 = __uint_as_float(hw[k] << 16), h1 = __uint_as_float(hw[k] & 0xFFFF0000u);
+      const float l0 = __uint_as_float(lw[k] << 16), l1 = __uint_as_float(lw[k] & 0xFFFF0000u);
+      sh = fmaf(h0, h0, fmaf(h1, h1, sh));
+      sl = fmaf(l0, l0, fmaf(l1, l1, sl));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    sh += __shfl_xor_sync(0xffffffffu, sh, o);
+    sl += __shfl_xor_sync(0xffffffffu, sl, o);
+  }
+  // |score_hi(v) - score(v)| <= (||lo|| + rho) wmax scale, rho = d 2^-24 (||hi|| + ||lo||) bounds
+  // the fp32 accumulation error of either evaluation; + a few ulps of |M| for the final rounding
+  const float nh = sqrtf(sh) * 1.0001f, nl = sqrtf(sl) * 1.0001f;
+  const float scale = a.sample ? a.inv_t : 1.f;
+  const float rho = (float)a.d * 5.9604645e-08f * (nh + nl);
+  const float win = 2.f * (nl + rho) * a.wmax * scale + 8.f * 1.1920929e-07f * fabsf(M) + 1e-6f;
+  const float thr = M - win;
+  const int req = a.row_req[row];
+  const uint64_t ses = a.req_session[req];
+  const uint32_t k0 = a.seed_lo ^ a.req_round[req], slot = (uint32_t)a.row_slot[row];
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  // exact score of local vocab id v (warp-collective; every lane returns the same value)
+  auto rescore = [&](int v) -> float {
+    const uint4* wr = reinterpret_cast<const uint4*>(a.w + (size_t)v * a.d);
+    float acc = 0.f;
+    for (int e = lane; e < nv; e += 32) {
+      const uint4 h = hi[e], l = lo[e], w = __ldg(wr + e);
+      const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w}, ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        // hi + lo is exact in fp32 (bf16 + bf16 below half an ulp of hi)
+        const float y0 = __uint_as_float(hw[k] << 16) + __uint_as_float(lw[k] << 16);
+        const float y1 = __uint_as_float(hw[k] & 0xFFFF0000u) + __uint_as_float(lw[k] & 0xFFFF0000u);
+        acc = fmaf(y0, __uint_as_float(ww[k] << 16), acc);
+        acc = fmaf(y1, __uint_as_float(ww[k] & 0xFFFF0000u), acc);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (!a.sample) return acc;
+    const int vg = a.vocab_off + v;
+    const U4 r = philox4x32_10(U4{(uint32_t)vg >> 2, slot, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0, a.seed_hi);
+    const float u = (float)((u4_word(r, vg & 3) >> 8) | 1u) * 5.9604644775390625e-08f;
+    return acc * a.inv_t + (-logf(-logf(u)));
+  };
+  auto consider = [&](int v) {
+    const float sc = rescore(v);
+    const int vg = a.vocab_off + v;
+    if (sc > best || (sc == best && vg < bi)) { best = sc; bi = vg; }
+  };
+  for (int t0 = 0; t0 < a.ntiles; t0 += 32) {
+    const int t = t0 + lane;
+    unsigned bal = __ballot_sync(0xffffffffu, t < a.ntiles && pv[t] >= thr);
+    while (bal) {
+      const int tt = t0 + __ffs(bal) - 1;
+      bal &= bal - 1;
+      if (pv2[tt] >= thr) {   // a second id of this tile may win: rescore the whole tile
+        const int v1 = min(a.vocab, (tt + 1) * 128);
+        for (int v = tt * 128; v < v1; ++v) consider(v);
+      } else {
+        consider(pi[tt] - a.vocab_off);
+      }
+    }
+  }
+  if (lane == 0) {
+    a.y[row] = bi;
+    a.score[row] = best;
+    if (a.row_target) a.row_target[row] = bi;
+    if (a.row_score) a.row_score[row] = best;
+  }
+}
+
+__global__ void k_row_norm_max(const bf16* __restrict__ w, int rows, int d, float* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const uint4* wr = reinterpret_cast<const uint4*>(w + (size_t)row * d);
+  float s = 0.f;
+  for (int e = lane; e < d / 8; e += 32) {
+    const uint4 x = wr[e];
+    const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float a0 = __uint_as_float(xw[k] << 16), a1 = __uint_as_float(xw[k] & 0xFFFF0000u);
+      s = fmaf(a0, a0, fmaf(a1, a1, s));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  // non-negative floats order like their bit patterns
+  if (lane == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(sqrtf(s)));
+}
+
 // ------------------------------------------------------------------------------ K10 walk
 // One warp per request; lane l examines nodes l and l+32 (N <= 64 for valid requests).
 __global__ void k_walk(const __grid_constant__ WalkArgs w) {
@@ -437,49 +553,6 @@ __global__ void k_set_len(int* __restrict__ cache_len, const __grid_constant__ S
   pdl_begin();
   const int i = threadIdx.x;
   if (i < a.n) cache_len[a.handle[i]] = a.len[i];
-}
-
-// --------------------------------------------------------------- Gumbel noise block (a9)
-// One thread per (row, 4 consecutive vocab ids): one Philox call yields the 4 words.  The local
-// vocab offset is added to the global id; when vocab_off is not a multiple of 4 the quads straddle
-// counters, so each thread evaluates its 4 ids separately.
-__global__ void k_gumbel_fill(float* __restrict__ noise, int R, int vocab, int vocab_off, const int* __restrict__ row_req,
-                              const int* __restrict__ row_slot, const uint32_t* __restrict__ req_round,
-                              const uint64_t* __restrict__ req_session, uint32_t seed_lo, uint32_t seed_hi) {
-  pdl_begin();
-  const int nq = (vocab + 3) / 4;
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= (long long)R * nq) return;
-  const int row = (int)(i / nq), q4 = (int)(i % nq);
-  const int req = row_req[row];
-  const uint64_t ses = req_session[req];
-  const uint32_t k0 = seed_lo ^ req_round[req];
-  const uint32_t slot = (uint32_t)row_slot[row];
-  float g[4];
-  if ((vocab_off & 3) == 0) {
-    const U4 w = philox4x32_10(U4{(uint32_t)((vocab_off >> 2) + q4), slot, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0,
-                               seed_hi);
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float u = (float)((ws[k] >> 8) | 1u) * 5.9604644775390625e-08f;
-      g[k] = -logf(-logf(u));
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t v = (uint32_t)(vocab_off + 4 * q4 + k);
-      const U4 w = philox4x32_10(U4{v >> 2, slot, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0, seed_hi);
-      const float u = (float)((u4_word(w, (int)(v & 3)) >> 8) | 1u) * 5.9604644775390625e-08f;
-      g[k] = -logf(-logf(u));
-    }
-  }
-  float* dst = noise + (size_t)row * vocab + 4 * q4;
-  if (4 * q4 + 3 < vocab && (vocab & 3) == 0) {
-    *reinterpret_cast<float4*>(dst) = make_float4(g[0], g[1], g[2], g[3]);
-  } else {
-    for (int k = 0; k < 4 && 4 * q4 + k < vocab; ++k) dst[k] = g[k];
-  }
 }
 
 // ------------------------------------------------------- NEXT-F2 dense-q speculative sampling
@@ -669,6 +742,16 @@ cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, 
   CK_RET(launch_k(k_lm_reduce, dim3((R + 3) / 4), dim3(128), 0, st, pv, pi, R, ntiles, y, score, row_target, row_score));
   return cudaGetLastError();
 }
+cudaError_t lm_refine_launch(const RefineArgs& a, cudaStream_t st, int* launches) {
+  if (launches) ++*launches;
+  CK_RET(launch_k(k_lm_refine, dim3((a.R + 3) / 4), dim3(128), 0, st, a));
+  return cudaGetLastError();
+}
+cudaError_t row_norm_max_launch(const bf16* w, int rows, int d, float* out, cudaStream_t st) {
+  CK_RET(cudaMemsetAsync(out, 0, sizeof(float), st));
+  k_row_norm_max<<<(rows + 7) / 8, 256, 0, st>>>(w, rows, d, out);
+  return cudaGetLastError();
+}
 cudaError_t walk_launch(const WalkArgs& w, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
   CK_RET(launch_k(k_walk, dim3((w.B + 3) / 4), dim3(128), 0, st, w));
@@ -680,15 +763,6 @@ cudaError_t commit_launch(const CommitArgs& c, cudaStream_t st, int* launches) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CK_RET(launch_k(k_commit_finalize, dim3((c.B + 127) / 128), dim3(128), 0, st, c));
-  return cudaGetLastError();
-}
-cudaError_t gumbel_fill_launch(float* noise, int R, int vocab, int vocab_off, const int* row_req, const int* row_slot,
-                               const uint32_t* req_round, const uint64_t* req_session, uint32_t seed_lo,
-                               uint32_t seed_hi, cudaStream_t st, int* launches) {
-  if (launches) ++*launches;
-  const long long n = (long long)R * ((vocab + 3) / 4);
-  CK_RET(launch_k(k_gumbel_fill, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, noise, R, vocab, vocab_off,
-                  row_req, row_slot, req_round, req_session, seed_lo, seed_hi));
   return cudaGetLastError();
 }
 cudaError_t pq_lse_launch(const PqArgs& a, cudaStream_t st, int* launches) {

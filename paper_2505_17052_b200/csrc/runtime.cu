@@ -36,6 +36,12 @@ bool attn_balanced(int max_pages) {
   return force >= 0 ? force == 1 : max_pages >= min_pages;
 }
 int num_sms() { return device_sms(); }
+// a9: hi-only LM head + exact candidate rescoring (default), or the hi/lo operand pair through the
+// MMA for every vocab id (SPECEDGE_LM_PAIR=1)
+bool lm_hi_only() {
+  static const bool pair = getenv("SPECEDGE_LM_PAIR") && getenv("SPECEDGE_LM_PAIR")[0] == '1';
+  return !pair;
+}
 
 thread_local int g_last_launches = 0;
 
@@ -116,9 +122,10 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
   size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
-  size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, attn_nch, attn_cnt, part_val, part_idx, y, score, tp_gather;
+  size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, attn_nch, attn_cnt, part_val, part_idx, part_val2, y, score,
+      tp_gather;
   size_t part_m, part_s, lse, row_qnode, pchild, resid_y, resid_s;   // SAMPLE_PQ_DENSE
-  size_t noise;                                                       // [R][V] Gumbel noise (sampled modes)
+  size_t draft_logits;                                                // [R][V] fp32 logits of a draft pass (NEXT-F3 only)
   size_t stage_in, stage_out, total;
   int B, R, n_splits_max;
 };
@@ -164,6 +171,7 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   const size_t vt = (c.vocab + 127) / 128;
   w.part_val = take(4 * (size_t)R * vt);
   w.part_idx = take(4 * (size_t)R * vt);
+  w.part_val2 = take(4 * (size_t)R * vt);
   w.y = take(4 * R);
   w.score = take(4 * R);
   w.tp_gather = take(8 * (size_t)(kMaxTp + 1) * R);   // TP C3: [tp][R](score, id) + own staging
@@ -174,7 +182,7 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.pchild = take(4 * R);
   w.resid_y = take(4 * R);
   w.resid_s = take(4 * R);
-  w.noise = take(4 * (size_t)R * c.vocab);
+  w.draft_logits = take(4 * (size_t)R * c.vocab);
   // staging for the host-buffer entry point: inputs then outputs
   w.stage_in = take((size_t)B * (4 + 4 + 4 + 8 + 4) + 4 * (B + 1) + (size_t)R * 12 + 64);
   w.stage_out = take((size_t)B * 12 + (size_t)R * 8 + (size_t)R * 8 + 64);
@@ -520,12 +528,6 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gl.row_slot = pa.row_slot;
     gl.req_round = di.round;
     gl.req_session = di.session_id;
-    if (sample || in->mode == SPECEDGE_SAMPLE_PQ_DENSE) {
-      gl.noise = (float*)P(w.noise);
-      KTimer _t(K_LM, st);
-      CK(gumbel_fill_launch((float*)gl.noise, R, m->vl, m->v0, pa.row_req, pa.row_slot, di.round, di.session_id,
-                            gl.seed_lo, gl.seed_hi, st, &launches));
-    }
     if (in->mode == SPECEDGE_SAMPLE_PQ_DENSE) {
       // NEXT-F2: pass 1 = Gumbel-max of l/T (bonus after full acceptance) + tile (max, sum exp);
       // pass 2 = p(child) and the Gumbel-max of log max(0, p - q) (bonus after a rejection)
@@ -584,6 +586,45 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
                             nullptr, st, &launches));
       }
       { KTimer _t(K_WALK, st); CK(pq_walk_launch(pq, st, &launches)); }
+    } else if (lm_hi_only()) {
+      // hi-only LM head (one MMA pass over the vocabulary instead of the hi/lo pair) + exact
+      // rescoring of the candidates its window cannot rule out (k_lm_refine, internal.h)
+      GemmArgs gh = gl;
+      gh.pair = 0;
+      gh.R = R;
+      gh.x_stride = 2 * c.d;   // the even (hi) rows of the interleaved final hidden
+      gh.top2 = 1;
+      gh.part_val2 = (float*)P(w.part_val2);
+      { KTimer _t(K_LM, st); CK(gemm_launch(EPI_ARGMAX, m->tm_lm, Hf, gh, st, &launches)); }
+      RefineArgs rf{};
+      rf.R = R;
+      rf.ntiles = (m->vl + 127) / 128;
+      rf.d = c.d;
+      rf.vocab = m->vl;
+      rf.vocab_off = m->v0;
+      rf.sample = gl.sample;
+      rf.inv_t = gl.inv_t;
+      rf.wmax = m->lm_wmax;
+      rf.part_val = gl.part_val;
+      rf.part_idx = gl.part_idx;
+      rf.part_val2 = gh.part_val2;
+      rf.hf = Hf;
+      rf.w = m->lm_head;
+      rf.seed_lo = gl.seed_lo;
+      rf.seed_hi = gl.seed_hi;
+      rf.row_req = pa.row_req;
+      rf.row_slot = pa.row_slot;
+      rf.req_round = di.round;
+      rf.req_session = di.session_id;
+      rf.y = y;
+      rf.score = (float*)P(w.score);
+      rf.row_target = tp ? nullptr : dout.row_target;
+      rf.row_score = tp ? nullptr : dout.row_score;
+      KTimer _tr(K_LMRED, st);
+      CK(lm_refine_launch(rf, st, &launches));
+      if (tp)
+        CK(tp_argmax_gather(y, (float*)P(w.score), R, (float*)P(w.tp_gather), m->tp_size, m->nccl, dout.row_target,
+                            dout.row_score, st, &launches));
     } else {
       { KTimer _t(K_LM, st); CK(gemm_launch(EPI_ARGMAX, m->tm_lm, Hf, gl, st, &launches)); }
       KTimer _tr(K_LMRED, st);
@@ -696,7 +737,20 @@ specedge_status run_graphed(specedge_model* m, const std::string& key, cudaStrea
       if (i) std::swap(m->graphs[i], m->graphs[0]);   // most recent first
       break;
     }
-  if (!exec) {
+  if (exec) {
+    ++m->graph_stats[0];
+  } else {
+    // a signature is captured on its second use: one-off shapes (a serving loop's ragged batches)
+    // run as plain launches on the caller's stream instead of paying a capture + instantiation
+    auto it = std::find(m->graph_seen.begin(), m->graph_seen.end(), key);
+    if (it == m->graph_seen.end()) {
+      if (m->graph_seen.size() >= 64) m->graph_seen.erase(m->graph_seen.begin());
+      m->graph_seen.push_back(key);
+      ++m->graph_stats[2];
+      return body(st);
+    }
+    m->graph_seen.erase(it);
+    ++m->graph_stats[1];
     CK(cudaStreamBeginCapture(m->gstream, cudaStreamCaptureModeThreadLocal));
     const specedge_status s = body(m->gstream);
     cudaGraph_t graph = nullptr;
@@ -709,7 +763,7 @@ specedge_status run_graphed(specedge_model* m, const std::string& key, cudaStrea
     const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     CK(ei);
-    if (m->graphs.size() >= 8) {
+    if (m->graphs.size() >= 32) {
       cudaGraphExecDestroy(m->graphs.back().exec);
       m->graphs.pop_back();
     }
@@ -858,6 +912,13 @@ specedge_status specedge_model_create_tp(const specedge_model_config* cfg, uint6
     if (!ok) return fail(SPECEDGE_E_CUDA);
   }
   if (!make_tmap_2d(&m->tm_lm, m->lm_head, Vl, d, 128)) return fail(SPECEDGE_E_CUDA);
+  {   // max_v ||W_v||_2 of this shard's LM-head rows: the hi-only LM head's rescoring window
+    float* dmax = dalloc<float>(m, 1);
+    if (!dmax || row_norm_max_launch(m->lm_head, (int)Vl, (int)d, dmax, 0) != cudaSuccess ||
+        cudaMemcpy(&m->lm_wmax, dmax, sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(SPECEDGE_E_CUDA);
+    m->lm_wmax *= 1.0001f;   // margin over the fp32 evaluation of the norm
+  }
   // RoPE table: angles in double (amb. A14), stored fp32
   const size_t half = hd / 2;
   std::vector<float> cs((size_t)c.max_position * half), sn((size_t)c.max_position * half);
@@ -1073,6 +1134,13 @@ specedge_status specedge_verify_batch(specedge_model* m, specedge_kvpool* pool, 
   return run_graphed(m, key, st, [&](cudaStream_t gs) {
     return run_verify(m, pool, in, di, dout, (uint8_t*)workspace, ws_bytes, gs, false, in->auto_commit != 0);
   });
+}
+
+specedge_status specedge_graph_stats(const specedge_model* m, int64_t* out3, int32_t reset) {
+  if (!m || !out3) return SPECEDGE_E_INVALID;
+  for (int i = 0; i < 3; ++i) out3[i] = m->graph_stats[i];
+  if (reset) for (int i = 0; i < 3; ++i) const_cast<specedge_model*>(m)->graph_stats[i] = 0;
+  return SPECEDGE_OK;
 }
 
 specedge_status specedge_kv_commit(specedge_model* m, specedge_kvpool* pool, const specedge_verify_in* in,
@@ -1363,7 +1431,7 @@ specedge_status specedge_draft_tree(specedge_model* m, specedge_kvpool* pool, in
     int* d_rows = (int*)(ws + w.y);
     int* d_tok = (int*)(ws + w.part_idx);
     float* d_lp = (float*)(ws + w.part_val);
-    float* logits = (float*)(ws + w.noise);   // [R][V] fp32 (the sampled modes' noise block)
+    float* logits = (float*)(ws + w.draft_logits);   // [R][V] fp32
     // inputs: kv, context_len, root_token, round, session (8 B), node_offset[2], parent[N], token[N]
     std::vector<int32_t> h32(5 + 2 + 2 * N + 2);
     h32[0] = handle;

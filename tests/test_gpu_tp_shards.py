@@ -42,8 +42,9 @@ def test_tp_shards_are_slices_of_the_tp1_model(api, shape):
     try:
         # sampled logical rows / columns of the full model (every row would be ~GBs of host copies)
         pick = lambda n, k: np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, k)]))
-        full_wo = _rows(full, 5, 0, pick(d, 24), H * hd)
-        full_wd = _rows(full, 8, 0, pick(d, 24), F)
+        wo_idx, wd_idx = pick(d, 24), pick(d, 24)
+        full_wo = _rows(full, 5, 0, wo_idx, H * hd)
+        full_wd = _rows(full, 8, 0, wd_idx, F)
         gains = [full.weight_rows(t, 0, 0, 1, d) for t in (10, 11, 12)]
         emb_idx = pick(V, 16)
         emb = _rows(full, 1, 0, emb_idx, d)
@@ -63,9 +64,9 @@ def test_tp_shards_are_slices_of_the_tp1_model(api, shape):
                         loc = pick(n_loc, 8)
                         assert np.array_equal(_rows(sh, t, 0, loc, d), _rows(full, t, 0, loc + off, d)), (tp, rank, t)
                     # row-parallel Wo / Wd: the shard's input columns of every output row
-                    wo = _rows(sh, 5, 0, pick(d, 24), Hl * hd)
+                    wo = _rows(sh, 5, 0, wo_idx, Hl * hd)
                     assert np.array_equal(wo, full_wo[:, rank * Hl * hd:(rank + 1) * Hl * hd]), (tp, rank, "wo")
-                    wd = _rows(sh, 8, 0, pick(d, 24), Fl)
+                    wd = _rows(sh, 8, 0, wd_idx, Fl)
                     assert np.array_equal(wd, full_wd[:, rank * Fl:(rank + 1) * Fl]), (tp, rank, "wd")
                     loc = pick(sh.vocab_n, 8)
                     assert np.array_equal(_rows(sh, 9, 0, loc, d), _rows(full, 9, 0, loc + sh.vocab0, d)), (tp, rank)

@@ -123,11 +123,31 @@ def test_rope_against_complex_rotation_and_invariants():
 
 
 def test_attention_against_torch_sdpa():
+    """The plain softmax (ATTN_P_F16 off) is SDPA to fp64 rounding; with the fp16 numerator
+    (R-precision) every weight carries one fp16 rounding of relative size <= 2^-11, so
+    |o - sdpa| <= 2^-11 * sum_j p_j |v_j| elementwise (p = the exact softmax) — a dropped term,
+    a wrong scale or a rounded denominator breaks one of the two."""
+    import oracle.numerics as N
     rng = np.random.default_rng(3)
     q, k, v = rng.standard_normal((7, 16)), rng.standard_normal((40, 16)), rng.standard_normal((40, 16))
     ref = torch.nn.functional.scaled_dot_product_attention(
         torch.from_numpy(q)[None], torch.from_numpy(k)[None], torch.from_numpy(v)[None])[0].numpy()
-    assert np.allclose(attention(q, k, v), ref, atol=1e-12)
+    N.ATTN_P_F16 = False
+    try:
+        assert np.allclose(attention(q, k, v), ref, rtol=0, atol=1e-12)
+    finally:
+        N.ATTN_P_F16 = True
+    o = attention(q, k, v)
+    p = softmax(q @ k.T / 4.0)
+    bound = 2.0 ** -11 * (p @ np.abs(v))
+    assert np.all(np.abs(o - ref) <= bound + 1e-12)
+    assert np.abs(o - ref).max() > 1e-7          # the rounding is really applied
+    # exponentials exactly representable in fp16 (equal scores -> p = 1): no rounding at all
+    qz = np.zeros((2, 16))
+    assert np.allclose(attention(qz, k, v), v.mean(axis=0)[None].repeat(2, 0), rtol=0, atol=1e-12)
+    # the denominator is the unrounded sum: weights of exp values 1 and e^-1 (fp16(e^-1) != e^-1)
+    w = N.attention_weights(np.array([[0.0, -1.0]]))
+    assert w[0, 0] == 1.0 / (1.0 + np.exp(-1.0)) and w[0, 1] == float(np.float16(np.exp(-1.0))) / (1.0 + np.exp(-1.0))
 
 
 def test_softmax_silu_closed_forms():
