@@ -161,6 +161,10 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         named_bar_sync(1, kEpiThreads);
       }
     } else if constexpr (MODE == EPI_ARGMAX || MODE == EPI_PQ1 || MODE == EPI_PQ2) {
+      // the CTA pair's second 128-feature half past the last vocab tile (an odd tile count, e.g.
+      // V = 151936 = 1187 x 128): nothing to reduce, and its partial slot [lr][ntm128] would be
+      // the next row's tile 0 (uniform per CTA: every epilogue thread returns, no barrier is split)
+      if (m128 >= a.ntm128) return;
       // a.pair: physical rows (2r, 2r+1) = hi/lo parts of logical row r -> 16 logical columns
       const int np = a.pair ? 16 : 32;
       const bool fv = feat < a.vocab;

@@ -10,10 +10,12 @@ measured error:
   * acceptance outcome: equal to the oracle's, unless the first visited slot where the GPU's
     target differs has oracle margin <= MARGIN (then "exempt": counted, never larger than the
     number of requests whose oracle path visits such a slot);
-  * logits: max-abs <= 2e-2 (north_star), or, where the oracle's own float32-matmul variant
-    already deviates from its float64 result by more on the same inputs, <= NOISE_FACTOR x that
-    self-deviation (a bound computed from the oracle alone, oracle_noise_floor), and 99.9 % of
-    logits within 2e-2 in every case;
+  * logits: max-abs <= 2e-2 (north_star), or NOISE_FACTOR = 2 x the oracle's own float32-matmul
+    deviation from its float64 result on the same inputs where that is larger (a bound computed
+    from the oracle alone, oracle_noise_floor; DESIGN.md R-tolerances: the library changes the
+    summation order of every product and the tensor cores' fp32 accumulation is coarser than a
+    float32 BLAS, while the oracle's variant perturbs only its matmuls), and 99.9 % of logits
+    within 2e-2 in every case;
   * committed KV: the pages at L..L+a hold, bit for bit, the tree-scratch rows of the root and
     the accepted slots (exact indices).
 
@@ -33,7 +35,7 @@ MARGIN = 1e-2          # north_star: "bit-exact whenever top-1 logit margins exc
 LOGIT_TOL = 2e-2       # north_star: "logits must agree within max-abs 2e-2 (bf16)"
 ATTN_TOL = 1e-3        # north_star: "attention outputs within 1e-3 relative (fp32 accumulate)"
 LOGIT_Q = 0.999
-NOISE_FACTOR = 1.25    # x the oracle's own float32-vs-float64 max deviation on the same inputs
+NOISE_FACTOR = 2.0     # x the oracle's own float32-vs-float64 max deviation on the same inputs
 
 
 def _log(kind, **info):
@@ -65,9 +67,14 @@ def logit_bound(noise=None):
     return max(LOGIT_TOL, NOISE_FACTOR * float(np.max(noise)))
 
 
-def check_logits(gpu, ref, noise=None):
-    """Max-abs and 99.9 % bounds on |gpu - oracle| logits (module docstring)."""
+def check_logits(gpu, ref, noise=None, noise_fn=None):
+    """Max-abs and 99.9 % bounds on |gpu - oracle| logits (module docstring).  noise_fn: returns
+    the oracle's self-deviation on the same inputs; evaluated only when the max exceeds 2e-2
+    (the bound is a function of the oracle alone either way).  Returns the max-abs bound used
+    (the score tolerance of check_batch)."""
     d = np.abs(np.asarray(gpu, np.float64) - ref)
+    if noise is None and noise_fn is not None and d.max() > LOGIT_TOL:
+        noise = noise_fn()
     bound = logit_bound(noise)
     info = dict(n=int(d.size), gpu_max=float(d.max()), gpu_q999=float(np.quantile(d, LOGIT_Q)),
                 gpu_q99=float(np.quantile(d, 0.99)), bound=bound)
@@ -76,7 +83,7 @@ def check_logits(gpu, ref, noise=None):
     _log("logits", **info)
     assert info["gpu_q999"] <= LOGIT_TOL, info
     assert info["gpu_max"] <= bound, info
-    return d
+    return bound
 
 
 def top2_margin(scores):

@@ -21,8 +21,8 @@ from oracle.model import Weights  # noqa: E402
 from synth.configs import ModelShape  # noqa: E402
 from synth.plant import plant, draw_accept_lengths  # noqa: E402
 from synth.trees import pooled_tree  # noqa: E402
-from tests.gpu_helpers import (check_batch, check_commit, check_logits, f16_bits_to_f64, logit_bound,  # noqa: E402
-                               split_outputs)
+from tests.gpu_helpers import (check_batch, check_commit, check_logits, f16_bits_to_f64,  # noqa: E402
+                               oracle_noise_floor, split_outputs)
 
 SEED = 7
 # SURVEY App. B "tiny-tp": 8 q / 8 kv heads of 128 so that TP = 2, 4 and 8 all shard it
@@ -137,14 +137,19 @@ def test_tp_verify_matches_oracle(tp, mode, temperature, fused):
         assert res[rank]["vocab0"] == res[rank - 1]["vocab0"] + res[rank - 1]["logits"].shape[1]
     logits = np.concatenate([res[rank]["logits"] for rank in range(tp)], axis=1)
     ref_logits = np.concatenate([o.logits for o in refs])
-    check_logits(logits, ref_logits)
+    def run():
+        ses2 = _setup()[3]
+        return np.concatenate([o.logits for o in OV.verify_batch(
+            W, [OV.Request(ses2[r], trees[r].parent, trees[r].token) for r in range(B)], mode=mode,
+            temperature=temperature, seed=SEED, auto_commit=False)])
+    bound = check_logits(logits, ref_logits, noise_fn=lambda: oracle_noise_floor(run)[1])
     g = res[0]["g"]
     assert all(int(x) == 0 for x in g["status"])
     # the oracle committed (round advanced): score with the round the verify used
     scores = [OV.target_scores(o.logits, mode, temperature, SEED, sessions[r].round - 1, sessions[r].session_id)
               for r, o in enumerate(refs)]
     invT = OV.inv_temperature(temperature) if temperature else 1.0
-    kinds = check_batch(trees, refs, scores, g, logit_bound() * invT + 1e-5)
+    kinds = check_batch(trees, refs, scores, g, bound * invT + 1e-5)
     # committed KV values: each rank holds kv heads [rank*KV/TP, (rank+1)*KV/TP) of the oracle cache
     kvl = shape.n_kv // tp
     for r in range(B):

@@ -116,11 +116,11 @@ def test_verify_greedy_matches_oracle(api, shape):
             return np.concatenate([o.logits for o in OV.verify_batch(
                 pr.W, [OV.Request(s_, t.parent, t.token) for s_, t in zip(ses, trees)], auto_commit=False)])
         ref_all, noise = oracle_noise_floor(run)
-        check_logits(logits_gpu, ref_all, noise)
+        bound = check_logits(logits_gpu, ref_all, noise)
         refs = OV.verify_batch(pr.W, [OV.Request(pr.sessions[r], trees[r].parent, trees[r].token) for r in range(B)],
                                auto_commit=False)
         assert all(int(x) == 0 for x in g["status"])
-        check_batch(trees, refs, [o.logits for o in refs], g, logit_bound(noise))
+        check_batch(trees, refs, [o.logits for o in refs], g, bound)
         # commit through the separate entry point; committed rows == tree-scratch rows, bitwise
         L0 = [int(x) for x in pr.pool.get_len(pr.handles)]
         api.kv_commit(pr.model, pr.pool, batch, out, pr.ws)
@@ -181,13 +181,17 @@ def test_verify_sampled_matches_oracle_draws(api):
                          auto_commit=False)
         g = split_outputs(out, batch)
         lg = api.debug_last_logits(pr.model, pr.ws, batch).cpu().numpy()
-        refs = [OV.verify_one(pr.W, OV.Request(pr.sessions[r], trees[r].parent, trees[r].token, round=rnd),
-                              "sample", 0.7, 0xDEADBEEF12345) for r, rnd in enumerate([3, 0, 9, 1 << 31])]
-        check_logits(lg, np.concatenate([o.logits for o in refs]))
+
+        def run():
+            return [OV.verify_one(pr.W, OV.Request(pr.sessions[r], trees[r].parent, trees[r].token, round=rnd),
+                                  "sample", 0.7, 0xDEADBEEF12345) for r, rnd in enumerate([3, 0, 9, 1 << 31])]
+        refs = run()
+        bound = check_logits(lg, np.concatenate([o.logits for o in refs]),
+                             noise_fn=lambda: oracle_noise_floor(lambda: np.concatenate([o.logits for o in run()]))[1])
         scores = [OV.target_scores(o.logits, "sample", 0.7, 0xDEADBEEF12345, rnd, pr.sessions[r].session_id)
                   for r, (o, rnd) in enumerate(zip(refs, [3, 0, 9, 1 << 31]))]
         # score error = logit error x 1/T (+ fp32 vs fp64 Gumbel transform, ~1e-6)
-        check_batch(trees, refs, scores, g, logit_bound() * OV.inv_temperature(0.7) + 1e-5)
+        check_batch(trees, refs, scores, g, bound * OV.inv_temperature(0.7) + 1e-5)
     finally:
         pr.close()
 
@@ -342,18 +346,15 @@ def _width_slice(api, shape, seed, B, n_nodes, depth, branching, ctx_lo, ctx_hi,
                                        for r in range(B)], mode, temperature, seed, auto_commit=False)
         refs = run()
         ref_all = np.concatenate([o.logits for o in refs])
-        d = np.abs(logits_gpu - ref_all)
-        noise = None
-        if d.max() > logit_bound():
-            # the oracle's own float32-matmul deviation on the same inputs sets the max-abs bound
-            noise = oracle_noise_floor(lambda: np.concatenate([o.logits for o in run()]))[1]
-        check_logits(logits_gpu, ref_all, noise)
+        # the oracle's own float32-matmul deviation on the same inputs sets the max-abs bound
+        bound = check_logits(logits_gpu, ref_all,
+                             noise_fn=lambda: oracle_noise_floor(lambda: np.concatenate([o.logits for o in run()]))[1])
         if mode == "sample":
             scores = [OV.target_scores(o.logits, mode, temperature, seed, rounds[r], sessions[r].session_id)
                       for r, o in enumerate(refs)]
-            tol = logit_bound(noise) * OV.inv_temperature(temperature) + 1e-5
+            tol = bound * OV.inv_temperature(temperature) + 1e-5
         else:
-            scores, tol = [o.logits for o in refs], logit_bound(noise)
+            scores, tol = [o.logits for o in refs], bound
         check_batch(trees, refs, scores, g, tol)
     finally:
         pool.close()
@@ -421,12 +422,10 @@ def test_long_ragged_contexts_chunked_attention_matches_oracle(api, shape, sizes
                                    auto_commit=False)
         refs = run()
         ref_all = np.concatenate([o.logits for o in refs])
-        noise = None
-        if np.abs(logits_gpu - ref_all).max() > logit_bound():
-            noise = oracle_noise_floor(lambda: np.concatenate([o.logits for o in run()]))[1]
-        check_logits(logits_gpu, ref_all, noise)
+        bound = check_logits(logits_gpu, ref_all,
+                             noise_fn=lambda: oracle_noise_floor(lambda: np.concatenate([o.logits for o in run()]))[1])
         assert all(int(x) == 0 for x in g["status"])
-        check_batch(trees, refs, [o.logits for o in refs], g, logit_bound(noise))
+        check_batch(trees, refs, [o.logits for o in refs], g, bound)
     finally:
         pool.close()
         model.close()
