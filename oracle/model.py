@@ -39,7 +39,7 @@ import math
 import numpy as np
 
 from . import philox
-from .numerics import bf16, f16, rmsnorm, rope, silu, attention, attention_weights
+from .numerics import bf16, f16, rmsnorm, rope, silu, attention, attention_weights, perturb
 
 # Matmul arithmetic of the oracle.  float64 is the reference; tests switch it to float32 (same
 # storage contract) to measure the oracle's own arithmetic-noise floor, against which the
@@ -186,23 +186,23 @@ class Cache:
 def _qkv(W: Weights, l, x, pos):
     s = W.shape
     Lw = W.layer(l)
-    h = bf16(rmsnorm(x, Lw["g_attn"], s.eps))
+    h = bf16(perturb(rmsnorm(x, Lw["g_attn"], s.eps)))
     q = _mm(h, Lw["wq"].T).reshape(-1, s.n_heads, s.head_dim)
     k = _mm(h, Lw["wk"].T).reshape(-1, s.n_kv, s.head_dim)
     v = _mm(h, Lw["wv"].T).reshape(-1, s.n_kv, s.head_dim)
-    q = f16(rope(q, pos, s.rope_theta))
-    k = f16(rope(k, pos, s.rope_theta))
-    return q, k, f16(v)
+    q = f16(perturb(rope(q, pos, s.rope_theta)))
+    k = f16(perturb(rope(k, pos, s.rope_theta)))
+    return q, k, f16(perturb(v))
 
 
 def _post_attn(W: Weights, l, x, o):
     """o [n, H, hd] fp64 attention output -> residual stream after the MLP."""
     s = W.shape
     Lw = W.layer(l)
-    O = bf16(o.reshape(o.shape[0], -1))
+    O = bf16(perturb(o.reshape(o.shape[0], -1)))
     x = x + _mm(O, Lw["wo"].T)             # residual stream is not a GEMM operand: not rounded
-    h2 = bf16(rmsnorm(x, Lw["g_mlp"], s.eps))
-    M = bf16(silu(_mm(h2, Lw["wg"].T)) * _mm(h2, Lw["wu"].T))
+    h2 = bf16(perturb(rmsnorm(x, Lw["g_mlp"], s.eps)))
+    M = bf16(perturb(silu(_mm(h2, Lw["wg"].T)) * _mm(h2, Lw["wu"].T)))
     return x + _mm(M, Lw["wd"].T)
 
 

@@ -45,6 +45,22 @@ def f32(x):
     return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
 
 
+# Noise-floor estimation (test infrastructure, off unless a test sets it): (rng, eps).  Every
+# activation storage point (model.py: h, q, k, v, O, M; attention_weights: P) first scales its
+# input by (1 + eps * U(-1, 1)) — an implementation whose fp32 arithmetic (summation order,
+# approximate exp2 / rsqrt, tensor-core accumulation) lands within eps of the exact pre-rounding
+# values.  Weights, embeddings and synthetic caches are never perturbed.
+PERTURB = None
+
+
+def perturb(x):
+    if PERTURB is None:
+        return x
+    rng, eps = PERTURB
+    x = np.asarray(x, np.float64)
+    return x * (1.0 + eps * rng.uniform(-1.0, 1.0, x.shape))
+
+
 def rmsnorm(x, g, eps):
     """RMSNorm (Llama/Qwen, SURVEY amb. A13): x / sqrt(mean(x^2) + eps) * g, over the last axis."""
     x = np.asarray(x, np.float64)
@@ -97,7 +113,7 @@ def attention_weights(s):
     s = np.asarray(s, np.float64)
     m = np.max(s, axis=-1, keepdims=True)
     e = np.exp(s - m)
-    num = f16(e) if ATTN_P_F16 else e
+    num = f16(perturb(e)) if ATTN_P_F16 else e
     return num / np.sum(e, axis=-1, keepdims=True)
 
 
