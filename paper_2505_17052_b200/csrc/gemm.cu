@@ -39,7 +39,7 @@ __host__ __device__ inline SmemLayout smem_layout(int stages, int BN) {
   L.b_off = L.a_off + stages * kABytes;
   L.xch_off = L.b_off + stages * (uint32_t)BN * 128u;
   L.red_off = L.xch_off + 128 * kXchStride * 4;
-  L.bar_off = L.red_off + 4 * 32 * 12;   // red_v, red_i, red_s2 [128] each
+  L.bar_off = L.red_off + 4 * 32 * 24;   // red_v, red_i [128]; top2: red_s2, red_i2 at +256, red_s3 at +512
   L.total = L.bar_off + (2 * stages + 4) * 8 + 16;
   return L;
 }
@@ -247,38 +247,74 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
       named_bar_sync(1, kEpiThreads);
       const int ngrp = 128 / np, per = 128 / ngrp;
       // tile argmax per row (ties -> lowest id: features scanned in increasing order); a.top2
-      // also keeps the tile's second-best score (k_lm_refine's candidate window, hi-only pass)
+      // also keeps the tile's second (score, id) and third score (k_lm_refine's candidate window,
+      // hi-only pass)
       float* red_s2 = red_v + 256;
+      int* red_i2 = red_i + 256;
+      float* red_s3 = red_v + 512;
       {
         const int jj = et % np, g = et / np;
-        float best = -INFINITY, sec = -INFINITY;
-        int bi = 0x7fffffff;
+        float b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
+        int i1 = 0x7fffffff, i2 = 0x7fffffff;
         for (int l = 0; l < per; ++l) {
           const float sc = xch[(g * per + l) * kXchStride + jj];
-          if (sc > best) { sec = best; best = sc; bi = a.vocab_off + m128 * 128 + g * per + l; }
-          else if (sc > sec) sec = sc;
+          const int id = a.vocab_off + m128 * 128 + g * per + l;
+          if (sc > b1) { b3 = b2; b2 = b1; i2 = i1; b1 = sc; i1 = id; }
+          else if (sc > b2) { b3 = b2; b2 = sc; i2 = id; }
+          else if (sc > b3) b3 = sc;
         }
-        red_v[g * np + jj] = best;
-        red_i[g * np + jj] = bi;
-        red_s2[g * np + jj] = sec;
+        red_v[g * np + jj] = b1;
+        red_i[g * np + jj] = i1;
+        if (a.top2) {
+          red_s2[g * np + jj] = b2;
+          red_i2[g * np + jj] = i2;
+          red_s3[g * np + jj] = b3;
+        }
       }
       named_bar_sync(1, kEpiThreads);
       if (et < np) {
         const int jj = et;
-        float best = red_v[jj], sec = red_s2[jj];
-        int bi = red_i[jj];
+        float b1 = red_v[jj], b2 = -INFINITY, b3 = -INFINITY;
+        int i1 = red_i[jj], i2 = 0x7fffffff;
+        if (a.top2) { b2 = red_s2[jj]; i2 = red_i2[jj]; b3 = red_s3[jj]; }
         for (int g = 1; g < ngrp; ++g) {
-          const float sc = red_v[g * np + jj];
-          if (sc > best) { sec = fmaxf(best, red_s2[g * np + jj]); best = sc; bi = red_i[g * np + jj]; }
-          else sec = fmaxf(sec, fmaxf(sc, red_s2[g * np + jj]));
+          // merge group g's sorted (b1 >= b2 >= b3) list; groups hold increasing ids, so a tie keeps
+          // the earlier (lower) id first
+          const float c1 = red_v[g * np + jj];
+          const int k1 = red_i[g * np + jj];
+          if (!a.top2) {
+            if (c1 > b1) { b1 = c1; i1 = k1; }
+            continue;
+          }
+          const float c2 = red_s2[g * np + jj], c3 = red_s3[g * np + jj];
+          const int k2 = red_i2[g * np + jj];
+          float v[6] = {b1, b2, b3, c1, c2, c3};
+          int id[6] = {i1, i2, 0, k1, k2, 0};
+          // three largest of the two lists, stable (own list first on ties)
+          float o[3];
+          int oi[3];
+          int p = 0, q = 3;
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const bool take_own = p < 3 && (q >= 6 || v[p] >= v[q]);
+            o[t] = take_own ? v[p] : v[q];
+            oi[t] = take_own ? id[p] : id[q];
+            if (take_own) ++p; else ++q;
+          }
+          b1 = o[0]; i1 = oi[0]; b2 = o[1]; i2 = oi[1]; b3 = o[2];
         }
         const int j = a.pair ? 2 * jj : jj;
         const int row = row_base + j;
         if (j < ncol && row < a.R) {
           const int lr = a.pair ? row >> 1 : row;
-          a.part_val[(size_t)lr * a.ntm128 + m128] = best;
-          a.part_idx[(size_t)lr * a.ntm128 + m128] = bi;
-          if (a.top2) a.part_val2[(size_t)lr * a.ntm128 + m128] = sec;
+          const size_t o = (size_t)lr * a.ntm128 + m128;
+          a.part_val[o] = b1;
+          a.part_idx[o] = i1;
+          if (a.top2) {
+            a.part_val2[o] = b2;
+            a.part_idx2[o] = i2;
+            a.part_val3[o] = b3;
+          }
         }
       }
       named_bar_sync(1, kEpiThreads);

@@ -332,25 +332,35 @@ __global__ void k_lm_reduce(const float* __restrict__ pv, const int* __restrict_
 }
 
 // ------------------------------------------------------------- K9c hi-only LM head refinement
-// One warp per row (RefineArgs in internal.h).  Lanes hold 8-element slices of the row; the window
-// uses the row's own ||hi||_2, ||lo||_2 (read once here, so tensor-parallel ranks need no extra
-// collective) and the shard's max_v ||W_v||_2.
-__global__ void k_lm_refine(const __grid_constant__ RefineArgs a) {
+// One warp per row (RefineArgs in internal.h).  The window uses the row's own ||hi||_2, ||lo||_2
+// (read here, so tensor-parallel ranks need no extra collective) and the shard's max_v ||W_v||_2.
+// Candidates are gathered first (ballot over the tiles), then rescored kRefineBatch at a time so
+// that the loads of several LM-head rows are in flight together.
+constexpr int kRefineBatch = 4;
+constexpr int kRefineList = 64;
+
+__global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ RefineArgs a) {
   pdl_begin();
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  __shared__ int s_list[4][kRefineList];
+  const int wib = threadIdx.x >> 5;
+  const int row = blockIdx.x * (blockDim.x >> 5) + wib;
   const int lane = threadIdx.x & 31;
   if (row >= a.R) return;
-  const float* pv = a.part_val + (size_t)row * a.ntiles;
-  const float* pv2 = a.part_val2 + (size_t)row * a.ntiles;
-  const int* pi = a.part_idx + (size_t)row * a.ntiles;
+  int* list = s_list[wib];
+  const size_t base = (size_t)row * a.ntiles;
+  const float* pv = a.part_val + base;
+  const float* pv2 = a.part_val2 + base;
+  const float* pv3 = a.part_val3 + base;
   const uint4* hi = reinterpret_cast<const uint4*>(a.hf + (size_t)(2 * row) * a.d);
   const uint4* lo = reinterpret_cast<const uint4*>(a.hf + (size_t)(2 * row + 1) * a.d);
   const int nv = a.d / 8;
   float M = -INFINITY;
-  for (int t = lane; t < a.ntiles; t += 32) M = fmaxf(M, pv[t]);
+#pragma unroll 8
+  for (int t = lane; t < a.ntiles; t += 32) M = fmaxf(M, __ldg(pv + t));
   float sh = 0.f, sl = 0.f;
+#pragma unroll 4
   for (int e = lane; e < nv; e += 32) {
-    const uint4 h = hi[e], l = lo[e];
+    const uint4 h = __ldg(hi + e), l = __ldg(lo + e);
     const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -377,48 +387,76 @@ __global__ void k_lm_refine(const __grid_constant__ RefineArgs a) {
   const uint32_t k0 = a.seed_lo ^ a.req_round[req], slot = (uint32_t)a.row_slot[row];
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  // exact score of local vocab id v (warp-collective; every lane returns the same value)
-  auto rescore = [&](int v) -> float {
-    const uint4* wr = reinterpret_cast<const uint4*>(a.w + (size_t)v * a.d);
-    float acc = 0.f;
-    for (int e = lane; e < nv; e += 32) {
-      const uint4 h = hi[e], l = lo[e], w = __ldg(wr + e);
-      const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w}, ww[4] = {w.x, w.y, w.z, w.w};
+  int n = 0;   // candidates in the list (warp-uniform)
+  // rescore list[0..n): exact (hi + lo) . W_v (+ Gumbel), kRefineBatch rows of W at a time
+  auto flush = [&]() {
+    for (int c0 = 0; c0 < n; c0 += kRefineBatch) {
+      const uint4* wr[kRefineBatch];
+      float acc[kRefineBatch];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        // hi + lo is exact in fp32 (bf16 + bf16 below half an ulp of hi)
-        const float y0 = __uint_as_float(hw[k] << 16) + __uint_as_float(lw[k] << 16);
-        const float y1 = __uint_as_float(hw[k] & 0xFFFF0000u) + __uint_as_float(lw[k] & 0xFFFF0000u);
-        acc = fmaf(y0, __uint_as_float(ww[k] << 16), acc);
-        acc = fmaf(y1, __uint_as_float(ww[k] & 0xFFFF0000u), acc);
+      for (int b = 0; b < kRefineBatch; ++b) {
+        wr[b] = reinterpret_cast<const uint4*>(a.w + (size_t)list[min(c0 + b, n - 1)] * a.d);
+        acc[b] = 0.f;
+      }
+#pragma unroll 2
+      for (int e = lane; e < nv; e += 32) {
+        const uint4 h = __ldg(hi + e), l = __ldg(lo + e);
+        uint4 w[kRefineBatch];
+#pragma unroll
+        for (int b = 0; b < kRefineBatch; ++b) w[b] = __ldg(wr[b] + e);
+        const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          // hi + lo is exact in fp32 (bf16 + bf16 below half an ulp of hi)
+          const float y0 = __uint_as_float(hw[k] << 16) + __uint_as_float(lw[k] << 16);
+          const float y1 = __uint_as_float(hw[k] & 0xFFFF0000u) + __uint_as_float(lw[k] & 0xFFFF0000u);
+#pragma unroll
+          for (int b = 0; b < kRefineBatch; ++b) {
+            const uint32_t ww = k == 0 ? w[b].x : (k == 1 ? w[b].y : (k == 2 ? w[b].z : w[b].w));
+            acc[b] = fmaf(y0, __uint_as_float(ww << 16), acc[b]);
+            acc[b] = fmaf(y1, __uint_as_float(ww & 0xFFFF0000u), acc[b]);
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < kRefineBatch; ++b) {
+        float v = acc[b];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (c0 + b >= n) continue;
+        const int vg = a.vocab_off + list[c0 + b];
+        if (a.sample) {
+          const U4 r = philox4x32_10(U4{(uint32_t)vg >> 2, slot, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0, a.seed_hi);
+          const float u = (float)((u4_word(r, vg & 3) >> 8) | 1u) * 5.9604644775390625e-08f;
+          v = v * a.inv_t + (-logf(-logf(u)));
+        }
+        if (v > best || (v == best && vg < bi)) { best = v; bi = vg; }
       }
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (!a.sample) return acc;
-    const int vg = a.vocab_off + v;
-    const U4 r = philox4x32_10(U4{(uint32_t)vg >> 2, slot, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0, a.seed_hi);
-    const float u = (float)((u4_word(r, vg & 3) >> 8) | 1u) * 5.9604644775390625e-08f;
-    return acc * a.inv_t + (-logf(-logf(u)));
+    __syncwarp();
+    n = 0;
   };
-  auto consider = [&](int v) {
-    const float sc = rescore(v);
-    const int vg = a.vocab_off + v;
-    if (sc > best || (sc == best && vg < bi)) { best = sc; bi = vg; }
+  auto push = [&](int v) {   // warp-uniform call
+    if (n == kRefineList) flush();
+    if (lane == 0) list[n] = v;
+    __syncwarp();
+    ++n;
   };
   for (int t0 = 0; t0 < a.ntiles; t0 += 32) {
     const int t = t0 + lane;
-    unsigned bal = __ballot_sync(0xffffffffu, t < a.ntiles && pv[t] >= thr);
+    unsigned bal = __ballot_sync(0xffffffffu, t < a.ntiles && __ldg(pv + t) >= thr);
     while (bal) {
       const int tt = t0 + __ffs(bal) - 1;
       bal &= bal - 1;
-      if (pv2[tt] >= thr) {   // a second id of this tile may win: rescore the whole tile
+      if (__ldg(pv3 + tt) >= thr) {   // a third id of this tile may win: every id of the tile
         const int v1 = min(a.vocab, (tt + 1) * 128);
-        for (int v = tt * 128; v < v1; ++v) consider(v);
+        for (int v = tt * 128; v < v1; ++v) push(v);
       } else {
-        consider(pi[tt] - a.vocab_off);
+        push(__ldg(a.part_idx + base + tt) - a.vocab_off);
+        if (__ldg(pv2 + tt) >= thr) push(__ldg(a.part_idx2 + base + tt) - a.vocab_off);
       }
     }
   }
+  flush();
   if (lane == 0) {
     a.y[row] = bi;
     a.score[row] = best;
