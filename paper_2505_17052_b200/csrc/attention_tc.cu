@@ -176,6 +176,7 @@ struct TcArgs {
   int slots_per_mt; // floor(128 / G)
   int prefetch;     // L2 prefetch distance in sub-tiles (0: off)
   unsigned long long* trace;   // debug (env SPECEDGE_ATTN_TRACE): clock64 stamps of CTA 0, else null
+  int exp_flags;               // experiment (SPECEDGE_ATTN_EXP): bit 0 = no MMAs for unit 1 in pair passes
 };
 
 #define TRACE(i)                                                                                  \
@@ -494,12 +495,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t kaddr = smem_u32(sK + (gi % NST) * PG_BYTES);
           const uint32_t b = (kc + k) & 1;
           const uint32_t s_tm = tmem + u * 256 + b * 64;
+          if (!((ta.exp_flags & 1) && pr && u == 1)) {
 #pragma unroll
           for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               tc_mma_f16(s_tm, umma_desc_sw128(qaddr + kb * 16384 + kk * 32),
                          umma_desc_sw128(kaddr + kb * 8192 + kk * 32), id_qk, (kb | kk) != 0);
+          }
           tc_commit(&s_full[u * 2 + b]);
           if (k == nk - 1) tc_commit(q_empty);   // last QK of the pass: Q may be reloaded
         };
@@ -515,10 +518,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t vaddr = smem_u32(sV + (gi % NST) * PG_BYTES);
           const uint32_t p_tm = tmem + u * 256 + b * 64;
           const uint32_t o_tm = tmem + u * 256 + 128;
+          if (!((ta.exp_flags & 1) && pr && u == 1)) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {   // 16 keys (8 packed fp16 columns) per k-step
             const uint64_t bd = umma_desc_mn_sw128(vaddr + kk * 2048, 64 * 128);
             tc_mma_ts(o_tm, p_tm + kk * 8, bd, id_pv, (k | kk) != 0);
+          }
           }
           tc_commit(&pv_done[u * 2 + b]);
           // kv_empty takes 2 arrivals per use: one per unit in a pair pass, both from the only
@@ -976,7 +981,8 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
   static const int pf = getenv("SPECEDGE_ATTN_PREFETCH") ? atoi(getenv("SPECEDGE_ATTN_PREFETCH")) : kPrefetchDefault;
   static unsigned long long* trace = nullptr;
   if (getenv("SPECEDGE_ATTN_TRACE") && !trace) cudaMalloc(&trace, 1024 * 8);
-  TcArgs ta{a, O, O_f32, spm, pf, trace};
+  static const int exp_flags = getenv("SPECEDGE_ATTN_EXP") ? atoi(getenv("SPECEDGE_ATTN_EXP")) : 0;
+  TcArgs ta{a, O, O_f32, spm, pf, trace, exp_flags};
   if (trace) cudaMemsetAsync(trace, 0, 1024 * 8, st);
   constexpr int NST = ring_stages(HD, NQ);
   const size_t smem = (size_t)NQ * 128 * HD * 2 + (size_t)NST * 2 * 64 * HD * 2 + 8 * (18 + 2 * NST) + 512 * 4 + 32;

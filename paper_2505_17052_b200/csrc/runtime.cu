@@ -307,7 +307,8 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     aa.nch_tab = (int*)P(w.attn_nch);
     // in-kernel merge when a (request, kv head) has at most one 128-row M-tile (cfg5: 85 rows);
     // bigger groups (cfg4: 520 rows) would stall the merging CTA's pipeline -> combine kernel
-    if ((in->max_nodes + 1) * G <= 128) {
+    static const int merge_rows = getenv("SPECEDGE_ATTN_MERGE_ROWS") ? atoi(getenv("SPECEDGE_ATTN_MERGE_ROWS")) : 128;
+    if ((in->max_nodes + 1) * G <= merge_rows) {
       aa.merge_cnt = (int*)P(w.attn_cnt);
       CK(cudaMemsetAsync(aa.merge_cnt, 0, sizeof(int) * (size_t)B * KV, st));   // self-resetting after
     }
