@@ -569,6 +569,130 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t win = rf == 1 ? ~0ull : (((1ull << (64 / rf)) - 1ull) << (rq * (64 / rf)));
       const int nk = nsub_u(p, u);
       float m_used = -INFINITY, l = 0.f;
+      // 64-bit visibility mask of sub-tile k's keys for my row
+      auto key_mask = [&](int k) -> uint64_t {
+        if (!valid_row) return 0ull;
+        const int sj = sub_of(p, j_of(p, u, k));
+        uint64_t mk;
+        if (sj < npg) {
+          const int kvalid = min(64, L - (p_begin + sj) * 64);
+          mk = kvalid >= 64 ? ~0ull : ((1ull << kvalid) - 1ull);
+        } else {
+          // key 0 = root, key k >= 1 = node k-1: visible iff root or ancestor-or-self of my node
+          const int th = th0 + sj - npg;
+          const uint64_t lo = slot > 0 ? ((anc << 1) | 1ull) : 1ull;
+          const uint64_t hi = slot > 0 ? (anc >> 63) : 0ull;
+          const int n = S - 64 * th;   // tree keys in this half
+          mk = (th ? hi : lo) & (n >= 64 ? ~0ull : ((1ull << n) - 1ull));
+        }
+        return mk & win;
+      };
+      // O *= alpha for the rows whose running max moved (warp-collective; PV(k-1) writes O and may
+      // still be in flight -> wait for it first)
+      auto rescale_o = [&](uint32_t kg, bool rescale, float alpha) {
+        if (!__any_sync(0xffffffffu, rescale)) return;
+        const uint32_t pb = (kg - 1) & 1;
+        mbar_wait(&pv_done[u * 2 + pb], ((kg - 1) >> 1) & 1);
+        tc_fence_after();
+        // tcgen05.ld/st are warp-collective (.sync.aligned): the whole warp runs the loop, rows
+        // without a rescale multiply by 1 (a per-lane branch here deadlocked the warp)
+        const float f = rescale ? alpha : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld_32x32b_x32(o_own + c * 32, ov);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * f);
+          tmem_st_32x32b_x32(o_own + c * 32, ov);
+        }
+      };
+      if (rf == 1 && !(ta.exp_flags & 2)) {
+        // ---- unreplicated tile, software-pipelined: S(k+1) is loaded from TMEM while P(k) is
+        // stored, and once a running max exists the exponentials start right away with it, the
+        // sub-tile max being tracked alongside (only a row whose max grew by more than 8 redoes
+        // its exponentials) — the same m_used sequence, hence the same bits, as the plain loop
+        uint32_t sv[64];
+        auto issue_ld = [&](int k, uint32_t (&dst)[64]) {
+          const uint32_t kg = kc + k, b = kg & 1;
+          mbar_wait(&s_full[u * 2 + b], (kg >> 1) & 1);
+          tc_fence_after();
+          tmem_ld_32x32b_x32(s_base + b * 64, *reinterpret_cast<uint32_t(*)[32]>(dst));
+          tmem_ld_32x32b_x32(s_base + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dst + 32));
+        };
+        auto step = [&](int k) {
+          const uint32_t kg = kc + k, b = kg & 1;
+          const uint32_t s_tm = s_base + b * 64;
+          tmem_ld_wait();
+          const uint64_t mk = key_mask(k);
+          const bool any = __any_sync(0xffffffffu, mk != 0ull);
+          const bool full = __all_sync(0xffffffffu, mk == ~0ull);
+          float ls = 0.f;
+          bool rescale = false;
+          float alpha = 1.f;
+          if (any) {
+            const uint32_t mlo = (uint32_t)mk, mhi = (uint32_t)(mk >> 32);
+            // P = 2^(s*scale - mb) as packed fp16 pairs (masked keys: -inf -> 0); returns the
+            // row sum, mx_out = the masked sub-tile max (log2 domain)
+            auto exps = [&](float mb, float& mx_out) {
+              float m0 = -INFINITY, m1 = -INFINITY, ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+              for (int e = 0; e < 64; e += 2) {
+                const uint32_t wd = e < 32 ? mlo : mhi;
+                const float s0 = (full || ((wd >> (e & 31)) & 1u)) ? __uint_as_float(sv[e]) : -INFINITY;
+                const float s1 = (full || ((wd >> ((e + 1) & 31)) & 1u)) ? __uint_as_float(sv[e + 1]) : -INFINITY;
+                m0 = fmaxf(m0, s0);
+                m1 = fmaxf(m1, s1);
+                const float p0 = ex2f(fmaf(s0, sl2, -mb));
+                const float p1 = ex2f(fmaf(s1, sl2, -mb));
+                ls0 += p0;
+                ls1 += p1;
+                sv[e >> 1] = pack2(p0, p1);   // in place: sv[e], sv[e + 1] are consumed
+              }
+              mx_out = fmaxf(m0, m1) * sl2;
+              return ls0 + ls1;
+            };
+            float mx;
+            const bool first = m_used == -INFINITY;
+            ls = exps(first ? 0.f : m_used, mx);
+            // a row whose max grew by more than 8 (or its first visible keys) takes the new max:
+            // reload S(k) from TMEM (still there) and redo the exponentials with it
+            const bool redo = (mx > m_used + 8.f) || (first && mx > -INFINITY);
+            if (__any_sync(0xffffffffu, redo)) {
+              if (redo) {
+                alpha = first ? 0.f : ex2f(m_used - mx);
+                rescale = k > 0 && !first;
+                l *= alpha;
+                m_used = mx;
+              }
+              tmem_ld_32x32b_x32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
+              tmem_ld_32x32b_x32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+              tmem_ld_wait();
+              float dummy;
+              ls = exps(m_used == -INFINITY ? 0.f : m_used, dummy);
+            }
+            l += ls;
+          }
+          if (any) {   // P packed into sv[0, 32)
+            tmem_st_32x32b_x16(s_tm, *reinterpret_cast<uint32_t(*)[16]>(sv));
+            tmem_st_32x32b_x16(s_tm + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+          } else {
+            uint32_t z[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) z[e] = 0u;
+            tmem_st_32x32b_x16(s_tm, z);
+            tmem_st_32x32b_x16(s_tm + 16, z);
+          }
+          tmem_st_wait();
+          // S(k+1) loads while this sub-tile's P is released (and O rescaled) below
+          if (k + 1 < nk) issue_ld(k + 1, sv);
+          if (any) rescale_o(kg, rescale, alpha);   // before PV(k) may add into O
+          tc_fence_before();
+          mbar_arrive(&p_full[u * 2 + b]);
+        };
+        if (nk > 0) issue_ld(0, sv);
+        for (int k = 0; k < nk; ++k) step(k);
+      } else
       for (int k = 0; k < nk; ++k) {
         const uint32_t kg = kc + k;
         const uint32_t b = kg & 1;
