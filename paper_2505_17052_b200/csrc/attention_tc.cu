@@ -636,18 +636,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             // row sum, mx_out = the masked sub-tile max (log2 domain)
             auto exps = [&](float mb, float& mx_out) {
               float m0 = -INFINITY, m1 = -INFINITY, ls0 = 0.f, ls1 = 0.f;
+              if (full) {
 #pragma unroll
-              for (int e = 0; e < 64; e += 2) {
-                const uint32_t wd = e < 32 ? mlo : mhi;
-                const float s0 = (full || ((wd >> (e & 31)) & 1u)) ? __uint_as_float(sv[e]) : -INFINITY;
-                const float s1 = (full || ((wd >> ((e + 1) & 31)) & 1u)) ? __uint_as_float(sv[e + 1]) : -INFINITY;
-                m0 = fmaxf(m0, s0);
-                m1 = fmaxf(m1, s1);
-                const float p0 = ex2f(fmaf(s0, sl2, -mb));
-                const float p1 = ex2f(fmaf(s1, sl2, -mb));
-                ls0 += p0;
-                ls1 += p1;
-                sv[e >> 1] = pack2(p0, p1);   // in place: sv[e], sv[e + 1] are consumed
+                for (int e = 0; e < 64; e += 2) {
+                  const float s0 = __uint_as_float(sv[e]), s1 = __uint_as_float(sv[e + 1]);
+                  m0 = fmaxf(m0, s0);
+                  m1 = fmaxf(m1, s1);
+                  const float p0 = ex2f(fmaf(s0, sl2, -mb));
+                  const float p1 = ex2f(fmaf(s1, sl2, -mb));
+                  ls0 += p0;
+                  ls1 += p1;
+                  sv[e >> 1] = pack2(p0, p1);   // in place: sv[e], sv[e + 1] are consumed
+                }
+              } else {
+#pragma unroll
+                for (int e = 0; e < 64; e += 2) {
+                  const uint32_t wd = e < 32 ? mlo : mhi;
+                  const float s0 = ((wd >> (e & 31)) & 1u) ? __uint_as_float(sv[e]) : -INFINITY;
+                  const float s1 = ((wd >> ((e + 1) & 31)) & 1u) ? __uint_as_float(sv[e + 1]) : -INFINITY;
+                  m0 = fmaxf(m0, s0);
+                  m1 = fmaxf(m1, s1);
+                  const float p0 = ex2f(fmaf(s0, sl2, -mb));
+                  const float p1 = ex2f(fmaf(s1, sl2, -mb));
+                  ls0 += p0;
+                  ls1 += p1;
+                  sv[e >> 1] = pack2(p0, p1);
+                }
               }
               mx_out = fmaxf(m0, m1) * sl2;
               return ls0 + ls1;
@@ -683,12 +697,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st_32x32b_x16(s_tm, z);
             tmem_st_32x32b_x16(s_tm + 16, z);
           }
-          tmem_st_wait();
-          // S(k+1) loads while this sub-tile's P is released (and O rescaled) below
-          if (k + 1 < nk) issue_ld(k + 1, sv);
           if (any) rescale_o(kg, rescale, alpha);   // before PV(k) may add into O
+          tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&p_full[u * 2 + b]);
+          // S(k+1): its load is in flight while the loop comes around
+          if (k + 1 < nk) issue_ld(k + 1, sv);
         };
         if (nk > 0) issue_ld(0, sv);
         for (int k = 0; k < nk; ++k) step(k);

@@ -924,7 +924,7 @@ void gemm_force_single(bool on) { g_force_single = on; }
 cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArgs a,
                         cudaStream_t st, int* launches) {
   const int g_num_sms = device_sms();
-  a.BN = gemm_pick_bn(a.R);
+  a.BN = a.bn_override > 0 ? a.bn_override : gemm_pick_bn(a.R);
   a.n_tiles_n = (a.R + a.BN - 1) / a.BN;
   a.n_tiles_m = (a.M + 127) / 128;
   a.ntm128 = a.n_tiles_m;

@@ -87,6 +87,7 @@ struct RmsSrc {                  // NEXT-F4: per-partial base pointers for k_rms
 
 struct GemmArgs {
   int M, R, K;            // weight rows (features), activation rows, reduction length
+  int bn_override;        // activation-row tile (multiple of 16, <= 256); 0: gemm_pick_bn(R)
   int x_stride;           // activation row stride in elements (0: K); the hi-only LM head reads
                           // the even (hi) rows of the interleaved hi/lo final hidden
   int BN, n_tiles_n, n_tiles_m, num_kb, stages, tmem_cols;

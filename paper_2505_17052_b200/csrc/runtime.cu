@@ -501,6 +501,8 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gu.K = c.d;
     gu.out_bf16 = Mb;
     gu.ld_out = c.ffn;
+    static const int bn_gu = getenv("SPECEDGE_BN_GATEUP") ? atoi(getenv("SPECEDGE_BN_GATEUP")) : 0;
+    gu.bn_override = bn_gu;
     { KTimer _t(K_GU, st); CK(gemm_launch(EPI_SWIGLU, Lw.tm_gu, Hn_in, gu, st, &launches)); }
     pendingY = fused ? f32_gemm_fused(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn) : f32_gemm(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn, true);
     if (pendingY < 0) return SPECEDGE_E_CUDA;
