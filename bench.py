@@ -13,8 +13,8 @@ SURVEY §8(e) replicas).
 NCCL all-reduce after O and down, all-gather of the vocab-shard argmax), 32 requests x
 64-node trees for the whole box, ctx U[3072, 5120]; `value` is the box's tokens/s ("strong").
 
---impl reference: the CPU oracle (oracle/, numpy float64) on the box's host cores, on a bounded
-sample of the same workload, extrapolated to the metric's unit (this tier's reference arm).
+--impl reference: the plain C++ oracle (oracle/cpp, float64, OpenMP) on the box's host cores, one
+whole request of the same workload per step (this tier's reference arm; measured, not extrapolated).
 """
 from __future__ import annotations
 
@@ -193,6 +193,33 @@ def setup_gpu(wl, rank, device, tp=None, model=None, pool=None, mb=0):
     assert all(s == 0 for s in status), status
     return dict(api=api, model=model, pool=pool, ws=ws, batch=batch, handles=handles, ctx=ctx, mode=mode,
                 trees=trees, planted=accept, accepted=got, R=R)
+
+
+def workload_config(wl, world=1, tp=False):
+    """The `config` object of both arms (rank 0's request sets; host-side, from the seeds)."""
+    from synth.plant import draw_accept_lengths
+    n_mb = wl.microbatches
+    rows = tokens = 0
+    for mb in range(n_mb):
+        trees = build_trees(wl, 64 * mb, wl.shape.vocab)
+        acc = draw_accept_lengths(np.random.default_rng([wl.ctx_seed + 11, 64 * mb]), trees, wl.accept_mu,
+                                  wl.accept_sigma)
+        rows += sum(t.n + 1 for t in trees)
+        tokens += sum(a + 1 for a in acc)
+    sh = wl.shape
+    split = world if tp else 1
+    weight_gb = 2.0 * sh.n_layers * ((sh.n_heads + 2 * sh.n_kv) * sh.head_dim * sh.d + sh.d * sh.n_heads * sh.head_dim +
+                                     3 * sh.ffn * sh.d) / split / 1e9 + 2.0 * sh.vocab * sh.d / split / 1e9
+    return {"workload": f"{wl.name}: {wl.shape.name}-shaped random-init, "
+                        f"{(str(n_mb) + ' microbatches x ') if n_mb > 1 else ''}{wl.n_requests} requests x "
+                        f"{wl.n_nodes}-node trees (D={wl.depth}, b={wl.branching}), ctx U[{wl.ctx_lo},"
+                        f"{wl.ctx_hi}], {wl.mode}",
+            ("requests_per_box" if tp else "requests_per_gpu"): wl.n_requests * n_mb,
+            "microbatches": n_mb, "rows_per_step": rows,
+            ("tokens_per_step_per_box" if tp else "tokens_per_step_per_gpu"): tokens,
+            "planted_tokens_per_verify": round(tokens / (wl.n_requests * n_mb), 3),
+            "l2": f"inputs larger than L2 ({weight_gb:.1f} GB of weights per GPU streamed every step)",
+            "parallelism": f"tp{world}" if tp else f"replicas x{world}"}
 
 
 def algorithmic_work(wl, st, tp=1):
@@ -396,23 +423,14 @@ def run_gpu(args, world, rank, local):
             dist.barrier()
             dist.destroy_process_group()
         return
-    sh = wl.shape
-    weight_gb = 2.0 * sh.n_layers * ((sh.n_heads + 2 * sh.n_kv) * sh.head_dim * sh.d + sh.d * sh.n_heads * sh.head_dim +
-                                     3 * sh.ffn * sh.d) / (world if tp else 1) / 1e9 + 2.0 * sh.vocab * sh.d / (world if tp else 1) / 1e9
+    cfgd = workload_config(wl, world, tp)
+    assert cfgd["rows_per_step"] == sum(m["R"] for m in mbs)
+    assert cfgd["tokens_per_step_per_box" if tp else "tokens_per_step_per_gpu"] == tokens_per_step
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{wl.name}: {wl.shape.name}-shaped random-init, "
-                               f"{(str(len(mbs)) + ' microbatches x ') if len(mbs) > 1 else ''}{wl.n_requests} requests x "
-                               f"{wl.n_nodes}-node trees (D={wl.depth}, b={wl.branching}), ctx U[{wl.ctx_lo},"
-                               f"{wl.ctx_hi}], {wl.mode}",
-                   ("requests_per_box" if tp else "requests_per_gpu"): wl.n_requests * len(mbs),
-                   "microbatches": len(mbs), "rows_per_step": sum(m["R"] for m in mbs),
-                   ("tokens_per_step_per_box" if tp else "tokens_per_step_per_gpu"): tokens_per_step,
-                   "planted_tokens_per_verify": round(tokens_per_step / (wl.n_requests * len(mbs)), 3),
-                   "l2": f"inputs larger than L2 ({weight_gb:.1f} GB of weights per GPU streamed every step)",
-                   "parallelism": f"tp{world}" if tp else f"replicas x{world}"},
+        "config": cfgd,
         "p50_ms": round(statistics.median(step_ms), 4), "p90_ms": round(float(np.quantile(step_ms, 0.9)), 4),
         "rows_per_s": round(replicas * sum(m["R"] for m in mbs) * args.steps / (total_ms / 1e3), 1),
         "roofline": roof,
@@ -569,71 +587,71 @@ def serving_leg(wl, model, device, steps=60, sessions_per_slot=2, seed=77):
 
 # ------------------------------------------------------------------------------- CPU oracle arm
 class OracleSample:
-    """The oracle, as it stands, on a bounded sample of the same workload: request 0's draft tree
-    (33 rows) through layer 0 of the model against its synthetic context, plus the LM head over a
-    4096-row vocab slice.  One sample ~ 1 s; extrapolated linearly to all layers, the full vocab
-    and all rows of the step.  Weight generation is setup (not timed)."""
-
-    VSLICE = 4096
+    """The plain C++ oracle (oracle/cpp/verify_ref.cpp, north_star's "plain, slow CPU C++
+    implementation"; pinned against the numpy oracle by tests/test_oracle_cpp.py), as it stands, on a
+    bounded sample of the same workload: whole requests of the step — request r's draft tree (its
+    N+1 rows) through every layer and the full-vocabulary LM head over its synthetic context, then
+    the target choice and the walk — one request per sample.  Verified tokens are counted with the
+    workload's planted acceptance profile (the GPU arm's accounting); the oracle's work per request
+    does not depend on acceptance.  Weight generation is setup (not timed)."""
 
     def __init__(self, wl, rank=0):
-        from oracle.model import Weights, Cache, gen_kv_fill
+        from oracle import cpp_ref
         from synth.plant import draw_accept_lengths
         self.wl = wl
-        s = wl.shape
         self.ctx = contexts(wl, rank)
-        self.trees = build_trees(wl, rank, s.vocab)
-        one = type(s)(**{**s.as_dict(), "n_layers": 1})
-        self.W = Weights(one, wl.weight_seed)
-        self.W.layer(0)
-        self.lm = self.W.lm_head_block(0, self.VSLICE)
-        L = self.ctx[0] - 1
-        self.cache = Cache(one)
-        self.cache.k[0] = gen_kv_fill(wl.ctx_seed, rank * 1000, 0, 0, L, s.n_kv, s.head_dim)
-        self.cache.v[0] = gen_kv_fill(wl.ctx_seed, rank * 1000, 0, 1, L, s.n_kv, s.head_dim)
+        self.trees = build_trees(wl, rank, wl.shape.vocab)
         acc = draw_accept_lengths(np.random.default_rng([wl.ctx_seed + 11, rank]), self.trees, wl.accept_mu,
                                   wl.accept_sigma)
-        self.tokens_per_step = sum(a + 1 for a in acc)
-        self.rows = sum(t.n + 1 for t in self.trees)
-        try:
-            from threadpoolctl import threadpool_info
-            self.cores = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
-        except Exception:
-            self.cores = os.cpu_count()
-
-    def step_seconds(self):
-        from oracle.model import tree_forward
-        s = self.wl.shape
+        self.tokens = [a + 1 for a in acc]
+        rng = np.random.default_rng([wl.ctx_seed + 7, rank])
+        self.roots = [int(t) for t in rng.integers(0, wl.shape.vocab, wl.n_requests)]
+        self.rank = rank
         t0 = time.perf_counter()
-        hf, _, _ = tree_forward(self.W, self.cache, 1, self.trees[0].parent, self.trees[0].token)
-        t_layer = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        _ = hf @ self.lm.T
-        t_lm = (time.perf_counter() - t0) * s.vocab / self.VSLICE
-        return (t_layer * s.n_layers + t_lm) * self.rows / (self.trees[0].n + 1)
+        self.model = cpp_ref.Model(wl.shape, wl.weight_seed)
+        self.setup_s = time.perf_counter() - t0
+        self.cores = cpp_ref.threads()
+        self.next = 0
 
-    def describe(self):
+    def run_one(self):
+        """Verify the next request of the step; returns (seconds, verified tokens)."""
+        r = self.next % self.wl.n_requests
+        self.next += 1
+        t = self.trees[r]
+        t0 = time.perf_counter()
+        self.model.verify(self.ctx[r] - 1, self.roots[r], t.parent, t.token, fill=(self.wl.ctx_seed, self.rank * 1000 + r),
+                          mode=self.wl.mode, temperature=self.wl.temperature, seed=self.wl.weight_seed,
+                          session=(self.rank << 32) | (1000 + r))
+        return time.perf_counter() - t0, self.tokens[r]
+
+    def describe(self, n):
         s = self.wl.shape
-        return (f"oracle (numpy fp64) on request 0 ({self.trees[0].n + 1} rows) of {self.wl.name}: layer 0 of "
-                f"{s.n_layers} + LM head over {self.VSLICE}/{s.vocab} vocab rows, extrapolated to {s.n_layers} "
-                f"layers, full vocab, {self.rows} rows; {self.tokens_per_step} verified tokens/step (planted)")
+        return (f"plain C++ oracle (float64, OpenMP, {self.cores} threads) on {n} whole request(s) of {self.wl.name}: "
+                f"{self.wl.n_nodes}+1 rows each through all {s.n_layers} layers and the {s.vocab}-row LM head over "
+                f"contexts of ~{int(np.mean(self.ctx))} tokens, + target choice and walk; tokens counted with the "
+                f"planted profile (mean {np.mean(self.tokens):.2f}/verify); weight generation {self.setup_s:.1f} s untimed")
+
+    def close(self):
+        self.model.close()
 
 
 def cpu_baseline(wl, budget_s=20.0, rank=0):
     smp = OracleSample(wl, rank)
-    secs = []
+    secs, toks = [], []
     t0 = time.perf_counter()
-    while time.perf_counter() - t0 < budget_s or len(secs) < 3:
-        secs.append(smp.step_seconds())
-        if len(secs) >= 50:
-            break
-    t_step = float(np.median(secs))
-    return {"value": round(smp.tokens_per_step / t_step, 4), "unit": UNIT, "cores": smp.cores, "kind": "oracle",
-            "sample": smp.describe() + f"; median of {len(secs)} samples",
-            "seconds_per_step_extrapolated": round(t_step, 2)}
+    while (time.perf_counter() - t0 < budget_s and len(secs) < wl.n_requests) or not secs:
+        s_, k_ = smp.run_one()
+        secs.append(s_)
+        toks.append(k_)
+    smp.close()
+    return {"value": round(sum(toks) / sum(secs), 4), "unit": UNIT, "cores": smp.cores, "kind": "oracle",
+            "sample": smp.describe(len(secs)), "seconds_per_request": round(float(np.mean(secs)), 3),
+            "measured_s": round(sum(secs), 2)}
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the C++ oracle as it stands on this box's host cores, on our arm's
+    workload; each step is one whole request of it (a bounded sample, measured, not extrapolated)."""
     from synth.configs import WORKLOADS
     if rank != 0:
         return
@@ -641,18 +659,23 @@ def run_reference(args, world, rank):
     t_all = time.perf_counter()
     smp = OracleSample(wl, rank)
     for _ in range(args.warmup):
-        smp.step_seconds()
-    secs = [smp.step_seconds() for _ in range(max(1, args.steps))]
-    t_step = float(np.median(secs))
-    v = smp.tokens_per_step / t_step
-    cb = {"value": round(v, 4), "unit": UNIT, "cores": smp.cores, "kind": "oracle", "sample": smp.describe()}
+        smp.run_one()
+    secs, toks = [], []
+    for _ in range(max(1, args.steps)):
+        s_, k_ = smp.run_one()
+        secs.append(s_)
+        toks.append(k_)
+    smp.close()
+    v = sum(toks) / sum(secs)
+    cb = {"value": round(v, 4), "unit": UNIT, "cores": smp.cores, "kind": "oracle", "sample": smp.describe(len(secs))}
     out = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_step, 1),
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * float(np.mean(secs)), 1),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"{wl.name}: {wl.shape.name}-shaped, {wl.n_requests} requests x {wl.n_nodes}-node "
-                                  f"trees (oracle sample, extrapolated)", "parallelism": "cpu"},
+           "config": workload_config(wl, 1),   # the same config object as our arm's N = 1 line
            "cpu_baseline": cb, "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                                        "d2h_bytes_per_step": 0},
+           "p50_ms": round(1e3 * float(np.median(secs)), 1),
+           "step_definition": "one whole request of the workload (its draft tree through the full model)",
            "wall_s": round(time.perf_counter() - t_all, 1)}
     print(json.dumps(out), flush=True)
 
