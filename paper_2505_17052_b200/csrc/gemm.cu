@@ -84,6 +84,15 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
             if (j < ncol && row < a.R)
               a.out_f32[(size_t)(row >> 1) * a.ldo + feat] = __uint_as_float(v[j]) + __uint_as_float(v[j + 1]);
           }
+        } else if (a.resid && a.splits == 1) {   // fused residual add, unsplit: X + Y0
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int row = row_base + j;
+            if (j < ncol && row < a.R) {
+              float* x = a.resid + (size_t)row * a.ldo + feat;
+              *x = *x + __uint_as_float(v[j]);
+            }
+          }
         } else {
           float* out = a.out_f32 + (size_t)sk * a.split_stride;   // K-split sk's partial
 #pragma unroll
@@ -693,6 +702,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive_leader(&tempty[acc]);
+      if constexpr (MODE == EPI_F32) {
+        if (a.resid && a.splits > 1) {
+          // fused residual add of a K-split tile: the last split of (tile, CTA half) to finish sums
+          // the partials from L2 in split order onto the residual stream (fence / counter /
+          // last-arriver; no CTA waits on another)
+          __threadfence();
+          named_bar_sync(1, kEpiThreads);
+          if (et == 0) {
+            int* cnt = a.tile_cnt + ((size_t)t * NC + qp) * 2 + hr;
+            const int prev = atomicAdd(cnt, 1);
+            red_i[0] = prev == a.splits - 1;
+            if (prev == a.splits - 1) *cnt = 0;   // ready for the next launch
+          }
+          named_bar_sync(1, kEpiThreads);
+          if (red_i[0]) {
+            __threadfence();
+            const int feat = (2 * p + (int)hr) * 128 + tl;
+            if (feat < a.M) {
+              const int r1 = min(a.R, (n + 1) * BN);
+              constexpr int RB = 8;   // rows per batch: all their loads are issued before any store
+              for (int r0 = n * BN; r0 < r1; r0 += RB) {
+                float acc_v[RB];
+#pragma unroll
+                for (int i = 0; i < RB; ++i)
+                  acc_v[i] = r0 + i < r1 ? __ldcg(a.resid + (size_t)(r0 + i) * a.ldo + feat) : 0.f;
+                for (int s2 = 0; s2 < a.splits; ++s2) {
+                  float y[RB];
+#pragma unroll
+                  for (int i = 0; i < RB; ++i)
+                    y[i] = r0 + i < r1 ? __ldcg(a.out_f32 + (size_t)s2 * a.split_stride + (size_t)(r0 + i) * a.ldo + feat)
+                                       : 0.f;
+#pragma unroll
+                  for (int i = 0; i < RB; ++i) acc_v[i] += y[i];
+                }
+#pragma unroll
+                for (int i = 0; i < RB; ++i)
+                  if (r0 + i < r1) a.resid[(size_t)(r0 + i) * a.ldo + feat] = acc_v[i];
+              }
+            }
+          }
+          named_bar_sync(1, kEpiThreads);   // red_i[0] is rewritten by the next tile
+        }
+      }
     }
     if (MODE == EPI_F32 && a.push && (et & 31) == 0) bulk_wait0();   // every pushed row has landed
   }
@@ -950,7 +1002,8 @@ cudaError_t gemm_launch(int mode, const CUtensorMap& tmW, const void* X, GemmArg
   // K-split (EPI_F32 only, caller provides max_splits slices of split_stride floats): give every
   // CTA >= 2 units so the epilogue of one overlaps the MMAs of the next, and fill the SMs.
   a.splits = 1;
-  if (mode == EPI_F32 && !a.pair && a.max_splits > 1 && ntiles < g_num_sms * 3 / 2) {
+  // (the single-CTA kernel has no split fixup: a fused residual add runs unsplit here)
+  if (mode == EPI_F32 && !a.pair && !a.resid && a.max_splits > 1 && ntiles < g_num_sms * 3 / 2) {
     int sp = (2 * g_num_sms + ntiles / 2) / ntiles;
     sp = std::min(sp, a.max_splits);
     while (sp > 1 && a.num_kb / sp < 8) --sp;

@@ -101,6 +101,13 @@ struct GemmArgs {
   // EPI_F32 / EPI_RESID (fp32 residual stream)
   float* out_f32;
   int ldo;
+  // EPI_F32 fused residual add (a6 / a8; CTA-pair kernel): resid[row][f] += the unit's K-split
+  // partials.  splits == 1: the epilogue adds its accumulator straight into resid; splits > 1:
+  // every split stores its partial, and the last of the tile's splits to finish (a per-(tile,
+  // half) counter in tile_cnt, zero between launches) computes ((X + Y0) + Y1) + ... in split order
+  // (the same order as k_rmsnorm's sum: deterministic) and stores it into resid.
+  float* resid;
+  int* tile_cnt;
   // EPI_F32 with push (NEXT-F4): each 32-row chunk is staged in shared memory and row r is sent
   // with a bulk async copy to rank o = r / rows_per_rank, slot [tp_src] of its receive buffer:
   // peer_out[o] + tp_src * slot_stride + (r - o * rows_per_rank) * ldo

@@ -123,10 +123,10 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 struct WsLayout {
   size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
   size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, attn_nch, attn_cnt, part_val, part_idx, part_val2, part_idx2, part_val3,
-      y, score, tp_gather;
+      tile_cnt, y, score, tp_gather;
   size_t part_m, part_s, lse, row_qnode, pchild, resid_y, resid_s;   // SAMPLE_PQ_DENSE
   size_t draft_logits;                                                // [R][V] fp32 logits of a draft pass (NEXT-F3 only)
-  size_t stage_in, stage_out, total;
+  size_t stage_in, stage_out, total, tile_cnt_bytes;
   int B, R, n_splits_max;
 };
 
@@ -172,6 +172,9 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.part_val = take(4 * (size_t)R * vt);
   w.part_idx = take(4 * (size_t)R * vt);
   w.part_val2 = take(4 * (size_t)R * vt);
+  // fused residual add: one counter per (256-feature tile, row tile, multicast slot, CTA half)
+  w.tile_cnt_bytes = 4 * (size_t)((c.d + 255) / 256) * ((R + 15) / 16 + 1) * 4 * 2;
+  w.tile_cnt = take(w.tile_cnt_bytes);
   w.part_idx2 = take(4 * (size_t)R * vt);
   w.part_val3 = take(4 * (size_t)R * vt);
   w.y = take(4 * R);
@@ -331,6 +334,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   aa.R = R;
   aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
 
+  if (!tp) CK(cudaMemsetAsync(P(w.tile_cnt), 0, w.tile_cnt_bytes, st));   // fused residual-add counters
   float* Y = (float*)P(w.Y);
   const size_t y_stride = ((size_t)R + kMaxTp) * std::max((H + 2 * KV) * hd, c.d);
   int pendingY = 0;   // K-split partials of the last down-proj not yet added to X
@@ -347,11 +351,19 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     // tiles on 74 pairs -> QKV + RoPE 1.42 -> 1.31 ms per step)
     g.unsplit_if_full = kind == K_QKV ? 1 : 0;
     g.split_stride = y_stride;
+    // O / down without tensor parallelism: the residual add (and the K-split sum) happens in the
+    // GEMM (GemmArgs::resid); the next RMSNorm reads only X (SPECEDGE_RESID_FUSE=0: the old path)
+    static const bool resid_fuse = !getenv("SPECEDGE_RESID_FUSE") || getenv("SPECEDGE_RESID_FUSE")[0] != '0';
+    const bool fuse = resid_fuse && !tp && (kind == K_O || kind == K_DOWN);
+    if (fuse) {
+      g.resid = X;
+      g.tile_cnt = (int*)P(w.tile_cnt);
+    }
     {
       KTimer _t(kind, st);
       if (gemm_launch(EPI_F32, tm, Xin, g, st, &launches) != cudaSuccess) return -1;
     }
-    const int ns = gemm_splits_last();
+    const int ns = fuse ? 0 : gemm_splits_last();
     if (tp && row_parallel) {
       if (tp_reduce_scatter_f32(Y, (size_t)Rl * Mrows, m->tp_rank, m->nccl, st) != cudaSuccess) return -1;
       ++launches;
