@@ -718,27 +718,37 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_bar_sync(1, kEpiThreads);
           if (red_i[0]) {
             __threadfence();
-            const int feat = (2 * p + (int)hr) * 128 + tl;
-            if (feat < a.M) {
+            // thread et: 4 consecutive features (float4) of rows et/32, et/32 + 4, ...; 4 rows per
+            // thread in flight at once, every load of a batch issued before its stores
+            const int f4 = (2 * p + (int)hr) * 128 + (et & 31) * 4;
+            if (f4 < a.M) {
               const int r1 = min(a.R, (n + 1) * BN);
-              constexpr int RB = 8;   // rows per batch: all their loads are issued before any store
-              for (int r0 = n * BN; r0 < r1; r0 += RB) {
-                float acc_v[RB];
+              constexpr int RB = 4;
+              for (int r0 = n * BN + (et >> 5); r0 < r1; r0 += 4 * RB) {
+                float4 acc_v[RB];
 #pragma unroll
-                for (int i = 0; i < RB; ++i)
-                  acc_v[i] = r0 + i < r1 ? __ldcg(a.resid + (size_t)(r0 + i) * a.ldo + feat) : 0.f;
+                for (int i = 0; i < RB; ++i) {
+                  const int row = r0 + 4 * i;
+                  acc_v[i] = row < r1 ? __ldcg(reinterpret_cast<const float4*>(a.resid + (size_t)row * a.ldo + f4))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
                 for (int s2 = 0; s2 < a.splits; ++s2) {
-                  float y[RB];
+                  float4 y[RB];
 #pragma unroll
-                  for (int i = 0; i < RB; ++i)
-                    y[i] = r0 + i < r1 ? __ldcg(a.out_f32 + (size_t)s2 * a.split_stride + (size_t)(r0 + i) * a.ldo + feat)
-                                       : 0.f;
+                  for (int i = 0; i < RB; ++i) {
+                    const int row = r0 + 4 * i;
+                    y[i] = row < r1 ? __ldcg(reinterpret_cast<const float4*>(a.out_f32 + (size_t)s2 * a.split_stride +
+                                                                              (size_t)row * a.ldo + f4))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                  }
 #pragma unroll
-                  for (int i = 0; i < RB; ++i) acc_v[i] += y[i];
+                  for (int i = 0; i < RB; ++i) {
+                    acc_v[i].x += y[i].x; acc_v[i].y += y[i].y; acc_v[i].z += y[i].z; acc_v[i].w += y[i].w;
+                  }
                 }
 #pragma unroll
                 for (int i = 0; i < RB; ++i)
-                  if (r0 + i < r1) a.resid[(size_t)(r0 + i) * a.ldo + feat] = acc_v[i];
+                  if (r0 + 4 * i < r1) *reinterpret_cast<float4*>(a.resid + (size_t)(r0 + 4 * i) * a.ldo + f4) = acc_v[i];
               }
             }
           }

@@ -351,10 +351,13 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     // tiles on 74 pairs -> QKV + RoPE 1.42 -> 1.31 ms per step)
     g.unsplit_if_full = kind == K_QKV ? 1 : 0;
     g.split_stride = y_stride;
-    // O / down without tensor parallelism: the residual add (and the K-split sum) happens in the
-    // GEMM (GemmArgs::resid); the next RMSNorm reads only X (SPECEDGE_RESID_FUSE=0: the old path)
-    static const bool resid_fuse = !getenv("SPECEDGE_RESID_FUSE") || getenv("SPECEDGE_RESID_FUSE")[0] != '0';
-    const bool fuse = resid_fuse && !tp && (kind == K_O || kind == K_DOWN);
+    // O / down without tensor parallelism, SPECEDGE_RESID_FUSE bit 0 (O) / bit 1 (down): the residual
+    // add (and the K-split sum) happens in the GEMM (GemmArgs::resid) and the next RMSNorm reads X
+    // only.  Off by default: measured on cfg2 the epilogue's global read-modify-write of X costs
+    // more than the RMSNorm saves (O 0.85 -> 2.05 ms, down 1.66 -> 2.48 ms vs RMSNorm 0.97 -> 0.56
+    // ms per step; profiles/README.md)
+    static const int resid_fuse = getenv("SPECEDGE_RESID_FUSE") ? atoi(getenv("SPECEDGE_RESID_FUSE")) : 0;
+    const bool fuse = !tp && ((kind == K_O && (resid_fuse & 1)) || (kind == K_DOWN && (resid_fuse & 2)));
     if (fuse) {
       g.resid = X;
       g.tile_cnt = (int*)P(w.tile_cnt);
