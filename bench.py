@@ -417,7 +417,8 @@ def run_gpu(args, world, rank, local):
             kernel_table[k]["gbs"] = round(w["bytes"] / per / 1e9, 1)
     serving = None
     if not tp and len(mbs) == 1 and not args.no_serving:
-        serving = serving_leg(wl, model, local)
+        # sessions = 2 x the batch capacity (edges = 2 x batch) and 4 x (a saturated server)
+        serving = {f"sessions_{k}x_capacity": serving_leg(wl, model, local, sessions_per_slot=k) for k in (2, 4)}
     if rank != 0:
         if dist:
             dist.barrier()

@@ -144,58 +144,58 @@ __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const f
                                                   const bf16* __restrict__ g, bf16* __restrict__ out, int d, float eps,
                                                   int split, const RmsSrc ys) {
   pdl_begin();
-  // blockDim.x = d / 16 rounded up to whole warps: thread t owns elements [16t, 16t+16), kept in
-  // registers across passes; padding lanes (16t >= d) hold zeros and neither load nor store, so the
-  // full-mask warp reductions below always run on complete warps
+  // blockDim.x = d / 16 rounded up to whole warps, T threads: thread t owns the float4 groups
+  // t + T*k (k < 4), i.e. elements [4(t + Tk), 4(t + Tk) + 4), kept in registers across passes —
+  // every warp-wide load / store covers 512 contiguous bytes; groups past d hold zeros and neither
+  // load nor store, so the full-mask warp reductions below always run on complete warps
   const int row = blockIdx.x;
-  const int i = threadIdx.x * 16;
-  const bool own = i < d;
-  float* x = X + (size_t)row * d + i;
+  const int T = blockDim.x;
+  const int t = threadIdx.x;
+  float* x = X + (size_t)row * d;
   __shared__ float red[32];
-  float xv[16];
+  float4 xv[4];
+  bool own[4];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) xv[k] = 0.f;
-  if (own) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 a = *reinterpret_cast<const float4*>(x + 4 * k);
-      xv[4 * k] = a.x; xv[4 * k + 1] = a.y; xv[4 * k + 2] = a.z; xv[4 * k + 3] = a.w;
-    }
+  for (int k = 0; k < 4; ++k) {
+    own[k] = 4 * (t + T * k) < d;
+    xv[k] = own[k] ? *reinterpret_cast<const float4*>(x + 4 * (t + T * k)) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  if constexpr (NY > 0) if (own) {
+  if constexpr (NY > 0) {
     float4 yv[NY][4];
 #pragma unroll
     for (int s = 0; s < NY; ++s)
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        yv[s][k] = __ldcs(reinterpret_cast<const float4*>((ys.p[0] ? ys.p[s] : Y + s * y_stride) + (size_t)row * d +
-                                                          i + 4 * k));
+        yv[s][k] = own[k] ? __ldcs(reinterpret_cast<const float4*>((ys.p[0] ? ys.p[s] : Y + s * y_stride) +
+                                                                    (size_t)row * d + 4 * (t + T * k)))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int s = 0; s < NY; ++s)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        xv[4 * k] += yv[s][k].x; xv[4 * k + 1] += yv[s][k].y; xv[4 * k + 2] += yv[s][k].z; xv[4 * k + 3] += yv[s][k].w;
+        xv[k].x += yv[s][k].x; xv[k].y += yv[s][k].y; xv[k].z += yv[s][k].z; xv[k].w += yv[s][k].w;
       }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      *reinterpret_cast<float4*>(x + 4 * k) = make_float4(xv[4 * k], xv[4 * k + 1], xv[4 * k + 2], xv[4 * k + 3]);
+      if (own[k]) *reinterpret_cast<float4*>(x + 4 * (t + T * k)) = xv[k];
   }
-  if constexpr (NY < 0) if (own) {
+  if constexpr (NY < 0) {
     for (int s = 0; s < -NY; ++s) {
-      const float* src = (ys.p[0] ? ys.p[s] : Y + s * y_stride) + (size_t)row * d + i;
+      const float* src = (ys.p[0] ? ys.p[s] : Y + s * y_stride) + (size_t)row * d;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float4 y = __ldcs(reinterpret_cast<const float4*>(src + 4 * k));
-        xv[4 * k] += y.x; xv[4 * k + 1] += y.y; xv[4 * k + 2] += y.z; xv[4 * k + 3] += y.w;
+        if (!own[k]) continue;
+        const float4 y = __ldcs(reinterpret_cast<const float4*>(src + 4 * (t + T * k)));
+        xv[k].x += y.x; xv[k].y += y.y; xv[k].z += y.z; xv[k].w += y.w;
       }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      *reinterpret_cast<float4*>(x + 4 * k) = make_float4(xv[4 * k], xv[4 * k + 1], xv[4 * k + 2], xv[4 * k + 3]);
+      if (own[k]) *reinterpret_cast<float4*>(x + 4 * (t + T * k)) = xv[k];
   }
   float ss = 0.f;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) ss += xv[k] * xv[k];
+  for (int k = 0; k < 4; ++k) ss += xv[k].x * xv[k].x + xv[k].y * xv[k].y + xv[k].z * xv[k].z + xv[k].w * xv[k].w;
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o, 32);
   const int nw = (blockDim.x + 31) >> 5;
   if (nw > 1) {
@@ -210,42 +210,33 @@ __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const f
     ss = red[0];
   }
   const float inv = rsqrtf(ss / (float)d + eps);
-  if (!own) return;
-  const uint4* gp = reinterpret_cast<const uint4*>(g + i);
-  uint32_t o[8], r[8];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const uint4 gu = gp[k];
-    const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
+  for (int k = 0; k < 4; ++k) {
+    if (!own[k]) continue;
+    const int e = 4 * (t + T * k);
+    const uint2 gu = *reinterpret_cast<const uint2*>(g + e);
+    const float xs[4] = {xv[k].x, xv[k].y, xv[k].z, xv[k].w};
+    const uint32_t gw[2] = {gu.x, gu.y};
+    uint32_t o[2], r[2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float y0 = xv[8 * k + 2 * q] * inv * __uint_as_float(gw[q] << 16);
-      const float y1 = xv[8 * k + 2 * q + 1] * inv * __uint_as_float(gw[q] & 0xFFFF0000u);
+    for (int q = 0; q < 2; ++q) {
+      const float y0 = xs[2 * q] * inv * __uint_as_float(gw[q] << 16);
+      const float y1 = xs[2 * q + 1] * inv * __uint_as_float(gw[q] & 0xFFFF0000u);
       __nv_bfloat162 p = __floats2bfloat162_rn(y0, y1);
-      o[4 * k + q] = *reinterpret_cast<uint32_t*>(&p);
-      const float h0 = __uint_as_float(o[4 * k + q] << 16), h1 = __uint_as_float(o[4 * k + q] & 0xFFFF0000u);
+      o[q] = *reinterpret_cast<uint32_t*>(&p);
+      const float h0 = __uint_as_float(o[q] << 16), h1 = __uint_as_float(o[q] & 0xFFFF0000u);
       __nv_bfloat162 pq = __floats2bfloat162_rn(y0 - h0, y1 - h1);
-      r[4 * k + q] = *reinterpret_cast<uint32_t*>(&pq);
+      r[q] = *reinterpret_cast<uint32_t*>(&pq);
     }
-  }
-  if (split) {
-    uint4* dh = reinterpret_cast<uint4*>(out + (size_t)(2 * row) * d + i);
-    uint4* dl = reinterpret_cast<uint4*>(out + (size_t)(2 * row + 1) * d + i);
-    dh[0] = make_uint4(o[0], o[1], o[2], o[3]);
-    dh[1] = make_uint4(o[4], o[5], o[6], o[7]);
-    dl[0] = make_uint4(r[0], r[1], r[2], r[3]);
-    dl[1] = make_uint4(r[4], r[5], r[6], r[7]);
-  } else if (ys.nout) {
-    // NEXT-F4 all-gather: this rank's normalised row into every rank's copy (NVLink stores)
-    for (int p = 0; p < ys.nout; ++p) {
-      uint4* dh = reinterpret_cast<uint4*>(ys.outp[p] + (size_t)row * d + i);
-      dh[0] = make_uint4(o[0], o[1], o[2], o[3]);
-      dh[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    if (split) {
+      *reinterpret_cast<uint2*>(out + (size_t)(2 * row) * d + e) = make_uint2(o[0], o[1]);
+      *reinterpret_cast<uint2*>(out + (size_t)(2 * row + 1) * d + e) = make_uint2(r[0], r[1]);
+    } else if (ys.nout) {
+      // NEXT-F4 all-gather: this rank's normalised row into every rank's copy (NVLink stores)
+      for (int p = 0; p < ys.nout; ++p) *reinterpret_cast<uint2*>(ys.outp[p] + (size_t)row * d + e) = make_uint2(o[0], o[1]);
+    } else {
+      *reinterpret_cast<uint2*>(out + (size_t)row * d + e) = make_uint2(o[0], o[1]);
     }
-  } else {
-    uint4* dh = reinterpret_cast<uint4*>(out + (size_t)row * d + i);
-    dh[0] = make_uint4(o[0], o[1], o[2], o[3]);
-    dh[1] = make_uint4(o[4], o[5], o[6], o[7]);
   }
 }
 
