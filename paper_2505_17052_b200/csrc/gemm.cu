@@ -39,7 +39,8 @@ __host__ __device__ inline SmemLayout smem_layout(int stages, int BN) {
   L.b_off = L.a_off + stages * kABytes;
   L.xch_off = L.b_off + stages * (uint32_t)BN * 128u;
   L.red_off = L.xch_off + 128 * kXchStride * 4;
-  L.bar_off = L.red_off + 4 * 32 * 24;   // red_v, red_i [128]; top2: red_s2, red_i2 at +256, red_s3 at +512
+  L.bar_off = L.red_off + 4 * 32 * 24;   // red_v, red_i [128]; top2: red_s2, red_i2 at +256, red_s3 at +512;
+                                         // noise row inputs at +640 (128 words)
   L.total = L.bar_off + (2 * stages + 4) * 8 + 16;
   return L;
 }
@@ -194,17 +195,30 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
       // The raw words are turned into noise in the score loop below, which overwrites the cells.
       const bool noisy = MODE == EPI_PQ2 || a.sample;
       const bool quad_ok = (a.vocab_off & 3) == 0;
-      if (noisy && quad_ok) {
-        const int qd = tl & 3;
-        for (int j4 = 0; j4 < np; j4 += 4) {
-          const int jj = j4 + qd;
-          const int j = a.pair ? 2 * jj : jj;
+      // the chunk's per-row Philox inputs (slot, session lo / hi, key word 0), gathered once by the
+      // first np threads into the free tail of the reduction area: the dependent row -> request ->
+      // session loads would otherwise sit on every lane's critical path
+      uint32_t* rinfo = reinterpret_cast<uint32_t*>(red_v + 640);   // [32][4]
+      if (noisy) {
+        if (et < np) {
+          const int j = a.pair ? 2 * et : et;
           const int row = min(row_base + j, a.R - 1);
           const int lr = a.pair ? row >> 1 : row;
           const int req = a.row_req[lr];
           const uint64_t ses = a.req_session[req];
-          const U4 w = philox4x32_10(U4{(uint32_t)vg >> 2, (uint32_t)a.row_slot[lr], (uint32_t)ses, (uint32_t)(ses >> 32)},
-                                     a.seed_lo ^ a.req_round[req], a.seed_hi);
+          rinfo[4 * et] = (uint32_t)a.row_slot[lr];
+          rinfo[4 * et + 1] = (uint32_t)ses;
+          rinfo[4 * et + 2] = (uint32_t)(ses >> 32);
+          rinfo[4 * et + 3] = a.seed_lo ^ a.req_round[req];
+        }
+        named_bar_sync(1, kEpiThreads);
+      }
+      if (noisy && quad_ok) {
+        const int qd = tl & 3;
+        for (int j4 = 0; j4 < np; j4 += 4) {
+          const int jj = j4 + qd;
+          const uint4 ri = *reinterpret_cast<const uint4*>(rinfo + 4 * jj);
+          const U4 w = philox4x32_10(U4{(uint32_t)vg >> 2, ri.x, ri.y, ri.z}, ri.w, a.seed_hi);
           uint32_t* cell = reinterpret_cast<uint32_t*>(xch) + (tl & ~3) * kXchStride + jj;
           cell[0] = w.x;
           cell[kXchStride] = w.y;
@@ -218,13 +232,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         if (quad_ok) {
           wd = reinterpret_cast<const uint32_t*>(xch)[tl * kXchStride + jj];
         } else {   // a vocab shard not aligned to 4 ids: this lane's own block
-          const int j = a.pair ? 2 * jj : jj;
-          const int row = min(row_base + j, a.R - 1);
-          const int lr = a.pair ? row >> 1 : row;
-          const int req = a.row_req[lr];
-          const uint64_t ses = a.req_session[req];
-          const U4 w = philox4x32_10(U4{(uint32_t)vg >> 2, (uint32_t)a.row_slot[lr], (uint32_t)ses, (uint32_t)(ses >> 32)},
-                                     a.seed_lo ^ a.req_round[req], a.seed_hi);
+          const uint4 ri = *reinterpret_cast<const uint4*>(rinfo + 4 * jj);
+          const U4 w = philox4x32_10(U4{(uint32_t)vg >> 2, ri.x, ri.y, ri.z}, ri.w, a.seed_hi);
           wd = u4_word(w, vg & 3);
         }
         const float u = (float)((wd >> 8) | 1u) * 5.9604644775390625e-08f;   // exact, in (0, 1)
@@ -297,20 +306,16 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           }
           const float c2 = red_s2[g * np + jj], c3 = red_s3[g * np + jj];
           const int k2 = red_i2[g * np + jj];
-          float v[6] = {b1, b2, b3, c1, c2, c3};
-          int id[6] = {i1, i2, 0, k1, k2, 0};
-          // three largest of the two lists, stable (own list first on ties)
-          float o[3];
-          int oi[3];
-          int p = 0, q = 3;
-#pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            const bool take_own = p < 3 && (q >= 6 || v[p] >= v[q]);
-            o[t] = take_own ? v[p] : v[q];
-            oi[t] = take_own ? id[p] : id[q];
-            if (take_own) ++p; else ++q;
-          }
-          b1 = o[0]; i1 = oi[0]; b2 = o[1]; i2 = oi[1]; b3 = o[2];
+          // insert group g's three (its ids are higher: strict > keeps ours first on ties; its own
+          // list is in order, so c1 precedes c2 on ties as well)
+          auto ins = [&](float val, int id) {
+            if (val > b1) { b3 = b2; b2 = b1; i2 = i1; b1 = val; i1 = id; }
+            else if (val > b2) { b3 = b2; b2 = val; i2 = id; }
+            else if (val > b3) b3 = val;
+          };
+          ins(c1, k1);
+          ins(c2, k2);
+          ins(c3, 0x7fffffff);
         }
         const int j = a.pair ? 2 * jj : jj;
         const int row = row_base + j;

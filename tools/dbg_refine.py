@@ -7,6 +7,9 @@ from paper_2505_17052_b200 import api
 from synth.configs import WORKLOADS
 from synth.trees import pooled_tree
 wl = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"]
+if len(sys.argv) > 2:   # override the mode: greedy / sample
+    import dataclasses
+    wl = dataclasses.replace(wl, mode=sys.argv[2], temperature=1.0 if sys.argv[2] == "sample" else 0.0)
 rng = np.random.default_rng(1)
 B = wl.n_requests
 ctx = [int(c) for c in rng.integers(wl.ctx_lo, wl.ctx_hi + 1, B)]
