@@ -215,7 +215,11 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
       }
       if (noisy && quad_ok) {
         const int qd = tl & 3;
-        for (int j4 = 0; j4 < np; j4 += 4) {
+        // unrolled: the up to 8 Philox blocks of a lane are independent chains (one epilogue warp
+        // per SM sub-partition has no other latency hiding)
+#pragma unroll
+        for (int j4 = 0; j4 < 32; j4 += 4) {
+          if (j4 >= np) break;
           const int jj = j4 + qd;
           const uint4 ri = *reinterpret_cast<const uint4*>(rinfo + 4 * jj);
           const U4 w = philox4x32_10(U4{(uint32_t)vg >> 2, ri.x, ri.y, ri.z}, ri.w, a.seed_hi);
