@@ -243,6 +243,13 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         const float u = (float)((wd >> 8) | 1u) * 5.9604644775390625e-08f;   // exact, in (0, 1)
         return -logf(-logf(u));
       };
+      // ---- the chunk's noise first, as 32 independent unrolled chains (the score loop below has
+      // data-dependent branches that would serialise the two logf evaluations per value)
+      float gn[32];
+      if (noisy) {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) gn[jj] = gumbel_at(jj);   // rows >= np: unused
+      }
       // ---- scores for the tile argmax
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj) {
@@ -258,10 +265,10 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
               const float pv = __expf(fmaf(l, a.inv_t, -a.lse[lr]));
               if (vg == a.node_token[qn]) a.pchild[lr] = pv;
               const float r = pv - a.draft_q[(size_t)qn * a.vocab_q + vg];
-              if (r > 0.f) sc = __logf(r) + gumbel_at(jj);
+              if (r > 0.f) sc = __logf(r) + gn[jj];
             }
           } else {
-            sc = a.sample ? l * a.inv_t + gumbel_at(jj) : l;
+            sc = a.sample ? l * a.inv_t + gn[jj] : l;
           }
         }
         xch[tl * kXchStride + jj] = sc;
