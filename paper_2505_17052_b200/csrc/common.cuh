@@ -42,6 +42,31 @@ __host__ __device__ __forceinline__ uint32_t u4_word(const U4& r, int i) {
   return i == 0 ? r.x : i == 1 ? r.y : i == 2 ? r.z : r.w;
 }
 
+// Gumbel noise of a Philox word (SURVEY amb. A9): u = ((w >> 8) | 1) 2^-24 in (0, 1), exact;
+// g = -log(-log u).  Evaluated with the SFU log2 (lg2.approx: absolute error <= 2^-22.6) except
+// where that loses relative accuracy in the inner log: for d = u - 1 in (-2^-5, 0) (exact),
+// -log u = -log1p(d) by its series to d^6 (relative error < 2e-9).  The inner value is then within
+// ~4e-6 relative of exact everywhere, the noise within ~4e-6 absolute (R-gumbel, DESIGN.md §4:
+// far below the 1e-2 margins at which targets must agree with the oracle's float64 noise).  The
+// LM-head epilogue and its refinement share this function, so both see identical bits.
+__device__ __forceinline__ float gumbel_of_word(uint32_t w) {
+  const uint32_t m = (w >> 8) | 1u;
+  const float u = (float)m * 5.9604644775390625e-08f;                     // exact
+  const float d = (float)((int32_t)m - (1 << 24)) * 5.9604644775390625e-08f;   // u - 1, exact
+  float l2;
+  asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(u));
+  // -log1p(d) = -d + d^2/2 - d^3/3 + d^4/4 - d^5/5 + d^6/6   (|d| < 2^-5)
+  float sr = fmaf(d, -1.f / 6.f, 1.f / 5.f);
+  sr = fmaf(sr, d, -1.f / 4.f);
+  sr = fmaf(sr, d, 1.f / 3.f);
+  sr = fmaf(sr, d, -1.f / 2.f);
+  sr = fmaf(sr, d, 1.f);
+  const float t = d > -0.03125f ? -d * sr : -0.6931471805599453f * l2;   // -log u > 0
+  float l2t;
+  asm("lg2.approx.f32 %0, %1;" : "=f"(l2t) : "f"(t));
+  return -0.6931471805599453f * l2t;
+}
+
 // signed 24-bit integer in [-2^23, 2^23) from a Philox word (exact in fp32)
 __host__ __device__ __forceinline__ float philox_i24(uint32_t w) {
   return (float)((int32_t)(w >> 8) - (1 << 23));

@@ -240,8 +240,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           const U4 w = philox4x32_10(U4{(uint32_t)vg >> 2, ri.x, ri.y, ri.z}, ri.w, a.seed_hi);
           wd = u4_word(w, vg & 3);
         }
-        const float u = (float)((wd >> 8) | 1u) * 5.9604644775390625e-08f;   // exact, in (0, 1)
-        return -logf(-logf(u));
+        return gumbel_of_word(wd);
       };
       // ---- the chunk's noise first, as 32 independent unrolled chains (the score loop below has
       // data-dependent branches that would serialise the two logf evaluations per value)

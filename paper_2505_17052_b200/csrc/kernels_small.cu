@@ -417,8 +417,7 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
         const int vg = a.vocab_off + list[c0 + b];
         if (a.sample) {
           const U4 r = philox4x32_10(U4{(uint32_t)vg >> 2, slot, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0, a.seed_hi);
-          const float u = (float)((u4_word(r, vg & 3) >> 8) | 1u) * 5.9604644775390625e-08f;
-          v = v * a.inv_t + (-logf(-logf(u)));
+          v = v * a.inv_t + gumbel_of_word(u4_word(r, vg & 3));
         }
         if (v > best || (v == best && vg < bi)) { best = v; bi = vg; }
       }
