@@ -345,11 +345,13 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
   const uint4* hi = reinterpret_cast<const uint4*>(a.hf + (size_t)(2 * row) * a.d);
   const uint4* lo = reinterpret_cast<const uint4*>(a.hf + (size_t)(2 * row + 1) * a.d);
   const int nv = a.d / 8;
+  // every load of a phase issued before its first use (one warp per row, ~4 warps per SM: memory
+  // latency, not bandwidth, bounds this kernel)
   float M = -INFINITY;
-#pragma unroll 8
+#pragma unroll 32
   for (int t = lane; t < a.ntiles; t += 32) M = fmaxf(M, __ldg(pv + t));
   float sh = 0.f, sl = 0.f;
-#pragma unroll 4
+#pragma unroll 16
   for (int e = lane; e < nv; e += 32) {
     const uint4 h = __ldg(hi + e), l = __ldg(lo + e);
     const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
@@ -389,7 +391,7 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
         wr[b] = reinterpret_cast<const uint4*>(a.w + (size_t)list[min(c0 + b, n - 1)] * a.d);
         acc[b] = 0.f;
       }
-#pragma unroll 2
+#pragma unroll 4
       for (int e = lane; e < nv; e += 32) {
         const uint4 h = __ldg(hi + e), l = __ldg(lo + e);
         uint4 w[kRefineBatch];
