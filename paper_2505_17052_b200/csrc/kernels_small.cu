@@ -348,19 +348,35 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
   // every load of a phase issued before its first use (one warp per row, ~4 warps per SM: memory
   // latency, not bandwidth, bounds this kernel)
   float M = -INFINITY;
-#pragma unroll 32
-  for (int t = lane; t < a.ntiles; t += 32) M = fmaxf(M, __ldg(pv + t));
-  float sh = 0.f, sl = 0.f;
-#pragma unroll 16
-  for (int e = lane; e < nv; e += 32) {
-    const uint4 h = __ldg(hi + e), l = __ldg(lo + e);
-    const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+  for (int t0 = 0; t0 < a.ntiles; t0 += 32 * 8) {
+    float v[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float h0 = __uint_as_float(hw[k] << 16), h1 = __uint_as_float(hw[k] & 0xFFFF0000u);
-      const float l0 = __uint_as_float(lw[k] << 16), l1 = __uint_as_float(lw[k] & 0xFFFF0000u);
-      sh = fmaf(h0, h0, fmaf(h1, h1, sh));
-      sl = fmaf(l0, l0, fmaf(l1, l1, sl));
+    for (int i = 0; i < 8; ++i) {
+      const int t = t0 + lane + 32 * i;
+      v[i] = t < a.ntiles ? __ldg(pv + t) : -INFINITY;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) M = fmaxf(M, v[i]);
+  }
+  float sh = 0.f, sl = 0.f;
+  for (int e0 = 0; e0 < nv; e0 += 32 * 4) {
+    uint4 h[4], l[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = e0 + lane + 32 * i;
+      h[i] = e < nv ? __ldg(hi + e) : make_uint4(0u, 0u, 0u, 0u);
+      l[i] = e < nv ? __ldg(lo + e) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t hw[4] = {h[i].x, h[i].y, h[i].z, h[i].w}, lw[4] = {l[i].x, l[i].y, l[i].z, l[i].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float h0 = __uint_as_float(hw[k] << 16), h1 = __uint_as_float(hw[k] & 0xFFFF0000u);
+        const float l0 = __uint_as_float(lw[k] << 16), l1 = __uint_as_float(lw[k] & 0xFFFF0000u);
+        sh = fmaf(h0, h0, fmaf(h1, h1, sh));
+        sl = fmaf(l0, l0, fmaf(l1, l1, sl));
+      }
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -391,12 +407,21 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
         wr[b] = reinterpret_cast<const uint4*>(a.w + (size_t)list[min(c0 + b, n - 1)] * a.d);
         acc[b] = 0.f;
       }
-#pragma unroll 4
-      for (int e = lane; e < nv; e += 32) {
-        const uint4 h = __ldg(hi + e), l = __ldg(lo + e);
-        uint4 w[kRefineBatch];
+      for (int e0 = 0; e0 < nv; e0 += 64) {
+        // two iterations' loads (2 x (hi, lo, 4 W rows)) in flight before any use
+        uint4 hh[2], ll[2], ww[2][kRefineBatch];
 #pragma unroll
-        for (int b = 0; b < kRefineBatch; ++b) w[b] = __ldg(wr[b] + e);
+        for (int i = 0; i < 2; ++i) {
+          const int e = e0 + lane + 32 * i;
+          const bool ok = e < nv;
+          hh[i] = ok ? __ldg(hi + e) : make_uint4(0u, 0u, 0u, 0u);
+          ll[i] = ok ? __ldg(lo + e) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int b = 0; b < kRefineBatch; ++b) ww[i][b] = ok ? __ldg(wr[b] + e) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+        const uint4 h = hh[i], l = ll[i];
         const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -405,10 +430,11 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
           const float y1 = __uint_as_float(hw[k] & 0xFFFF0000u) + __uint_as_float(lw[k] & 0xFFFF0000u);
 #pragma unroll
           for (int b = 0; b < kRefineBatch; ++b) {
-            const uint32_t ww = k == 0 ? w[b].x : (k == 1 ? w[b].y : (k == 2 ? w[b].z : w[b].w));
-            acc[b] = fmaf(y0, __uint_as_float(ww << 16), acc[b]);
-            acc[b] = fmaf(y1, __uint_as_float(ww & 0xFFFF0000u), acc[b]);
+            const uint32_t wv = k == 0 ? ww[i][b].x : (k == 1 ? ww[i][b].y : (k == 2 ? ww[i][b].z : ww[i][b].w));
+            acc[b] = fmaf(y0, __uint_as_float(wv << 16), acc[b]);
+            acc[b] = fmaf(y1, __uint_as_float(wv & 0xFFFF0000u), acc[b]);
           }
+        }
         }
       }
 #pragma unroll
