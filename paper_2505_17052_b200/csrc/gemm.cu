@@ -39,9 +39,8 @@ __host__ __device__ inline SmemLayout smem_layout(int stages, int BN) {
   L.b_off = L.a_off + stages * kABytes;
   L.xch_off = L.b_off + stages * (uint32_t)BN * 128u;
   L.red_off = L.xch_off + 128 * kXchStride * 4;
-  L.bar_off = L.red_off + 4 * 32 * 36;   // red_v, red_i [128] each; top2: red_s2 / red_i2 at +256,
-                                         // red_s3 / red_i3 at +512, red_s4 at +768; noise row inputs at
-                                         // +1024 (128 words)
+  L.bar_off = L.red_off + 4 * 32 * 24;   // red_v, red_i [128]; top2: red_s2, red_i2 at +256, red_s3 at +512;
+                                         // noise row inputs at +640 (128 words)
   L.total = L.bar_off + (2 * stages + 4) * 8 + 16;
   return L;
 }
@@ -199,7 +198,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
       // the chunk's per-row Philox inputs (slot, session lo / hi, key word 0), gathered once by the
       // first np threads into the free tail of the reduction area: the dependent row -> request ->
       // session loads would otherwise sit on every lane's critical path
-      uint32_t* rinfo = reinterpret_cast<uint32_t*>(red_v + 1024);   // [32][4]
+      uint32_t* rinfo = reinterpret_cast<uint32_t*>(red_v + 640);   // [32][4]
       if (noisy) {
         if (et < np) {
           const int j = a.pair ? 2 * et : et;
@@ -276,24 +275,21 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
       named_bar_sync(1, kEpiThreads);
       const int ngrp = 128 / np, per = 128 / ngrp;
       // tile argmax per row (ties -> lowest id: features scanned in increasing order); a.top2
-      // also keeps the tile's second and third (score, id) and fourth score (k_lm_refine's
-      // candidate window, hi-only pass)
+      // also keeps the tile's second (score, id) and third score (k_lm_refine's candidate window,
+      // hi-only pass)
       float* red_s2 = red_v + 256;
       int* red_i2 = red_i + 256;
       float* red_s3 = red_v + 512;
-      int* red_i3 = red_i + 512;
-      float* red_s4 = red_v + 768;
       {
         const int jj = et % np, g = et / np;
-        float b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY, b4 = -INFINITY;
-        int i1 = 0x7fffffff, i2 = 0x7fffffff, i3 = 0x7fffffff;
+        float b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
+        int i1 = 0x7fffffff, i2 = 0x7fffffff;
         for (int l = 0; l < per; ++l) {
           const float sc = xch[(g * per + l) * kXchStride + jj];
           const int id = a.vocab_off + m128 * 128 + g * per + l;
-          if (sc > b1) { b4 = b3; b3 = b2; i3 = i2; b2 = b1; i2 = i1; b1 = sc; i1 = id; }
-          else if (sc > b2) { b4 = b3; b3 = b2; i3 = i2; b2 = sc; i2 = id; }
-          else if (sc > b3) { b4 = b3; b3 = sc; i3 = id; }
-          else if (sc > b4) b4 = sc;
+          if (sc > b1) { b3 = b2; b2 = b1; i2 = i1; b1 = sc; i1 = id; }
+          else if (sc > b2) { b3 = b2; b2 = sc; i2 = id; }
+          else if (sc > b3) b3 = sc;
         }
         red_v[g * np + jj] = b1;
         red_i[g * np + jj] = i1;
@@ -301,31 +297,35 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           red_s2[g * np + jj] = b2;
           red_i2[g * np + jj] = i2;
           red_s3[g * np + jj] = b3;
-          red_i3[g * np + jj] = i3;
-          red_s4[g * np + jj] = b4;
         }
       }
       named_bar_sync(1, kEpiThreads);
       if (et < np) {
         const int jj = et;
-        float b1 = red_v[jj], b2 = -INFINITY, b3 = -INFINITY, b4 = -INFINITY;
-        int i1 = red_i[jj], i2 = 0x7fffffff, i3 = 0x7fffffff;
-        if (a.top2) { b2 = red_s2[jj]; i2 = red_i2[jj]; b3 = red_s3[jj]; i3 = red_i3[jj]; b4 = red_s4[jj]; }
-        // insert another group's sorted four (its ids are higher: strict > keeps ours first on
-        // ties; its own list is in order, so its earlier entries precede its later ones as well)
-        auto ins = [&](float val, int id) {
-          if (val > b1) { b4 = b3; b3 = b2; i3 = i2; b2 = b1; i2 = i1; b1 = val; i1 = id; }
-          else if (val > b2) { b4 = b3; b3 = b2; i3 = i2; b2 = val; i2 = id; }
-          else if (val > b3) { b4 = b3; b3 = val; i3 = id; }
-          else if (val > b4) b4 = val;
-        };
+        float b1 = red_v[jj], b2 = -INFINITY, b3 = -INFINITY;
+        int i1 = red_i[jj], i2 = 0x7fffffff;
+        if (a.top2) { b2 = red_s2[jj]; i2 = red_i2[jj]; b3 = red_s3[jj]; }
         for (int g = 1; g < ngrp; ++g) {
-          ins(red_v[g * np + jj], red_i[g * np + jj]);
-          if (a.top2) {
-            ins(red_s2[g * np + jj], red_i2[g * np + jj]);
-            ins(red_s3[g * np + jj], red_i3[g * np + jj]);
-            ins(red_s4[g * np + jj], 0x7fffffff);
+          // merge group g's sorted (b1 >= b2 >= b3) list; groups hold increasing ids, so a tie keeps
+          // the earlier (lower) id first
+          const float c1 = red_v[g * np + jj];
+          const int k1 = red_i[g * np + jj];
+          if (!a.top2) {
+            if (c1 > b1) { b1 = c1; i1 = k1; }
+            continue;
           }
+          const float c2 = red_s2[g * np + jj], c3 = red_s3[g * np + jj];
+          const int k2 = red_i2[g * np + jj];
+          // insert group g's three (its ids are higher: strict > keeps ours first on ties; its own
+          // list is in order, so c1 precedes c2 on ties as well)
+          auto ins = [&](float val, int id) {
+            if (val > b1) { b3 = b2; b2 = b1; i2 = i1; b1 = val; i1 = id; }
+            else if (val > b2) { b3 = b2; b2 = val; i2 = id; }
+            else if (val > b3) b3 = val;
+          };
+          ins(c1, k1);
+          ins(c2, k2);
+          ins(c3, 0x7fffffff);
         }
         const int j = a.pair ? 2 * jj : jj;
         const int row = row_base + j;
@@ -338,8 +338,6 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
             a.part_val2[o] = b2;
             a.part_idx2[o] = i2;
             a.part_val3[o] = b3;
-            a.part_idx3[o] = i3;
-            a.part_val4[o] = b4;
           }
         }
       }

@@ -126,12 +126,10 @@ struct GemmArgs {
   // EPI_ARGMAX
   float* part_val;        // [R][n_tiles_m]
   int* part_idx;
-  int top2;               // also store the tile's second / third (score, id) and fourth score: hi-only LM head
+  int top2;               // also store the tile's second-best (score, id) and third score: hi-only LM head
   float* part_val2;
   int* part_idx2;
   float* part_val3;
-  int* part_idx3;
-  float* part_val4;
   int vocab, sample;      // vocab: rows of this (vocab-shard) LM head
   int vocab_off;          // global id of local row 0 (tensor parallel vocab shard)
   float inv_t;
@@ -257,11 +255,11 @@ cudaError_t qkv_rope_launch(const RopeArgs& r, cudaStream_t st, int* launches);
 cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, int* y, float* score,
                              int* row_target, float* row_score, cudaStream_t st, int* launches);
 // a9 second stage of the hi-only LM head (k_lm_refine): the GEMM scores every vocab id with the
-// hi part of the final hidden only; per (row, tile) it keeps the best three (value, id) and the
-// fourth best value.  |lo . W_v| <= ||lo||_2 max_v ||W_v||_2 (Cauchy-Schwarz), so the true argmax of
+// hi part of the final hidden only; per (row, tile) it keeps the best two (value, id) and the third
+// best value.  |lo . W_v| <= ||lo||_2 max_v ||W_v||_2 (Cauchy-Schwarz), so the true argmax of
 // (hi + lo) . W lies among the ids whose hi score is within W_r = 2 (||lo|| + rho) wmax scale of the
-// best hi score (rho: fp32 accumulation error bound); every such candidate (a tile's best three,
-// or all 128 ids of a tile whose fourth best also falls in the window) is rescored exactly
+// best hi score (rho: fp32 accumulation error bound); every such candidate (a tile's best and
+// second, or all 128 ids of a tile whose third best also falls in the window) is rescored exactly
 // with (hi + lo) . W_v on the CUDA cores, and the argmax of the rescored set (ties -> lowest id) is
 // the row's target.
 struct RefineArgs {
@@ -272,8 +270,6 @@ struct RefineArgs {
   const float* part_val2;   // [R][ntiles]
   const int* part_idx2;     // [R][ntiles]
   const float* part_val3;   // [R][ntiles]
-  const int* part_idx3;     // [R][ntiles]
-  const float* part_val4;   // [R][ntiles]
   const bf16* hf;           // [2R][d]: hi row 2r, lo row 2r+1
   const bf16* w;            // LM head shard [vocab][d]
   uint32_t seed_lo, seed_hi;

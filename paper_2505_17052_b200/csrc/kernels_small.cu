@@ -465,14 +465,12 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
     while (bal) {
       const int tt = t0 + __ffs(bal) - 1;
       bal &= bal - 1;
-      const float v2 = __ldg(pv2 + tt), v3 = __ldg(pv3 + tt), v4 = __ldg(a.part_val4 + base + tt);
-      if (v4 >= thr) {   // a fourth id of this tile may win: every id of the tile
+      if (__ldg(pv3 + tt) >= thr) {   // a third id of this tile may win: every id of the tile
         const int v1 = min(a.vocab, (tt + 1) * 128);
         for (int v = tt * 128; v < v1; ++v) push(v);
       } else {
         push(__ldg(a.part_idx + base + tt) - a.vocab_off);
-        if (v2 >= thr) push(__ldg(a.part_idx2 + base + tt) - a.vocab_off);
-        if (v3 >= thr) push(__ldg(a.part_idx3 + base + tt) - a.vocab_off);
+        if (__ldg(pv2 + tt) >= thr) push(__ldg(a.part_idx2 + base + tt) - a.vocab_off);
       }
     }
   }

@@ -123,7 +123,7 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 struct WsLayout {
   size_t req_L, req_h, req_row0, req_S, row_tok, row_pos, row_req, row_slot, row_anc;
   size_t X, Y, Hn, Hf, Q, O, M, tree_kv, opart, mpart, lpart, attn_nch, attn_cnt, part_val, part_idx, part_val2, part_idx2, part_val3,
-      part_idx3, part_val4, tile_cnt, y, score, tp_gather;
+      tile_cnt, y, score, tp_gather;
   size_t part_m, part_s, lse, row_qnode, pchild, resid_y, resid_s;   // SAMPLE_PQ_DENSE
   size_t draft_logits;                                                // [R][V] fp32 logits of a draft pass (NEXT-F3 only)
   size_t stage_in, stage_out, total, tile_cnt_bytes;
@@ -177,8 +177,6 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.tile_cnt = take(w.tile_cnt_bytes);
   w.part_idx2 = take(4 * (size_t)R * vt);
   w.part_val3 = take(4 * (size_t)R * vt);
-  w.part_idx3 = take(4 * (size_t)R * vt);
-  w.part_val4 = take(4 * (size_t)R * vt);
   w.y = take(4 * R);
   w.score = take(4 * R);
   w.tp_gather = take(8 * (size_t)(kMaxTp + 1) * R);   // TP C3: [tp][R](score, id) + own staging
@@ -619,8 +617,6 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
       gh.part_val2 = (float*)P(w.part_val2);
       gh.part_idx2 = (int*)P(w.part_idx2);
       gh.part_val3 = (float*)P(w.part_val3);
-      gh.part_idx3 = (int*)P(w.part_idx3);
-      gh.part_val4 = (float*)P(w.part_val4);
       { KTimer _t(K_LM, st); CK(gemm_launch(EPI_ARGMAX, m->tm_lm, Hf, gh, st, &launches)); }
       RefineArgs rf{};
       rf.R = R;
@@ -636,8 +632,6 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
       rf.part_val2 = gh.part_val2;
       rf.part_idx2 = gh.part_idx2;
       rf.part_val3 = gh.part_val3;
-      rf.part_idx3 = gh.part_idx3;
-      rf.part_val4 = gh.part_val4;
       rf.hf = Hf;
       rf.w = m->lm_head;
       rf.seed_lo = gl.seed_lo;
