@@ -176,7 +176,8 @@ struct TcArgs {
   int slots_per_mt; // floor(128 / G)
   int prefetch;     // L2 prefetch distance in sub-tiles (0: off)
   unsigned long long* trace;   // debug (env SPECEDGE_ATTN_TRACE): clock64 stamps of CTA 0, else null
-  int exp_flags;               // experiment (SPECEDGE_ATTN_EXP): bit 0 = no MMAs for unit 1 in pair passes
+  int exp_flags;               // experiment (SPECEDGE_ATTN_EXP): bit 0 = no MMAs for unit 1 in pair passes,
+                               // bit 1 = plain softmax loop, bit 2 = full M-tiles only (timing; wrong tails)
 };
 
 #define TRACE(i)                                                                                  \
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     r = rr; g = gg; c_idx = cc; nch = nc;
     S = S_of(r); L = a.req_L[r]; row0 = a.req_row0[r]; h = a.req_h[r];
     n_mt = (S + spm - 1) / spm;
+    if (ta.exp_flags & 4) n_mt = max(1, S / spm);   // experiment: full M-tiles only (no tail pass)
     // pass p: M-tiles 2p, 2p+1 ("pair") or the last one alone; with one Q tile (NQ = 1, chosen
     // when every request fits one M-tile) every pass is a single pass over M-tile p
     n_pass = NQ == 2 ? (n_mt + 1) / 2 : n_mt;
