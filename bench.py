@@ -434,6 +434,9 @@ def run_gpu(args, world, rank, local):
         "config": cfgd,
         "p50_ms": round(statistics.median(step_ms), 4), "p90_ms": round(float(np.quantile(step_ms, 0.9)), 4),
         "rows_per_s": round(replicas * sum(m["R"] for m in mbs) * args.steps / (total_ms / 1e3), 1),
+        # the planted draw's mean tokens/verify differs from the profile mean (Table 1);
+        # the same step time at the profile mean exactly:
+        "tokens_per_s_at_profile_mean": round(value * wl.accept_mu * wl.n_requests * len(mbs) / tokens_per_step, 1),
         "roofline": roof,
         "kernels": kernel_table,
         "kernels_note": "per-kernel ms from an event-instrumented calibration pass of the same steps "
