@@ -53,10 +53,19 @@ def reduce_max(value: float, dist=None, device=None) -> float:
     return float(t.item())
 
 
-def box_throughput(world: int, tokens_per_step_per_rank: int, steps: int, max_ms: float) -> float:
-    """Whole-box verified tokens/s: every rank verifies its own replica's batch each step (weak
-    scaling), the window is the slowest rank's."""
-    return world * tokens_per_step_per_rank * steps / (max_ms / 1e3)
+def reduce_sum(value: float, dist=None, device=None) -> float:
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def box_throughput(tokens_per_step_box: float, steps: int, max_ms: float) -> float:
+    """Whole-box verified tokens/s: the tokens all replicas verify per step (each rank its own
+    batch: weak scaling; summed over ranks), the window is the slowest rank's."""
+    return tokens_per_step_box * steps / (max_ms / 1e3)
 
 
 def _peaks():
@@ -349,7 +358,10 @@ def run_gpu(args, world, rank, local):
     assert acc_all == tokens_per_step, "accepted counts changed between steps"
     total_ms = reduce_max(total_ms, dist, f"cuda:{local}")
     replicas = 1 if tp else world   # TP: one model (one request set) spans the box
-    value = box_throughput(replicas, tokens_per_step, args.steps, total_ms)
+    # replicas verify different request sets: sum their tokens (and rows) over the ranks
+    box_tokens = tokens_per_step if tp else reduce_sum(tokens_per_step, dist, f"cuda:{local}")
+    box_rows = sum(m["R"] for m in mbs) if tp else reduce_sum(sum(m["R"] for m in mbs), dist, f"cuda:{local}")
+    value = box_throughput(box_tokens, args.steps, total_ms)
 
     # ---- end-to-end through the host-buffer C-ABI entry point (copies inside the timed region);
     # microbatches are verified one after another from the host (the synchronous public call)
@@ -376,6 +388,7 @@ def run_gpu(args, world, rank, local):
     e2e_ms = e0.elapsed_time(e1)
     e2e_ms = reduce_max(e2e_ms, dist, f"cuda:{local}")
     e2e_tokens = sum(int((m["ho"]["accepted_len"].numpy() + 1).sum()) for m in mbs)
+    e2e_box = e2e_tokens if tp else reduce_sum(e2e_tokens, dist, f"cuda:{local}")
     h2d = sum(m["hb"].nbytes() for m in mbs)
     d2h = sum(4 * (3 * m["hb"].num_requests + 2 * m["hb"].total_nodes + 2 * (m["hb"].total_nodes +
                                                                           m["hb"].num_requests)) for m in mbs)
@@ -433,15 +446,15 @@ def run_gpu(args, world, rank, local):
         "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": cfgd,
         "p50_ms": round(statistics.median(step_ms), 4), "p90_ms": round(float(np.quantile(step_ms, 0.9)), 4),
-        "rows_per_s": round(replicas * sum(m["R"] for m in mbs) * args.steps / (total_ms / 1e3), 1),
+        "rows_per_s": round(box_rows * args.steps / (total_ms / 1e3), 1),
         # the planted draw's mean tokens/verify differs from the profile mean (Table 1);
         # the same step time at the profile mean exactly:
-        "tokens_per_s_at_profile_mean": round(value * wl.accept_mu * wl.n_requests * len(mbs) / tokens_per_step, 1),
+        "tokens_per_s_at_profile_mean": round(value * wl.accept_mu * wl.n_requests * len(mbs) * replicas / box_tokens, 1),
         "roofline": roof,
         "kernels": kernel_table,
         "kernels_note": "per-kernel ms from an event-instrumented calibration pass of the same steps "
                         "(each event pair adds a few us of stream time; small kernels read high)",
-        "e2e": {"value": round(box_throughput(replicas, e2e_tokens, args.steps, e2e_ms), 1), "unit": UNIT,
+        "e2e": {"value": round(box_throughput(e2e_box, args.steps, e2e_ms), 1), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches), "clocks": clk.result(),
     }

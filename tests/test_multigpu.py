@@ -1,6 +1,6 @@
 """N > 1 path on CPU (per-GPU replicas, no collective on the data path).
 world_size-2 gloo process groups stand in for the NCCL ranks: the only cross-rank operations of the
-benchmark are the barrier and the max-over-ranks timing reduction; the data path itself must be
+benchmark are the barrier, the max-over-ranks timing reduction and the sum of the replicas' verified tokens; the data path itself must be
 independent of placement (a request verified on any rank gives the same outcome)."""
 import os
 import socket
@@ -41,7 +41,9 @@ def _worker(rank, world, port, q):
     o = OV.verify_one(W, OV.Request(ses, tree.parent, tree.token), "sample", 0.7, 99)
     # 3) per-rank workloads differ (replicas verify different requests)
     ctx = bench.contexts(CFG2, rank)
-    q.put((rank, mx, bench.box_throughput(world, 72, 10, mx), o.accepted_token, o.bonus, ctx))
+    # tokens verified per step differ per replica (70 on rank 0, 74 on rank 1): summed over ranks
+    box_tokens = bench.reduce_sum(70 + 4 * rank, dist)
+    q.put((rank, mx, bench.box_throughput(box_tokens, 10, mx), o.accepted_token, o.bonus, ctx))
     dist.destroy_process_group()
 
 
@@ -58,6 +60,6 @@ def test_two_rank_replicas_gloo():
         assert p.exitcode == 0
     (r0, mx0, v0, acc0, b0, c0), (r1, mx1, v1, acc1, b1, c1) = res
     assert mx0 == mx1 == 150.0                       # slowest rank's clock
-    assert v0 == v1 == pytest.approx(2 * 72 * 10 / 0.150)
+    assert v0 == v1 == pytest.approx((70 + 74) * 10 / 0.150)
     assert (acc0, b0) == (acc1, b1)                  # same request -> same outcome on any rank
     assert c0 != c1                                  # replicas own different requests
