@@ -323,21 +323,26 @@ __global__ void k_lm_reduce(const float* __restrict__ pv, const int* __restrict_
 }
 
 // ------------------------------------------------------------- K9c hi-only LM head refinement
-// One warp per row (RefineArgs in internal.h).  The window uses the row's own ||hi||_2, ||lo||_2
-// (read here, so tensor-parallel ranks need no extra collective) and the shard's max_v ||W_v||_2.
-// Candidates are gathered first (ballot over the tiles), then rescored kRefineBatch at a time so
-// that the loads of several LM-head rows are in flight together.
+// One 4-warp block per row (RefineArgs in internal.h).  The window uses the row's own ||hi||_2,
+// ||lo||_2 (read here, so tensor-parallel ranks need no extra collective) and the shard's
+// max_v ||W_v||_2.  The warps split the tiles (max, candidate gathering into a shared list) and the
+// row (norms), then rescore the list kRefineBatch LM-head rows at a time, warp w taking batches
+// w, w+4, ...; the per-warp winners are combined in (score desc, id asc) order, so the result does
+// not depend on the gathering order.
 constexpr int kRefineBatch = 4;
-constexpr int kRefineList = 64;
+constexpr int kRefineWarps = 4;
+constexpr int kRefineList = 1024;
 
-__global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ RefineArgs a) {
+__global__ void __launch_bounds__(kRefineWarps * 32) k_lm_refine(const __grid_constant__ RefineArgs a) {
   pdl_begin();
-  __shared__ int s_list[4][kRefineList];
-  const int wib = threadIdx.x >> 5;
-  const int row = blockIdx.x * (blockDim.x >> 5) + wib;
-  const int lane = threadIdx.x & 31;
-  if (row >= a.R) return;
-  int* list = s_list[wib];
+  __shared__ int s_list[kRefineList];
+  __shared__ int s_n, s_over;
+  __shared__ float s_red[3][kRefineWarps];
+  __shared__ float s_best[kRefineWarps];
+  __shared__ int s_bi[kRefineWarps];
+  const int row = blockIdx.x;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
   const size_t base = (size_t)row * a.ntiles;
   const float* pv = a.part_val + base;
   const float* pv2 = a.part_val2 + base;
@@ -345,30 +350,29 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
   const uint4* hi = reinterpret_cast<const uint4*>(a.hf + (size_t)(2 * row) * a.d);
   const uint4* lo = reinterpret_cast<const uint4*>(a.hf + (size_t)(2 * row + 1) * a.d);
   const int nv = a.d / 8;
-  // every load of a phase issued before its first use (one warp per row, ~4 warps per SM: memory
-  // latency, not bandwidth, bounds this kernel)
-  float M = -INFINITY;
-  for (int t0 = 0; t0 < a.ntiles; t0 += 32 * 8) {
-    float v[8];
+  if (tid == 0) { s_n = 0; s_over = 0; }
+  // ---- phase 1: best hi score of the row, ||hi||, ||lo|| (all loads of a batch before any use)
+  float M = -INFINITY, sh = 0.f, sl = 0.f;
+  for (int t0 = 0; t0 < a.ntiles; t0 += 128 * 4) {
+    float v[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int t = t0 + lane + 32 * i;
+    for (int i = 0; i < 4; ++i) {
+      const int t = t0 + tid + 128 * i;
       v[i] = t < a.ntiles ? __ldg(pv + t) : -INFINITY;
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) M = fmaxf(M, v[i]);
+    for (int i = 0; i < 4; ++i) M = fmaxf(M, v[i]);
   }
-  float sh = 0.f, sl = 0.f;
-  for (int e0 = 0; e0 < nv; e0 += 32 * 4) {
-    uint4 h[4], l[4];
+  for (int e0 = 0; e0 < nv; e0 += 128 * 2) {
+    uint4 h[2], l[2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int e = e0 + lane + 32 * i;
+    for (int i = 0; i < 2; ++i) {
+      const int e = e0 + tid + 128 * i;
       h[i] = e < nv ? __ldg(hi + e) : make_uint4(0u, 0u, 0u, 0u);
       l[i] = e < nv ? __ldg(lo + e) : make_uint4(0u, 0u, 0u, 0u);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 2; ++i) {
       const uint32_t hw[4] = {h[i].x, h[i].y, h[i].z, h[i].w}, lw[4] = {l[i].x, l[i].y, l[i].z, l[i].w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -384,6 +388,11 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
     sh += __shfl_xor_sync(0xffffffffu, sh, o);
     sl += __shfl_xor_sync(0xffffffffu, sl, o);
   }
+  if (lane == 0) { s_red[0][w] = M; s_red[1][w] = sh; s_red[2][w] = sl; }
+  __syncthreads();
+  M = -INFINITY; sh = 0.f; sl = 0.f;
+#pragma unroll
+  for (int i = 0; i < kRefineWarps; ++i) { M = fmaxf(M, s_red[0][i]); sh += s_red[1][i]; sl += s_red[2][i]; }
   // |score_hi(v) - score(v)| <= (||lo|| + rho) wmax scale, rho = d 2^-24 (||hi|| + ||lo||) bounds
   // the fp32 accumulation error of either evaluation; + a few ulps of |M| for the final rounding
   const float nh = sqrtf(sh) * 1.0001f, nl = sqrtf(sl) * 1.0001f;
@@ -391,24 +400,42 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
   const float rho = (float)a.d * 5.9604645e-08f * (nh + nl);
   const float win = 2.f * (nl + rho) * a.wmax * scale + 8.f * 1.1920929e-07f * fabsf(M) + 1e-6f;
   const float thr = M - win;
+  // ---- phase 2: gather the candidates (a tile's best / second, or all of a tile whose third
+  // score is inside the window)
+  auto push = [&](int v) {
+    const int at = atomicAdd(&s_n, 1);
+    if (at < kRefineList) s_list[at] = v;
+    else s_over = 1;
+  };
+  for (int t = tid; t < a.ntiles; t += kRefineWarps * 32) {
+    if (__ldg(pv + t) < thr) continue;
+    if (__ldg(pv3 + t) >= thr) {
+      const int v1 = min(a.vocab, (t + 1) * 128);
+      for (int v = t * 128; v < v1; ++v) push(v);
+    } else {
+      push(__ldg(a.part_idx + base + t) - a.vocab_off);
+      if (__ldg(pv2 + t) >= thr) push(__ldg(a.part_idx2 + base + t) - a.vocab_off);
+    }
+  }
+  __syncthreads();
+  const int n = min(s_n, kRefineList);
+  const bool over = s_over != 0;
+  // ---- phase 3: exact (hi + lo) . W_v (+ Gumbel) of the candidates, kRefineBatch rows of W per pass
   const int req = a.row_req[row];
   const uint64_t ses = a.req_session[req];
   const uint32_t k0 = a.seed_lo ^ a.req_round[req], slot = (uint32_t)a.row_slot[row];
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  int n = 0;   // candidates in the list (warp-uniform)
-  // rescore list[0..n): exact (hi + lo) . W_v (+ Gumbel), kRefineBatch rows of W at a time
-  auto flush = [&]() {
-    for (int c0 = 0; c0 < n; c0 += kRefineBatch) {
+  auto rescore = [&](auto id_of, int cnt, int c_begin, int c_step) {
+    for (int c0 = c_begin * kRefineBatch; c0 < cnt; c0 += c_step * kRefineBatch) {
       const uint4* wr[kRefineBatch];
       float acc[kRefineBatch];
 #pragma unroll
-      for (int b = 0; b < kRefineBatch; ++b) {
-        wr[b] = reinterpret_cast<const uint4*>(a.w + (size_t)list[min(c0 + b, n - 1)] * a.d);
-        acc[b] = 0.f;
+      for (int bb = 0; bb < kRefineBatch; ++bb) {
+        wr[bb] = reinterpret_cast<const uint4*>(a.w + (size_t)id_of(min(c0 + bb, cnt - 1)) * a.d);
+        acc[bb] = 0.f;
       }
       for (int e0 = 0; e0 < nv; e0 += 64) {
-        // two iterations' loads (2 x (hi, lo, 4 W rows)) in flight before any use
         uint4 hh[2], ll[2], ww[2][kRefineBatch];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -417,32 +444,31 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
           hh[i] = ok ? __ldg(hi + e) : make_uint4(0u, 0u, 0u, 0u);
           ll[i] = ok ? __ldg(lo + e) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-          for (int b = 0; b < kRefineBatch; ++b) ww[i][b] = ok ? __ldg(wr[b] + e) : make_uint4(0u, 0u, 0u, 0u);
+          for (int bb = 0; bb < kRefineBatch; ++bb) ww[i][bb] = ok ? __ldg(wr[bb] + e) : make_uint4(0u, 0u, 0u, 0u);
         }
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-        const uint4 h = hh[i], l = ll[i];
-        const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+          const uint32_t hw[4] = {hh[i].x, hh[i].y, hh[i].z, hh[i].w}, lw[4] = {ll[i].x, ll[i].y, ll[i].z, ll[i].w};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          // hi + lo is exact in fp32 (bf16 + bf16 below half an ulp of hi)
-          const float y0 = __uint_as_float(hw[k] << 16) + __uint_as_float(lw[k] << 16);
-          const float y1 = __uint_as_float(hw[k] & 0xFFFF0000u) + __uint_as_float(lw[k] & 0xFFFF0000u);
+          for (int k = 0; k < 4; ++k) {
+            // hi + lo is exact in fp32 (bf16 + bf16 below half an ulp of hi)
+            const float y0 = __uint_as_float(hw[k] << 16) + __uint_as_float(lw[k] << 16);
+            const float y1 = __uint_as_float(hw[k] & 0xFFFF0000u) + __uint_as_float(lw[k] & 0xFFFF0000u);
 #pragma unroll
-          for (int b = 0; b < kRefineBatch; ++b) {
-            const uint32_t wv = k == 0 ? ww[i][b].x : (k == 1 ? ww[i][b].y : (k == 2 ? ww[i][b].z : ww[i][b].w));
-            acc[b] = fmaf(y0, __uint_as_float(wv << 16), acc[b]);
-            acc[b] = fmaf(y1, __uint_as_float(wv & 0xFFFF0000u), acc[b]);
+            for (int bb = 0; bb < kRefineBatch; ++bb) {
+              const uint32_t wv = k == 0 ? ww[i][bb].x : (k == 1 ? ww[i][bb].y : (k == 2 ? ww[i][bb].z : ww[i][bb].w));
+              acc[bb] = fmaf(y0, __uint_as_float(wv << 16), acc[bb]);
+              acc[bb] = fmaf(y1, __uint_as_float(wv & 0xFFFF0000u), acc[bb]);
+            }
           }
-        }
         }
       }
 #pragma unroll
-      for (int b = 0; b < kRefineBatch; ++b) {
-        float v = acc[b];
+      for (int bb = 0; bb < kRefineBatch; ++bb) {
+        float v = acc[bb];
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (c0 + b >= n) continue;
-        const int vg = a.vocab_off + list[c0 + b];
+        if (c0 + bb >= cnt) continue;
+        const int vg = a.vocab_off + id_of(c0 + bb);
         if (a.sample) {
           const U4 r = philox4x32_10(U4{(uint32_t)vg >> 2, slot, (uint32_t)ses, (uint32_t)(ses >> 32)}, k0, a.seed_hi);
           v = v * a.inv_t + gumbel_of_word(u4_word(r, vg & 3));
@@ -450,32 +476,22 @@ __global__ void __launch_bounds__(128) k_lm_refine(const __grid_constant__ Refin
         if (v > best || (v == best && vg < bi)) { best = v; bi = vg; }
       }
     }
-    __syncwarp();
-    n = 0;
   };
-  auto push = [&](int v) {   // warp-uniform call
-    if (n == kRefineList) flush();
-    if (lane == 0) list[n] = v;
-    __syncwarp();
-    ++n;
-  };
-  for (int t0 = 0; t0 < a.ntiles; t0 += 32) {
-    const int t = t0 + lane;
-    unsigned bal = __ballot_sync(0xffffffffu, t < a.ntiles && __ldg(pv + t) >= thr);
-    while (bal) {
-      const int tt = t0 + __ffs(bal) - 1;
-      bal &= bal - 1;
-      if (__ldg(pv3 + tt) >= thr) {   // a third id of this tile may win: every id of the tile
-        const int v1 = min(a.vocab, (tt + 1) * 128);
-        for (int v = tt * 128; v < v1; ++v) push(v);
-      } else {
-        push(__ldg(a.part_idx + base + tt) - a.vocab_off);
-        if (__ldg(pv2 + tt) >= thr) push(__ldg(a.part_idx2 + base + tt) - a.vocab_off);
-      }
+  rescore([&](int c) { return s_list[c]; }, n, w, kRefineWarps);
+  if (over && w == 0) {
+    // more than kRefineList candidates (only when whole tiles pile up): warp 0 rescores every id of
+    // every tile inside the window; duplicates of the list are harmless (same score, same id)
+    for (int t = 0; t < a.ntiles; ++t) {
+      if (__ldg(pv + t) < thr) continue;
+      const int v0 = t * 128, cnt = min(a.vocab, v0 + 128) - v0;
+      rescore([&](int c) { return v0 + c; }, cnt, 0, 1);
     }
   }
-  flush();
-  if (lane == 0) {
+  if (lane == 0) { s_best[w] = best; s_bi[w] = bi; }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 1; i < kRefineWarps; ++i)
+      if (s_best[i] > best || (s_best[i] == best && s_bi[i] < bi)) { best = s_best[i]; bi = s_bi[i]; }
     a.y[row] = bi;
     a.score[row] = best;
     if (a.row_target) a.row_target[row] = bi;
@@ -800,7 +816,7 @@ cudaError_t lm_reduce_launch(const float* pv, const int* pi, int R, int ntiles, 
 }
 cudaError_t lm_refine_launch(const RefineArgs& a, cudaStream_t st, int* launches) {
   if (launches) ++*launches;
-  CK_RET(launch_k(k_lm_refine, dim3((a.R + 3) / 4), dim3(128), 0, st, a));
+  CK_RET(launch_k(k_lm_refine, dim3(a.R), dim3(kRefineWarps * 32), 0, st, a));
   return cudaGetLastError();
 }
 cudaError_t row_norm_max_launch(const bf16* w, int rows, int d, float* out, cudaStream_t st) {
