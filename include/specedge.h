@@ -147,6 +147,13 @@ specedge_status specedge_model_tp_info(const specedge_model* model, int32_t* tp_
  * E_CUDA: allocation / IPC / NCCL failure (the model stays on the NCCL path).  Synchronous;
  * `stream` carries the handle all-gather. */
 specedge_status specedge_tp_fused_enable(specedge_model* model, int32_t max_rows, void* stream);
+/* The reduce-scatter path in effect: 0 NCCL (fused path off), 1 push (epilogue bulk copies into the
+ * owners' receive slots), 2 pull (SPECEDGE_TP_F4=pull: the owner's RMSNorm loads every rank's rows),
+ * 3 NVLS (SPECEDGE_TP_F4=nvls: every rank's partial lives in its own buffer bound to one CUDA
+ * multicast object; the owner's RMSNorm loads the rank sum with multimem.ld_reduce, reduced in
+ * the NVSwitch).  NVLS falls back to push, on every rank, when the multicast object cannot be set
+ * up (no multicast support, file-descriptor exchange refused).  Host only. */
+int32_t specedge_tp_fused_mode(const specedge_model* model);
 
 /* KV page pool of `num_pages` pages x 64 tokens x all layers (fp16 K and V), zero-initialised,
  * with room for `max_handles` sessions.  Synchronous. */

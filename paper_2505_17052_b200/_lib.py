@@ -30,7 +30,7 @@ EXPORTS = [
     "specedge_model_tp_info", "specedge_calibrate_draft_depth", "specedge_scheduler_create",
     "specedge_scheduler_destroy", "specedge_scheduler_admit", "specedge_scheduler_plan",
     "specedge_scheduler_complete", "specedge_scheduler_observe", "specedge_scheduler_state",
-    "specedge_draft_tree", "specedge_tp_fused_enable", "specedge_graph_stats",
+    "specedge_draft_tree", "specedge_tp_fused_enable", "specedge_graph_stats", "specedge_tp_fused_mode",
 ]
 KERNEL_KINDS = ["prep", "embed", "rmsnorm", "gemm_qkv", "attention", "attn_combine", "gemm_o", "gemm_gateup",
                 "gemm_down", "gemm_lmhead", "lm_reduce", "walk", "commit", "qkv_rope"]
@@ -103,6 +103,7 @@ def load(path: str = LIB_PATH):
         "specedge_debug_attention": [P, P, P, P, P, P, I32, I32, I32, I32, I32, P, P, SZ, P],
         "specedge_last_launch_count": [],
         "specedge_graph_stats": [P, P, I32],
+        "specedge_tp_fused_mode": [P],
         "specedge_set_kernel_timing": [I32],
         "specedge_kernel_times": [P, P, I32],
         "specedge_tp_unique_id": [P],

@@ -87,6 +87,10 @@ class Model:
         reduce-scatter of their fp32 updates over NVLink peer memory (specedge_tp_fused_enable)."""
         L.check(self.lib.specedge_tp_fused_enable(self.h, max_rows, _stream(stream)), "tp_fused_enable")
 
+    def tp_fused_mode(self) -> str:
+        """The reduce-scatter path in effect (include/specedge.h specedge_tp_fused_mode)."""
+        return {0: "nccl", 1: "push", 2: "pull", 3: "nvls"}[int(self.lib.specedge_tp_fused_mode(self.h))]
+
     def close(self):
         if self.h:
             self.lib.specedge_model_destroy(self.h)

@@ -80,6 +80,7 @@ enum GemmMode : int {
 
 constexpr int kMaxFusedTp = 8;   // NEXT-F4: ranks of the fused GEMM -> reduce-scatter (a box's 8 GPUs)
 struct RmsSrc {                  // NEXT-F4: per-partial base pointers for k_rmsnorm (p[0] == null: unused)
+  const float* mc;               // NVLS: multicast address of this rank's rows (the rank sum is loaded)
   const float* p[kMaxFusedTp];
   bf16* outp[kMaxFusedTp];       // NEXT-F4 all-gather: the normalised row also goes to every rank
   int nout;                      // (split == 0 only); 0: unused
@@ -386,6 +387,8 @@ int tp_fused_enable(specedge_model* m, int max_rows, cudaStream_t st);
 cudaError_t tp_fused_signal(specedge_model* m, cudaStream_t st, int* launches);
 cudaError_t tp_fused_wait(specedge_model* m, cudaStream_t st, int* launches);
 void tp_fused_close(specedge_model* m);
+int tp_nvls_enable(specedge_model* m, int max_rows, cudaStream_t st);
+void tp_nvls_close(specedge_model* m);
 int tp_unique_id(uint8_t* out128);
 int tp_comm_init(void** comm, const uint8_t* id128, int rank, int size);
 void tp_comm_destroy(void* comm);
@@ -415,6 +418,14 @@ struct specedge_model {
   // NEXT-F4 (tp.cu): this rank's row-parallel GEMM output [R_max][d] fp32 + flag words [tp],
   // the peers' mappings of theirs, the epoch of the last signalled collective
   int tp_fused_rows = 0;                 // capacity (rows); 0 = fused path off
+  // NEXT-F4 NVLS variant (SPECEDGE_TP_F4=nvls): one multicast object over all ranks' [2][R_max][d]
+  // fp32 partial buffers; the row-parallel GEMM stores into its own unicast mapping, the owner's
+  // RMSNorm reads the rank sum with multimem.ld_reduce through the multicast mapping
+  bool tp_nvls = false;
+  float* tp_nvls_uc = nullptr;           // this rank's physical buffer (unicast VA)
+  float* tp_nvls_mc = nullptr;           // the multicast VA (reads reduce over every rank)
+  size_t tp_nvls_bytes = 0, tp_nvls_buf = 0;   // mapped size, floats per half
+  unsigned long long tp_nvls_mem = 0, tp_nvls_mch = 0;   // CUmemGenericAllocationHandle x2
   float* tp_recv = nullptr;              // pull: [R_max][d]; push: [2][tp][ceil(R_max/tp)][d]
   size_t tp_fused_slot = 0;              // push: floats per [src] slot
   se::bf16* tp_hn = nullptr;             // all-gathered normalised rows [R_max][d] (this rank's copy)

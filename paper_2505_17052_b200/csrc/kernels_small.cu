@@ -165,10 +165,22 @@ __global__ void __launch_bounds__(1024) k_rmsnorm(float* __restrict__ X, const f
 #pragma unroll
     for (int s = 0; s < NY; ++s)
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        yv[s][k] = own[k] ? __ldcs(reinterpret_cast<const float4*>((ys.p[0] ? ys.p[s] : Y + s * y_stride) +
-                                                                    (size_t)row * d + 4 * (t + T * k)))
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k = 0; k < 4; ++k) {
+        if (!own[k]) {
+          yv[s][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else if (NY == 1 && ys.mc) {   // NVLS: the sum over all ranks' partials, reduced in the switch
+          const float* pm = ys.mc + (size_t)row * d + 4 * (t + T * k);
+          float4 v;
+          asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                       : "l"(pm)
+                       : "memory");
+          yv[s][k] = v;
+        } else {
+          yv[s][k] = __ldcs(reinterpret_cast<const float4*>((ys.p[0] ? ys.p[s] : Y + s * y_stride) + (size_t)row * d +
+                                                            4 * (t + T * k)));
+        }
+      }
 #pragma unroll
     for (int s = 0; s < NY; ++s)
 #pragma unroll

@@ -382,6 +382,7 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   static const bool f4_pull = getenv("SPECEDGE_TP_F4") && std::string(getenv("SPECEDGE_TP_F4")) == "pull";
   bool fused_pending = false;   // a row-parallel partial is waiting in the ranks' buffers
   const float* push_src = nullptr;   // push: the receive buffer holding this rank's tp slots
+  const float* nvls_src = nullptr;   // NVLS: multicast address of the pending partial (all rows)
   auto f32_gemm_fused = [&](int kind, const CUtensorMap& tm, const void* Xin, int Mrows, int K) -> int {
     GemmArgs g{};
     g.M = Mrows;
@@ -391,7 +392,13 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     g.ldo = Mrows;
     g.max_splits = 1;
     g.split_stride = 0;
-    if (!f4_pull) {
+    if (m->tp_nvls) {
+      // NVLS: the partial goes to this rank's own half of the multicast-bound buffer
+      const size_t boff = (size_t)m->tp_fused_buf * m->tp_nvls_buf;
+      g.out_f32 = m->tp_nvls_uc + boff;
+      nvls_src = m->tp_nvls_mc + boff;
+      m->tp_fused_buf ^= 1;
+    } else if (!f4_pull) {
       const size_t boff = (size_t)m->tp_fused_buf * m->tp_size * m->tp_fused_slot;
       g.push = 1;
       g.tp_src = m->tp_rank;
@@ -420,7 +427,12 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     const bool ag_fused = fused && f4_ag && !split;
     const bool partial = fused_pending;
     RmsSrc ys{};
-    if (partial) {   // this rank's rows of every rank's partial, summed in rank order
+    int nYf = nY;
+    if (partial && nvls_src) {   // NVLS: the rank sum of this rank's rows in one multimem load
+      CK(tp_fused_wait(m, st, &launches));
+      ys.mc = nvls_src + (size_t)r0 * c.d;
+      nYf = 1;
+    } else if (partial) {   // this rank's rows of every rank's partial, summed in rank order
       CK(tp_fused_wait(m, st, &launches));
       for (int p = 0; p < m->tp_size; ++p)
         ys.p[p] = push_src ? push_src + (size_t)p * m->tp_fused_slot
@@ -434,12 +446,13 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     {
       KTimer _t(K_RMSNORM, st);
       if (nloc)
-        CK(rmsnorm_launch(X + (size_t)r0 * c.d, partial ? nullptr : Y + (size_t)r0 * c.d, nY, partial ? 0 : y_stride,
+        CK(rmsnorm_launch(X + (size_t)r0 * c.d, partial ? nullptr : Y + (size_t)r0 * c.d, nYf, partial ? 0 : y_stride,
                           gain, out + (size_t)(split ? 2 : 1) * r0 * c.d, nloc, c.d, c.eps, st, &launches, split,
                           (partial || ag_fused) ? &ys : nullptr));
     }
     fused_pending = false;
     push_src = nullptr;
+    nvls_src = nullptr;
     if (ag_fused) {
       CK(tp_fused_signal(m, st, &launches));
       CK(tp_fused_wait(m, st, &launches));
@@ -984,6 +997,13 @@ specedge_status specedge_tp_fused_enable(specedge_model* m, int32_t max_rows, vo
   if (r == -1 || r == -2) return SPECEDGE_E_INVALID;
   m->tp_fused_rows = 0;
   return SPECEDGE_E_CUDA;
+}
+
+int32_t specedge_tp_fused_mode(const specedge_model* m) {
+  if (!m || !m->tp_fused_rows) return 0;
+  if (m->tp_nvls) return 3;
+  static const bool f4_pull = getenv("SPECEDGE_TP_F4") && std::string(getenv("SPECEDGE_TP_F4")) == "pull";
+  return f4_pull ? 2 : 1;
 }
 
 specedge_status specedge_model_destroy(specedge_model* m) {

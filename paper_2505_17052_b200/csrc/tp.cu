@@ -10,10 +10,15 @@
 #include "internal.h"
 
 #include <dlfcn.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 namespace se {
@@ -276,10 +281,205 @@ int tp_fused_enable(specedge_model* m, int max_rows, cudaStream_t st) {
                   ncclSuccess;
   cudaStreamSynchronize(st);
   cudaFree(one);
-  return ok ? 0 : -5;
+  if (!ok) return -5;
+  // NVLS variant on request; any failure leaves the push path in place (collective decision)
+  static const bool want_nvls = getenv("SPECEDGE_TP_F4") && std::string(getenv("SPECEDGE_TP_F4")) == "nvls";
+  if (want_nvls) {
+    const int r = tp_nvls_enable(m, max_rows, st);
+    if (r != 0 && getenv("SPECEDGE_DEBUG")) fprintf(stderr, "libspecedge: NVLS setup failed (%d), push path kept\n", r);
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------------------------
+// NEXT-F4, NVLS variant (SPECEDGE_TP_F4=nvls).  One CUDA multicast object spans the ranks; every
+// rank binds its own physical [2][R_max][d] fp32 buffer to it and maps both the buffer (unicast:
+// its row-parallel GEMM stores its partial there) and the multicast object (its RMSNorm loads the
+// rank sum of its own rows with multimem.ld_reduce: the reduction happens in the NVSwitch, each
+// partial crosses NVLink once).  Rank 0 creates the object and exports a POSIX file descriptor; the
+// others duplicate it with pidfd_getfd (pid and fd travel through the NCCL communicator).  Buffer
+// halves alternate per collective exactly like the push variant's receive buffers.
+// ---------------------------------------------------------------------------------------------
+namespace {
+struct CuDrv {
+  bool tried = false, ok = false;
+  CUresult (*MulticastCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+  CUresult (*MulticastGetGranularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
+  CUresult (*MulticastAddDevice)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+  CUresult (*MulticastBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                               unsigned long long) = nullptr;
+  CUresult (*MulticastUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+  CUresult (*MemCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*MemRelease)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*MemAddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*MemAddressFree)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*MemMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*MemUnmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*MemSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*MemExportToShareableHandle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
+                                         unsigned long long) = nullptr;
+  CUresult (*MemImportFromShareableHandle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType) = nullptr;
+  CUresult (*DeviceGet)(CUdevice*, int) = nullptr;
+};
+CuDrv& drv() {
+  static CuDrv d;
+  if (d.tried) return d;
+  d.tried = true;
+  auto get = [](const char* name) -> void* {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return p;
+  };
+#define SE_DRV(f) d.f = reinterpret_cast<decltype(d.f)>(get("cu" #f))
+  SE_DRV(MulticastCreate);
+  SE_DRV(MulticastGetGranularity);
+  SE_DRV(MulticastAddDevice);
+  SE_DRV(MulticastBindMem);
+  SE_DRV(MulticastUnbind);
+  SE_DRV(MemCreate);
+  SE_DRV(MemRelease);
+  SE_DRV(MemAddressReserve);
+  SE_DRV(MemAddressFree);
+  SE_DRV(MemMap);
+  SE_DRV(MemUnmap);
+  SE_DRV(MemSetAccess);
+  SE_DRV(MemExportToShareableHandle);
+  SE_DRV(MemImportFromShareableHandle);
+  SE_DRV(DeviceGet);
+#undef SE_DRV
+  d.ok = d.MulticastCreate && d.MulticastGetGranularity && d.MulticastAddDevice && d.MulticastBindMem &&
+         d.MulticastUnbind && d.MemCreate && d.MemRelease && d.MemAddressReserve && d.MemAddressFree && d.MemMap &&
+         d.MemUnmap && d.MemSetAccess && d.MemExportToShareableHandle && d.MemImportFromShareableHandle && d.DeviceGet;
+  return d;
+}
+}  // namespace
+
+// Collective (every rank): returns 0, or < 0 with nothing mapped (the caller keeps the push path)
+int tp_nvls_enable(specedge_model* m, int max_rows, cudaStream_t st) {
+  CuDrv& D = drv();
+  if (!D.ok || !m->nccl) return -1;
+  const int tp = m->tp_size;
+  CUdevice dev;
+  if (D.DeviceGet(&dev, m->device) != CUDA_SUCCESS) return -1;
+  const size_t half = (size_t)max_rows * m->cfg.d;
+  CUmulticastObjectProp mp{};
+  mp.numDevices = (unsigned)tp;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t gran = 0;
+  mp.size = 2 * half * sizeof(float);
+  if (D.MulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !gran) return -1;
+  const size_t bytes = (mp.size + gran - 1) / gran * gran;
+  mp.size = bytes;
+  // rank 0 creates and exports; (pid, fd) of rank 0 reach every rank through the communicator
+  CUmemGenericAllocationHandle mc = 0;
+  long long info[2] = {0, -1};   // ranks != 0 contribute (0, -1) to the sum
+  int rc = 0;
+  int fd0 = -1;
+  if (m->tp_rank == 0) {
+    int& fd = fd0;
+    if (D.MulticastCreate(&mc, &mp) != CUDA_SUCCESS) rc = -2;
+    else if (D.MemExportToShareableHandle(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS) rc = -2;
+    info[0] = (long long)getpid();
+    info[1] = rc == 0 ? fd : -1;
+  }
+  long long* dinfo = nullptr;
+  if (cudaMalloc(&dinfo, sizeof(info)) != cudaSuccess) return -3;
+  cudaMemcpy(dinfo, info, sizeof(info), cudaMemcpyHostToDevice);
+  const bool bc = nccl().AllReduce(dinfo, dinfo, 2, ncclInt64, ncclSum, reinterpret_cast<ncclComm_t>(m->nccl), st) ==
+                  ncclSuccess;   // ranks != 0 contribute zeros
+  cudaStreamSynchronize(st);
+  cudaMemcpy(info, dinfo, sizeof(info), cudaMemcpyDeviceToHost);
+  cudaFree(dinfo);
+  info[1] += (tp - 1);   // the tp - 1 other ranks each contributed -1
+  if (!bc || info[1] < 0) return -4;
+  if (m->tp_rank != 0) {
+    const int pidfd = (int)syscall(SYS_pidfd_open, (pid_t)info[0], 0);
+    const int fd = pidfd >= 0 ? (int)syscall(SYS_pidfd_getfd, pidfd, (int)info[1], 0) : -1;
+    if (pidfd >= 0) close(pidfd);
+    if (fd < 0 || D.MemImportFromShareableHandle(&mc, (void*)(intptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) !=
+                      CUDA_SUCCESS)
+      rc = -5;
+    if (fd >= 0) close(fd);
+  }
+  if (rc == 0 && D.MulticastAddDevice(mc, dev) != CUDA_SUCCESS) rc = -6;
+  // every rank must have added its device before memory is bound: barrier, and agree on success
+  int* dok = nullptr;
+  if (cudaMalloc(&dok, sizeof(int)) != cudaSuccess) return -3;
+  const int fail = rc != 0 ? 1 : 0;
+  cudaMemcpy(dok, &fail, sizeof(int), cudaMemcpyHostToDevice);
+  nccl().AllReduce(dok, dok, 1, ncclInt32, ncclSum, reinterpret_cast<ncclComm_t>(m->nccl), st);
+  cudaStreamSynchronize(st);
+  int nfail = 1;
+  cudaMemcpy(&nfail, dok, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(dok);
+  if (fd0 >= 0) close(fd0);   // every rank holds its own reference now
+  if (nfail) return -7;
+  // this rank's physical memory, bound into the object and mapped twice
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = m->device;
+  CUmemGenericAllocationHandle mem = 0;
+  CUdeviceptr uva = 0, mva = 0;
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = m->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  bool ok = D.MemCreate(&mem, bytes, &ap, 0) == CUDA_SUCCESS;
+  ok = ok && D.MulticastBindMem(mc, 0, mem, 0, bytes, 0) == CUDA_SUCCESS;
+  ok = ok && D.MemAddressReserve(&uva, bytes, gran, 0, 0) == CUDA_SUCCESS;
+  ok = ok && D.MemMap(uva, bytes, 0, mem, 0) == CUDA_SUCCESS;
+  ok = ok && D.MemSetAccess(uva, bytes, &acc, 1) == CUDA_SUCCESS;
+  ok = ok && D.MemAddressReserve(&mva, bytes, gran, 0, 0) == CUDA_SUCCESS;
+  ok = ok && D.MemMap(mva, bytes, 0, mc, 0) == CUDA_SUCCESS;
+  ok = ok && D.MemSetAccess(mva, bytes, &acc, 1) == CUDA_SUCCESS;
+  // agree again (a rank that failed here leaves the others on the push path as well)
+  int* dok2 = nullptr;
+  cudaMalloc(&dok2, sizeof(int));
+  const int fail2 = ok ? 0 : 1;
+  cudaMemcpy(dok2, &fail2, sizeof(int), cudaMemcpyHostToDevice);
+  nccl().AllReduce(dok2, dok2, 1, ncclInt32, ncclSum, reinterpret_cast<ncclComm_t>(m->nccl), st);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(&nfail, dok2, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(dok2);
+  m->tp_nvls_mem = mem;
+  m->tp_nvls_mch = mc;
+  m->tp_nvls_uc = reinterpret_cast<float*>(uva);
+  m->tp_nvls_mc = reinterpret_cast<float*>(mva);
+  m->tp_nvls_bytes = bytes;
+  m->tp_nvls_buf = half;
+  if (nfail) {
+    tp_nvls_close(m);
+    return -8;
+  }
+  cudaMemset(m->tp_nvls_uc, 0, bytes);
+  cudaDeviceSynchronize();
+  m->tp_nvls = true;
+  return 0;
+}
+
+void tp_nvls_close(specedge_model* m) {
+  CuDrv& D = drv();
+  if (!D.ok) return;
+  cudaDeviceSynchronize();
+  const size_t bytes = m->tp_nvls_bytes;
+  if (m->tp_nvls_mc) D.MemUnmap(reinterpret_cast<CUdeviceptr>(m->tp_nvls_mc), bytes);
+  if (m->tp_nvls_uc) D.MemUnmap(reinterpret_cast<CUdeviceptr>(m->tp_nvls_uc), bytes);
+  if (m->tp_nvls_mc) D.MemAddressFree(reinterpret_cast<CUdeviceptr>(m->tp_nvls_mc), bytes);
+  if (m->tp_nvls_uc) D.MemAddressFree(reinterpret_cast<CUdeviceptr>(m->tp_nvls_uc), bytes);
+  CUdevice dev;
+  if (m->tp_nvls_mch && D.DeviceGet(&dev, m->device) == CUDA_SUCCESS) D.MulticastUnbind(m->tp_nvls_mch, dev, 0, bytes);
+  if (m->tp_nvls_mem) D.MemRelease(m->tp_nvls_mem);
+  if (m->tp_nvls_mch) D.MemRelease(m->tp_nvls_mch);
+  m->tp_nvls_mc = m->tp_nvls_uc = nullptr;
+  m->tp_nvls_mem = m->tp_nvls_mch = 0;
+  m->tp_nvls = false;
 }
 
 void tp_fused_close(specedge_model* m) {
+  if (m->tp_nvls_bytes) tp_nvls_close(m);
   for (void* q : m->tp_ipc_opened) cudaIpcCloseMemHandle(q);
   m->tp_ipc_opened.clear();
 }

@@ -58,8 +58,9 @@ def _worker(rank, tp, nccl_id, mode, temperature, q, fused=False):
         from paper_2505_17052_b200 import api
         shape, W, prompts, sessions, trees = _setup()
         model = api.Model(shape, SEED, device=rank, max_position=4096, tp_rank=rank, tp_size=tp, nccl_id=nccl_id)
-        if fused:   # NEXT-F4: O / down GEMM epilogues store straight into the owner's receive slots
+        if fused:   # NEXT-F4: "push" (epilogue bulk copies into the owners' receive slots) or "nvls"
             model.tp_fused_enable(4 * 65)
+            assert model.tp_fused_mode() == fused, model.tp_fused_mode()
         cap = max(len(p) for p in prompts) + 256
         pool = api.KVPool(model, ((cap + 63) // 64) * len(prompts) + 4, len(prompts) + 4)
         B = len(prompts)
@@ -99,6 +100,10 @@ def _run_tp(tp, mode, temperature, fused=False):
     import torch.multiprocessing as mp
     from paper_2505_17052_b200 import api
     nccl_id = api.tp_unique_id()
+    if fused == "nvls":   # read by the spawned workers' library at tp_fused_enable
+        os.environ["SPECEDGE_TP_F4"] = "nvls"
+    else:
+        os.environ.pop("SPECEDGE_TP_F4", None)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, tp, nccl_id, mode, temperature, q, fused)) for r in range(tp)]
@@ -117,9 +122,11 @@ def _run_tp(tp, mode, temperature, fused=False):
 
 @pytest.mark.parametrize("tp", [2, 4, 8])
 @pytest.mark.parametrize("mode,temperature,fused", [("greedy", 0.0, False), ("sample", 1.0, False),
-                                                   ("greedy", 0.0, True), ("sample", 1.0, True)])
+                                                   ("greedy", 0.0, "push"), ("sample", 1.0, "push"),
+                                                   ("greedy", 0.0, "nvls"), ("sample", 1.0, "nvls")])
 def test_tp_verify_matches_oracle(tp, mode, temperature, fused):
-    """fused: NEXT-F4 GEMM -> reduce-scatter over NVLink peer memory instead of NCCL for C1/C2."""
+    """fused: NEXT-F4 GEMM -> reduce-scatter over NVLink peer memory ("push") or through an NVLS
+    multicast object with in-switch reduction ("nvls") instead of NCCL for C1/C2."""
     _needs_gpus(tp)
     os.environ.setdefault("NCCL_DEBUG", "WARN")
     res = _run_tp(tp, mode, temperature, fused)
