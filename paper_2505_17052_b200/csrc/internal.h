@@ -426,6 +426,7 @@ struct specedge_model {
   float* tp_nvls_mc = nullptr;           // the multicast VA (reads reduce over every rank)
   size_t tp_nvls_bytes = 0, tp_nvls_buf = 0;   // mapped size, floats per half
   unsigned long long tp_nvls_mem = 0, tp_nvls_mch = 0;   // CUmemGenericAllocationHandle x2
+  bool tp_nvls_bound = false;
   float* tp_recv = nullptr;              // pull: [R_max][d]; push: [2][tp][ceil(R_max/tp)][d]
   size_t tp_fused_slot = 0;              // push: floats per [src] slot
   se::bf16* tp_hn = nullptr;             // all-gathered normalised rows [R_max][d] (this rank's copy)

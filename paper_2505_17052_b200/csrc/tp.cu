@@ -358,7 +358,10 @@ CuDrv& drv() {
 
 // Collective (every rank): returns 0, or < 0 with nothing mapped (the caller keeps the push path)
 int tp_nvls_enable(specedge_model* m, int max_rows, cudaStream_t st) {
+  static const bool dbg = getenv("SPECEDGE_DEBUG") != nullptr;
+#define NVLS_STEP(msg) do { if (dbg) { fprintf(stderr, "[nvls rank %d] %s\n", m->tp_rank, msg); fflush(stderr); } } while (0)
   CuDrv& D = drv();
+  NVLS_STEP(D.ok ? "driver entry points ok" : "driver entry points missing");
   if (!D.ok || !m->nccl) return -1;
   const int tp = m->tp_size;
   CUdevice dev;
@@ -387,6 +390,7 @@ int tp_nvls_enable(specedge_model* m, int max_rows, cudaStream_t st) {
   long long* dinfo = nullptr;
   if (cudaMalloc(&dinfo, sizeof(info)) != cudaSuccess) return -3;
   cudaMemcpy(dinfo, info, sizeof(info), cudaMemcpyHostToDevice);
+  NVLS_STEP("created / exported; exchanging (pid, fd)");
   const bool bc = nccl().AllReduce(dinfo, dinfo, 2, ncclInt64, ncclSum, reinterpret_cast<ncclComm_t>(m->nccl), st) ==
                   ncclSuccess;   // ranks != 0 contribute zeros
   cudaStreamSynchronize(st);
@@ -403,7 +407,9 @@ int tp_nvls_enable(specedge_model* m, int max_rows, cudaStream_t st) {
       rc = -5;
     if (fd >= 0) close(fd);
   }
+  NVLS_STEP(rc == 0 ? "imported" : "import failed");
   if (rc == 0 && D.MulticastAddDevice(mc, dev) != CUDA_SUCCESS) rc = -6;
+  NVLS_STEP(rc == 0 ? "device added" : "add device failed");
   // every rank must have added its device before memory is bound: barrier, and agree on success
   int* dok = nullptr;
   if (cudaMalloc(&dok, sizeof(int)) != cudaSuccess) return -3;
@@ -421,14 +427,22 @@ int tp_nvls_enable(specedge_model* m, int max_rows, cudaStream_t st) {
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = m->device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;   // as the multicast object's
   CUmemGenericAllocationHandle mem = 0;
   CUdeviceptr uva = 0, mva = 0;
   CUmemAccessDesc acc{};
   acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   acc.location.id = m->device;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  bool ok = D.MemCreate(&mem, bytes, &ap, 0) == CUDA_SUCCESS;
-  ok = ok && D.MulticastBindMem(mc, 0, mem, 0, bytes, 0) == CUDA_SUCCESS;
+  CUresult cr = D.MemCreate(&mem, bytes, &ap, 0);
+  bool ok = cr == CUDA_SUCCESS;
+  if (dbg) fprintf(stderr, "[nvls rank %d] cuMemCreate(%zu) -> %d\n", m->tp_rank, bytes, (int)cr);
+  bool bound = false;
+  if (ok) {
+    cr = D.MulticastBindMem(mc, 0, mem, 0, bytes, 0);
+    bound = ok = cr == CUDA_SUCCESS;
+    if (dbg) fprintf(stderr, "[nvls rank %d] cuMulticastBindMem -> %d (gran %zu)\n", m->tp_rank, (int)cr, gran);
+  }
   ok = ok && D.MemAddressReserve(&uva, bytes, gran, 0, 0) == CUDA_SUCCESS;
   ok = ok && D.MemMap(uva, bytes, 0, mem, 0) == CUDA_SUCCESS;
   ok = ok && D.MemSetAccess(uva, bytes, &acc, 1) == CUDA_SUCCESS;
@@ -450,6 +464,7 @@ int tp_nvls_enable(specedge_model* m, int max_rows, cudaStream_t st) {
   m->tp_nvls_mc = reinterpret_cast<float*>(mva);
   m->tp_nvls_bytes = bytes;
   m->tp_nvls_buf = half;
+  m->tp_nvls_bound = bound;
   if (nfail) {
     tp_nvls_close(m);
     return -8;
@@ -457,6 +472,8 @@ int tp_nvls_enable(specedge_model* m, int max_rows, cudaStream_t st) {
   cudaMemset(m->tp_nvls_uc, 0, bytes);
   cudaDeviceSynchronize();
   m->tp_nvls = true;
+  NVLS_STEP("mapped: NVLS on");
+#undef NVLS_STEP
   return 0;
 }
 
@@ -470,7 +487,8 @@ void tp_nvls_close(specedge_model* m) {
   if (m->tp_nvls_mc) D.MemAddressFree(reinterpret_cast<CUdeviceptr>(m->tp_nvls_mc), bytes);
   if (m->tp_nvls_uc) D.MemAddressFree(reinterpret_cast<CUdeviceptr>(m->tp_nvls_uc), bytes);
   CUdevice dev;
-  if (m->tp_nvls_mch && D.DeviceGet(&dev, m->device) == CUDA_SUCCESS) D.MulticastUnbind(m->tp_nvls_mch, dev, 0, bytes);
+  if (m->tp_nvls_bound && D.DeviceGet(&dev, m->device) == CUDA_SUCCESS) D.MulticastUnbind(m->tp_nvls_mch, dev, 0, bytes);
+  m->tp_nvls_bound = false;
   if (m->tp_nvls_mem) D.MemRelease(m->tp_nvls_mem);
   if (m->tp_nvls_mch) D.MemRelease(m->tp_nvls_mch);
   m->tp_nvls_mc = m->tp_nvls_uc = nullptr;
