@@ -24,10 +24,18 @@ namespace se {
 
 namespace {
 
-constexpr int kThreads = 192;          // warp0 TMA, warp1 MMA + TMEM alloc, warps2-5 epilogue
-constexpr int kEpiThreads = 128;
+// warp 0 TMA, warp 1 MMA + TMEM alloc, warps 2..9 epilogue in kEpiGroups groups of four warps
+// (one per TMEM lane quarter each): group g takes the accumulator's 32-column chunks c = g mod 2,
+// with its own exchange / reduction buffers and named barrier 1 + g, so a tile's epilogue (the
+// unoverlapped tail of every GEMM launch) runs on twice the warps
+constexpr int kEpiGroups = 2;
+constexpr int kEpiThreads = 128;        // per group
+constexpr int kThreads = 64 + kEpiGroups * kEpiThreads;
+constexpr uint32_t kXchBytes = 128 * 33 * 4;
+constexpr uint32_t kRedBytes = 4 * 32 * 24;
 constexpr uint32_t kABytes = 128 * 128;  // 128 rows x 64 bf16
 constexpr int kXchStride = 33;
+
 
 struct SmemLayout {
   uint32_t a_off, b_off, xch_off, red_off, bar_off, total;
@@ -37,10 +45,11 @@ __host__ __device__ inline SmemLayout smem_layout(int stages, int BN) {
   SmemLayout L;
   L.a_off = 0;
   L.b_off = L.a_off + stages * kABytes;
-  L.xch_off = L.b_off + stages * (uint32_t)BN * 128u;
-  L.red_off = L.xch_off + 128 * kXchStride * 4;
-  L.bar_off = L.red_off + 4 * 32 * 24;   // red_v, red_i [128]; top2: red_s2, red_i2 at +256, red_s3 at +512;
-                                         // noise row inputs at +640 (128 words)
+  L.xch_off = L.b_off + stages * (uint32_t)BN * 128u;   // [kEpiGroups][kXchBytes]
+  L.red_off = L.xch_off + kEpiGroups * kXchBytes;          // [kEpiGroups][kRedBytes]: red_v, red_i [128];
+                                                           // top2: red_s2, red_i2 at +256, red_s3 at +512;
+                                                           // noise row inputs at +640 (128 words)
+  L.bar_off = L.red_off + kEpiGroups * kRedBytes;
   L.total = L.bar_off + (2 * stages + 4) * 8 + 16;
   return L;
 }
@@ -51,7 +60,8 @@ __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g));
 // for feature = m128*128 + tl (tl = TMEM lane) and row = row_base + j, j < ncol.
 template <int MODE>
 __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)[32], int m128, int tl, int et,
-                                          int row_base, int ncol, int sk, float* xch, float* red_v, int* red_i) {
+                                          int row_base, int ncol, int sk, float* xch, float* red_v, int* red_i,
+                                          int bar) {
     const int feat = m128 * 128 + tl;
     if constexpr (MODE == EPI_F32) {
       if (a.push) {
@@ -62,7 +72,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         // the tile's features below M.
         for (int j = 0; j < 32; ++j) xch[j * 128 + tl] = feat < a.M ? __uint_as_float(v[j]) : 0.f;
         fence_proxy_async_smem();
-        named_bar_sync(1, kEpiThreads);
+        named_bar_sync(bar, kEpiThreads);
         const uint32_t nbytes = (uint32_t)min(128, a.M - m128 * 128) * 4u;
         if ((et & 31) == 0) {   // one issuing lane per epilogue warp, 8 rows each
           for (int j = (et >> 5) * 8; j < min(ncol, (et >> 5) * 8 + 8); ++j) {
@@ -76,7 +86,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           bulk_commit();
           bulk_wait_read0();   // the staging buffer may be overwritten
         }
-        named_bar_sync(1, kEpiThreads);
+        named_bar_sync(bar, kEpiThreads);
       } else if (feat < a.M) {
         if (a.pair) {   // physical rows 2r, 2r+1 hold hi/lo parts of logical row r
 #pragma unroll
@@ -107,7 +117,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
       // tile rows: lanes 0..63 = gate features m*64 + i, lanes 64..127 = up features
 #pragma unroll
       for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
-      named_bar_sync(1, kEpiThreads);
+      named_bar_sync(bar, kEpiThreads);
       const int f = et & 63, half = et >> 6;
       const int fo = m128 * 64 + f;
 #pragma unroll
@@ -119,7 +129,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           a.out_bf16[(size_t)row * a.ld_out + fo] = __float2bfloat16_rn(silu_f(g) * u);
         }
       }
-      named_bar_sync(1, kEpiThreads);
+      named_bar_sync(bar, kEpiThreads);
     } else if constexpr (MODE == EPI_QKV) {
       // 128-feature tile m128 = one head (head_dim 128): q heads [0, H), k heads [H, H+KV), v
       // heads after.  q / k: rotate-half RoPE at row_pos (pairs (i, i+64) sit in lanes i and
@@ -140,7 +150,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
-        named_bar_sync(1, kEpiThreads);
+        named_bar_sync(bar, kEpiThreads);
         const int f = et & 63, hsel = et >> 6;   // pair (f, f + 64), rows [16 hsel, 16 hsel + 16)
         f16* const base = head < H ? Qo + (size_t)head * 128
                                    : kv + (((size_t)a.layer * 2 + 0) * KV + (head - H)) * a.R_cap * 128;
@@ -168,7 +178,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           dst[f] = __float2half_rn(x1 * cs[jj] - x2 * sn[jj]);
           dst[f + 64] = __float2half_rn(x2 * cs[jj] + x1 * sn[jj]);
         }
-        named_bar_sync(1, kEpiThreads);
+        named_bar_sync(bar, kEpiThreads);
       }
     } else if constexpr (MODE == EPI_ARGMAX || MODE == EPI_PQ1 || MODE == EPI_PQ2) {
       // the CTA pair's second 128-feature half past the last vocab tile (an odd tile count, e.g.
@@ -211,7 +221,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           rinfo[4 * et + 2] = (uint32_t)(ses >> 32);
           rinfo[4 * et + 3] = a.seed_lo ^ a.req_round[req];
         }
-        named_bar_sync(1, kEpiThreads);
+        named_bar_sync(bar, kEpiThreads);
       }
       if (noisy && quad_ok) {
         const int qd = tl & 3;
@@ -272,7 +282,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
         }
         xch[tl * kXchStride + jj] = sc;
       }
-      named_bar_sync(1, kEpiThreads);
+      named_bar_sync(bar, kEpiThreads);
       const int ngrp = 128 / np, per = 128 / ngrp;
       // tile argmax per row (ties -> lowest id: features scanned in increasing order); a.top2
       // also keeps the tile's second (score, id) and third score (k_lm_refine's candidate window,
@@ -299,7 +309,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           red_s3[g * np + jj] = b3;
         }
       }
-      named_bar_sync(1, kEpiThreads);
+      named_bar_sync(bar, kEpiThreads);
       if (et < np) {
         const int jj = et;
         float b1 = red_v[jj], b2 = -INFINITY, b3 = -INFINITY;
@@ -341,7 +351,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           }
         }
       }
-      named_bar_sync(1, kEpiThreads);
+      named_bar_sync(bar, kEpiThreads);
       if constexpr (MODE == EPI_PQ1) {
         // ---- tile (max, sum exp) of l/T for the row's log-sum-exp
 #pragma unroll
@@ -351,7 +361,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           const float l = logit(jj, lr);
           xch[tl * kXchStride + jj] = l == l ? l * a.inv_t : -INFINITY;
         }
-        named_bar_sync(1, kEpiThreads);
+        named_bar_sync(bar, kEpiThreads);
         float* red_s = reinterpret_cast<float*>(red_i);
         {
           const int jj = et % np, g = et / np;
@@ -363,7 +373,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
           red_v[g * np + jj] = m;
           red_s[g * np + jj] = sm;
         }
-        named_bar_sync(1, kEpiThreads);
+        named_bar_sync(bar, kEpiThreads);
         if (et < np) {
           const int jj = et;
           float m = -INFINITY;
@@ -379,7 +389,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
             a.part_s[(size_t)lr * a.ntm128 + m128] = sm;
           }
         }
-        named_bar_sync(1, kEpiThreads);
+        named_bar_sync(bar, kEpiThreads);
       }
     }
 }
@@ -417,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiThreads);
+      mbar_init(&tempty[i], kEpiGroups * kEpiThreads);
     }
     fence_barrier_init();
   }
@@ -485,7 +495,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------------ epilogue
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int tl = q * 32 + lane;      // tile-local feature (TMEM lane)
-    const int et = threadIdx.x - 64;   // 0..127 epilogue thread id
+    const int gi = (warp - 2) >> 2;    // epilogue group
+    const int et = (threadIdx.x - 64) & (kEpiThreads - 1);   // 0..127 thread id within the group
+    float* gxch = xch + gi * (kXchBytes / 4);
+    float* gred_v = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(red_v) + gi * kRedBytes);
+    int* gred_i = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(red_i) + gi * kRedBytes);
     int it = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
       const int t = u / a.splits, sk = u % a.splits;
@@ -495,13 +509,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int nchunks = (BN + 31) / 32;
-      for (int c = 0; c < nchunks; ++c) {
+      for (int c = gi; c < nchunks; c += kEpiGroups) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
         tmem_ld_wait();
         const int row_base = n * BN + c * 32;
         const int ncol = min(32, BN - c * 32);
-        epi_chunk<MODE>(a, v, m, tl, et, row_base, ncol, sk, xch, red_v, red_i);
+        epi_chunk<MODE>(a, v, m, tl, et, row_base, ncol, sk, gxch, gred_v, gred_i, 1 + gi);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -625,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 2 * kEpiThreads);   // epilogue threads of both CTAs
+      mbar_init(&tempty[i], 2 * kEpiGroups * kEpiThreads);   // epilogue threads of both CTAs
     }
     fence_barrier_init();
   }
@@ -697,7 +711,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int q = warp & 3;
     const int tl = q * 32 + lane;
-    const int et = threadIdx.x - 64;
+    const int gi = (warp - 2) >> 2;    // epilogue group
+    const int et = (threadIdx.x - 64) & (kEpiThreads - 1);   // 0..127 thread id within the group
+    float* gxch = xch + gi * (kXchBytes / 4);
+    float* gred_v = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(red_v) + gi * kRedBytes);
+    int* gred_i = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(red_i) + gi * kRedBytes);
     int it = 0;
     for (int u = cl; u < nunits; u += ncl, ++it) {
       const int t = u / a.splits, sk = u % a.splits;
@@ -707,13 +725,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int nchunks = (BN + 31) / 32;
-      for (int c = 0; c < nchunks; ++c) {
+      for (int c = gi; c < nchunks; c += kEpiGroups) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
         tmem_ld_wait();
         const int row_base = n * BN + c * 32;
         const int ncol = min(32, BN - c * 32);
-        epi_chunk<MODE>(a, v, 2 * p + (int)hr, tl, et, row_base, ncol, sk, xch, red_v, red_i);
+        epi_chunk<MODE>(a, v, 2 * p + (int)hr, tl, et, row_base, ncol, sk, gxch, gred_v, gred_i, 1 + gi);
       }
       tc_fence_before();
       mbar_arrive_leader(&tempty[acc]);
@@ -721,9 +739,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (a.resid && a.splits > 1) {
           // fused residual add of a K-split tile: the last split of (tile, CTA half) to finish sums
           // the partials from L2 in split order onto the residual stream (fence / counter /
-          // last-arriver; no CTA waits on another)
+          // last-arriver; no CTA waits on another); both epilogue groups' stores precede the count,
+          // group 0 does the rest
           __threadfence();
-          named_bar_sync(1, kEpiThreads);
+          named_bar_sync(3, kEpiGroups * kEpiThreads);
+        }
+        if (a.resid && a.splits > 1 && gi == 0) {
           if (et == 0) {
             int* cnt = a.tile_cnt + ((size_t)t * NC + qp) * 2 + hr;
             const int prev = atomicAdd(cnt, 1);
