@@ -55,6 +55,14 @@ __host__ __device__ inline SmemLayout smem_layout(int stages, int BN) {
 }
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+__device__ __forceinline__ uint32_t pack2_f16(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
 
 // Epilogue of one 32-column chunk of a 128-feature accumulator tile.  v[j] = D[feature][row]
 // for feature = m128*128 + tl (tl = TMEM lane) and row = row_base + j, j < ncol.
@@ -118,15 +126,23 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
 #pragma unroll
       for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
       named_bar_sync(bar, kEpiThreads);
-      const int f = et & 63, half = et >> 6;
-      const int fo = m128 * 64 + f;
+      // transposed: item (row j, group i) = output features m*64 + [8i, 8i+8), one 16-B store;
+      // the 8 lanes of a row write its 128 contiguous bytes (4 rows per warp instruction)
+      const int i = et & 7;
+      const int fo = m128 * 64 + 8 * i;
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        const int j = half * 16 + jj;
+      for (int it = 0; it < 2; ++it) {
+        const int j = (et >> 3) + 16 * it;
         const int row = row_base + j;
         if (j < ncol && row < a.R && fo < a.M / 2) {
-          const float g = xch[f * kXchStride + j], u = xch[(f + 64) * kXchStride + j];
-          a.out_bf16[(size_t)row * a.ld_out + fo] = __float2bfloat16_rn(silu_f(g) * u);
+          float y[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float g = xch[(8 * i + e) * kXchStride + j], u = xch[(8 * i + 64 + e) * kXchStride + j];
+            y[e] = silu_f(g) * u;
+          }
+          *reinterpret_cast<uint4*>(a.out_bf16 + (size_t)row * a.ld_out + fo) =
+              make_uint4(pack2_bf16(y[0], y[1]), pack2_bf16(y[2], y[3]), pack2_bf16(y[4], y[5]), pack2_bf16(y[6], y[7]));
         }
       }
       named_bar_sync(bar, kEpiThreads);
@@ -135,51 +151,63 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const uint32_t (&v)
       // heads after.  q / k: rotate-half RoPE at row_pos (pairs (i, i+64) sit in lanes i and
       // i+64, exchanged through shared memory as in the SwiGLU epilogue); v: plain fp16 copy.
       // Same arithmetic and rounding as k_qkv_rope (fp32 in, one fp16 rounding out).
+      // The chunk is transposed through shared memory so that every store is 16 B of one row:
+      // item (row j, group i) = features [8i, 8i+8) and their rotate-half partners [8i+64, 8i+72);
+      // the 8 lanes of a row write its 2 x 128 contiguous bytes (4 rows per warp instruction).
       const int head = m128;
       const int H = a.n_heads, KV = a.n_kv;
       f16* const Qo = reinterpret_cast<f16*>(a.out_bf16);
       f16* const kv = reinterpret_cast<f16*>(a.tree_kv);
-      if (head >= H + KV) {   // v head: lane tl = element tl of the row
-        const int kvh = head - H - KV;
-#pragma unroll 4
-        for (int j = 0; j < 32; ++j) {
-          const int row = row_base + j;
-          if (j < ncol && row < a.R)
-            kv[((((size_t)a.layer * 2 + 1) * KV + kvh) * a.R_cap + row) * 128 + tl] = __float2half_rn(__uint_as_float(v[j]));
-        }
-      } else {
+      const bool is_v = head >= H + KV;
+      f16* const base = head < H ? Qo + (size_t)head * 128
+                        : kv + (((size_t)a.layer * 2 + (is_v ? 1 : 0)) * KV + (head - H - (is_v ? KV : 0))) *
+                                   a.R_cap * 128;
+      const size_t rstride = head < H ? (size_t)H * 128 : 128;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
-        named_bar_sync(bar, kEpiThreads);
-        const int f = et & 63, hsel = et >> 6;   // pair (f, f + 64), rows [16 hsel, 16 hsel + 16)
-        f16* const base = head < H ? Qo + (size_t)head * 128
-                                   : kv + (((size_t)a.layer * 2 + 0) * KV + (head - H)) * a.R_cap * 128;
-        const size_t rstride = head < H ? (size_t)H * 128 : 128;
-        // all 16 rows' positions, then all cos / sin, in flight together (the epilogue must not
-        // serialise on dependent global loads)
-        int pos[16];
+      for (int j = 0; j < 32; ++j) xch[tl * kXchStride + j] = __uint_as_float(v[j]);
+      named_bar_sync(bar, kEpiThreads);
+      const int i = et & 7;
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int row = row_base + hsel * 16 + jj;
-          pos[jj] = (hsel * 16 + jj < ncol && row < a.R) ? __ldg(a.row_pos + row) : -1;
-        }
-        float cs[16], sn[16];
+      for (int it = 0; it < 2; ++it) {
+        const int j = (et >> 3) + 16 * it;
+        const int row = row_base + j;
+        if (j < ncol && row < a.R) {
+          float x1[8], x2[8];
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          cs[jj] = pos[jj] >= 0 ? __ldg(a.rope_cos + (size_t)pos[jj] * 64 + f) : 0.f;
-          sn[jj] = pos[jj] >= 0 ? __ldg(a.rope_sin + (size_t)pos[jj] * 64 + f) : 0.f;
-        }
+          for (int e = 0; e < 8; ++e) {
+            x1[e] = xch[(8 * i + e) * kXchStride + j];
+            x2[e] = xch[(8 * i + 64 + e) * kXchStride + j];
+          }
+          uint4 o1, o2;
+          if (is_v) {
+            o1 = make_uint4(pack2_f16(x1[0], x1[1]), pack2_f16(x1[2], x1[3]), pack2_f16(x1[4], x1[5]),
+                            pack2_f16(x1[6], x1[7]));
+            o2 = make_uint4(pack2_f16(x2[0], x2[1]), pack2_f16(x2[2], x2[3]), pack2_f16(x2[4], x2[5]),
+                            pack2_f16(x2[6], x2[7]));
+          } else {
+            const int pos = __ldg(a.row_pos + row);
+            const float4* cp = reinterpret_cast<const float4*>(a.rope_cos + (size_t)pos * 64 + 8 * i);
+            const float4* sp = reinterpret_cast<const float4*>(a.rope_sin + (size_t)pos * 64 + 8 * i);
+            const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
+            const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            float r1[8], r2[8];
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          if (pos[jj] < 0) continue;
-          const int j = hsel * 16 + jj;
-          const float x1 = xch[f * kXchStride + j], x2 = xch[(f + 64) * kXchStride + j];
-          f16* dst = base + (size_t)(row_base + j) * rstride;
-          dst[f] = __float2half_rn(x1 * cs[jj] - x2 * sn[jj]);
-          dst[f + 64] = __float2half_rn(x2 * cs[jj] + x1 * sn[jj]);
+            for (int e = 0; e < 8; ++e) {
+              r1[e] = x1[e] * cs[e] - x2[e] * sn[e];
+              r2[e] = x2[e] * cs[e] + x1[e] * sn[e];
+            }
+            o1 = make_uint4(pack2_f16(r1[0], r1[1]), pack2_f16(r1[2], r1[3]), pack2_f16(r1[4], r1[5]),
+                            pack2_f16(r1[6], r1[7]));
+            o2 = make_uint4(pack2_f16(r2[0], r2[1]), pack2_f16(r2[2], r2[3]), pack2_f16(r2[4], r2[5]),
+                            pack2_f16(r2[6], r2[7]));
+          }
+          f16* dst = base + (size_t)row * rstride + 8 * i;
+          *reinterpret_cast<uint4*>(dst) = o1;
+          *reinterpret_cast<uint4*>(dst + 64) = o2;
         }
-        named_bar_sync(bar, kEpiThreads);
       }
+      named_bar_sync(bar, kEpiThreads);
     } else if constexpr (MODE == EPI_ARGMAX || MODE == EPI_PQ1 || MODE == EPI_PQ2) {
       // the CTA pair's second 128-feature half past the last vocab tile (an odd tile count, e.g.
       // V = 151936 = 1187 x 128): nothing to reduce, and its partial slot [lr][ntm128] would be
