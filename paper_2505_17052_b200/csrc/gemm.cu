@@ -622,6 +622,32 @@ __device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr, uint32_t ncols)
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
+// Work unit u of the CTA-pair kernel: tile t, K-slice sk, k-blocks [kb0, kb1); tail: one of the
+// last-wave tiles' K-parts (GemmArgs::n_full)
+struct Unit {
+  int t, sk, kb0, kb1;
+  bool tail;
+};
+__device__ __forceinline__ Unit unit_of(const GemmArgs& a, int u) {
+  Unit r;
+  const int nf = a.n_full * a.splits;
+  if (u < nf) {
+    r.t = u / a.splits;
+    r.sk = u % a.splits;
+    r.kb0 = r.sk * a.kb_per_split;
+    r.kb1 = min(a.num_kb, r.kb0 + a.kb_per_split);
+    r.tail = false;
+  } else {
+    const int v = u - nf;
+    r.t = a.n_full + v / a.tail_split;
+    r.sk = v % a.tail_split;
+    r.kb0 = r.sk * a.kb_tail;
+    r.kb1 = min(a.num_kb, r.kb0 + a.kb_tail);
+    r.tail = true;
+  }
+  return r;
+}
+
 // Launched with clusters of 2*nc CTAs: nc CTA pairs compute the nc N-tiles of one 256-feature
 // weight tile; pair 0 loads the weight halves once and multicasts them to every pair (the
 // activation tiles differ per pair), which divides the L2->SM weight traffic by nc.
@@ -680,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // cluster work unit = (256-feature tile p, N-tile group, K-split); pair qp takes N-tile
   // group * nc + qp (tiles past the activations read zeros and store nothing)
   const int ntiles = a.n_tiles_m * a.n_groups;   // n_tiles_m counts 256-feature pairs here
-  const int nunits = ntiles * a.splits;
+  const int nunits = a.n_full * a.splits + (ntiles - a.n_full) * a.tail_split;
   const int cl = blockIdx.x / (2 * NC), ncl = gridDim.x / (2 * NC);
 
   if (warp == 0) {
@@ -690,10 +716,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cl; u < nunits; u += ncl) {
-        const int t = u / a.splits, sk = u % a.splits;
-        const int p = t / a.n_groups, n = (t % a.n_groups) * NC + qp;
-        const int kb0 = sk * a.kb_per_split, kb1 = min(a.num_kb, kb0 + a.kb_per_split);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const Unit un = unit_of(a, u);
+        const int p = un.t / a.n_groups, n = (un.t % a.n_groups) * NC + qp;
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + b_bytes));
           else mbar_arrive_leader(&full[stage]);
@@ -714,8 +739,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int u = cl; u < nunits; u += ncl, ++it) {
-        const int sk = u % a.splits;
-        const int kb0 = sk * a.kb_per_split, kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        const Unit un = unit_of(a, u);
+        const int kb0 = un.kb0, kb1 = un.kb1;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -746,13 +771,73 @@ __global__ void __launch_bounds__(kThreads, 1)
     int* gred_i = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(red_i) + gi * kRedBytes);
     int it = 0;
     for (int u = cl; u < nunits; u += ncl, ++it) {
-      const int t = u / a.splits, sk = u % a.splits;
+      const Unit un = unit_of(a, u);
+      const int t = un.t, sk = un.sk;
       const int p = t / a.n_groups, n = (t % a.n_groups) * NC + qp;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int nchunks = (BN + 31) / 32;
+      if constexpr (MODE == EPI_SWIGLU) {
+        if (un.tail) {
+          // last-wave K-part: accumulator -> tail_buf[tail tile][part][pair][half][BN rows][128]
+          // (coalesced over features), then the last part of (tile, pair, half) to finish sums the
+          // parts in part order from L2 and runs the epilogue (fence / counter / last-arriver, no
+          // CTA waits on another; a + b == b + a keeps any two-part order exact as well)
+          const int ti = t - a.n_full;
+          const size_t part_elems = (size_t)BN * 128;
+          float* const tb = a.tail_buf + ((size_t)ti * a.tail_split * NC + qp) * 2 * part_elems + hr * part_elems;
+          const size_t part_stride = (size_t)NC * 2 * part_elems;
+          for (int c = gi; c < nchunks; c += kEpiGroups) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+            tmem_ld_wait();
+            float* dst = tb + (size_t)sk * part_stride + (size_t)(c * 32) * 128 + tl;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c * 32 + j < BN) dst[(size_t)j * 128] = __uint_as_float(v[j]);
+          }
+          tc_fence_before();
+          mbar_arrive_leader(&tempty[acc]);
+          __threadfence();
+          named_bar_sync(3, kEpiGroups * kEpiThreads);
+          if (gi == 0 && et == 0) {
+            int* cnt = a.tile_cnt + ((size_t)ti * NC + qp) * 2 + hr;
+            const int prev = atomicAdd(cnt, 1);
+            red_i[0] = prev == a.tail_split - 1;
+            if (prev == a.tail_split - 1) *cnt = 0;   // ready for the next launch
+          }
+          named_bar_sync(3, kEpiGroups * kEpiThreads);
+          if (red_i[0]) {
+            __threadfence();
+            for (int c = gi; c < nchunks; c += kEpiGroups) {
+              // part by part (in order), all 32 rows' loads of a part in flight together
+              float sv[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) sv[j] = 0.f;
+              const float* src = tb + (size_t)(c * 32) * 128 + tl;
+              const int nj = min(32, BN - c * 32);
+#pragma unroll
+              for (int s2 = 0; s2 < 8; ++s2) {
+                if (s2 >= a.tail_split) break;
+                float y[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) y[j] = j < nj ? __ldcg(src + (size_t)s2 * part_stride + (size_t)j * 128) : 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) sv[j] += y[j];
+              }
+              uint32_t v[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(sv[j]);
+              epi_chunk<MODE>(a, v, 2 * p + (int)hr, tl, et, n * BN + c * 32, min(32, BN - c * 32), 0, gxch, gred_v,
+                              gred_i, 1 + gi);
+            }
+          }
+          named_bar_sync(3, kEpiGroups * kEpiThreads);   // red_i[0] is rewritten by the next tail unit
+          continue;
+        }
+      }
       for (int c = gi; c < nchunks; c += kEpiGroups) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
@@ -1029,9 +1114,38 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
   }
   a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
   g_last_splits = a.splits;
+  // last-wave K split of the SwiGLU GEMM (stream-K style): the tail of ntiles % nclusters tiles
+  // would otherwise leave the other clusters idle for a whole tile; split it into ts K-parts,
+  // ts minimising the tail phase ceil(tail * ts / nclusters) / ts (in tile times) plus a
+  // per-part cost of 0.04.  Off by default (SPECEDGE_TAIL_SPLIT=1 picks ts, =n forces it):
+  // measured on cfg2 (ts = 3) gate/up 3.80 vs 3.38 ms per step — the parts alone would give 3.09,
+  // but the last arriver's fixup (fence, counter, L2 reads of the parts, then the SwiGLU
+  // epilogue: ~17 us on the critical path) costs more than the idle tail it removes
+  // (profiles/README.md)
+  a.n_full = ntiles;
+  a.tail_split = 1;
+  a.kb_tail = a.num_kb;
+  static const int env_ts = getenv("SPECEDGE_TAIL_SPLIT") ? atoi(getenv("SPECEDGE_TAIL_SPLIT")) : -1;
+  if (mode == EPI_SWIGLU && a.tail_buf && a.tile_cnt && env_ts > 0 && ntiles > nclusters) {
+    const int tail = ntiles % nclusters;
+    int best = 1;
+    double best_cost = 1.0;
+    for (int ts = 2; ts <= 8 && tail > 0; ++ts) {
+      if (a.num_kb / ts < 8) break;
+      if ((size_t)tail * ts * nc * 2 * a.BN * 128 * 4 > a.tail_cap) break;
+      const double cost = (double)((tail * ts + nclusters - 1) / nclusters) / ts + 0.04 * ts;
+      if (env_ts > 1 ? ts == env_ts : cost < best_cost) { best = ts; best_cost = cost; }
+    }
+    if (best > 1) {
+      a.n_full = ntiles - tail;
+      a.tail_split = best;
+      a.kb_tail = (a.num_kb + best - 1) / best;
+    }
+  }
   GemmArgs b = a;
   b.n_tiles_m = n_pairs;      // the kernel iterates 256-feature pairs
-  const int grid = 2 * nc * std::min(ntiles * a.splits, nclusters);
+  const int nunits_h = a.n_full * a.splits + (ntiles - a.n_full) * a.tail_split;
+  const int grid = 2 * nc * std::min(nunits_h, nclusters);
   if (launches) ++*launches;
   switch (mode) {
     case EPI_F32: return launch_mode2<EPI_F32>(tmW, tmX, b, smem, grid, st);

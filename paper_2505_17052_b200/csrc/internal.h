@@ -98,6 +98,14 @@ struct GemmArgs {
   int n_groups;           // CTA-pair kernel: ceil(n_tiles_n / nc)
   int splits, kb_per_split, max_splits;   // K-split (EPI_F32): slice sk at out_f32 + sk*split_stride
   int unsplit_if_full;    // EPI_F32: no K-split when the tiles already fill >= 90 % of one wave
+  // CTA-pair kernel, last-wave K split (EPI_SWIGLU): tiles [0, n_full) run whole (or in `splits`
+  // K-slices); each tile t >= n_full runs as tail_split K-parts of kb_tail k-blocks whose fp32
+  // accumulators go to tail_buf, and the last part of (tile, pair, half) to finish (counter in
+  // tile_cnt) sums them in part order and runs the epilogue (set by gemm_launch; tail_buf /
+  // tail_cap / tile_cnt from the caller, nullptr: no tail split)
+  int n_full, tail_split, kb_tail;
+  float* tail_buf;
+  size_t tail_cap;        // bytes
   size_t split_stride;
   // EPI_F32 / EPI_RESID (fp32 residual stream)
   float* out_f32;

@@ -173,7 +173,8 @@ WsLayout ws_layout(const specedge_model_config& c, int B, int R) {
   w.part_idx = take(4 * (size_t)R * vt);
   w.part_val2 = take(4 * (size_t)R * vt);
   // fused residual add: one counter per (256-feature tile, row tile, multicast slot, CTA half)
-  w.tile_cnt_bytes = 4 * (size_t)((c.d + 255) / 256) * ((R + 15) / 16 + 1) * 4 * 2;
+  // + 2048 counters for the SwiGLU GEMM's last-wave K-parts (< 256 clusters x <= 4 pairs x 2 halves)
+  w.tile_cnt_bytes = 4 * (size_t)((c.d + 255) / 256) * ((R + 15) / 16 + 1) * 4 * 2 + 4 * 2048;
   w.tile_cnt = take(w.tile_cnt_bytes);
   w.part_idx2 = take(4 * (size_t)R * vt);
   w.part_val3 = take(4 * (size_t)R * vt);
@@ -532,6 +533,11 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
     gu.ld_out = c.ffn;
     static const int bn_gu = getenv("SPECEDGE_BN_GATEUP") ? atoi(getenv("SPECEDGE_BN_GATEUP")) : 0;
     gu.bn_override = bn_gu;
+    if (!tp) {   // last-wave K-parts of the gate/up GEMM go through Y (free between a6's norm and a8)
+      gu.tail_buf = Y;
+      gu.tail_cap = 4 * (size_t)kGemmSplits * ((size_t)R + kMaxTp) * std::max((size_t)(H + 2 * KV) * hd, (size_t)c.d);
+      gu.tile_cnt = (int*)P(w.tile_cnt);
+    }
     { KTimer _t(K_GU, st); CK(gemm_launch(EPI_SWIGLU, Lw.tm_gu, Hn_in, gu, st, &launches)); }
     pendingY = fused ? f32_gemm_fused(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn) : f32_gemm(K_DOWN, Lw.tm_d, Mb, c.d, c.ffn, true);
     if (pendingY < 0) return SPECEDGE_E_CUDA;

@@ -1,7 +1,7 @@
 """Alternate kernel paths behind environment switches (read once per process, so each runs the
 end-to-end parity subset in a subprocess): forced balanced attention on short contexts, one-Q-tile
 passes, half-height replicated query tiles, the QKV GEMM with fp32 output + the separate RoPE kernel
-(the fused RoPE epilogue is the default).  Each must
+(the fused RoPE epilogue is the default), the gate/up GEMM's last wave in K-parts with a last-arriver fixup.  Each must
 stay parity-green against the oracle exactly like the default path (tests/test_gpu_verify.py)."""
 import os
 import subprocess
@@ -15,7 +15,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("env", [{"SPECEDGE_ATTN_BALANCED": "1"}, {"SPECEDGE_ATTN_NQ": "1"},
-                                 {"SPECEDGE_ATTN_HALF_TILES": "1"}, {"SPECEDGE_QKV_FUSED": "0"}],
+                                 {"SPECEDGE_ATTN_HALF_TILES": "1"}, {"SPECEDGE_QKV_FUSED": "0"},
+                                 {"SPECEDGE_TAIL_SPLIT": "3"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_alternate_path_parity(env):
     torch = pytest.importorskip("torch")
