@@ -705,7 +705,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_begin();   // setup above overlaps the previous kernel; global reads/writes only from here
   // cluster work unit = (256-feature tile p, N-tile group, K-split); pair qp takes N-tile
   // group * nc + qp (tiles past the activations read zeros and store nothing)
-  const int ntiles = a.n_tiles_m * a.n_groups;   // n_tiles_m counts 256-feature pairs here
+  // n_tiles_m counts 256-feature pairs here; mcx: n_groups counts groups of nc pairs
+  const int ntiles = a.mcx ? a.n_groups * a.n_tiles_n : a.n_tiles_m * a.n_groups;
+  // cluster tile t -> this pair's 256-feature tile p and activation tile n
+  auto tile_pn = [&](int t, int& p, int& n) {
+    if (a.mcx) {
+      p = (t / a.n_tiles_n) * NC + qp;
+      n = t % a.n_tiles_n;
+    } else {
+      p = t / a.n_groups;
+      n = (t % a.n_groups) * NC + qp;
+    }
+  };
   const int nunits = a.n_full * a.splits + (ntiles - a.n_full) * a.tail_split;
   const int cl = blockIdx.x / (2 * NC), ncl = gridDim.x / (2 * NC);
 
@@ -717,17 +728,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int u = cl; u < nunits; u += ncl) {
         const Unit un = unit_of(a, u);
-        const int p = un.t / a.n_groups, n = (un.t % a.n_groups) * NC + qp;
+        int p, n;
+        tile_pn(un.t, p, n);
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + b_bytes));
           else mbar_arrive_leader(&full[stage]);
-          if (NC == 1)
+          if (NC == 1 || a.mcx)
             tma_load_2d_2sm(sA + stage * kABytes, &tmA, &full[stage], kb * 64, p * 256 + (int)hr * 128, pol_w);
           else if (qp == 0)
             tma_load_2d_2sm_mc(sA + stage * kABytes, &tmA, &full[stage], kb * 64, p * 256 + (int)hr * 128, mask_half,
                                pol_w);
-          tma_load_2d_2sm(sB + stage * b_bytes, &tmB, &full[stage], kb * 64, n * BN + (int)hr * HB, pol_x);
+          if (NC == 1 || !a.mcx)
+            tma_load_2d_2sm(sB + stage * b_bytes, &tmB, &full[stage], kb * 64, n * BN + (int)hr * HB, pol_x);
+          else if (qp == 0)
+            tma_load_2d_2sm_mc(sB + stage * b_bytes, &tmB, &full[stage], kb * 64, n * BN + (int)hr * HB, mask_half,
+                               pol_x);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
@@ -773,12 +789,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = cl; u < nunits; u += ncl, ++it) {
       const Unit un = unit_of(a, u);
       const int t = un.t, sk = un.sk;
-      const int p = t / a.n_groups, n = (t % a.n_groups) * NC + qp;
+      int p, n;
+      tile_pn(t, p, n);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int nchunks = (BN + 31) / 32;
+      if (p >= a.n_tiles_m) {   // mcx: a pair past the last 256-feature tile computed zeros
+        tc_fence_before();
+        mbar_arrive_leader(&tempty[acc]);
+        continue;
+      }
       if constexpr (MODE == EPI_SWIGLU) {
         if (un.tail) {
           // last-wave K-part: accumulator -> tail_buf[tail tile][part][pair][half][BN rows][128]
@@ -1087,9 +1109,14 @@ cudaError_t gemm_launch_pair(int mode, const CUtensorMap& tmW, const void* X, Ge
   else if (a.n_tiles_n % 3 == 0) nc = 3;
   else if (a.n_tiles_n % 4 == 0) nc = 4;
   else if (a.n_tiles_n % 2 == 0) nc = 2;
+  // SPECEDGE_GEMM_MCX=k: clusters of k pairs sharing the activation tile instead (pair 0
+  // multicasts X; the weights are read per pair)
+  static const int env_mcx = getenv("SPECEDGE_GEMM_MCX") ? atoi(getenv("SPECEDGE_GEMM_MCX")) : 0;
+  a.mcx = (env_mcx > 1 && n_pairs >= 2 && !a.pair) ? 1 : 0;
+  if (a.mcx) nc = std::min(std::min(env_mcx, 4), n_pairs);
   a.nc = nc;
-  a.n_groups = (a.n_tiles_n + nc - 1) / nc;
-  const int ntiles = n_pairs * a.n_groups;
+  a.n_groups = a.mcx ? (n_pairs + nc - 1) / nc : (a.n_tiles_n + nc - 1) / nc;
+  const int ntiles = a.mcx ? a.n_groups * a.n_tiles_n : n_pairs * a.n_groups;
   cudaError_t pe = cudaSuccess;
   int nclusters = 0;
   switch (mode) {

@@ -95,7 +95,10 @@ struct GemmArgs {
   int ntm128;             // 128-feature tiles (stride of the ARGMAX partials)
   int pair;               // EPI_F32/EPI_ARGMAX: rows (2r, 2r+1) are hi/lo bf16 parts of row r
   int nc;                 // CTA-pair kernel: pairs per cluster sharing one weight tile (TMA multicast)
-  int n_groups;           // CTA-pair kernel: ceil(n_tiles_n / nc)
+  int n_groups;           // CTA-pair kernel: ceil(n_tiles_n / nc) (mcx: ceil(256-feature pairs / nc))
+  int mcx;                // CTA-pair kernel: the nc pairs of a cluster share the ACTIVATION tile (pair
+                          // qp takes weight tile group * nc + qp, pair 0 multicasts X) instead of the
+                          // weight tile
   int splits, kb_per_split, max_splits;   // K-split (EPI_F32): slice sk at out_f32 + sk*split_stride
   int unsplit_if_full;    // EPI_F32: no K-split when the tiles already fill >= 90 % of one wave
   // CTA-pair kernel, last-wave K split (EPI_SWIGLU): tiles [0, n_full) run whole (or in `splits`
