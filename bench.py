@@ -3,7 +3,9 @@
 Workload (N=1 and per GPU): cfg2 = BASELINE.json configs[1] — Llama-3-8B-shaped random-init
 decoder, 16 requests x 32-node draft trees (pooled top-budget trees, D=7, b=4),
 committed contexts ~ U[768, 1280] (mean 1k, synthetic KV), greedy verification, acceptance
-planted to the paper's tokens/verify profile (3.98 +- 1.55, Table 1).
+planted to the paper's tokens/verify profile (3.98 +- 1.55, Table 1): lengths drawn
+from that normal law, then moved so that every request set's mean is the profile mean (64 tokens per
+16 requests = 4.0 per verify on every rank; synth.plant.draw_accept_lengths_at_mean).
 A step = one specedge_verify_batch(auto_commit=1) (all of SURVEY §8(a) a1-a11) + a rewind of the
 cached lengths so every step sees identical inputs.  Multi-GPU: one process per GPU, each an
 independent replica with its own 16 requests (weak scaling, no collective on the data path;
@@ -145,7 +147,7 @@ def setup_gpu(wl, rank, device, tp=None, model=None, pool=None, mb=0):
     model/pool/mb: build microbatch mb's requests on an existing model and KV pool (cfg3's A/B)."""
     import torch
     from paper_2505_17052_b200 import api
-    from synth.plant import plant, draw_accept_lengths
+    from synth.plant import plant, draw_accept_lengths_at_mean
     shape = wl.shape
     if tp is not None:
         rank = 0   # one request set for the whole box
@@ -190,7 +192,7 @@ def setup_gpu(wl, rank, device, tp=None, model=None, pool=None, mb=0):
         off = b.node_offset.cpu().numpy()
         return [rt[off[i] + i: off[i + 1] + i + 1] for i in range(wl.n_requests)]
 
-    accept = draw_accept_lengths(np.random.default_rng([wl.ctx_seed + 11, rank]), trees, wl.accept_mu,
+    accept = draw_accept_lengths_at_mean(np.random.default_rng([wl.ctx_seed + 11, rank]), trees, wl.accept_mu,
                                  wl.accept_sigma)
     trees = plant(trees, targets, accept, shape.vocab, np.random.default_rng([wl.ctx_seed + 13, rank]))
     batch = make_batch(trees)
@@ -206,12 +208,12 @@ def setup_gpu(wl, rank, device, tp=None, model=None, pool=None, mb=0):
 
 def workload_config(wl, world=1, tp=False):
     """The `config` object of both arms (rank 0's request sets; host-side, from the seeds)."""
-    from synth.plant import draw_accept_lengths
+    from synth.plant import draw_accept_lengths_at_mean
     n_mb = wl.microbatches
     rows = tokens = 0
     for mb in range(n_mb):
         trees = build_trees(wl, 64 * mb, wl.shape.vocab)
-        acc = draw_accept_lengths(np.random.default_rng([wl.ctx_seed + 11, 64 * mb]), trees, wl.accept_mu,
+        acc = draw_accept_lengths_at_mean(np.random.default_rng([wl.ctx_seed + 11, 64 * mb]), trees, wl.accept_mu,
                                   wl.accept_sigma)
         rows += sum(t.n + 1 for t in trees)
         tokens += sum(a + 1 for a in acc)
@@ -447,8 +449,8 @@ def run_gpu(args, world, rank, local):
         "config": cfgd,
         "p50_ms": round(statistics.median(step_ms), 4), "p90_ms": round(float(np.quantile(step_ms, 0.9)), 4),
         "rows_per_s": round(box_rows * args.steps / (total_ms / 1e3), 1),
-        # the planted draw's mean tokens/verify differs from the profile mean (Table 1);
-        # the same step time at the profile mean exactly:
+        # the planted mean tokens/verify is the profile mean rounded to whole tokens per request
+        # set (Table 1); the same step time at the profile mean exactly:
         "tokens_per_s_at_profile_mean": round(value * wl.accept_mu * wl.n_requests * len(mbs) * replicas / box_tokens, 1),
         "roofline": roof,
         "kernels": kernel_table,
@@ -614,11 +616,11 @@ class OracleSample:
 
     def __init__(self, wl, rank=0):
         from oracle import cpp_ref
-        from synth.plant import draw_accept_lengths
+        from synth.plant import draw_accept_lengths_at_mean
         self.wl = wl
         self.ctx = contexts(wl, rank)
         self.trees = build_trees(wl, rank, wl.shape.vocab)
-        acc = draw_accept_lengths(np.random.default_rng([wl.ctx_seed + 11, rank]), self.trees, wl.accept_mu,
+        acc = draw_accept_lengths_at_mean(np.random.default_rng([wl.ctx_seed + 11, rank]), self.trees, wl.accept_mu,
                                   wl.accept_sigma)
         self.tokens = [a + 1 for a in acc]
         rng = np.random.default_rng([wl.ctx_seed + 7, rank])

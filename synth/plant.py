@@ -29,6 +29,23 @@ def draw_accept_lengths(rng: np.random.Generator, trees: list[Tree], mu: float, 
     return out
 
 
+def draw_accept_lengths_at_mean(rng: np.random.Generator, trees: list[Tree], mu: float, sigma: float):
+    """draw_accept_lengths, then the batch total moved to round((mu - 1) * B) (the bench's workload:
+    every request set, on every rank, verifies the profile mean mu of Table 1 per request, P:375-385,
+    instead of whatever its random draw gave): the largest lengths are lowered / the smallest raised,
+    one token at a time, within [0, depth_max]."""
+    a = draw_accept_lengths(rng, trees, mu, sigma)
+    dmax = [int(t.depth().max()) if t.n else 0 for t in trees]
+    target = int(round((mu - 1.0) * len(trees)))
+    while sum(a) > target and any(x > 0 for x in a):
+        i = max(range(len(a)), key=lambda j: (a[j], -j))
+        a[i] -= 1
+    while sum(a) < target and any(x < d for x, d in zip(a, dmax)):
+        i = min((j for j in range(len(a)) if a[j] < dmax[j]), key=lambda j: (a[j], j))
+        a[i] += 1
+    return a
+
+
 def plant(trees: list[Tree], targets, accept_len: list[int], vocab: int,
           rng: np.random.Generator) -> list[Tree]:
     trees = [t.copy() for t in trees]

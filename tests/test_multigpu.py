@@ -63,3 +63,20 @@ def test_two_rank_replicas_gloo():
     assert v0 == v1 == pytest.approx((70 + 74) * 10 / 0.150)
     assert (acc0, b0) == (acc1, b1)                  # same request -> same outcome on any rank
     assert c0 != c1                                  # replicas own different requests
+
+
+def test_bench_acceptance_profile_is_the_table1_mean_on_every_rank():
+    """The bench plants acceptance lengths whose request-set total is round((mu - 1) B) on every rank
+    (Table 1 profile mean), within each tree's depth; the spread of the normal draw stays."""
+    from synth.configs import WORKLOADS
+    from synth.plant import draw_accept_lengths_at_mean
+    import bench
+    for name in ("cfg2", "cfg3", "cfg5", "cfg4"):
+        wl = WORKLOADS[name]
+        for rank in range(4):
+            trees = bench.build_trees(wl, rank, wl.shape.vocab)
+            a = draw_accept_lengths_at_mean(np.random.default_rng([wl.ctx_seed + 11, rank]), trees, wl.accept_mu,
+                                            wl.accept_sigma)
+            assert sum(a) == int(round((wl.accept_mu - 1.0) * wl.n_requests)), (name, rank, a)
+            assert all(0 <= x <= int(t.depth().max()) for x, t in zip(a, trees))
+            assert len(set(a)) > 1
