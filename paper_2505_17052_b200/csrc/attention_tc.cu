@@ -403,22 +403,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t nscr = 0;            // scr_done completions consumed
       Cursor cu = cursor0();
       while (next_item(cu)) {
+      TRACE(900);
       if (balanced && c_idx == 0) a.nch_tab[r * a.KV + g] = nch;   // for the combine kernel
       const int* pages = a.block_table + (size_t)h * a.max_pages_per_seq + p_begin;
       for (int p = 0; p < n_pass; ++p, ++gp) {
-        const int nq = pair_pass(p) ? 2 : 1;
-        mbar_wait(q_empty, (gp & 1) ^ 1);
-        uint32_t qbytes = 0;
-        for (int u = 0; u < nq; ++u) qbytes += (uint32_t)rep_of(p, u) * (128 / rep_of(p, u) / G) * G * 128 * KB;
-        mbar_expect_tx(q_full, qbytes);
-        for (int u = 0; u < nq; ++u) {
-          const int rf = rep_of(p, u);
-          const CUtensorMap* tq = rf == 4 ? &tmQ4 : (rf == 2 ? &tmQ2 : &tmQ);
-          for (int rr = 0; rr < rf; ++rr)
-            for (int kb = 0; kb < KB; ++kb)
-              tma_load_3d(sQ + u * QT_BYTES + kb * 128 * 128 + rr * (128 / rf) * 128, tq, q_full, kb * 64, g * G,
-                          row0 + mt_of(p, u) * spm);
-        }
+        // the pass's Q tiles, issued right after its first K/V sub-tile: the K/V stream (HBM) is
+        // the long pole, Q (just written by the QKV GEMM) comes from L2
+        auto issue_q = [&]() {
+          const int nq = pair_pass(p) ? 2 : 1;
+          mbar_wait(q_empty, (gp & 1) ^ 1);
+          uint32_t qbytes = 0;
+          for (int u = 0; u < nq; ++u) qbytes += (uint32_t)rep_of(p, u) * (128 / rep_of(p, u) / G) * G * 128 * KB;
+          mbar_expect_tx(q_full, qbytes);
+          for (int u = 0; u < nq; ++u) {
+            const int rf = rep_of(p, u);
+            const CUtensorMap* tq = rf == 4 ? &tmQ4 : (rf == 2 ? &tmQ2 : &tmQ);
+            for (int rr = 0; rr < rf; ++rr)
+              for (int kb = 0; kb < KB; ++kb)
+                tma_load_3d(sQ + u * QT_BYTES + kb * 128 * 128 + rr * (128 / rf) * 128, tq, q_full, kb * 64, g * G,
+                            row0 + mt_of(p, u) * spm);
+          }
+          if (gp == 0) TRACE(901);
+        };
         // the previous pass's epilogue merged replicas through the K/V ring: no K/V load may land
         // in the ring before that merge is done (o_empty of that pass)
         if (scratch) mbar_wait(scr_done, nscr++ & 1);
@@ -436,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_prefetch_l2_2d(&tmPool, kb * 64, rk + a.KV * 64);
           }
         };
+        if (gp == 0) TRACE(902);
         const int kPrefetch = ta.prefetch;
         for (int jj = 0; jj < kPrefetch; ++jj) prefetch(jj);
         for (int j = 0; j < nsub; ++j) {
@@ -465,7 +472,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (gp == 0) TRACE(j);
           if (++stage == NST) { stage = 0; phase ^= 1; }
+          if (j == 0) issue_q();
         }
+        if (nsub == 0) issue_q();
       }
       }
     }
@@ -485,7 +494,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int p = 0; p < n_pass; ++p, ++gp) {
         const bool pr = pair_pass(p);
         const int nk = nsub_u(p, u);
+        if (gp == 0) TRACE(910 + u);
         mbar_wait(q_full, gp & 1);
+        if (gp == 0) TRACE(912 + u);
         tc_fence_after();
         // QK of this unit's k-th sub-tile of the pass into S buffer (kc + k) & 1
         auto issue_qk = [&](int k) {
@@ -509,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (k == nk - 1) tc_commit(q_empty);   // last QK of the pass: Q may be reloaded
         };
         for (int k = 0; k < 2 && k < nk; ++k) issue_qk(k);
+        if (gp == 0) TRACE(914 + u);
         if (nk == 0) tc_commit(q_empty);
         for (int k = 0; k < nk; ++k) {
           const uint32_t kg = kc + k;
@@ -1149,7 +1161,8 @@ cudaError_t launch_tc(const AttnArgs& a, int B, bf16* O, float* O_f32, cudaStrea
       cudaMemcpy(hb, trace, sizeof(hb), cudaMemcpyDeviceToHost);
       const unsigned long long t0 = hb[1000];
       auto d = [&](int i) { return hb[i] ? (long long)(hb[i] - t0) : -1LL; };
-      fprintf(stderr, "attn trace CTA0: end=%lld\n", d(1001));
+      fprintf(stderr, "attn trace CTA0: end=%lld item=%lld qissued=%lld page=%lld | mma u0: pre_q=%lld q=%lld qk01=%lld u1: pre_q=%lld q=%lld qk01=%lld\n",
+              d(1001), d(900), d(901), d(902), d(910), d(912), d(914), d(911), d(913), d(915));
       for (int k = 0; k < 16; ++k)
         fprintf(stderr, " k%2d PIPE u0: load=%6lld kv=%6lld s=%6lld p=%6lld || u1: load=%6lld kv=%6lld s=%6lld p=%6lld\n", k,
                 d(2 * k), d(640 + k), d(256 + k), d(384 + k), d(2 * k + 1), d(704 + k), d(320 + k), d(448 + k));
