@@ -69,7 +69,64 @@ __global__ void k_rate(int N, int ts, int reps, long long* out) {
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
 }
 
+// Latency of a short dependent group (the attention's per-sub-tile chains): n MMAs into one
+// accumulator, commit, wait -> cycles from the first issue to the mbarrier completing
+__global__ void k_lat(int N, int ts, int n, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* A = sm;
+  uint8_t* B = sm + 16384;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 49152 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint64_t ad = umma_desc_sw128(smem_u32(A));
+    const uint64_t bd = umma_desc_sw128(smem_u32(B));
+    uint32_t ph = 0;
+    long long best = 1LL << 60;
+    for (int rep = 0; rep < 16; ++rep) {
+      const long long t0 = clock64();
+      for (int k = 0; k < n; ++k) {
+        if (ts) mma_ts(tmem, tmem + 384, bd, idesc, k > 0);
+        else tc_mma_f16(tmem, ad, bd, idesc, k > 0);
+      }
+      tc_commit(&bar);
+      while (!mbar_try_wait(&bar, ph)) {}
+      ph ^= 1;
+      const long long t1 = clock64();
+      if (rep > 2 && t1 - t0 < best) best = t1 - t0;
+    }
+    out[0] = best;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
 int main() {
+  {
+    long long* dl;
+    cudaMalloc(&dl, 8);
+    cudaFuncSetAttribute(k_lat, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    for (int ts = 0; ts < 2; ++ts)
+      for (int N : {64, 128})
+        for (int n : {1, 4, 8}) {
+          k_lat<<<1, 128, 64 * 1024>>>(N, ts, n, dl);
+          long long h;
+          cudaMemcpy(&h, dl, 8, cudaMemcpyDeviceToHost);
+          printf("latency %s M=128 N=%3d: %d dependent MMAs -> %lld cycles issue-to-complete\n", ts ? "TS" : "SS", N, n, h);
+        }
+  }
   long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(k_rate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
