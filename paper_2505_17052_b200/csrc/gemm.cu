@@ -1,8 +1,9 @@
 // tcgen05 / TMEM / TMA GEMM with fused epilogues for the verify step's dense contractions
 // (QKV, O-proj, gate/up + SwiGLU, down, LM head + vocab argmax /
-// Gumbel-max).  QKV / O / down store fp32 per-K-split partials; RoPE + K/V scatter and the residual
-// add are applied by the following elementwise kernels (kernels_small.cu), which sum the splits in
-// a fixed order (deterministic).  P:173 ("a single forward pass" over
+// Gumbel-max).  O / down (and QKV when it must be K-split) store fp32 per-K-split partials, summed
+// in a fixed order (deterministic) by the following elementwise kernels (kernels_small.cu: the
+// residual add + RMSNorm, or RoPE + K/V scatter); an unsplit QKV GEMM applies RoPE and the K/V
+// scatter in its own epilogue (EPI_QKV).  P:173 ("a single forward pass" over
 // all draft tokens) makes these weight-streaming GEMMs with N = R rows of the whole batch.
 //
 // Orientation ("swap-AB"): D^T[feature][row] = W[feature][:] . X[row][:].  Weights take the
