@@ -1061,15 +1061,17 @@ int gemm_splits_last() { return g_last_splits; }
 
 // Activation-row tile: the fewest <= 256-row tiles, rows rounded up to a multiple of 16
 // (measured: 5 x 224 beats 6 x 176 for the 1056-row LM head; larger N per MMA instruction)
-// The QKV projection runs with the fused RoPE epilogue (EPI_QKV, never K-split) when the fp32
-// path would not split it either: its pair tiles fill 90-100 % of one wave of CTA pairs, or at
-// least 1.5 waves (host-side estimate with one pair per two SMs).
+// The QKV projection runs with the fused RoPE epilogue (EPI_QKV, never K-split) when its pair
+// tiles fit one wave of CTA pairs (one tile time; the fp32 path's K-split partials + RoPE kernel
+// cost more: cfg5, 56 tiles, QKV + RoPE 2.0 -> 1.52 ms per step) or fill at least 1.5 waves
+// (host-side estimate with one pair per two SMs); between the two the fp32 path's K split
+// balances the waves better.
 bool gemm_qkv_fused_ok(int M, int R) {
   const int g_num_sms = device_sms();
   const int bn = gemm_pick_bn(R);
   const int ntiles = ((M + 255) / 256) * ((R + bn - 1) / bn);
   const int nc = g_num_sms / 2;
-  return (ntiles * 10 >= nc * 9 && ntiles <= nc) || ntiles * 2 >= nc * 3;
+  return ntiles <= nc || ntiles * 2 >= nc * 3;
 }
 
 int gemm_pick_bn(int R) {

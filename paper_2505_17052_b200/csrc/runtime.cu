@@ -465,12 +465,12 @@ specedge_status run_verify(specedge_model* m, specedge_kvpool* pool, const spece
   };
   static const bool f4_ag_on = getenv("SPECEDGE_TP_F4_AG") && getenv("SPECEDGE_TP_F4_AG")[0] == '1';
   bf16* const Hn_in = (fused && f4_ag_on) ? m->tp_hn : Hn;   // operand of the column-parallel GEMMs
-  // QKV GEMM with the RoPE epilogue (head_dim 128, when it would run unsplit anyway; off with
-  // SPECEDGE_QKV_FUSED=0).  Measured on cfg2: 1.13-1.16 ms per step vs 1.00 + 0.35 ms with the
+  // QKV GEMM with the RoPE epilogue (head_dim 128, when gemm_qkv_fused_ok; off with
+  // SPECEDGE_QKV_FUSED=0, forced with =2).  Measured on cfg2: 1.13-1.16 ms per step vs 1.00 + 0.35 ms with the
   // fp32 round trip and the separate RoPE kernel (the epilogue stores 16 B per lane after a
   // shared-memory transpose; with 2-B scattered stores it was 1.57 ms)
-  static const bool qkv_fuse_env = !(getenv("SPECEDGE_QKV_FUSED") && getenv("SPECEDGE_QKV_FUSED")[0] == '0');
-  const bool qkv_fused = qkv_fuse_env && hd == 128 && gemm_qkv_fused_ok((H + 2 * KV) * hd, R);
+  static const int qkv_fuse_env = getenv("SPECEDGE_QKV_FUSED") ? atoi(getenv("SPECEDGE_QKV_FUSED")) : 1;
+  const bool qkv_fused = qkv_fuse_env > 0 && hd == 128 && (qkv_fuse_env == 2 || gemm_qkv_fused_ok((H + 2 * KV) * hd, R));
   for (int l = 0; l < c.n_layers; ++l) {
     g_dbg_layer = l;
     const auto& Lw = m->layers[l];
