@@ -48,8 +48,14 @@ inline int device_sms() {
 // Launch (optionally with programmatic stream serialisation: kernels call pdl_begin() before any
 // global access; enabled by SPECEDGE_PDL=1).
 bool pdl_enabled();
+// Every kernel of the step asks for the max-shared-memory carveout (the GEMMs and the attention
+// need it), so consecutive kernels never change the SM's L1 / shared split (SPECEDGE_CARVEOUT=0:
+// driver default for the small kernels).  Once per (kernel, device).
+bool carveout_first(const void* kern);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  if (carveout_first(reinterpret_cast<const void*>(kern)))
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

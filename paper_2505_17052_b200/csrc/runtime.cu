@@ -11,6 +11,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <tuple>
 #include <vector>
 
@@ -18,6 +19,15 @@ using namespace se;
 
 // Programmatic dependent launch: off by default (SPECEDGE_PDL=1 enables).  Measured on cfg2
 // under graph replay it does not shorten the step (the inter-kernel gaps are already ~1 us).
+bool se::carveout_first(const void* kern) {
+  static const bool on = !(getenv("SPECEDGE_CARVEOUT") && getenv("SPECEDGE_CARVEOUT")[0] == '0');
+  if (!on) return false;
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> seen;
+  std::lock_guard<std::mutex> lk(mu);
+  return seen.insert({kern, current_device()}).second;
+}
+
 bool se::pdl_enabled() {
   static const bool on = getenv("SPECEDGE_PDL") && getenv("SPECEDGE_PDL")[0] == '1';
   return on;
