@@ -52,6 +52,8 @@ bool pdl_enabled();
 // need it), so consecutive kernels never change the SM's L1 / shared split (SPECEDGE_CARVEOUT=0:
 // driver default for the small kernels).  Once per (kernel, device).
 bool carveout_first(const void* kern);
+void carveout_skip(const void* kern);   // leave this kernel at the driver default
+int carveout_mode();                    // SPECEDGE_CARVEOUT: 1 (default) all kernels, 2 all but RMSNorm, 0 none
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   if (carveout_first(reinterpret_cast<const void*>(kern)))

@@ -800,6 +800,16 @@ cudaError_t rmsnorm_launch(float* X, const float* Y, int nY, size_t y_stride, co
   if (launches) ++*launches;
   const int threads = (d / 16 + 31) & ~31;   // whole warps; d % 64 == 0 and d <= 16384 (model creation)
   const RmsSrc src = ys ? *ys : RmsSrc{};
+  if (carveout_mode() == 2) {
+    static PerDeviceOnce once;
+    if (once.first()) {
+      carveout_skip(reinterpret_cast<const void*>(k_rmsnorm<0>));
+      carveout_skip(reinterpret_cast<const void*>(k_rmsnorm<1>));
+      carveout_skip(reinterpret_cast<const void*>(k_rmsnorm<2>));
+      carveout_skip(reinterpret_cast<const void*>(k_rmsnorm<3>));
+      carveout_skip(reinterpret_cast<const void*>(k_rmsnorm<4>));
+    }
+  }
   switch (nY) {
     case 0: CK_RET(launch_k(k_rmsnorm<0>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;
     case 1: CK_RET(launch_k(k_rmsnorm<1>, dim3(R), dim3(threads), 0, st, X, Y, y_stride, g, out, d, eps, split, src)); break;

@@ -19,13 +19,22 @@ using namespace se;
 
 // Programmatic dependent launch: off by default (SPECEDGE_PDL=1 enables).  Measured on cfg2
 // under graph replay it does not shorten the step (the inter-kernel gaps are already ~1 us).
+namespace {
+std::mutex g_carve_mu;
+std::set<std::pair<const void*, int>> g_carve_seen;
+}  // namespace
+int se::carveout_mode() {
+  static const int m = getenv("SPECEDGE_CARVEOUT") ? atoi(getenv("SPECEDGE_CARVEOUT")) : 1;
+  return m;
+}
 bool se::carveout_first(const void* kern) {
-  static const bool on = !(getenv("SPECEDGE_CARVEOUT") && getenv("SPECEDGE_CARVEOUT")[0] == '0');
-  if (!on) return false;
-  static std::mutex mu;
-  static std::set<std::pair<const void*, int>> seen;
-  std::lock_guard<std::mutex> lk(mu);
-  return seen.insert({kern, current_device()}).second;
+  if (carveout_mode() == 0) return false;
+  std::lock_guard<std::mutex> lk(g_carve_mu);
+  return g_carve_seen.insert({kern, current_device()}).second;
+}
+void se::carveout_skip(const void* kern) {
+  std::lock_guard<std::mutex> lk(g_carve_mu);
+  g_carve_seen.insert({kern, current_device()});
 }
 
 bool se::pdl_enabled() {
