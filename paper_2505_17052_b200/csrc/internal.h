@@ -45,8 +45,8 @@ inline int device_sms() {
   return v;
 }
 
-// Launch (optionally with programmatic stream serialisation: kernels call pdl_begin() before any
-// global access; enabled by SPECEDGE_PDL=1).
+// Launch with programmatic stream serialisation (kernels call pdl_begin() before any global
+// access; SPECEDGE_PDL=0 turns it off).
 bool pdl_enabled();
 // Every kernel of the step asks for the max-shared-memory carveout (the GEMMs and the attention
 // need it), so consecutive kernels never change the SM's L1 / shared split (SPECEDGE_CARVEOUT=0:
